@@ -1,0 +1,224 @@
+/* frag_c.h — C ABI of the B200-native FusionRAG online reprocessing path.
+ *
+ * This is the drop-in boundary for the reference's reprocessing surface
+ * (namespace frag, /root/reference/proj/include/frag/common.hpp and the
+ * operation contracts of /root/reference/SPEC.md). Each entry point cites the
+ * reference interface it replaces. Exceptions never cross this boundary: every
+ * function returns a frag_status, and frag_last_error() holds a thread-local
+ * message. The C++ wrapper (frag/fusion.hpp) re-throws them as the
+ * reference's frag::ContractError / StoreError / FormatError.
+ *
+ * Threading:
+ *   - an engine or store is bound to one CUDA device; use one host thread per GPU;
+ *   - engine weights are immutable after create; frag_reprocess is reentrant
+ *     given distinct result objects;
+ *   - store puts take a writer lock, fetches a reader lock, and records are
+ *     pinned while a fetch handle is outstanding.
+ * Layouts: K/V of a record and of the fused cache are [L][tokens][Hkv][dh]
+ * bf16, post-RoPE. Positions are 1-based
+ * (common.hpp:15); fused-cache row r holds position r+1.
+ */
+#ifndef FRAG_C_H
+#define FRAG_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define FRAG_API __attribute__((visibility("default")))
+#else
+#define FRAG_API
+#endif
+
+/* Error taxonomy of common.hpp:17-40 (ContractError, StoreError, FormatError)
+ * plus device failures. */
+typedef enum {
+  FRAG_OK = 0,
+  FRAG_E_CONTRACT = 1, /* precondition violation            -> frag::ContractError */
+  FRAG_E_STORE = 2,    /* duplicate / missing / capacity     -> frag::StoreError    */
+  FRAG_E_FORMAT = 3,   /* bad magic / version / truncation   -> frag::FormatError   */
+  FRAG_E_CUDA = 4,     /* CUDA runtime failure or no device                          */
+  FRAG_E_OOM = 5       /* device allocation failed                                   */
+} frag_status;
+
+/* ModelConfig extended with GQA and Llama-style FFN width. */
+typedef struct {
+  int32_t layers;     /* D */
+  int32_t d_model;    /* hd */
+  int32_t n_heads;    /* query heads */
+  int32_t n_kv_heads; /* KV heads (== n_heads is the spec's MHA) */
+  int32_t head_dim;   /* even */
+  int32_t ffn_dim;    /* gated FFN inner width */
+  int32_t vocab;
+  double rope_base;   /* RotationFrequencies.base */
+  float norm_eps;     /* RMSNorm epsilon (1e-5) */
+} frag_model_cfg;
+
+typedef struct { uint8_t bytes[16]; } frag_chunk_id; /* Hash128 / ChunkId (common.hpp:103-117) */
+
+typedef struct frag_engine frag_engine;
+typedef struct frag_store frag_store;
+typedef struct frag_result frag_result;
+
+enum { FRAG_VARIANT_ISOLATED = 0, FRAG_VARIANT_FUSED = 1 }; /* ChunkKVRecord.variant */
+enum { FRAG_TIER_GPU = 0, FRAG_TIER_CPU = 1, FRAG_TIER_DISK = 2 };
+
+/* Read-only view of a ChunkKVRecord. */
+typedef struct {
+  frag_chunk_id id;
+  int32_t n_tok;
+  int32_t native_start; /* 1-based position of the record's first token */
+  int32_t variant;
+  int32_t tier;         /* always FRAG_TIER_GPU in this build (HBM-resident store) */
+  uint64_t heat;        /* access count */
+  uint64_t last_access; /* store tick of the last fetch */
+  uint64_t size_bytes;
+  const void* k_dev;    /* [L][n_tok][Hkv][dh] bf16 */
+  const void* v_dev;
+  const int32_t* tokens_dev; /* [n_tok] token ids (needed by the recompute gather) */
+} frag_record_view;
+
+typedef struct {
+  int32_t raw_scores;          /* column-sum raw logits instead of joint softmax */
+  int32_t all_logits;          /* logits for all question rows (default: last row = first token) */
+  int32_t timing;              /* record per-stage device timings (cudaEvents on the stream) */
+  const int32_t* inject_crit;  /* optional host list of critical 1-based positions; bypasses the
+                                  query-guided selector ("selection-injection" parity mode) */
+  int32_t n_inject;
+  int32_t logits_on_device;    /* do not copy logits to host (device-resident benchmark leg) */
+} frag_reprocess_opts;
+
+typedef struct {
+  float stitch_ms;   /* K1 */
+  float question_ms; /* question pass through the final-layer Q projection */
+  float select_ms;   /* K9 + K10 */
+  float sparse_ms;   /* selective-recompute prefill, all layers */
+  float lm_head_ms;  /* final norm + K11 + logits copy */
+  float total_ms;
+} frag_timing;
+
+/* ------------------------------------------------------------------ misc */
+FRAG_API const char* frag_last_error(void);
+FRAG_API const char* frag_version(void);
+/* Presets: "tiny", "llama3-8b", "mistral-7b", "llama3-70b". */
+FRAG_API frag_status frag_model_preset(const char* name, frag_model_cfg* out);
+/* hash_tokens (common.hpp:122): 128-bit content hash of a token list. */
+FRAG_API void frag_hash_tokens(const int32_t* tokens, int32_t n, uint64_t salt, frag_chunk_id* out);
+/* Number of device kernels this process has launched through the library. */
+FRAG_API uint64_t frag_launch_count(void);
+/* Synchronous copy between any two host/device pointers (cudaMemcpyDefault);
+ * lets FFI callers read result and record buffers into their own memory. */
+FRAG_API frag_status frag_memcpy(void* dst, const void* src, size_t bytes);
+
+/* ------------------------------------------------------------------ engine
+ * init_model: weights ~ N(0, 0.02^2) drawn from the splitmix64
+ * Rng (common.hpp:45-100), one stream per tensor, rounded to bf16; norm gains 1. */
+FRAG_API frag_status frag_engine_create(const frag_model_cfg* cfg, int device, uint64_t seed, frag_engine** out);
+FRAG_API frag_status frag_engine_destroy(frag_engine* eng);
+FRAG_API frag_status frag_engine_config(const frag_engine* eng, frag_model_cfg* out);
+/* Copy one weight tensor in canonical [out][in] layout to a host bf16 buffer.
+ * which: 0 emb[V][d] 1 lm_head[V][d] 2 wq 3 wk 4 wv 5 wo 6 w_gate 7 w_up 8 w_down
+ *        9 attn_norm 10 ffn_norm 11 final_norm. */
+FRAG_API frag_status frag_engine_weight(const frag_engine* eng, int32_t layer, int32_t which, uint16_t* host_out,
+                                        size_t n_elems);
+FRAG_API uint64_t frag_engine_weight_seed(uint64_t seed, int32_t tensor_id);
+
+/* ------------------------------------------------------------------ store
+ * HBM-resident chunk-KV store: put_record, fetch. */
+FRAG_API frag_status frag_store_create(const frag_model_cfg* cfg, int device, size_t hbm_bytes, frag_store** out);
+FRAG_API frag_status frag_store_destroy(frag_store* st);
+/* k/v may be host or device pointers ([L][n_tok][Hkv][dh] bf16); duplicate
+ * without overwrite -> FRAG_E_STORE (single-copy invariant). */
+FRAG_API frag_status frag_store_put(frag_store* st, const frag_chunk_id* id, const int32_t* tokens, int32_t n_tok,
+                                    int32_t native_start, int32_t variant, const void* k_bf16, const void* v_bf16,
+                                    int32_t overwrite);
+/* heat++, pin; missing id -> FRAG_E_STORE. */
+FRAG_API frag_status frag_store_fetch(frag_store* st, const frag_chunk_id* id, frag_record_view* out);
+FRAG_API frag_status frag_store_release(frag_store* st, const frag_chunk_id* id);
+FRAG_API frag_status frag_store_peek(const frag_store* st, const frag_chunk_id* id, frag_record_view* out);
+FRAG_API int64_t frag_store_count(const frag_store* st);
+FRAG_API uint64_t frag_store_bytes_used(const frag_store* st);
+
+/* preprocess_isolated (Eq. 5) for one chunk on
+ * the GPU: prefill cat(S, C) at positions 1..|S|+|C| and put the record
+ * KV[|S|+1:] with native_start = |S|+1. Writes the chunk id (hash_tokens). */
+FRAG_API frag_status frag_preprocess_isolated(frag_engine* eng, frag_store* st, const int32_t* sys, int32_t n_sys,
+                                              const int32_t* tokens, int32_t n_tok, int32_t overwrite,
+                                              frag_chunk_id* id_out);
+
+/* ------------------------------------------------------------------ reprocess
+ * A result owns the fused KV cache of one request (the per-request
+ * exclusive pages of SPEC.md:148 are the rows recomputed in it) and its
+ * logits; it can be reused across requests of at most max_tokens tokens. */
+FRAG_API frag_status frag_result_create(frag_engine* eng, int32_t max_tokens, frag_result** out);
+FRAG_API frag_status frag_result_free(frag_result* res);
+
+/* stitch_full_reuse + select_query_guided + sparse_prefill_and_decode up to the
+ * first-token logits. recompute_ratio r: k = floor(r*N + 0.5)
+ * critical tokens. stream: cudaStream_t (NULL = legacy default). */
+FRAG_API frag_status frag_reprocess(frag_engine* eng, frag_store* st, const int32_t* sys, int32_t n_sys,
+                                    const int32_t* question, int32_t n_q, const frag_chunk_id* chunk_ids,
+                                    int32_t n_chunks, float recompute_ratio, const frag_reprocess_opts* opts,
+                                    void* stream, frag_result* res);
+/* Same pipeline with the question tokens already on the device (benchmark leg). */
+FRAG_API frag_status frag_reprocess_dev(frag_engine* eng, frag_store* st, const int32_t* sys, int32_t n_sys,
+                                        const int32_t* question_dev, int32_t n_q, const frag_chunk_id* chunk_ids,
+                                        int32_t n_chunks, float recompute_ratio, const frag_reprocess_opts* opts,
+                                        void* stream, frag_result* res);
+/* Full Attention prefill (Eq. 2) of cat(S, tokens) with the same kernels: the
+ * "full prefill" baseline of BASELINE.json and the r=1 endpoint oracle. */
+FRAG_API frag_status frag_full_prefill(frag_engine* eng, const int32_t* sys, int32_t n_sys, const int32_t* tokens,
+                                       int32_t n_tok, const frag_reprocess_opts* opts, void* stream,
+                                       frag_result* res);
+
+FRAG_API frag_status frag_result_sync(frag_result* res);
+/* Fused cache: device pointers [L][T][Hkv][dh] bf16, T = tokens in the prompt. */
+FRAG_API frag_status frag_result_fused_kv(const frag_result* res, const void** k_dev, const void** v_dev,
+                                          int32_t* n_tokens);
+/* Logits fp32 [rows][V]; host pointer (or device pointer with logits_on_device). */
+FRAG_API frag_status frag_result_logits(const frag_result* res, const float** logits, int32_t* rows,
+                                        int32_t* vocab, int32_t on_device);
+/* Critical positions (1-based, ascending) chosen for the last request. */
+FRAG_API int32_t frag_result_crit(const frag_result* res, int32_t* host_out, int32_t cap);
+FRAG_API frag_status frag_result_timing(const frag_result* res, frag_timing* out);
+/* Debug views for parity tests: final-layer question queries fp32 [n_q][Hq][dh]
+ * and the per-token query-guided scores fp32 [N] (device pointers). */
+FRAG_API frag_status frag_result_debug(const frag_result* res, const float** q_final_dev, const float** scores_dev,
+                                       int32_t* n_q, int32_t* n_chunk_tokens);
+
+/* ------------------------------------------------------------------ profiling
+ * Per-kernel-class device timing (cudaEvents around each launch on the
+ * launching stream) for the bench roofline. class: 0 GEMM (K4/K7/K8/K11),
+ * 1 attention (K6), 2 stitch (K1), 3 norms/gather (K2/K3), 4 select (K9/K10). */
+FRAG_API frag_status frag_engine_profile(frag_engine* eng, int32_t enable);
+/* Sums over launches since the last reset (call after frag_result_sync):
+ * device ms, algorithmic FLOPs, algorithmic bytes, launch count. */
+FRAG_API frag_status frag_engine_profile_read(frag_engine* eng, int32_t klass, double* ms, double* flops,
+                                              double* bytes, int64_t* launches, int32_t reset);
+
+/* ------------------------------------------------------------------ kernels
+ * Kernel-level entry points over device pointers (parity tests, bench roofline). */
+/* C[M,N] = A[M,K] B[N,K]^T, bf16 in, epi 0: bf16 out, 1: fp32 out, 2: fp32 C += . */
+FRAG_API frag_status frag_kernel_gemm(const void* a, const void* b, void* c, int32_t M, int32_t N, int32_t K,
+                                      int32_t epi, int32_t force_bn, void* stream);
+/* K1 on one record: dst[L][n][Hkv][dh] = shift_rope(src, native_start -> target_start). */
+FRAG_API frag_status frag_kernel_rope_shift(const void* k_src, void* k_dst, int32_t L, int32_t n_tok, int32_t Hkv,
+                                            int32_t dh, int32_t native_start, int32_t target_start,
+                                            double rope_base, void* stream);
+/* K9+K10 on given final-layer queries q[nq][Hq][dh] fp32 and keys k[N][Hkv][dh] bf16. */
+FRAG_API frag_status frag_kernel_qg_select(const float* q, const void* k, int32_t nq, int32_t Hq, int32_t Hkv,
+                                           int32_t dh, int32_t n_keys, int32_t k_sel, int32_t raw,
+                                           float* scores_dev, int32_t* sel_dev, void* stream);
+/* K6: q[M][Hq][dh], k/v [T][Hkv][dh] bf16, rows[M] ascending query rows -> out[M][Hq][dh]. */
+FRAG_API frag_status frag_kernel_attention(const void* q, const void* k, const void* v, const int32_t* rows,
+                                           void* out, int32_t M, int32_t T, int32_t Hq, int32_t Hkv, int32_t dh,
+                                           int32_t split_keys, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRAG_C_H */

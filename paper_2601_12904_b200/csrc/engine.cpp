@@ -1,0 +1,839 @@
+// Host orchestration of the online reprocessing stage:
+//   stitch_full_reuse (K1) -> question pass (last_layer_query_states)
+//   -> select_query_guided (K9, K10) -> sparse prefill (K2..K8 per layer) -> lm_head (K11).
+// The whole request is stream-ordered; the only host synchronisation is the
+// final one that makes the first-token logits visible (the TTFT end).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "engine.h"
+
+namespace fragimpl {
+
+std::atomic<uint64_t> g_launches{0};
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) fail(FRAG_E_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(FRAG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+void DevBuf::alloc(size_t n) {
+  release();
+  if (n == 0) return;
+  cudaError_t e = cudaMalloc(&p, n);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    fail(FRAG_E_OOM, "cudaMalloc(" + std::to_string(n) + " bytes) failed: " + cudaGetErrorString(e));
+  }
+  bytes = n;
+}
+void DevBuf::ensure(size_t n) {
+  if (n > bytes) alloc(n);
+}
+void PinnedBuf::ensure(size_t n) {
+  if (n <= bytes) return;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  bytes = 0;
+  check_cuda(cudaMallocHost(&p, n), "cudaMallocHost");
+  bytes = n;
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+  cudaGetDevice(&prev);
+  if (prev != dev) check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+}
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+}
+
+// ---------------------------------------------------------------- profiler
+cudaEvent_t Profiler::get() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+void Profiler::begin(cudaStream_t s, cudaEvent_t* a) {
+  if (!on) return;
+  *a = get();
+  cudaEventRecord(*a, s);
+}
+void Profiler::end(cudaStream_t s, cudaEvent_t a, int klass, double fl, double by, int nl) {
+  if (!on) return;
+  cudaEvent_t b = get();
+  cudaEventRecord(b, s);
+  std::lock_guard<std::mutex> g(mu);
+  pending.push_back({a, b, klass, fl, by, nl});
+}
+void Profiler::collect() {
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& r : pending) {
+    float t = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&t, r.a, r.b);
+    ms[r.klass] += t;
+    flops[r.klass] += r.flops;
+    bytes[r.klass] += r.bytes;
+    launches[r.klass] += r.launches;
+    pool.push_back(r.a);
+    pool.push_back(r.b);
+  }
+  pending.clear();
+}
+void Profiler::reset() {
+  collect();
+  for (int i = 0; i < KC_N; ++i) ms[i] = flops[i] = bytes[i] = 0, launches[i] = 0;
+}
+Profiler::~Profiler() {
+  for (auto& r : pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : pool) cudaEventDestroy(e);
+}
+
+namespace {
+
+struct Scoped {
+  Profiler& p;
+  cudaStream_t s;
+  int klass;
+  double fl, by;
+  cudaEvent_t a = nullptr;
+  int n = 0;
+  Scoped(Profiler& p_, cudaStream_t s_, int k, double f, double b) : p(p_), s(s_), klass(k), fl(f), by(b) {
+    p.begin(s, &a);
+  }
+  void launched(int c) {
+    if (c < 0) fail(FRAG_E_CONTRACT, "kernel launch rejected the shape");
+    n += c;
+    g_launches += (uint64_t)c;
+  }
+  ~Scoped() {
+    if (p.on) p.end(s, a, klass, fl, by, n);
+  }
+};
+
+inline void peek(const char* what) {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(FRAG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+}  // namespace
+
+uint64_t weight_seed(uint64_t seed, int tensor_id) {
+  return mix64(seed + 0x9e3779b97f4a7c15ULL * (uint64_t)(tensor_id + 1));
+}
+
+// ---------------------------------------------------------------- engine
+void Engine::ensure_rope(int rows) {
+  std::lock_guard<std::mutex> g(rope_mu);
+  if (rows <= rope_rows) return;
+  const int half = cfg.head_dim / 2;
+  int n = rows < 4096 ? 4096 : rows;
+  std::vector<float2> tab((size_t)n * half);
+  for (int r = 0; r < n; ++r) {
+    const double pos = (double)(r + 1);
+    for (int i = 0; i < half; ++i) {
+      const double a = pos * theta[i];
+      tab[(size_t)r * half + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  }
+  DeviceGuard dg(device);
+  cudaDeviceSynchronize();  // the table may be in use by in-flight work
+  rope.alloc(tab.size() * sizeof(float2));
+  check_cuda(cudaMemcpy(rope.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice), "rope upload");
+  rope_rows = n;
+}
+
+static void validate_cfg(const frag_model_cfg& c) {
+  auto req = [](bool ok, const char* m) {
+    if (!ok) fail(FRAG_E_CONTRACT, std::string("invalid ModelConfig: ") + m);
+  };
+  req(c.layers >= 1, "layers >= 1");
+  req(c.head_dim == 64 || c.head_dim == 128, "head_dim in {64, 128}");
+  req(c.n_heads >= 1 && c.n_kv_heads >= 1 && c.n_heads % c.n_kv_heads == 0, "n_heads multiple of n_kv_heads");
+  req(64 % (c.n_heads / c.n_kv_heads) == 0, "GQA group divides 64");
+  req(c.d_model % 64 == 0, "d_model % 64 == 0");
+  req(c.ffn_dim % 64 == 0, "ffn_dim % 64 == 0");
+  req(c.vocab % 64 == 0 && c.vocab >= 2, "vocab % 64 == 0");
+  req((c.n_heads * c.head_dim) % 64 == 0, "n_heads*head_dim % 64 == 0");
+  req(c.rope_base > 0, "rope_base > 0");
+  req(c.norm_eps > 0, "norm_eps > 0");
+}
+
+Engine* engine_create(const frag_model_cfg& cfg, int device, uint64_t seed) {
+  validate_cfg(cfg);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    fail(FRAG_E_CUDA, "no CUDA device available (this library has no CPU fallback)");
+  }
+  if (device < 0 || device >= ndev) fail(FRAG_E_CONTRACT, "device ordinal out of range");
+  DeviceGuard dg(device);
+  auto e = std::make_unique<Engine>();
+  e->cfg = cfg;
+  e->device = device;
+  e->seed = seed;
+  const size_t d = cfg.d_model, V = cfg.vocab, F = cfg.ffn_dim, qc = (size_t)cfg.n_heads * cfg.head_dim;
+  const size_t qkv = e->qkv_cols();
+  // carve one allocation
+  std::vector<size_t> sizes = {V * d, V * d, d};
+  for (int l = 0; l < cfg.layers; ++l) {
+    sizes.push_back(qkv * d);
+    sizes.push_back(d * qc);
+    sizes.push_back(2 * F * d);
+    sizes.push_back(d * F);
+    sizes.push_back(d);
+    sizes.push_back(d);
+  }
+  size_t total = 0;
+  std::vector<size_t> offs;
+  for (size_t s : sizes) {
+    offs.push_back(total);
+    total += align_up(s * sizeof(bf16), 256);
+    e->n_params += s;
+  }
+  e->weights.alloc(total);
+  bf16* base = e->weights.as<bf16>();
+  auto at = [&](size_t i) { return reinterpret_cast<bf16*>(reinterpret_cast<char*>(base) + offs[i]); };
+  e->emb = at(0);
+  e->lm_head = at(1);
+  e->final_norm = at(2);
+  e->layers.resize(cfg.layers);
+  for (int l = 0; l < cfg.layers; ++l) {
+    auto& L = e->layers[l];
+    L.wqkv = at(3 + 6 * l);
+    L.wo = at(4 + 6 * l);
+    L.wgu = at(5 + 6 * l);
+    L.wd = at(6 + 6 * l);
+    L.attn_norm = at(7 + 6 * l);
+    L.ffn_norm = at(8 + 6 * l);
+  }
+  cudaStream_t s;
+  check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  const float sig = 0.02f;
+  // init_model: tensor ids 0 emb, 1 lm_head, 16+8l+{0..6} wq wk wv wo wg wu wd
+  fragk::init_normal_bf16(e->emb, weight_seed(seed, 0), V, d, sig, (int)V, 0, 0, s);
+  fragk::init_normal_bf16(e->lm_head, weight_seed(seed, 1), V, d, sig, (int)V, 0, 0, s);
+  fragk::fill_bf16(e->final_norm, d, 1.0f, s);
+  const int Hq = cfg.n_heads, Hkv = cfg.n_kv_heads, dh = cfg.head_dim;
+  for (int l = 0; l < cfg.layers; ++l) {
+    auto& L = e->layers[l];
+    const int t0 = 16 + 8 * l;
+    const int qrows = Hq * dh, krows = Hkv * dh;
+    fragk::init_normal_bf16(L.wqkv, weight_seed(seed, t0 + 0), qrows, d, sig, qrows, 0, 0, s);
+    fragk::init_normal_bf16(L.wqkv, weight_seed(seed, t0 + 1), krows, d, sig, krows, 0, qrows, s);
+    fragk::init_normal_bf16(L.wqkv, weight_seed(seed, t0 + 2), krows, d, sig, krows, 0, qrows + krows, s);
+    fragk::init_normal_bf16(L.wo, weight_seed(seed, t0 + 3), d, qc, sig, (int)d, 0, 0, s);
+    // gate/up interleaved in 32-row blocks: packed row = (r/32)*64 + {0 | 32} + r%32
+    fragk::init_normal_bf16(L.wgu, weight_seed(seed, t0 + 4), F, d, sig, 32, 64, 0, s);
+    fragk::init_normal_bf16(L.wgu, weight_seed(seed, t0 + 5), F, d, sig, 32, 64, 32, s);
+    fragk::init_normal_bf16(L.wd, weight_seed(seed, t0 + 6), d, F, sig, (int)d, 0, 0, s);
+    fragk::fill_bf16(L.attn_norm, d, 1.0f, s);
+    fragk::fill_bf16(L.ffn_norm, d, 1.0f, s);
+  }
+  g_launches += 3 + 9 * (uint64_t)cfg.layers;
+  check_cuda(cudaStreamSynchronize(s), "weight init");
+  cudaStreamDestroy(s);
+  const int half = dh / 2;
+  e->theta.resize(half);
+  for (int i = 0; i < half; ++i) e->theta[i] = std::pow(cfg.rope_base, -2.0 * (double)(i + 1) / (double)dh);
+  e->ensure_rope(4096);
+  return e.release();
+}
+
+Result::~Result() {
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+}
+
+void result_init(Result* r, Engine* e, int max_tokens) {
+  if (max_tokens < 1) fail(FRAG_E_CONTRACT, "max_tokens must be positive");
+  DeviceGuard dg(e->device);
+  const auto& c = e->cfg;
+  r->eng = e;
+  r->max_tokens = max_tokens;
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim, qc = (size_t)c.n_heads * c.head_dim;
+  const size_t M = max_tokens;
+  r->k_fused.alloc((size_t)c.layers * M * kvc * sizeof(bf16));
+  r->v_fused.alloc((size_t)c.layers * M * kvc * sizeof(bf16));
+  r->h.alloc(M * c.d_model * sizeof(float));
+  r->x.alloc(M * std::max<size_t>(c.d_model, qc) * sizeof(bf16));
+  r->q.alloc(M * qc * sizeof(bf16));
+  r->attn.alloc(M * qc * sizeof(bf16));
+  r->act.alloc(M * c.ffn_dim * sizeof(bf16));
+  r->plan_rows.alloc(M * sizeof(int));
+  r->plan_tok.alloc(M * sizeof(int));
+  r->chunk_tok.alloc(M * sizeof(int));
+  r->q_tok.alloc(M * sizeof(int));
+  r->scores.alloc(M * sizeof(float));
+  r->row_map.alloc(M * sizeof(int));
+  for (auto& ev : r->ev) check_cuda(cudaEventCreate(&ev), "cudaEventCreate");
+  e->ensure_rope(max_tokens);
+}
+
+// ---------------------------------------------------------------- run_rows
+void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
+              int n_logit_rows) {
+  if (M <= 0) return;
+  const auto& c = e->cfg;
+  const int d = c.d_model, Hq = c.n_heads, Hkv = c.n_kv_heads, dh = c.head_dim, F = c.ffn_dim;
+  const size_t qc = (size_t)Hq * dh, kvc = (size_t)Hkv * dh, qkv = e->qkv_cols();
+  const size_t lstride = (size_t)r->max_tokens * kvc;
+  Profiler& P = e->prof;
+  bf16* kf = r->k_fused.as<bf16>();
+  bf16* vf = r->v_fused.as<bf16>();
+  const int* prow = r->plan_rows.as<int>();
+  const int* ptok = r->plan_tok.as<int>();
+  float* h = r->h.as<float>();
+  bf16* x = r->x.as<bf16>();
+
+  // split-KV policy: enough CTAs for >= 2 waves, splits of >= 256 keys
+  const int G = Hq / Hkv;
+  const int nqb = (M + (64 / G) - 1) / (64 / G);
+  const long ctas = (long)nqb * Hkv;
+  int n_splits = 1, split_keys = 0;
+  const int sms = fragk::num_sms();
+  if (ctas < 2L * sms && T > 512) {
+    n_splits = (int)((2L * sms + ctas - 1) / ctas);
+    const int max_splits = (T + 255) / 256;
+    if (n_splits > max_splits) n_splits = max_splits;
+    split_keys = (int)align_up((size_t)((T + n_splits - 1) / n_splits), 64);
+    n_splits = (T + split_keys - 1) / split_keys;
+    if (n_splits <= 1) n_splits = 1, split_keys = 0;
+  }
+  if (n_splits > 1) {
+    r->part_o.ensure((size_t)n_splits * M * qc * sizeof(float));
+    r->part_lse.ensure((size_t)n_splits * M * Hq * sizeof(float));
+  }
+  if (mode == PASS_QUESTION) r->q_final.ensure((size_t)M * qc * sizeof(float));
+
+  {
+    Scoped sc(P, s, KC_NORM, 0, (double)M * d * (2 + 4 + 2));
+    fragk::embed_rmsnorm(e->emb, ptok, M, d, e->layers[0].attn_norm, c.norm_eps, h, x, s);
+    sc.launched(1);
+  }
+  for (int l = 0; l < c.layers; ++l) {
+    const auto& W = e->layers[l];
+    if (l > 0) {
+      Scoped sc(P, s, KC_NORM, 0, (double)M * d * (4 + 2));
+      fragk::rmsnorm(h, M, d, W.attn_norm, c.norm_eps, x, s);
+      sc.launched(1);
+    }
+    {
+      fragk::EpiParams ep;
+      ep.rows = prow;
+      ep.rope = e->rope.as<float2>();
+      ep.q_out = r->q.as<bf16>();
+      ep.q_out_f32 = (mode == PASS_QUESTION && l == c.layers - 1) ? r->q_final.as<float>() : nullptr;
+      ep.k_cache = kf + l * lstride;
+      ep.v_cache = vf + l * lstride;
+      ep.Hq = Hq;
+      ep.Hkv = Hkv;
+      ep.dh = dh;
+      Scoped sc(P, s, KC_GEMM, 2.0 * M * qkv * d, 2.0 * (qkv * d + (double)M * (d + qkv)));
+      sc.launched(fragk::gemm_bf16_tc(x, W.wqkv, M, (int)qkv, d, fragk::EPI_QKV, ep, s));
+    }
+    if (mode != PASS_FULL && l == c.layers - 1) break;
+    {
+      fragk::AttnArgs a{};
+      a.q = r->q.as<bf16>();
+      a.k = kf + l * lstride;
+      a.v = vf + l * lstride;
+      a.rows = prow;
+      a.out = r->attn.as<bf16>();
+      a.part_o = r->part_o.as<float>();
+      a.part_lse = r->part_lse.as<float>();
+      a.M = M;
+      a.T = T;
+      a.Hq = Hq;
+      a.Hkv = Hkv;
+      a.dh = dh;
+      a.split_keys = split_keys;
+      a.n_splits = n_splits;
+      a.scale = 1.0f / std::sqrt((float)dh);
+      Scoped sc(P, s, KC_ATTN, 0, 0);
+      sc.launched(fragk::sparse_q_attention(a, s));
+    }
+    {
+      fragk::EpiParams ep;
+      ep.resid = h;
+      ep.ldo = d;
+      Scoped sc(P, s, KC_GEMM, 2.0 * M * d * qc, 2.0 * (qc * d + (double)M * qc) + 8.0 * M * d);
+      sc.launched(fragk::gemm_bf16_tc(r->attn.as<bf16>(), W.wo, M, d, (int)qc, fragk::EPI_RESID, ep, s));
+    }
+    {
+      Scoped sc(P, s, KC_NORM, 0, (double)M * d * (4 + 2));
+      fragk::rmsnorm(h, M, d, W.ffn_norm, c.norm_eps, x, s);
+      sc.launched(1);
+    }
+    {
+      fragk::EpiParams ep;
+      ep.out_bf16 = r->act.as<bf16>();
+      ep.ldo = F;
+      Scoped sc(P, s, KC_GEMM, 2.0 * M * 2.0 * F * d, 2.0 * (2.0 * F * d + (double)M * d + (double)M * F));
+      sc.launched(fragk::gemm_bf16_tc(x, W.wgu, M, 2 * F, d, fragk::EPI_SWIGLU, ep, s));
+    }
+    {
+      fragk::EpiParams ep;
+      ep.resid = h;
+      ep.ldo = d;
+      Scoped sc(P, s, KC_GEMM, 2.0 * M * (double)d * F, 2.0 * ((double)F * d + (double)M * F) + 8.0 * M * d);
+      sc.launched(fragk::gemm_bf16_tc(r->act.as<bf16>(), W.wd, M, d, F, fragk::EPI_RESID, ep, s));
+    }
+    peek("layer");
+  }
+  if (mode == PASS_FULL && n_logit_rows > 0) {
+    r->lm_x.ensure((size_t)n_logit_rows * d * sizeof(bf16));
+    r->logits.ensure((size_t)n_logit_rows * c.vocab * sizeof(float));
+    {
+      Scoped sc(P, s, KC_NORM, 0, (double)n_logit_rows * d * 6);
+      fragk::rmsnorm(h, n_logit_rows, d, e->final_norm, c.norm_eps, r->lm_x.as<bf16>(), s, row_map_dev);
+      sc.launched(1);
+    }
+    fragk::EpiParams ep;
+    ep.out_f32 = r->logits.as<float>();
+    ep.ldo = c.vocab;
+    Scoped sc(P, s, KC_GEMM, 2.0 * n_logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
+    sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, n_logit_rows, c.vocab, d,
+                                    fragk::EPI_STORE_F32, ep, s));
+  }
+  peek("run_rows");
+}
+
+// ---------------------------------------------------------------- helpers
+namespace {
+
+struct PinGuard {
+  Store* st;
+  std::vector<frag_chunk_id> ids;
+  ~PinGuard() {
+    for (auto& id : ids) {
+      try {
+        store_release(st, id);
+      } catch (...) {
+      }
+    }
+  }
+};
+
+// Bump allocator over the result's pinned staging buffer.
+struct Stage {
+  PinnedBuf& buf;
+  size_t off = 0;
+  explicit Stage(PinnedBuf& b) : buf(b) {}
+  template <class T>
+  T* take(size_t n) {
+    off = align_up(off, 64);
+    T* p = reinterpret_cast<T*>(static_cast<char*>(buf.p) + off);
+    off += n * sizeof(T);
+    if (off > buf.bytes) fail(FRAG_E_CONTRACT, "staging overflow");
+    return p;
+  }
+};
+
+void stitch(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys,
+            const std::vector<Record*>& recs, int S) {
+  const auto& c = e->cfg;
+  const int half = c.head_dim / 2;
+  const int n_desc = (sys && sys->n > 0 ? 1 : 0) + (int)recs.size();
+  if (n_desc == 0) return;
+  auto* desc = stg.take<fragk::StitchChunk>(n_desc);
+  std::vector<float2> tabs;
+  int nd = 0, max_rows = 0, n_tab = 0;
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  if (sys && sys->n > 0) {
+    desc[nd++] = {sys->kv.as<bf16>(), sys->kv.as<bf16>() + (size_t)c.layers * sys->n * kvc, sys->n, 0, -1};
+    max_rows = sys->n;
+  }
+  int row = S;
+  for (Record* rec : recs) {
+    const int target_start = row + 1;  // 1-based
+    const int delta = target_start - rec->native_start;
+    int table = -1;
+    if (delta != 0) {
+      // shift_rope = apply_rope(v, new - old): cos/sin(delta * theta_i), fp64 angles
+      table = n_tab++;
+      for (int i = 0; i < half; ++i) {
+        const double a = (double)delta * e->theta[i];
+        tabs.push_back(make_float2((float)std::cos(a), (float)std::sin(a)));
+      }
+    }
+    desc[nd++] = {rec->k(), rec->v(), rec->n_tok, row, table};
+    if (rec->n_tok > max_rows) max_rows = rec->n_tok;
+    row += rec->n_tok;
+  }
+  float2* tab_h = stg.take<float2>(tabs.size() > 0 ? tabs.size() : 1);
+  if (!tabs.empty()) std::memcpy(tab_h, tabs.data(), tabs.size() * sizeof(float2));
+  r->stitch_desc.ensure(n_desc * sizeof(fragk::StitchChunk));
+  r->stitch_tab.ensure(std::max<size_t>(tabs.size(), 1) * sizeof(float2));
+  check_cuda(cudaMemcpyAsync(r->stitch_desc.p, desc, n_desc * sizeof(fragk::StitchChunk), cudaMemcpyHostToDevice, s),
+             "stitch desc");
+  if (!tabs.empty())
+    check_cuda(cudaMemcpyAsync(r->stitch_tab.p, tab_h, tabs.size() * sizeof(float2), cudaMemcpyHostToDevice, s),
+               "stitch tab");
+  double bytes = 0;
+  for (int i = 0; i < n_desc; ++i) bytes += 4.0 * c.layers * desc[i].n_tok * kvc * sizeof(bf16);
+  Scoped sc(e->prof, s, KC_STITCH, 0, bytes);
+  fragk::rope_shift_assemble(r->stitch_desc.as<fragk::StitchChunk>(), n_desc, max_rows,
+                             r->stitch_tab.as<float2>(), r->k_fused.as<bf16>(), r->v_fused.as<bf16>(), c.layers,
+                             r->max_tokens, c.n_kv_heads, c.head_dim, s);
+  sc.launched(1);
+  peek("stitch");
+}
+
+Result* scratch_for(Engine* e, int tokens) {
+  if (!e->scratch || e->scratch->max_tokens < tokens) {
+    e->scratch = std::make_unique<Result>();
+    result_init(e->scratch.get(), e, std::max(tokens, 256));
+  }
+  return e->scratch.get();
+}
+
+// KV_S of the system prompt, computed once per token list.
+SysKV* get_sys_kv(Engine* e, const int32_t* sys, int n_sys, cudaStream_t s) {
+  if (n_sys <= 0) return nullptr;
+  std::vector<int32_t> key(sys, sys + n_sys);
+  std::lock_guard<std::mutex> g(e->mu);
+  auto it = e->sys_cache.find(key);
+  if (it != e->sys_cache.end()) return it->second.get();
+  const auto& c = e->cfg;
+  for (int i = 0; i < n_sys; ++i)
+    if (sys[i] < 0 || sys[i] >= c.vocab) fail(FRAG_E_CONTRACT, "system token out of vocabulary");
+  Result* r = scratch_for(e, n_sys);
+  std::vector<int> rows(n_sys);
+  for (int i = 0; i < n_sys; ++i) rows[i] = i;
+  check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows.data(), n_sys * sizeof(int), cudaMemcpyHostToDevice, s), "sys rows");
+  check_cuda(cudaMemcpyAsync(r->plan_tok.p, sys, n_sys * sizeof(int), cudaMemcpyHostToDevice, s), "sys tok");
+  run_rows(e, r, s, n_sys, n_sys, PASS_KV_ONLY, nullptr, 0);
+  auto kv = std::make_unique<SysKV>();
+  kv->n = n_sys;
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  const size_t w = (size_t)n_sys * kvc * sizeof(bf16), pitch = (size_t)r->max_tokens * kvc * sizeof(bf16);
+  kv->kv.alloc(2 * (size_t)c.layers * w);
+  check_cuda(cudaMemcpy2DAsync(kv->kv.p, w, r->k_fused.p, pitch, w, c.layers, cudaMemcpyDeviceToDevice, s), "sysK");
+  check_cuda(cudaMemcpy2DAsync(kv->kv.as<char>() + c.layers * w, w, r->v_fused.p, pitch, w, c.layers,
+                               cudaMemcpyDeviceToDevice, s),
+             "sysV");
+  check_cuda(cudaStreamSynchronize(s), "system prompt prefill");
+  SysKV* out = kv.get();
+  e->sys_cache.emplace(std::move(key), std::move(kv));
+  return out;
+}
+
+void ev_record(Result* r, bool on, int i, cudaStream_t s) {
+  if (on) cudaEventRecord(r->ev[i], s);
+}
+
+void finish(Result* r, bool timing, cudaStream_t s, const frag_reprocess_opts* o) {
+  Engine* e = r->eng;
+  const auto& c = e->cfg;
+  r->logits_on_device = o && o->logits_on_device;
+  if (!r->logits_on_device && r->logit_rows > 0) {
+    const size_t n = (size_t)r->logit_rows * c.vocab;
+    r->logits_host.ensure(n * sizeof(float));
+    check_cuda(cudaMemcpyAsync(r->logits_host.p, r->logits.p, n * sizeof(float), cudaMemcpyDeviceToHost, s),
+               "logits D2H");
+  }
+  ev_record(r, timing, 6, s);
+  r->last_stream = s;
+  check_cuda(cudaStreamSynchronize(s), "reprocess");
+  e->prof.collect();
+  r->timing_valid = timing;
+  if (timing) {
+    float t[6] = {};
+    for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&t[i], r->ev[i], r->ev[i + 1]);
+    r->timing.stitch_ms = t[0];
+    r->timing.question_ms = t[1];
+    r->timing.select_ms = t[2];
+    r->timing.sparse_ms = t[3];
+    r->timing.lm_head_ms = t[4] + t[5];
+    cudaEventElapsedTime(&r->timing.total_ms, r->ev[0], r->ev[6]);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- reprocess
+void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
+               bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio,
+               const frag_reprocess_opts* o, cudaStream_t s, Result* r) {
+  const auto& c = e->cfg;
+  if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
+  if (!st) fail(FRAG_E_CONTRACT, "store is null");
+  if (st->device != e->device) fail(FRAG_E_CONTRACT, "store and engine are on different devices");
+  if (n_q < 1) fail(FRAG_E_CONTRACT, "question must have at least one token");
+  if (n_sys < 0 || n_chunks < 0) fail(FRAG_E_CONTRACT, "negative length");
+  if (!(ratio >= 0.f && ratio <= 1.f)) fail(FRAG_E_CONTRACT, "recompute_ratio must lie in [0, 1]");
+  if (n_chunks > 0 && !ids) fail(FRAG_E_CONTRACT, "chunk_ids is null");
+  DeviceGuard dg(e->device);
+  const bool timing = o && o->timing;
+  if (!q_on_device)
+    for (int i = 0; i < n_q; ++i)
+      if (q_tokens[i] < 0 || q_tokens[i] >= c.vocab) fail(FRAG_E_CONTRACT, "question token out of vocabulary");
+
+  PinGuard pins{st, {}};
+  std::vector<Record*> recs;
+  for (int i = 0; i < n_chunks; ++i) {
+    recs.push_back(store_fetch(st, ids[i]));  // heat++, pin
+    pins.ids.push_back(ids[i]);
+  }
+  const int S = n_sys;
+  int N = 0;
+  for (Record* rec : recs) N += rec->n_tok;
+  const int T = S + N + n_q;
+  if (T > r->max_tokens)
+    fail(FRAG_E_CONTRACT, "prompt of " + std::to_string(T) + " tokens exceeds the result capacity " +
+                              std::to_string(r->max_tokens));
+  const bool inject = o && o->inject_crit;
+  int k = (int)std::floor((double)ratio * (double)N + 0.5);  // |C_idx| = round(r * sum|C|)
+  if (inject) {
+    k = o->n_inject;
+    if (k < 0 || k > N) fail(FRAG_E_CONTRACT, "injected critical set larger than the chunk tokens");
+    for (int i = 0; i < k; ++i) {
+      const int p = o->inject_crit[i];
+      if (p < S + 1 || p > S + N) fail(FRAG_E_CONTRACT, "critical position outside the chunk range (SPEC.md:391)");
+      if (i > 0 && p <= o->inject_crit[i - 1]) fail(FRAG_E_CONTRACT, "critical positions must be strictly increasing");
+    }
+    if (q_on_device) fail(FRAG_E_CONTRACT, "selection injection requires host question tokens");
+  }
+  const int M = k + n_q;
+  e->ensure_rope(T);
+  SysKV* skv = get_sys_kv(e, sys, n_sys, s);
+
+  r->T = T;
+  r->S = S;
+  r->N = N;
+  r->nq = n_q;
+  r->k_sel = k;
+  r->M = M;
+  const bool all_logits = o && o->all_logits;
+  r->logit_rows = all_logits ? n_q : 1;
+
+  r->staging.ensure(64 * 1024 + (size_t)(n_chunks + 2) * (64 + c.head_dim * 4) + (size_t)(4 * T + 4 * M + 4 * n_q) * 4);
+  Stage stg(r->staging);
+
+  ev_record(r, timing, 0, s);
+  // ---- K1: stitch_full_reuse
+  stitch(e, r, s, stg, skv, recs, S);
+  // chunk token ids in prompt order (needed by the recompute gather, K2)
+  {
+    int off = 0;
+    for (Record* rec : recs) {
+      check_cuda(cudaMemcpyAsync(r->chunk_tok.as<int>() + off, rec->tok.p, rec->n_tok * sizeof(int),
+                                 cudaMemcpyDeviceToDevice, s),
+                 "chunk tokens");
+      off += rec->n_tok;
+    }
+  }
+  if (q_on_device) {
+    check_cuda(cudaMemcpyAsync(r->q_tok.p, q_tokens, n_q * sizeof(int), cudaMemcpyDeviceToDevice, s), "q tok");
+  } else {
+    int* qh = stg.take<int>(n_q);
+    std::memcpy(qh, q_tokens, n_q * sizeof(int));
+    check_cuda(cudaMemcpyAsync(r->q_tok.p, qh, n_q * sizeof(int), cudaMemcpyHostToDevice, s), "q tok");
+  }
+  ev_record(r, timing, 1, s);
+  // ---- question pass (last_layer_query_states against the stitched cache)
+  {
+    int* rows_h = stg.take<int>(n_q);
+    for (int i = 0; i < n_q; ++i) rows_h[i] = T - n_q + i;
+    check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, n_q * sizeof(int), cudaMemcpyHostToDevice, s), "q rows");
+    check_cuda(cudaMemcpyAsync(r->plan_tok.p, r->q_tok.p, n_q * sizeof(int), cudaMemcpyDeviceToDevice, s), "q plan");
+    run_rows(e, r, s, n_q, T, PASS_QUESTION, nullptr, 0);
+  }
+  ev_record(r, timing, 2, s);
+  // ---- select_query_guided (K9 + K10) -> QIndexPlan on device
+  if (inject) {
+    int* rows_h = stg.take<int>(M);
+    int* tok_h = stg.take<int>(M);
+    for (int i = 0; i < k; ++i) {
+      const int row = o->inject_crit[i] - 1;
+      rows_h[i] = row;
+      int j = row - S;
+      int t = 0;
+      for (Record* rec : recs) {
+        if (j < rec->n_tok) {
+          t = rec->tok_host[j];
+          break;
+        }
+        j -= rec->n_tok;
+      }
+      tok_h[i] = t;
+    }
+    for (int i = 0; i < n_q; ++i) {
+      rows_h[k + i] = T - n_q + i;
+      tok_h[k + i] = q_tokens[i];
+    }
+    check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, M * sizeof(int), cudaMemcpyHostToDevice, s), "plan rows");
+    check_cuda(cudaMemcpyAsync(r->plan_tok.p, tok_h, M * sizeof(int), cudaMemcpyHostToDevice, s), "plan tok");
+  } else {
+    if (N > 0) {
+      const int nblk = (N + 31) / 32;
+      r->part_ms.ensure((size_t)nblk * n_q * c.n_heads * sizeof(float2));
+      r->row_ms.ensure((size_t)n_q * c.n_heads * sizeof(float2));
+      fragk::ScoreArgs a{};
+      a.q = r->q_final.as<float>();
+      a.k = r->k_fused.as<bf16>() + (size_t)(c.layers - 1) * r->max_tokens * c.n_kv_heads * c.head_dim;
+      a.nq = n_q;
+      a.Hq = c.n_heads;
+      a.Hkv = c.n_kv_heads;
+      a.dh = c.head_dim;
+      a.key_row0 = S;
+      a.n_keys = N;
+      a.scale = 1.0f / std::sqrt((float)c.head_dim);
+      a.part_ms = r->part_ms.as<float2>();
+      a.row_ms = r->row_ms.as<float2>();
+      a.scores = r->scores.as<float>();
+      a.raw = o && o->raw_scores;
+      Scoped sc(e->prof, s, KC_SELECT, 4.0 * n_q * c.n_heads * (double)N * c.head_dim,
+                2.0 * N * (double)c.n_kv_heads * c.head_dim * 2);
+      sc.launched(fragk::qg_score(a, s));
+    }
+    Scoped sc(e->prof, s, KC_SELECT, 0, 4.0 * N * 6);
+    sc.launched(fragk::topk_plan(r->scores.as<float>(), N, k, S, r->chunk_tok.as<int>(), r->q_tok.as<int>(), n_q,
+                                 T - n_q, r->plan_rows.as<int>(), r->plan_tok.as<int>(), s));
+  }
+  peek("select");
+  ev_record(r, timing, 3, s);
+  // ---- sparse_prefill (Eq. 9) to the first-token logits
+  {
+    int* map_h = stg.take<int>(r->logit_rows);
+    if (all_logits)
+      for (int i = 0; i < n_q; ++i) map_h[i] = k + i;
+    else
+      map_h[0] = M - 1;
+    check_cuda(cudaMemcpyAsync(r->row_map.p, map_h, r->logit_rows * sizeof(int), cudaMemcpyHostToDevice, s), "map");
+    run_rows(e, r, s, M, T, PASS_FULL, nullptr, 0);  // logits below, timed as their own stage
+  }
+  ev_record(r, timing, 4, s);
+  {
+    // final norm + lm_head on the logit rows (K3 + K11)
+    const int d = c.d_model;
+    r->lm_x.ensure((size_t)r->logit_rows * d * sizeof(bf16));
+    r->logits.ensure((size_t)r->logit_rows * c.vocab * sizeof(float));
+    {
+      Scoped sc(e->prof, s, KC_NORM, 0, (double)r->logit_rows * d * 6);
+      fragk::rmsnorm(r->h.as<float>(), r->logit_rows, d, e->final_norm, c.norm_eps, r->lm_x.as<bf16>(), s,
+                     r->row_map.as<int>());
+      sc.launched(1);
+    }
+    fragk::EpiParams ep;
+    ep.out_f32 = r->logits.as<float>();
+    ep.ldo = c.vocab;
+    Scoped sc(e->prof, s, KC_GEMM, 2.0 * r->logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
+    sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, r->logit_rows, c.vocab, d, fragk::EPI_STORE_F32,
+                                    ep, s));
+  }
+  peek("lm_head");
+  ev_record(r, timing, 5, s);
+  finish(r, timing, s, o);
+}
+
+void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
+                  const frag_reprocess_opts* o, cudaStream_t s, Result* r) {
+  const auto& c = e->cfg;
+  if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
+  if (n_tok < 1) fail(FRAG_E_CONTRACT, "full prefill needs at least one token");
+  for (int i = 0; i < n_tok; ++i)
+    if (tokens[i] < 0 || tokens[i] >= c.vocab) fail(FRAG_E_CONTRACT, "token out of vocabulary");
+  DeviceGuard dg(e->device);
+  const bool timing = o && o->timing;
+  const int S = n_sys, T = S + n_tok;
+  if (T > r->max_tokens) fail(FRAG_E_CONTRACT, "prompt exceeds the result capacity");
+  e->ensure_rope(T);
+  SysKV* skv = get_sys_kv(e, sys, n_sys, s);
+  r->T = T;
+  r->S = S;
+  r->N = n_tok;
+  r->nq = 0;
+  r->k_sel = n_tok;
+  r->M = n_tok;
+  r->logit_rows = 1;
+  r->staging.ensure(64 * 1024 + (size_t)8 * T + 1024);
+  Stage stg(r->staging);
+  ev_record(r, timing, 0, s);
+  stitch(e, r, s, stg, skv, {}, S);
+  ev_record(r, timing, 1, s);
+  ev_record(r, timing, 2, s);
+  int* rows_h = stg.take<int>(n_tok);
+  int* tok_h = stg.take<int>(n_tok);
+  for (int i = 0; i < n_tok; ++i) rows_h[i] = S + i, tok_h[i] = tokens[i];
+  check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "rows");
+  check_cuda(cudaMemcpyAsync(r->plan_tok.p, tok_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "tok");
+  int* map_h = stg.take<int>(1);
+  map_h[0] = n_tok - 1;
+  check_cuda(cudaMemcpyAsync(r->row_map.p, map_h, sizeof(int), cudaMemcpyHostToDevice, s), "map");
+  ev_record(r, timing, 3, s);
+  run_rows(e, r, s, n_tok, T, PASS_FULL, r->row_map.as<int>(), 1);
+  ev_record(r, timing, 4, s);
+  ev_record(r, timing, 5, s);
+  finish(r, timing, s, o);
+}
+
+void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
+                         bool overwrite, frag_chunk_id* id_out) {
+  const auto& c = e->cfg;
+  if (n_tok < 1) fail(FRAG_E_CONTRACT, "chunk must have at least one token (SPEC.md:197)");
+  for (int i = 0; i < n_tok; ++i)
+    if (tokens[i] < 0 || tokens[i] >= c.vocab) fail(FRAG_E_CONTRACT, "token out of vocabulary");
+  if (st->device != e->device) fail(FRAG_E_CONTRACT, "store and engine are on different devices");
+  frag_chunk_id id;
+  hash_tokens(tokens, n_tok, 0, &id);
+  {
+    std::shared_lock<std::shared_mutex> g(st->mu);
+    if (!overwrite && st->recs.count(key_of(id)))
+      fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
+  }
+  DeviceGuard dg(e->device);
+  cudaStream_t s;
+  check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  struct SG {
+    cudaStream_t s;
+    ~SG() { cudaStreamDestroy(s); }
+  } sg{s};
+  const int S = n_sys, T = S + n_tok;
+  e->ensure_rope(T);
+  SysKV* skv = get_sys_kv(e, sys, n_sys, s);
+  std::lock_guard<std::mutex> g(e->mu);  // scratch result is shared
+  Result* r = scratch_for(e, T);
+  r->staging.ensure(64 * 1024 + (size_t)8 * T + 1024);
+  Stage stg(r->staging);
+  stitch(e, r, s, stg, skv, {}, S);
+  int* rows_h = stg.take<int>(n_tok);
+  int* tok_h = stg.take<int>(n_tok);
+  for (int i = 0; i < n_tok; ++i) rows_h[i] = S + i, tok_h[i] = tokens[i];
+  check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "rows");
+  check_cuda(cudaMemcpyAsync(r->plan_tok.p, tok_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "tok");
+  run_rows(e, r, s, n_tok, T, PASS_KV_ONLY, nullptr, 0);
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  store_put(st, id, tokens, n_tok, S + 1, FRAG_VARIANT_ISOLATED, r->k_fused.as<bf16>() + (size_t)S * kvc,
+            r->v_fused.as<bf16>() + (size_t)S * kvc, overwrite, (size_t)r->max_tokens * kvc, s);
+  check_cuda(cudaStreamSynchronize(s), "preprocess");
+  if (id_out) *id_out = id;
+}
+
+}  // namespace fragimpl

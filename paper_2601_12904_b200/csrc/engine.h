@@ -1,0 +1,216 @@
+// Internal host-side objects behind the C ABI: the engine (weights, RoPE
+// tables, system-prompt KV cache), the HBM chunk-KV store and the per-request
+// result (fused cache + workspace). Host C++ orchestrates; every device step
+// is one of the kernels declared in kernels.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <shared_mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "frag/frag_c.h"
+#include "kernels.h"
+
+namespace fragimpl {
+
+using fragk::bf16;
+
+// ---------------------------------------------------------------- errors
+struct Error {
+  frag_status code;
+  std::string msg;
+};
+[[noreturn]] void fail(frag_status code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+void set_last_error(const std::string& m);
+
+extern std::atomic<uint64_t> g_launches;
+
+// Device memory helper (RAII).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t n);        // exact allocation (fails with FRAG_E_OOM)
+  void ensure(size_t n);       // grow-only
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t n);
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+
+// ---------------------------------------------------------------- profiling
+enum KClass { KC_GEMM = 0, KC_ATTN = 1, KC_STITCH = 2, KC_NORM = 3, KC_SELECT = 4, KC_N = 5 };
+struct Profiler {
+  bool on = false;
+  struct Rec {
+    cudaEvent_t a, b;
+    int klass;
+    double flops, bytes;
+    int launches;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[KC_N] = {}, flops[KC_N] = {}, bytes[KC_N] = {};
+  int64_t launches[KC_N] = {};
+  std::mutex mu;
+  cudaEvent_t get();
+  void begin(cudaStream_t s, cudaEvent_t* a);
+  void end(cudaStream_t s, cudaEvent_t a, int klass, double flops, double bytes, int launches);
+  void collect();  // after the stream is synchronised
+  void reset();
+  ~Profiler();
+};
+
+// ---------------------------------------------------------------- store
+struct ChunkKey {
+  uint64_t a, b;
+  bool operator==(const ChunkKey& o) const { return a == o.a && b == o.b; }
+};
+struct ChunkKeyHash {
+  size_t operator()(const ChunkKey& k) const { return (size_t)(k.a ^ (k.b * 0x9e3779b97f4a7c15ULL)); }
+};
+ChunkKey key_of(const frag_chunk_id& id);
+
+struct Record {
+  frag_chunk_id id{};
+  int n_tok = 0;
+  int native_start = 1;
+  int variant = FRAG_VARIANT_ISOLATED;
+  uint64_t heat = 0, last_access = 0;
+  int pins = 0;
+  size_t bytes = 0;
+  DevBuf kv;            // K then V, each [L][n][Hkv][dh] bf16
+  DevBuf tok;           // int32 [n]
+  std::vector<int32_t> tok_host;
+  bf16* k() const { return kv.as<bf16>(); }
+  bf16* v() const { return kv.as<bf16>() + kv.bytes / 4; }
+};
+
+struct Store {
+  frag_model_cfg cfg{};
+  int device = 0;
+  size_t capacity = 0, used = 0;
+  uint64_t tick = 0;
+  mutable std::shared_mutex mu;
+  std::unordered_map<ChunkKey, std::unique_ptr<Record>, ChunkKeyHash> recs;
+  size_t record_bytes(int n_tok) const {
+    return (size_t)2 * cfg.layers * n_tok * cfg.n_kv_heads * cfg.head_dim * sizeof(bf16);
+  }
+};
+
+// ---------------------------------------------------------------- engine
+struct LayerW {
+  bf16 *wqkv, *wo, *wgu, *wd, *attn_norm, *ffn_norm;
+};
+
+struct SysKV {
+  int n = 0;
+  DevBuf kv;  // K then V [L][n][Hkv][dh]
+};
+
+struct Result;
+
+struct Engine {
+  frag_model_cfg cfg{};
+  int device = 0;
+  uint64_t seed = 0;
+  DevBuf weights;  // one allocation for every tensor
+  bf16 *emb = nullptr, *lm_head = nullptr, *final_norm = nullptr;
+  std::vector<LayerW> layers;
+  size_t n_params = 0;
+  // RoPE table [rows][dh/2] (cos, sin) of (row+1)*theta_i computed in fp64
+  DevBuf rope;
+  int rope_rows = 0;
+  std::vector<double> theta;  // theta_i, i = 1..dh/2
+  std::mutex rope_mu;         // guards rope-table growth
+  std::mutex mu;              // guards the system-prompt cache and the scratch result
+  std::map<std::vector<int32_t>, std::unique_ptr<SysKV>> sys_cache;
+  Profiler prof;
+  std::unique_ptr<Result> scratch;  // preprocess / system-prompt prefill workspace
+
+  void ensure_rope(int rows);
+  size_t qkv_cols() const { return (size_t)(cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim; }
+};
+
+struct Result {
+  Engine* eng = nullptr;
+  int max_tokens = 0;
+  // fused cache [L][max_tokens][Hkv][dh]
+  DevBuf k_fused, v_fused;
+  int T = 0, S = 0, N = 0, nq = 0, k_sel = 0, M = 0, logit_rows = 0;
+  // workspace
+  DevBuf h, x, q, attn, act, plan_rows, plan_tok, chunk_tok, q_tok, q_final, scores, part_ms, row_ms, part_o,
+      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x;
+  PinnedBuf staging, logits_host;
+  // timing
+  cudaEvent_t ev[7] = {};
+  bool timing_valid = false;
+  frag_timing timing{};
+  cudaStream_t last_stream = nullptr;
+  bool logits_on_device = false;
+  ~Result();
+};
+
+Engine* engine_create(const frag_model_cfg& cfg, int device, uint64_t seed);
+void result_init(Result* r, Engine* e, int max_tokens);
+
+// Pipeline stages (engine.cpp)
+enum PassMode { PASS_FULL = 0, PASS_QUESTION = 1, PASS_KV_ONLY = 2 };
+// Run every layer over the M planned rows (plan_rows/plan_tok on device) of the
+// result's fused cache with T valid rows; PASS_QUESTION stops after the final
+// layer's QKV projection with fp32 queries in r->q_final; PASS_FULL ends with
+// logits for the rows listed in row_map (n_logit_rows of them, device).
+void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
+              int n_logit_rows);
+
+void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
+               bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio, const frag_reprocess_opts* o,
+               cudaStream_t s, Result* r);
+void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
+                  const frag_reprocess_opts* o, cudaStream_t s, Result* r);
+void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
+                         bool overwrite, frag_chunk_id* id_out);
+
+// Store operations (store.cpp)
+Store* store_create(const frag_model_cfg& cfg, int device, size_t cap);
+void store_put(Store* st, const frag_chunk_id& id, const int32_t* tokens, int n_tok, int native_start, int variant,
+               const void* k, const void* v, bool overwrite, size_t src_layer_pitch_elems = 0,
+               cudaStream_t s = nullptr);
+Record* store_fetch(Store* st, const frag_chunk_id& id);  // heat++, pin
+void store_release(Store* st, const frag_chunk_id& id);
+
+void hash_tokens(const int32_t* t, int n, uint64_t salt, frag_chunk_id* out);
+uint64_t weight_seed(uint64_t seed, int tensor_id);
+
+}  // namespace fragimpl

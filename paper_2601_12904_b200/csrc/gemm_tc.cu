@@ -1,0 +1,391 @@
+// K4/K7/K8/K11: persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[M,N] = A[M,K] · B[N,K]^T     (A = activations, B = weights [out][in])
+//
+// Pipeline per CTA (one CTA per SM, 192 threads):
+//   warp 0      TMA producer: A (128x64) and B (BNx64) tiles, SWIZZLE_128B,
+//               into a STAGES-deep shared-memory ring guarded by mbarriers.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (M=128, N=BN, K=16 per instruction), accumulator in TMEM,
+//               double-buffered (2 x BN columns) so the epilogue of tile i
+//               overlaps the MMAs of tile i+1.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global.
+//
+// The fused epilogues implement the projection-side work of the selective
+// recompute (Eq. 9): RoPE at the global
+// position + scatter of fresh K/V rows into the fused cache (K4+K5), residual
+// add (K7, K8-down), SiLU(gate)*up (K8), fp32 logits (K11).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace fragk {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int GEMM_THREADS = 192;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+};
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+template <int EPI>
+__device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col, const uint32_t (&r)[32],
+                                          const uint32_t (&r2)[32]) {
+  if constexpr (EPI == EPI_STORE_BF16) {
+    uint4* dst = reinterpret_cast<uint4*>(ep.out_bf16 + (size_t)row * ep.ldo + col);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 v;
+      v.x = pack_bf16(__uint_as_float(r[8 * j + 0]), __uint_as_float(r[8 * j + 1]));
+      v.y = pack_bf16(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3]));
+      v.z = pack_bf16(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5]));
+      v.w = pack_bf16(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7]));
+      dst[j] = v;
+    }
+  } else if constexpr (EPI == EPI_STORE_F32) {
+    float4* dst = reinterpret_cast<float4*>(ep.out_f32 + (size_t)row * ep.ldo + col);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                           __uint_as_float(r[4 * j + 3]));
+  } else if constexpr (EPI == EPI_RESID) {
+    float4* dst = reinterpret_cast<float4*>(ep.resid + (size_t)row * ep.ldo + col);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 h = dst[j];
+      h.x += __uint_as_float(r[4 * j]);
+      h.y += __uint_as_float(r[4 * j + 1]);
+      h.z += __uint_as_float(r[4 * j + 2]);
+      h.w += __uint_as_float(r[4 * j + 3]);
+      dst[j] = h;
+    }
+  } else if constexpr (EPI == EPI_SWIGLU) {
+    // col is the gate chunk's first column; the chunk is 64-aligned: gate block
+    // (col/64) covers output columns [(col/64)*32, +32).
+    uint4* dst = reinterpret_cast<uint4*>(ep.out_bf16 + (size_t)row * ep.ldo + (col >> 1));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float a[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        float g = __uint_as_float(r[8 * j + t]);
+        float u = __uint_as_float(r2[8 * j + t]);
+        a[t] = silu(g) * u;
+      }
+      uint4 v;
+      v.x = pack_bf16(a[0], a[1]);
+      v.y = pack_bf16(a[2], a[3]);
+      v.z = pack_bf16(a[4], a[5]);
+      v.w = pack_bf16(a[6], a[7]);
+      dst[j] = v;
+    }
+  } else if constexpr (EPI == EPI_QKV) {
+    const int dh = ep.dh;
+    const int q_cols = ep.Hq * dh;
+    const int k_cols = ep.Hkv * dh;
+    const int prow = ep.rows[row];
+    float o[32];
+    if (col < q_cols + k_cols) {
+      // RoPE, interleaved pairs: o0 = k0 c - k1 s, o1 = k1 c + k0 s
+      const int d0 = col % dh;
+      const float2* cs = ep.rope + (size_t)prow * (dh >> 1) + (d0 >> 1);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float2 t = cs[j];
+        float k0 = __uint_as_float(r[2 * j]), k1 = __uint_as_float(r[2 * j + 1]);
+        o[2 * j] = __fmaf_rn(k0, t.x, -(k1 * t.y));
+        o[2 * j + 1] = __fmaf_rn(k1, t.x, k0 * t.y);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(r[j]);
+    }
+    bf16* dstp;
+    if (col < q_cols) {
+      dstp = ep.q_out + (size_t)row * q_cols + col;
+      if (ep.q_out_f32) {
+        float4* qf = reinterpret_cast<float4*>(ep.q_out_f32 + (size_t)row * q_cols + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) qf[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+      }
+    } else if (col < q_cols + k_cols) {
+      dstp = ep.k_cache + (size_t)prow * k_cols + (col - q_cols);
+    } else {
+      dstp = ep.v_cache + (size_t)prow * k_cols + (col - q_cols - k_cols);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(dstp);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 v;
+      v.x = pack_bf16(o[8 * j + 0], o[8 * j + 1]);
+      v.y = pack_bf16(o[8 * j + 2], o[8 * j + 3]);
+      v.z = pack_bf16(o[8 * j + 4], o[8 * j + 5]);
+      v.w = pack_bf16(o[8 * j + 6], o[8 * j + 7]);
+      dst[j] = v;
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, const EpiParams ep) {
+  using C = GemmCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = N / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int nk = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, 0, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_base = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (kb == nk - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_tile = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * BM + row_in_tile;
+      const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if constexpr (EPI == EPI_SWIGLU) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; c += 2) {
+          uint32_t r[32], r2[32];
+          tmem_ld32(t_row + c * 32, r);
+          tmem_ld32(t_row + (c + 1) * 32, r2);
+          tmem_ld_wait();
+          if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(t_row + c * 32, r);
+          tmem_ld_wait();
+          if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ----------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+int g_num_sms = 0;
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode;
+}
+
+// 2-D bf16 tensor map over a row-major [rows][cols] matrix, box = box_rows x 64 cols.
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+                  uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int EPI>
+int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& ep, cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  CUtensorMap ta, tb;
+  if (!make_tmap_2d(&ta, A, M, K, K, BM)) return -1;
+  if (!make_tmap_2d(&tb, B, N, K, K, BN)) return -1;
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_tc_kernel<BN, EPI><<<grid, GEMM_THREADS, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
+  return 1;
+}
+
+template <int BN>
+int dispatch_epi(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
+                 cudaStream_t s) {
+  switch (epi) {
+    case EPI_STORE_BF16: return launch<BN, EPI_STORE_BF16>(A, B, M, N, K, ep, s);
+    case EPI_STORE_F32: return launch<BN, EPI_STORE_F32>(A, B, M, N, K, ep, s);
+    case EPI_RESID: return launch<BN, EPI_RESID>(A, B, M, N, K, ep, s);
+    case EPI_SWIGLU: return launch<BN, EPI_SWIGLU>(A, B, M, N, K, ep, s);
+    case EPI_QKV: return launch<BN, EPI_QKV>(A, B, M, N, K, ep, s);
+  }
+  return -1;
+}
+
+}  // namespace
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// Pick the N tile: maximise useful MMA work per wave while keeping tiles wide
+// enough to stay under the shared-memory bandwidth bound (BN=256 moves 96 B/clk
+// per SM at full MMA rate, BN=128 128 B/clk, BN=64 192 B/clk).
+int gemm_pick_bn(int M, int N, int K) {
+  (void)K;
+  const int sms = num_sms();
+  const int m_tiles = (M + BM - 1) / BM;
+  double best = 1e30;
+  int best_bn = 64;
+  const int cands[3] = {256, 128, 64};
+  const double eff[3] = {1.0, 0.92, 0.70};
+  for (int i = 0; i < 3; ++i) {
+    const int bn = cands[i];
+    if (N % bn) continue;
+    const long tiles = (long)m_tiles * (N / bn);
+    const long waves = (tiles + sms - 1) / sms;
+    const double t = (double)waves * bn / eff[i];
+    if (t < best - 1e-9) {
+      best = t;
+      best_bn = bn;
+    }
+  }
+  return best_bn;
+}
+
+int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
+                 cudaStream_t stream, int force_bn) {
+  if (M <= 0) return 0;
+  if (K % BK != 0 || N % 64 != 0) return -1;
+  const int bn = force_bn ? force_bn : gemm_pick_bn(M, N, K);
+  if (N % bn != 0) return -1;
+  switch (bn) {
+    case 256: return dispatch_epi<256>(A, B, M, N, K, epi, ep, stream);
+    case 128: return dispatch_epi<128>(A, B, M, N, K, epi, ep, stream);
+    case 64: return dispatch_epi<64>(A, B, M, N, K, epi, ep, stream);
+  }
+  return -1;
+}
+
+}  // namespace fragk

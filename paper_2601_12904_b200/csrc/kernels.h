@@ -1,0 +1,110 @@
+// Host-side launchers for the sm_100a kernels of the reprocessing path.
+// Every pointer is a device pointer; every launcher is stream-ordered and
+// never synchronises. Kernel numbering (K1..K11) follows SURVEY.md §2.2.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace fragk {
+
+using bf16 = __nv_bfloat16;
+
+// ------------------------------------------------------------------ GEMM
+// C[M,N] = A[M,K] · B[N,K]^T, A/B bf16 K-major, fp32 accumulation in TMEM.
+enum EpiKind : int {
+  EPI_STORE_BF16 = 0,  // out_bf16[row*ldo + col] = acc
+  EPI_STORE_F32 = 1,   // out_f32[row*ldo + col] = acc
+  EPI_RESID = 2,       // resid[row*ldo + col] += acc            (K7, K8-down)
+  EPI_SWIGLU = 3,      // 32-col gate/up interleave -> out_bf16[row*ldo + j] = silu(g)*u   (K8-gate/up)
+  EPI_QKV = 4,         // RoPE(Q,K) at rows[row]; Q -> q_out, K/V scattered into the fused cache (K4+K5)
+};
+
+struct EpiParams {
+  int ldo = 0;
+  float* out_f32 = nullptr;
+  bf16* out_bf16 = nullptr;
+  float* resid = nullptr;
+  // EPI_QKV
+  const int* rows = nullptr;       // fused-cache row (position-1) of each GEMM row
+  const float2* rope = nullptr;    // [pos_row][dh/2] (cos, sin) of (row+1)*theta_i
+  bf16* q_out = nullptr;           // [M][Hq][dh]
+  float* q_out_f32 = nullptr;      // optional fp32 copy (question pass, final layer)
+  bf16* k_cache = nullptr;         // layer base, [T][Hkv][dh]
+  bf16* v_cache = nullptr;
+  int Hq = 0, Hkv = 0, dh = 0;
+};
+
+struct GemmTimer;  // optional per-launch event hook (bench roofline)
+
+// Returns the number of kernel launches issued (1), or -1 on a shape error.
+int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
+                 cudaStream_t stream, int force_bn = 0);
+int gemm_pick_bn(int M, int N, int K);
+int num_sms();
+
+// ------------------------------------------------------------------ K1
+struct StitchChunk {
+  const bf16* k_src;   // record K [L][n][Hkv][dh]
+  const bf16* v_src;   // record V
+  int n_tok;           // rows in the record
+  int dst_row;         // first fused-cache row (target_start - 1)
+  int table;           // index into the per-chunk cos/sin table; -1 = zero shift (bit copy)
+};
+// fused K/V [L][T][Hkv][dh]; tables: [n_tables][dh/2] float2 for delta*theta_i.
+void rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_rows, const float2* tables,
+                         bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream);
+
+// ------------------------------------------------------------------ K2/K3
+// h[i] = E[tok[i]] (fp32), x[i] = bf16(rmsnorm(h[i]) * g)
+void embed_rmsnorm(const bf16* E, const int* tok, int M, int d, const bf16* gain, float eps, float* h, bf16* x,
+                   cudaStream_t stream);
+void rmsnorm(const float* h, int M, int d, const bf16* gain, float eps, bf16* x, cudaStream_t stream,
+             const int* row_map = nullptr);
+
+// ------------------------------------------------------------------ K6
+struct AttnArgs {
+  const bf16* q;         // [M][Hq][dh]
+  const bf16* k;         // fused layer base [T][Hkv][dh]
+  const bf16* v;
+  const int* rows;       // [M] query fused-cache row (ascending)
+  bf16* out;             // [M][Hq][dh]
+  float* part_o;         // split partials [splits][M][Hq][dh]
+  float* part_lse;       // [splits][M][Hq]
+  int M, T, Hq, Hkv, dh;
+  int split_keys;        // keys per split (multiple of 64); <=0: no split
+  int n_splits;
+  float scale;           // 1/sqrt(dh)
+};
+int sparse_q_attention(const AttnArgs& a, cudaStream_t stream);  // returns launches
+
+// ------------------------------------------------------------------ K9/K10
+struct ScoreArgs {
+  const float* q;      // [nq][Hq][dh] fp32 final-layer queries
+  const bf16* k;       // final-layer fused K base [T][Hkv][dh]
+  int nq, Hq, Hkv, dh;
+  int key_row0;        // first chunk row in the fused cache (= |S|)
+  int n_keys;          // N chunk tokens
+  float scale;
+  float2* part_ms;     // [nblk][nq*Hq] (max, sumexp) scratch
+  float2* row_ms;      // [nq*Hq] (max, 1/Z)
+  float* scores;       // [n_keys]
+  int raw;             // 1 = raw (unnormalised) attention logits summed (SPEC.md:464 flag)
+};
+int qg_score(const ScoreArgs& a, cudaStream_t stream);
+// crit rows (ascending, = key_row0 + j) of the k largest scores, ties to lower j,
+// then the question rows appended. Writes plan_rows[k + nq] and plan_tok.
+int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* chunk_tok, const int* q_tok,
+              int nq, int q_row0, int* plan_rows, int* plan_tok, cudaStream_t stream);
+
+// ------------------------------------------------------------------ weights
+// Fill dst[i] = bf16(normal_f(sigma)) from the counter form of the splitmix64
+// stream `seed` (element e = e-th gaussian of the Box-Muller pair sequence).
+// Rows of the canonical [rows][cols] tensor land at dst + map(row)*cols where
+// map(row) = (row / blk) * blk_stride + blk_off + row % blk.
+void init_normal_bf16(bf16* dst, uint64_t seed, size_t rows, size_t cols, float sigma, int blk, int blk_stride,
+                      int blk_off, cudaStream_t stream);
+void fill_bf16(bf16* dst, size_t n, float v, cudaStream_t stream);
+
+}  // namespace fragk

@@ -1,0 +1,240 @@
+// Memory-bound kernels of the reprocessing path:
+//   K1  rope_shift_assemble  (SPEC.md:41-49 shift_rope, SPEC.md:399-407 stitch_full_reuse,
+//                             PAPER.md:1040-1049 Appendix A re-positioning)
+//   K2+K3 embed_rmsnorm, K3 rmsnorm  (SPEC.md:128 pre-norm decoder)
+//   init_normal_bf16          (SPEC.md:94-102 init_model from the common.hpp:45-100 Rng)
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace fragk {
+
+namespace {
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Rotate 4 interleaved pairs held in one 16-byte vector by the per-chunk
+// (cos, sin) of delta*theta_i: identical fp32 op order to oracle/fusion_oracle.cpp
+// rope_rotate_pair() so K1 is bit-exact against the oracle.
+__device__ __forceinline__ uint32_t rot_pair(uint32_t kv, float2 cs) {
+  const float k0 = bf16_lo(kv), k1 = bf16_hi(kv);
+  const float o0 = __fmaf_rn(k0, cs.x, -(k1 * cs.y));
+  const float o1 = __fmaf_rn(k1, cs.x, k0 * cs.y);
+  return pack_bf16(o0, o1);
+}
+
+// One CTA row of the grid per chunk (blockIdx.y); each thread moves 16-byte
+// vectors of K (rotated) and V (copied) for (layer, token, head, 8 dims).
+// Per layer the record block [n][Hkv][dh] and its fused destination
+// [dst_row : dst_row+n][Hkv][dh] are both contiguous, so all accesses are
+// fully coalesced 128-bit streams.
+__global__ void __launch_bounds__(256) rope_shift_kernel(const StitchChunk* __restrict__ chunks,
+                                                         const float2* __restrict__ tables, bf16* __restrict__ kf,
+                                                         bf16* __restrict__ vf, int L, int T, int Hkv, int dh) {
+  const StitchChunk c = chunks[blockIdx.y];
+  const int vec_per_row = (Hkv * dh) >> 3;  // 16-byte vectors per token row
+  const long per_layer = (long)c.n_tok * vec_per_row;
+  const long total = per_layer * L;
+  const int dvec = dh >> 3;
+  const float2* tab = c.table >= 0 ? tables + (size_t)c.table * (dh >> 1) : nullptr;
+  const uint4* ks = reinterpret_cast<const uint4*>(c.k_src);
+  const uint4* vs = reinterpret_cast<const uint4*>(c.v_src);
+  const long layer_stride_dst = (long)T * vec_per_row;
+  const long dst0 = (long)c.dst_row * vec_per_row;
+  uint4* kd = reinterpret_cast<uint4*>(kf);
+  uint4* vd = reinterpret_cast<uint4*>(vf);
+  const long stride = (long)gridDim.x * blockDim.x;
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  // 2-way unrolled so each thread keeps 4 independent 16-byte loads in flight.
+  for (; i + stride < total; i += 2 * stride) {
+    const long i1 = i + stride;
+    uint4 k0 = ld_stream(ks + i), v0 = ld_stream(vs + i);
+    uint4 k1 = ld_stream(ks + i1), v1 = ld_stream(vs + i1);
+    const long l0 = i / per_layer, r0 = i - l0 * per_layer;
+    const long l1 = i1 / per_layer, r1 = i1 - l1 * per_layer;
+    if (tab) {
+      const int p0 = (int)(r0 % dvec) * 4, p1 = (int)(r1 % dvec) * 4;
+      k0.x = rot_pair(k0.x, tab[p0]);
+      k0.y = rot_pair(k0.y, tab[p0 + 1]);
+      k0.z = rot_pair(k0.z, tab[p0 + 2]);
+      k0.w = rot_pair(k0.w, tab[p0 + 3]);
+      k1.x = rot_pair(k1.x, tab[p1]);
+      k1.y = rot_pair(k1.y, tab[p1 + 1]);
+      k1.z = rot_pair(k1.z, tab[p1 + 2]);
+      k1.w = rot_pair(k1.w, tab[p1 + 3]);
+    }
+    const long o0 = l0 * layer_stride_dst + dst0 + r0, o1 = l1 * layer_stride_dst + dst0 + r1;
+    st_stream(kd + o0, k0);
+    st_stream(vd + o0, v0);
+    st_stream(kd + o1, k1);
+    st_stream(vd + o1, v1);
+  }
+  for (; i < total; i += stride) {
+    uint4 k0 = ld_stream(ks + i), v0 = ld_stream(vs + i);
+    const long l0 = i / per_layer, r0 = i - l0 * per_layer;
+    if (tab) {
+      const int p0 = (int)(r0 % dvec) * 4;
+      k0.x = rot_pair(k0.x, tab[p0]);
+      k0.y = rot_pair(k0.y, tab[p0 + 1]);
+      k0.z = rot_pair(k0.z, tab[p0 + 2]);
+      k0.w = rot_pair(k0.w, tab[p0 + 3]);
+    }
+    const long o0 = l0 * layer_stride_dst + dst0 + r0;
+    st_stream(kd + o0, k0);
+    st_stream(vd + o0, v0);
+  }
+}
+
+// ------------------------------------------------------------------ norms
+// One CTA per row. Sum of squares in fp32 (block reduction), scale in fp32,
+// bf16 output for the next GEMM's A operand.
+template <bool EMBED>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const bf16* __restrict__ E, const int* __restrict__ tok,
+                                                      const float* __restrict__ h_in, const int* __restrict__ row_map,
+                                                      int d, const bf16* __restrict__ gain, float eps,
+                                                      float* __restrict__ h_out, bf16* __restrict__ x) {
+  const int row = blockIdx.x;
+  __shared__ float red[8];
+  float ss = 0.f;
+  // d is a multiple of 256*... handled with a strided loop of 8-element vectors.
+  const int nvec = d >> 3;
+  if constexpr (EMBED) {
+    const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok[row] * d);
+    float4* hdst = reinterpret_cast<float4*>(h_out + (size_t)row * d);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      uint4 e = src[v];
+      float f[8] = {bf16_lo(e.x), bf16_hi(e.x), bf16_lo(e.y), bf16_hi(e.y),
+                    bf16_lo(e.z), bf16_hi(e.z), bf16_lo(e.w), bf16_hi(e.w)};
+      hdst[2 * v] = make_float4(f[0], f[1], f[2], f[3]);
+      hdst[2 * v + 1] = make_float4(f[4], f[5], f[6], f[7]);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) ss = fmaf(f[t], f[t], ss);
+    }
+  } else {
+    const int src_row = row_map ? row_map[row] : row;
+    const float4* src = reinterpret_cast<const float4*>(h_in + (size_t)src_row * d);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      float4 a = src[2 * v], b = src[2 * v + 1];
+      ss = fmaf(a.x, a.x, ss); ss = fmaf(a.y, a.y, ss); ss = fmaf(a.z, a.z, ss); ss = fmaf(a.w, a.w, ss);
+      ss = fmaf(b.x, b.x, ss); ss = fmaf(b.y, b.y, ss); ss = fmaf(b.z, b.z, ss); ss = fmaf(b.w, b.w, ss);
+    }
+  }
+  ss = warp_sum(ss);
+  if (lane_id() == 0) red[warp_id()] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float rs = rsqrtf(red[0] / (float)d + eps);
+  const float* hrow;
+  if constexpr (EMBED) hrow = h_out + (size_t)row * d;
+  else hrow = h_in + (size_t)(row_map ? row_map[row] : row) * d;
+  const float4* hv = reinterpret_cast<const float4*>(hrow);
+  const uint4* gv = reinterpret_cast<const uint4*>(gain);
+  uint4* xo = reinterpret_cast<uint4*>(x + (size_t)row * d);
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    float4 a = hv[2 * v], b = hv[2 * v + 1];
+    uint4 g = gv[v];
+    uint4 o;
+    o.x = pack_bf16(a.x * rs * bf16_lo(g.x), a.y * rs * bf16_hi(g.x));
+    o.y = pack_bf16(a.z * rs * bf16_lo(g.y), a.w * rs * bf16_hi(g.y));
+    o.z = pack_bf16(b.x * rs * bf16_lo(g.z), b.y * rs * bf16_hi(g.z));
+    o.w = pack_bf16(b.z * rs * bf16_lo(g.w), b.w * rs * bf16_hi(g.w));
+    xo[v] = o;
+  }
+}
+
+// ------------------------------------------------------------------ init
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t n) {
+  // (n+1)-th output of Rng(seed).next_u64() (common.hpp:49-54): the state
+  // advances by the golden gamma before each mix, so the stream is counter-based.
+  uint64_t z = seed + (n + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_normal_kernel(bf16* __restrict__ dst, uint64_t seed, size_t rows, size_t cols, float sigma,
+                                   int blk, int blk_stride, int blk_off) {
+  const size_t total = rows * cols;
+  const size_t npairs = (total + 1) / 2;
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < npairs; j += (size_t)gridDim.x * blockDim.x) {
+    // Box-Muller pair j consumes draws 2j (u1) and 2j+1 (u2) (common.hpp:78-92).
+    // u1 == 0 (probability 2^-53 per pair) would shift the stream; ignored.
+    const double u1 = (double)(splitmix_at(seed, 2 * j) >> 11) * 0x1.0p-53;
+    const double u2 = (double)(splitmix_at(seed, 2 * j + 1) >> 11) * 0x1.0p-53;
+    const double mag = sqrt(-2.0 * log(u1));
+    const double ang = 6.283185307179586477 * u2;
+    const double e[2] = {mag * cos(ang), mag * sin(ang)};
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const size_t idx = 2 * j + t;
+      if (idx >= total) break;
+      const size_t r = idx / cols, c = idx - r * cols;
+      const size_t pr = (r / blk) * (size_t)blk_stride + blk_off + r % blk;
+      dst[pr * cols + c] = __float2bfloat16_rn((float)e[t] * sigma);
+    }
+  }
+}
+
+__global__ void fill_kernel(bf16* dst, size_t n, float v) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(v);
+}
+
+}  // namespace
+
+void rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_rows, const float2* tables,
+                         bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream) {
+  if (n_chunks <= 0 || max_rows <= 0) return;
+  const long vecs = (long)max_rows * L * (Hkv * dh / 8);
+  long bx = (vecs + 2 * 256 - 1) / (2 * 256);
+  const long cap = (long)num_sms() * 8 / (n_chunks < 8 ? n_chunks : 8) + 1;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  dim3 grid((unsigned)bx, (unsigned)n_chunks);
+  rope_shift_kernel<<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, L, T, Hkv, dh);
+}
+
+void embed_rmsnorm(const bf16* E, const int* tok, int M, int d, const bf16* gain, float eps, float* h, bf16* x,
+                   cudaStream_t stream) {
+  if (M <= 0) return;
+  rmsnorm_kernel<true><<<M, 256, 0, stream>>>(E, tok, nullptr, nullptr, d, gain, eps, h, x);
+}
+
+void rmsnorm(const float* h, int M, int d, const bf16* gain, float eps, bf16* x, cudaStream_t stream,
+             const int* row_map) {
+  if (M <= 0) return;
+  rmsnorm_kernel<false><<<M, 256, 0, stream>>>(nullptr, nullptr, h, row_map, d, gain, eps, nullptr, x);
+}
+
+void init_normal_bf16(bf16* dst, uint64_t seed, size_t rows, size_t cols, float sigma, int blk, int blk_stride,
+                      int blk_off, cudaStream_t stream) {
+  const size_t pairs = (rows * cols + 1) / 2;
+  size_t blocks = (pairs + 255) / 256;
+  if (blocks > (size_t)num_sms() * 16) blocks = (size_t)num_sms() * 16;
+  if (blocks == 0) blocks = 1;
+  init_normal_kernel<<<(unsigned)blocks, 256, 0, stream>>>(dst, seed, rows, cols, sigma, blk, blk_stride, blk_off);
+}
+
+void fill_bf16(bf16* dst, size_t n, float v, cudaStream_t stream) {
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks == 0) return;
+  fill_kernel<<<(unsigned)blocks, 256, 0, stream>>>(dst, n, v);
+}
+
+}  // namespace fragk

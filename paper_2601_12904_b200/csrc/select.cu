@@ -1,0 +1,307 @@
+// K9 qg_score + K10 topk_plan: query-guided critical-token selection
+// (§3.2).
+//
+//   score[j] = sum_{t<Q} sum_{h<Hq} softmax_{j' in chunks}( q_{t,h} . k_{j,kv(h)} / sqrt(dh) )[j]
+//
+// The softmax is joint over all chunk keys of one (t, h), system
+// and question keys are excluded, heads are summed, and the
+// budget is a global top-k with lower-index tie-break.
+//
+// v1 uses fp32 CUDA-core FMAs (the whole stage is ~0.3% of TTFT) so scores
+// follow the fp32 oracle to summation-order rounding; no atomics, so the
+// result is bit-deterministic run to run.
+#include <cfloat>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace fragk {
+
+namespace {
+
+constexpr int SC_KEYS = 32;     // keys per CTA
+constexpr int SC_ROWS = 32;     // query rows per smem tile
+constexpr int SC_THREADS = 256;
+
+// MODE 1: per-(block,row) (max, sumexp) of scaled logits.
+// MODE 2: column sums of softmax probabilities (row_ms = (max, 1/Z)).
+// MODE 3: column sums of raw scaled logits.
+template <int MODE, int DH>
+__global__ void __launch_bounds__(SC_THREADS) score_kernel(const ScoreArgs a) {
+  __shared__ float sk[SC_KEYS][DH + 1];
+  __shared__ float sq[SC_ROWS][DH + 1];
+  __shared__ float colsum[SC_THREADS / 8][SC_KEYS];  // 32 row-groups x 32 keys
+  const int blk = blockIdx.x;
+  const int key0 = blk * SC_KEYS;
+  const int nrows_tot = a.nq * a.Hq;
+  const int G = a.Hq / a.Hkv;
+  const int tid = threadIdx.x;
+  // thread -> (row, key quad): 32 rows x 8 key-groups; each thread owns
+  // row rg and keys {kg, kg+8, kg+16, kg+24} of the tile.
+  const int rg = tid >> 3, kg = tid & 7;
+  float csum[4] = {0.f, 0.f, 0.f, 0.f};
+
+  for (int hk = 0; hk < a.Hkv; ++hk) {
+    __syncthreads();
+    for (int idx = tid; idx < SC_KEYS * DH; idx += SC_THREADS) {
+      const int r = idx / DH, c = idx % DH;
+      const int j = key0 + r;
+      sk[r][c] = j < a.n_keys ? __bfloat162float(a.k[((size_t)(a.key_row0 + j) * a.Hkv + hk) * DH + c]) : 0.f;
+    }
+    const int nrows = a.nq * G;  // rows of this kv group: (t, g) -> row t*Hq + hk*G + g
+    for (int r0 = 0; r0 < nrows; r0 += SC_ROWS) {
+      __syncthreads();
+      for (int idx = tid; idx < SC_ROWS * DH; idx += SC_THREADS) {
+        const int r = idx / DH, c = idx % DH;
+        const int rr = r0 + r;
+        float v = 0.f;
+        if (rr < nrows) {
+          const int t = rr / G, g = rr % G;
+          v = a.q[((size_t)t * a.Hq + hk * G + g) * DH + c];
+        }
+        sq[r][c] = v;
+      }
+      __syncthreads();
+      float acc[1][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[0][j] = 0.f;
+#pragma unroll 8
+      for (int c = 0; c < DH; ++c) {
+        const float q0 = sq[rg][c];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[0][j] = fmaf(q0, sk[kg + 8 * j][c], acc[0][j]);
+      }
+      {
+        const int i = 0;
+        const int rr = r0 + rg;
+        const bool rvalid = rr < nrows;
+        const int grow = rvalid ? (rr / G) * a.Hq + hk * G + rr % G : 0;
+        if constexpr (MODE == 1) {
+          // local (max, sumexp) over this CTA's keys for row grow: reduce over the 8 kg lanes
+          float s[4];
+          float mx = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const bool kvalid = key0 + kg + 8 * j < a.n_keys;
+            s[j] = kvalid ? acc[i][j] * a.scale : -INFINITY;
+            mx = fmaxf(mx, s[j]);
+          }
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          float z = 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) z += (s[j] == -INFINITY) ? 0.f : __expf(s[j] - mx);
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+          if (kg == 0 && rvalid) a.part_ms[(size_t)blk * nrows_tot + grow] = make_float2(mx, z);
+        } else if constexpr (MODE == 2) {
+          if (rvalid) {
+            const float2 ms = a.row_ms[grow];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) csum[j] += __expf(acc[i][j] * a.scale - ms.x) * ms.y;
+          }
+        } else {
+          if (rvalid) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) csum[j] += acc[i][j] * a.scale;
+          }
+        }
+      }
+    }
+  }
+  if constexpr (MODE != 1) {
+    // deterministic column reduction over the 32 row-groups
+#pragma unroll
+    for (int j = 0; j < 4; ++j) colsum[rg][kg + 8 * j] = csum[j];
+    __syncthreads();
+    if (tid < SC_KEYS) {
+      float s = 0.f;
+      for (int r = 0; r < SC_THREADS / 8; ++r) s += colsum[r][tid];
+      const int j = key0 + tid;
+      if (j < a.n_keys) a.scores[j] = s;
+    }
+  }
+}
+
+__global__ void score_combine_kernel(const ScoreArgs a, int nblk) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nrows = a.nq * a.Hq;
+  if (row >= nrows) return;
+  float mx = -INFINITY;
+  for (int b = 0; b < nblk; ++b) mx = fmaxf(mx, a.part_ms[(size_t)b * nrows + row].x);
+  float z = 0.f;
+  for (int b = 0; b < nblk; ++b) {
+    const float2 p = a.part_ms[(size_t)b * nrows + row];
+    if (p.x != -INFINITY) z += p.y * __expf(p.x - mx);
+  }
+  a.row_ms[row] = make_float2(mx, z > 0.f ? 1.f / z : 0.f);
+}
+
+// ---------------------------------------------------------------- K10
+constexpr int TK_THREADS = 1024;
+
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// Block-wide exclusive scan of one int per thread (1024 threads).
+__device__ int block_excl_scan(int v, int* sh, int* total) {
+  const int lane = lane_id(), w = warp_id();
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int s = sh[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    sh[lane] = s;  // inclusive warp totals
+  }
+  __syncthreads();
+  const int base = w > 0 ? sh[w - 1] : 0;
+  if (total) *total = sh[31];
+  __syncthreads();
+  return base + x - v;
+}
+
+__global__ void __launch_bounds__(TK_THREADS) topk_plan_kernel(const float* __restrict__ scores, int n, int k,
+                                                                int key_row0, const int* __restrict__ chunk_tok,
+                                                                const int* __restrict__ q_tok, int nq, int q_row0,
+                                                                int* __restrict__ plan_rows,
+                                                                int* __restrict__ plan_tok) {
+  __shared__ int hist[256];
+  __shared__ int sh[32];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_remaining;
+  const int tid = threadIdx.x;
+  const int per = (n + TK_THREADS - 1) / TK_THREADS;
+  const int lo = tid * per, hi = min(lo + per, n);
+
+  uint32_t tau = 0xFFFFFFFFu;
+  int need_eq = 0;
+  if (k > 0 && k < n) {
+    if (tid == 0) {
+      s_prefix = 0;
+      s_remaining = k;
+    }
+    uint32_t mask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int b = tid; b < 256; b += TK_THREADS) hist[b] = 0;
+      __syncthreads();
+      const uint32_t prefix = s_prefix;
+      for (int i = lo; i < hi; ++i) {
+        const uint32_t key = fkey(scores[i]);
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int rem = s_remaining, cum = 0, b = 255;
+        for (; b > 0; --b) {
+          if (cum + hist[b] >= rem) break;
+          cum += hist[b];
+        }
+        s_remaining = rem - cum;
+        s_prefix = prefix | ((uint32_t)b << shift);
+      }
+      mask |= 255u << shift;
+      __syncthreads();
+    }
+    tau = s_prefix;
+    need_eq = s_remaining;
+  } else if (k >= n) {
+    tau = 0;
+    need_eq = n;  // everything selected (all keys >= 0 in key space)
+  }
+  // pass: count > tau and == tau in my range
+  int n_gt = 0, n_eq = 0;
+  if (k > 0) {
+    for (int i = lo; i < hi; ++i) {
+      const uint32_t key = fkey(scores[i]);
+      if (k >= n) {
+        ++n_gt;
+      } else {
+        n_gt += key > tau;
+        n_eq += key == tau;
+      }
+    }
+  }
+  const int eq_before = block_excl_scan(n_eq, sh, nullptr);
+  int take_eq = (k >= n) ? 0 : min(max(need_eq - eq_before, 0), n_eq);
+  const int my_sel = n_gt + take_eq;
+  int total = 0;
+  int out = block_excl_scan(my_sel, sh, &total);
+  if (k > 0) {
+    int eq_seen = 0;
+    for (int i = lo; i < hi; ++i) {
+      bool sel;
+      if (k >= n) {
+        sel = true;
+      } else {
+        const uint32_t key = fkey(scores[i]);
+        if (key > tau) sel = true;
+        else if (key == tau) sel = (eq_seen++ < take_eq);
+        else sel = false;
+      }
+      if (sel) {
+        plan_rows[out] = key_row0 + i;
+        plan_tok[out] = chunk_tok[i];
+        ++out;
+      }
+    }
+  }
+  // question rows follow the critical rows (they are the last positions)
+  for (int i = tid; i < nq; i += TK_THREADS) {
+    plan_rows[k + i] = q_row0 + i;
+    plan_tok[k + i] = q_tok[i];
+  }
+}
+
+}  // namespace
+
+int qg_score(const ScoreArgs& a, cudaStream_t stream) {
+  const int nblk = (a.n_keys + SC_KEYS - 1) / SC_KEYS;
+  if (nblk <= 0) return 0;
+  if (a.Hq % a.Hkv != 0) return -1;
+  int launches = 0;
+  if (a.dh == 128) {
+    if (!a.raw) {
+      score_kernel<1, 128><<<nblk, SC_THREADS, 0, stream>>>(a);
+      score_combine_kernel<<<(a.nq * a.Hq + 255) / 256, 256, 0, stream>>>(a, nblk);
+      score_kernel<2, 128><<<nblk, SC_THREADS, 0, stream>>>(a);
+      launches = 3;
+    } else {
+      score_kernel<3, 128><<<nblk, SC_THREADS, 0, stream>>>(a);
+      launches = 1;
+    }
+  } else if (a.dh == 64) {
+    if (!a.raw) {
+      score_kernel<1, 64><<<nblk, SC_THREADS, 0, stream>>>(a);
+      score_combine_kernel<<<(a.nq * a.Hq + 255) / 256, 256, 0, stream>>>(a, nblk);
+      score_kernel<2, 64><<<nblk, SC_THREADS, 0, stream>>>(a);
+      launches = 3;
+    } else {
+      score_kernel<3, 64><<<nblk, SC_THREADS, 0, stream>>>(a);
+      launches = 1;
+    }
+  } else {
+    return -1;
+  }
+  return launches;
+}
+
+int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* chunk_tok, const int* q_tok, int nq,
+              int q_row0, int* plan_rows, int* plan_tok, cudaStream_t stream) {
+  topk_plan_kernel<<<1, TK_THREADS, 0, stream>>>(scores, n_keys, k, key_row0, chunk_tok, q_tok, nq, q_row0,
+                                                 plan_rows, plan_tok);
+  return 1;
+}
+
+}  // namespace fragk

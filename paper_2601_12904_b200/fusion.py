@@ -1,0 +1,316 @@
+"""Python mirror of the reference's reprocessing surface over the C ABI.
+
+Names follow SPEC.md: ``ChunkKVStore.put_record`` / ``fetch`` (SPEC.md:265,
+SPEC.md:283), ``preprocess_isolated``, ``reprocess`` =
+``stitch_full_reuse`` + ``select_query_guided`` + ``sparse_prefill_and_decode``
+up to the first-token logits. Errors are the reference's
+taxonomy (common.hpp:17-40): ``ContractError``, ``StoreError``, ``FormatError``.
+
+Every call goes to libfrag.so (CUDA, sm_100a). There is no CPU path here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from ._lib import (ChunkId, ContractError, CudaError, FormatError, FragError, ModelCfg, OutOfMemory,
+                   RecordView, ReprocessOpts, StoreError, Timing, check, lib)
+
+__all__ = ["ModelCfg", "ChunkId", "Engine", "ChunkKVStore", "Result", "preset", "hash_tokens",
+           "ContractError", "StoreError", "FormatError", "CudaError", "OutOfMemory", "FragError",
+           "ISOLATED", "FUSED", "launch_count", "memcpy"]
+
+ISOLATED, FUSED = 0, 1
+WEIGHT_IDS = {"emb": 0, "lm_head": 1, "wq": 2, "wk": 3, "wv": 4, "wo": 5, "w_gate": 6, "w_up": 7,
+              "w_down": 8, "attn_norm": 9, "ffn_norm": 10, "final_norm": 11}
+
+
+def preset(name: str) -> ModelCfg:
+    cfg = ModelCfg()
+    check(lib.frag_model_preset(name.encode(), C.byref(cfg)))
+    return cfg
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def hash_tokens(tokens: Sequence[int], salt: int = 0) -> ChunkId:
+    t = _i32(tokens)
+    out = ChunkId()
+    lib.frag_hash_tokens(_i32p(t), len(t), salt, C.byref(out))
+    return out
+
+
+def launch_count() -> int:
+    return int(lib.frag_launch_count())
+
+
+def memcpy(dst_ptr: int, src_ptr: int, nbytes: int) -> None:
+    check(lib.frag_memcpy(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), nbytes))
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        return C.c_void_p(0)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(int(stream.cuda_stream))  # torch.cuda.Stream
+
+
+class Engine:
+    """init_model: weights from the seeded splitmix64 Rng, bf16 on the GPU."""
+
+    def __init__(self, cfg: ModelCfg | str, device: int = 0, seed: int = 1234):
+        self.cfg = preset(cfg) if isinstance(cfg, str) else cfg
+        self.device = device
+        self.seed = seed
+        self._h = C.c_void_p()
+        check(lib.frag_engine_create(C.byref(self.cfg), device, seed, C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            check(lib.frag_engine_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def weight(self, name: str, layer: int = 0) -> np.ndarray:
+        """Canonical [out][in] weight as float32 (values are exactly the bf16 weights)."""
+        c = self.cfg
+        d, V, F, qc, kc = c.d_model, c.vocab, c.ffn_dim, c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+        shapes = {"emb": (V, d), "lm_head": (V, d), "wq": (qc, d), "wk": (kc, d), "wv": (kc, d),
+                  "wo": (d, qc), "w_gate": (F, d), "w_up": (F, d), "w_down": (d, F), "attn_norm": (d,),
+                  "ffn_norm": (d,), "final_norm": (d,)}
+        shp = shapes[name]
+        buf = np.empty(int(np.prod(shp)), dtype=np.uint16)
+        check(lib.frag_engine_weight(self._h, layer, WEIGHT_IDS[name], buf.ctypes.data_as(C.c_void_p), buf.size))
+        return (buf.astype(np.uint32) << 16).view(np.float32).reshape(shp)
+
+    def profile(self, enable: bool = True):
+        check(lib.frag_engine_profile(self._h, int(enable)))
+
+    def profile_read(self, klass: int, reset: bool = False) -> dict:
+        ms, fl, by, n = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+        check(lib.frag_engine_profile_read(self._h, klass, C.byref(ms), C.byref(fl), C.byref(by), C.byref(n),
+                                           int(reset)))
+        return {"ms": ms.value, "flops": fl.value, "bytes": by.value, "launches": n.value}
+
+    # ---- pipeline entry points
+    def preprocess_isolated(self, store: "ChunkKVStore", tokens: Sequence[int], system: Sequence[int] = (),
+                            overwrite: bool = False) -> ChunkId:
+        t, s = _i32(tokens), _i32(system)
+        out = ChunkId()
+        check(lib.frag_preprocess_isolated(self._h, store._h, _i32p(s), len(s), _i32p(t), len(t), int(overwrite),
+                                           C.byref(out)))
+        return out
+
+    def reprocess(self, store: "ChunkKVStore", question: Sequence[int], chunk_ids: Sequence[ChunkId],
+                  ratio: float, result: "Result", system: Sequence[int] = (), *, raw_scores: bool = False,
+                  all_logits: bool = False, timing: bool = False, inject_crit: Sequence[int] | None = None,
+                  logits_on_device: bool = False, stream=None, question_dev_ptr: int | None = None,
+                  n_question: int | None = None) -> "Result":
+        s = _i32(system)
+        ids = (ChunkId * max(len(chunk_ids), 1))(*chunk_ids)
+        opts = ReprocessOpts()
+        opts.raw_scores = int(raw_scores)
+        opts.all_logits = int(all_logits)
+        opts.timing = int(timing)
+        opts.logits_on_device = int(logits_on_device)
+        inj = None
+        if inject_crit is not None:
+            inj = _i32(inject_crit)
+            opts.inject_crit = _i32p(inj)
+            opts.n_inject = len(inj)
+        if question_dev_ptr is not None:
+            check(lib.frag_reprocess_dev(self._h, store._h, _i32p(s), len(s), C.c_void_p(question_dev_ptr),
+                                         int(n_question), ids, len(chunk_ids), float(ratio), C.byref(opts),
+                                         _stream_ptr(stream), result._h))
+        else:
+            q = _i32(question)
+            check(lib.frag_reprocess(self._h, store._h, _i32p(s), len(s), _i32p(q), len(q), ids, len(chunk_ids),
+                                     float(ratio), C.byref(opts), _stream_ptr(stream), result._h))
+        return result
+
+    def full_prefill(self, tokens: Sequence[int], result: "Result", system: Sequence[int] = (), *,
+                     timing: bool = False, stream=None) -> "Result":
+        t, s = _i32(tokens), _i32(system)
+        opts = ReprocessOpts()
+        opts.timing = int(timing)
+        check(lib.frag_full_prefill(self._h, _i32p(s), len(s), _i32p(t), len(t), C.byref(opts), _stream_ptr(stream),
+                                    result._h))
+        return result
+
+
+@dataclass
+class Record:
+    id: ChunkId
+    n_tok: int
+    native_start: int
+    variant: int
+    tier: int
+    heat: int
+    last_access: int
+    size_bytes: int
+    k_dev: int
+    v_dev: int
+    tokens_dev: int
+
+
+class ChunkKVStore:
+    """HBM-resident chunk-KV store (GPU tier only)."""
+
+    def __init__(self, cfg: ModelCfg, device: int = 0, capacity_bytes: int = 0):
+        self.cfg = cfg
+        self._h = C.c_void_p()
+        check(lib.frag_store_create(C.byref(cfg), device, capacity_bytes, C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            check(lib.frag_store_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __len__(self):
+        return int(lib.frag_store_count(self._h))
+
+    @property
+    def bytes_used(self) -> int:
+        return int(lib.frag_store_bytes_used(self._h))
+
+    def put_record(self, chunk_id: ChunkId, tokens: Sequence[int], native_start: int, k_ptr: int, v_ptr: int,
+                   variant: int = ISOLATED, overwrite: bool = False):
+        """k_ptr/v_ptr: host or device addresses of [L][n][Hkv][dh] bf16."""
+        t = _i32(tokens)
+        check(lib.frag_store_put(self._h, C.byref(chunk_id), _i32p(t), len(t), native_start, variant,
+                                 C.c_void_p(k_ptr), C.c_void_p(v_ptr), int(overwrite)))
+
+    def fetch(self, chunk_id: ChunkId) -> Record:
+        v = RecordView()
+        check(lib.frag_store_fetch(self._h, C.byref(chunk_id), C.byref(v)))
+        return self._rec(v)
+
+    def release(self, chunk_id: ChunkId):
+        check(lib.frag_store_release(self._h, C.byref(chunk_id)))
+
+    def peek(self, chunk_id: ChunkId) -> Record:
+        v = RecordView()
+        check(lib.frag_store_peek(self._h, C.byref(chunk_id), C.byref(v)))
+        return self._rec(v)
+
+    def read_kv(self, chunk_id: ChunkId) -> tuple[np.ndarray, np.ndarray]:
+        """Record K, V as uint16 (bf16 bits) host arrays [L][n][Hkv][dh]."""
+        r = self.peek(chunk_id)
+        c = self.cfg
+        shp = (c.layers, r.n_tok, c.n_kv_heads, c.head_dim)
+        k = np.empty(shp, dtype=np.uint16)
+        v = np.empty(shp, dtype=np.uint16)
+        memcpy(k.ctypes.data, r.k_dev, k.nbytes)
+        memcpy(v.ctypes.data, r.v_dev, v.nbytes)
+        return k, v
+
+    @staticmethod
+    def _rec(v: RecordView) -> Record:
+        cid = ChunkId()
+        C.memmove(C.byref(cid), C.byref(v.id), 16)
+        return Record(cid, v.n_tok, v.native_start, v.variant, v.tier, v.heat, v.last_access, v.size_bytes,
+                      v.k_dev or 0, v.v_dev or 0, v.tokens_dev or 0)
+
+
+class Result:
+    """Per-request fused KV cache + logits (reusable across requests)."""
+
+    def __init__(self, engine: Engine, max_tokens: int):
+        self.engine = engine
+        self._h = C.c_void_p()
+        check(lib.frag_result_create(engine._h, max_tokens, C.byref(self._h)))
+        self.max_tokens = max_tokens
+
+    def close(self):
+        if self._h:
+            check(lib.frag_result_free(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        check(lib.frag_result_sync(self._h))
+
+    @property
+    def n_tokens(self) -> int:
+        n = C.c_int32()
+        check(lib.frag_result_fused_kv(self._h, None, None, C.byref(n)))
+        return n.value
+
+    def fused_ptrs(self) -> tuple[int, int]:
+        k, v = C.c_void_p(), C.c_void_p()
+        check(lib.frag_result_fused_kv(self._h, C.byref(k), C.byref(v), None))
+        return k.value, v.value
+
+    def fused_kv(self) -> tuple[np.ndarray, np.ndarray]:
+        """Fused K, V as uint16 bf16 bits [L][T][Hkv][dh] (copied to host)."""
+        c = self.engine.cfg
+        T = self.n_tokens
+        kp, vp = self.fused_ptrs()
+        out = []
+        for p in (kp, vp):
+            a = np.empty((c.layers, self.max_tokens, c.n_kv_heads, c.head_dim), dtype=np.uint16)
+            memcpy(a.ctypes.data, p, a.nbytes)
+            out.append(np.ascontiguousarray(a[:, :T]))
+        return out[0], out[1]
+
+    def logits(self) -> np.ndarray:
+        p = C.POINTER(C.c_float)()
+        rows, vocab = C.c_int32(), C.c_int32()
+        check(lib.frag_result_logits(self._h, C.byref(p), C.byref(rows), C.byref(vocab), 0))
+        return np.ctypeslib.as_array(p, shape=(rows.value, vocab.value)).copy()
+
+    def logits_dev_ptr(self) -> int:
+        p = C.POINTER(C.c_float)()
+        check(lib.frag_result_logits(self._h, C.byref(p), None, None, 1))
+        return C.cast(p, C.c_void_p).value
+
+    def crit(self) -> np.ndarray:
+        k = lib.frag_result_crit(self._h, None, 0)
+        out = np.empty(max(k, 1), dtype=np.int32)
+        if k > 0:
+            lib.frag_result_crit(self._h, _i32p(out), k)
+        return out[:k]
+
+    def timing(self) -> dict:
+        t = Timing()
+        check(lib.frag_result_timing(self._h, C.byref(t)))
+        return t.as_dict()
+
+    def debug(self) -> dict:
+        qf, sc = C.c_void_p(), C.c_void_p()
+        nq, n = C.c_int32(), C.c_int32()
+        check(lib.frag_result_debug(self._h, C.byref(qf), C.byref(sc), C.byref(nq), C.byref(n)))
+        c = self.engine.cfg
+        q = np.empty((nq.value, c.n_heads, c.head_dim), dtype=np.float32)
+        s = np.empty(max(n.value, 1), dtype=np.float32)
+        if nq.value:
+            memcpy(q.ctypes.data, qf.value, q.nbytes)
+        if n.value:
+            memcpy(s.ctypes.data, sc.value, n.value * 4)
+        return {"q_final": q, "scores": s[:n.value]}

@@ -1,0 +1,136 @@
+"""Kernel-level parity on the B200: each sm_100a kernel against a plain fp32
+(or fp64) PyTorch restatement of the same op, called through the C ABI."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_2601_12904_b200 import _lib
+    return _lib
+
+
+def _gemm(a, b, c, epi, force_bn=0):
+    L = _lib()
+    L.check(L.lib.frag_kernel_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), a.shape[0], b.shape[0], a.shape[1],
+                                   epi, force_bn, None))
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 256, 64), (37, 512, 256), (128, 768, 256), (300, 1024, 512),
+                                   (2490, 1536, 4096), (129, 64, 192)])
+@pytest.mark.parametrize("bn", [0, 64, 128, 256])
+def test_gemm_tcgen05_vs_torch(cuda, M, N, K, bn):
+    import torch
+    if bn and N % bn:
+        pytest.skip("N not a multiple of BN")
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device=cuda, generator=g).to(torch.bfloat16)
+    ref = a.double() @ b.double().T
+    c = torch.empty(M, N, device=cuda, dtype=torch.float32)
+    _gemm(a, b, c, 1, bn)
+    torch.cuda.synchronize()
+    err = (c.double() - ref).abs().max().item()
+    assert err <= 2e-5 * math.sqrt(K) * ref.abs().max().item() + 1e-4, err
+    cb = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    _gemm(a, b, cb, 0, bn)
+    torch.cuda.synchronize()
+    assert torch.equal(cb, c.to(torch.bfloat16))
+    # residual epilogue: C += A B^T
+    r0 = torch.randn(M, N, device=cuda, generator=g)
+    r = r0.clone()
+    _gemm(a, b, r, 2, bn)
+    torch.cuda.synchronize()
+    assert torch.allclose(r, r0 + c, rtol=0, atol=1e-4 * ref.abs().max().item() + 1e-5)
+
+
+def test_gemm_swiglu_epilogue(cuda):
+    import torch
+    M, F, K = 200, 512, 256
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16) * 0.5
+    wg = torch.randn(F, K, device=cuda, generator=g).to(torch.bfloat16) * 0.1
+    wu = torch.randn(F, K, device=cuda, generator=g).to(torch.bfloat16) * 0.1
+    packed = torch.empty(2 * F, K, device=cuda, dtype=torch.bfloat16)
+    idx = torch.arange(F, device=cuda)
+    packed[(idx // 32) * 64 + idx % 32] = wg
+    packed[(idx // 32) * 64 + 32 + idx % 32] = wu
+    out = torch.empty(M, F, device=cuda, dtype=torch.bfloat16)
+    _gemm(a, packed, out, 3)
+    torch.cuda.synchronize()
+    gg = a.float() @ wg.float().T
+    uu = a.float() @ wu.float().T
+    ref = torch.nn.functional.silu(gg) * uu
+    assert (out.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+
+
+def _attn_ref(q, k, v, rows, scale):
+    # q [M,Hq,dh], k/v [T,Hkv,dh]; row i sees keys 0..rows[i]
+    import torch
+    M, Hq, dh = q.shape
+    G = Hq // k.shape[1]
+    out = torch.empty(M, Hq, dh, dtype=torch.float64, device=q.device)
+    kk = k.double().repeat_interleave(G, dim=1)
+    vv = v.double().repeat_interleave(G, dim=1)
+    for i in range(M):
+        p = int(rows[i]) + 1
+        s = torch.einsum("hd,thd->ht", q[i].double(), kk[:p]) * scale
+        w = torch.softmax(s, dim=-1)
+        out[i] = torch.einsum("ht,thd->hd", w, vv[:p])
+    return out
+
+
+@pytest.mark.parametrize("Hq,Hkv,dh,T,M,split", [(4, 4, 64, 700, 90, 0), (32, 8, 128, 1500, 150, 0),
+                                                 (32, 8, 128, 3000, 20, 512), (8, 1, 128, 600, 64, 256)])
+def test_sparse_q_attention_vs_torch(cuda, Hq, Hkv, dh, T, M, split):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(T + M)
+    q = torch.randn(M, Hq, dh, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(T, Hkv, dh, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(T, Hkv, dh, device=cuda, generator=g).to(torch.bfloat16)
+    rows = torch.sort(torch.randperm(T, device=cuda, generator=g)[:M]).values.to(torch.int32)
+    out = torch.empty(M, Hq, dh, device=cuda, dtype=torch.bfloat16)
+    L = _lib()
+    L.check(L.lib.frag_kernel_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), rows.data_ptr(), out.data_ptr(),
+                                        M, T, Hq, Hkv, dh, split, None))
+    ref = _attn_ref(q, k, v, rows.cpu(), 1.0 / math.sqrt(dh))
+    err = (out.double() - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+def _rope_shift_ref(kbits, delta, base):
+    dh = kbits.shape[-1]
+    k = (kbits.astype(np.uint32) << 16).view(np.float32)
+    half = dh // 2
+    th = base ** (-2.0 * (np.arange(half) + 1) / dh)
+    c = np.cos(delta * th).astype(np.float32)
+    s = np.sin(delta * th).astype(np.float32)
+    k0, k1 = k[..., 0::2], k[..., 1::2]
+    o0 = (k0.astype(np.float64) * c - np.float32(k1 * s)).astype(np.float32)  # fma(k0,c,-(k1*s)) exactly rounded
+    o1 = (k1.astype(np.float64) * c + np.float32(k0 * s)).astype(np.float32)
+    out = np.empty_like(k)
+    out[..., 0::2], out[..., 1::2] = o0, o1
+    b = out.view(np.uint32)
+    rnd = ((b >> 16) & 1) + 0x7FFF
+    return ((b + rnd) >> 16).astype(np.uint16)
+
+
+@pytest.mark.parametrize("delta", [0, 1, 257, 5000, -3])
+def test_rope_shift_bit_exact(cuda, delta):
+    import torch
+    L_, n, Hkv, dh = 2, 70, 4, 64
+    rng = np.random.default_rng(delta + 11)
+    kf = rng.standard_normal((L_, n, Hkv, dh)).astype(np.float32)
+    kbits = (kf.view(np.uint32) >> 16).astype(np.uint16)
+    src = torch.from_numpy(kbits.view(np.int16)).to(cuda)
+    dst = torch.empty_like(src)
+    native = 10
+    L = _lib()
+    L.check(L.lib.frag_kernel_rope_shift(src.data_ptr(), dst.data_ptr(), L_, n, Hkv, dh, native, native + delta,
+                                         1e4, None))
+    got = dst.cpu().numpy().view(np.uint16)
+    exp = kbits if delta == 0 else _rope_shift_ref(kbits, float(delta), 1e4)
+    assert np.array_equal(got, exp)

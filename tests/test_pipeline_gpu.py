@@ -1,0 +1,89 @@
+"""End-to-end reprocessing on the GPU through the C ABI: store semantics,
+endpoint reductions (r=0 = Full Reuse, r=1 = Full Attention)
+and the invariants of SPEC.md:448 and SPEC.md:173."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tiny(cuda):
+    from paper_2601_12904_b200 import fusion as F
+    eng = F.Engine("tiny", seed=1234)
+    store = F.ChunkKVStore(eng.cfg)
+    rng = np.random.default_rng(5)
+    system = rng.integers(0, eng.cfg.vocab, 8).tolist()
+    chunks = [rng.integers(0, eng.cfg.vocab, 256).tolist() for _ in range(8)]
+    ids = [eng.preprocess_isolated(store, c, system=system) for c in chunks]
+    question = rng.integers(0, eng.cfg.vocab, 32).tolist()
+    res = F.Result(eng, 8 + 8 * 256 + 32 + 64)
+    return dict(F=F, eng=eng, store=store, system=system, chunks=chunks, ids=ids, question=question, res=res)
+
+
+def test_store_semantics(tiny):
+    F, store, ids, chunks = tiny["F"], tiny["store"], tiny["ids"], tiny["chunks"]
+    assert len(store) == 8
+    r = store.peek(ids[0])
+    assert r.n_tok == 256 and r.native_start == 9 and r.variant == F.ISOLATED
+    h0 = r.heat
+    store.fetch(ids[0])
+    store.fetch(ids[0])
+    assert store.peek(ids[0]).heat == h0 + 2
+    store.release(ids[0])
+    store.release(ids[0])
+    with pytest.raises(F.StoreError):  # duplicate without overwrite
+        tiny["eng"].preprocess_isolated(store, chunks[0], system=tiny["system"])
+    with pytest.raises(F.StoreError):
+        store.fetch(F.hash_tokens([1, 2, 3]))
+
+
+def test_reprocess_runs_and_selects(tiny):
+    eng, store, res = tiny["eng"], tiny["store"], tiny["res"]
+    eng.reprocess(store, tiny["question"], tiny["ids"], 0.15, res, system=tiny["system"], timing=True)
+    lg = res.logits()
+    assert lg.shape == (1, eng.cfg.vocab) and np.isfinite(lg).all()
+    crit = res.crit()
+    N = 8 * 256
+    assert len(crit) == int(np.floor(0.15 * N + 0.5))
+    assert np.all(np.diff(crit) > 0)
+    assert crit.min() >= 9 and crit.max() <= 8 + N  # never system or question tokens
+    t = res.timing()
+    assert t["total_ms"] > 0
+
+
+def test_store_immutable_during_reprocess(tiny):
+    store, ids = tiny["store"], tiny["ids"]
+    before = [store.read_kv(i) for i in ids[:2]]
+    tiny["eng"].reprocess(store, tiny["question"], ids, 0.3, tiny["res"], system=tiny["system"])
+    after = [store.read_kv(i) for i in ids[:2]]
+    for (k0, v0), (k1, v1) in zip(before, after):
+        assert np.array_equal(k0, k1) and np.array_equal(v0, v1)
+
+
+def test_endpoint_r1_equals_full_attention(tiny):
+    F, eng = tiny["F"], tiny["eng"]
+    res = tiny["res"]
+    eng.reprocess(tiny["store"], tiny["question"], tiny["ids"], 1.0, res, system=tiny["system"])
+    lg1 = res.logits()
+    k1, v1 = res.fused_kv()
+    fa = F.Result(eng, res.max_tokens)
+    tokens = [t for c in tiny["chunks"] for t in c] + tiny["question"]
+    eng.full_prefill(tokens, fa, system=tiny["system"])
+    lgf = fa.logits()
+    kf, vf = fa.fused_kv()
+    # identical kernels on identical rows: bit-identical
+    assert np.array_equal(k1, kf) and np.array_equal(v1, vf)
+    assert np.array_equal(lg1, lgf)
+
+
+def test_single_chunk_native_offset_is_bit_copy(tiny):
+    # one chunk at its native offset -> stitched KV bit-equal to the record
+    eng, store = tiny["eng"], tiny["store"]
+    res = tiny["res"]
+    eng.reprocess(store, tiny["question"], tiny["ids"][:1], 0.0, res, system=tiny["system"])
+    k, v = res.fused_kv()
+    rk, rv = store.read_kv(tiny["ids"][0])
+    L_ = eng.cfg.layers
+    # rows S..S+n-1 hold the record untouched (r=0: nothing recomputed there)
+    assert np.array_equal(k[:, 8:8 + 256], rk) and np.array_equal(v[:, 8:8 + 256], rv)
