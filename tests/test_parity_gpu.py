@@ -98,7 +98,12 @@ def test_selection_bit_exact_on_identical_inputs(tiny):
         c = tiny["eng"].cfg
         N = 8 * 256
         qf = g["debug"]["q_final"]
-        keys = O.bf16_bits_to_f32(g["k"][c.layers - 1, S:S + N])
+        # selection reads the STITCHED final-layer keys (before the sparse pass
+        # overwrites the critical rows): the oracle stitch of the same records,
+        # bit-exact with K1 (test_stitch_rows_bit_exact)
+        chunks = [(r["k"], r["v"], r["native_start"], S + i * 256) for i, r in enumerate(tiny["recs"])]
+        ko, _ = O.stitch(c, chunks, S + N)
+        keys = ko[c.layers - 1, S:S + N]
         k = int(np.floor(ratio * N + 0.5))
         scores, sel = O.select(qf, keys, k)
         gpu_sel = g["crit"] - S - 1
@@ -165,9 +170,11 @@ def test_llama8b_width_two_layer_parity(cuda):
     rk = O.bf16_bits_to_f32(O.f32_to_bf16_bits(out["k"]))
     gk = O.bf16_bits_to_f32(g["k"])
     assert _rel_l2(gk, rk) <= 3e-2
-    # selection on identical inputs
+    # selection on identical inputs (stitched keys, before the sparse pass)
     N = 4 * 256
-    keys = O.bf16_bits_to_f32(g["k"][1, :N])
+    chunks = [(r["k"], r["v"], r["native_start"], i * 256) for i, r in enumerate(t["recs"])]
+    ko, _ = O.stitch(cfg, chunks, N)
+    keys = ko[1]
     scores, sel = O.select(g["debug"]["q_final"], keys, len(g["crit"]))
     tau = np.sort(scores)[::-1][len(sel) - 1]
     diff = set((g["crit"] - 1).tolist()) ^ set(sel.tolist())
