@@ -1,0 +1,337 @@
+// K6 on the 5th-gen tensor cores: sparse-Q causal attention over the fused KV
+// cache.
+//
+// Only the selected query rows (critical + question, ascending fused rows p_i)
+// are computed; row i attends fused rows [0, p_i]. The fused cache already
+// holds this layer's fresh K/V at every selected row (scattered by the QKV
+// GEMM epilogue), so stale entries are replaced and earlier critical tokens'
+// fresh K/V are visible in the same pass.
+//
+// One CTA = one tile of 128 query rows (128/G tokens x G heads of one GQA
+// group, so every K/V tile is shared by the whole group) x one key split.
+//   warp 0      TMA: Q tile once; K and V tiles (128 keys x dh, SWIZZLE_128B)
+//               into a 2-stage ring.
+//   warp 1      TMEM alloc + single-thread tcgen05.mma issue:
+//                 S_j = Q K_j^T   (M=128, N=128 keys, K=dh; both K-major)
+//                 O  += P_j V_j   (M=128, N=dh, K=128 keys; P K-major in smem,
+//                                  V MN-major straight from the TMA tile)
+//               S is double-buffered in TMEM so S_{j+1} overlaps softmax j.
+//   warps 2..5  softmax, one thread per query row (TMEM lane): tcgen05.ld the
+//               S row, causal mask by position, online softmax with lazy
+//               rescale (O in TMEM is only rescaled when the row max grows by
+//               more than 2^8), P -> bf16 -> swizzled smem; epilogue O / l.
+// Split-KV partials (O normalised per split + LSE) are merged by
+// attn_combine_kernel (attn.cu).
+#include <cuda.h>
+
+#include <cfloat>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace fragk {
+
+namespace {
+
+constexpr int AT_ROWS = 128;
+constexpr int AT_KEYS = 128;
+constexpr int AT_THREADS = 192;
+constexpr float RESCALE_THRESH = 8.0f;  // log2 units
+
+template <int DH>
+struct AttCfg {
+  static constexpr int ATOMS = DH / 64;                       // 64-column swizzle atoms per row
+  static constexpr uint32_t Q_BYTES = AT_ROWS * DH * 2;       // [ATOMS][128][64]
+  static constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;      // one of K or V per stage
+  static constexpr uint32_t P_BYTES = AT_ROWS * AT_KEYS * 2;  // [2 atoms][128][64]
+  static constexpr size_t SMEM = 1024 + Q_BYTES + 4 * (size_t)KV_BYTES + 2 * (size_t)P_BYTES + 256;
+  static constexpr int TMEM_S0 = 0, TMEM_S1 = 128, TMEM_O = 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int G, int n_qblocks) {
+  using C = AttCfg<DH>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + C::Q_BYTES;          // [2 stages]
+  uint8_t* sV = sK + 2 * C::KV_BYTES;     // [2 stages]
+  uint8_t* sP = sV + 2 * C::KV_BYTES;     // [2 buffers]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* v_full = bar + 3;    // [2]
+  uint64_t* kv_empty = bar + 5;  // [2]
+  uint64_t* s_full = bar + 7;    // [2]
+  uint64_t* s_empty = bar + 9;   // [2]
+  uint64_t* p_full = bar + 11;   // [2]
+  uint64_t* pv_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int qb = n_qblocks - 1 - (int)blockIdx.x;  // heaviest (latest rows) first
+  const int hk = blockIdx.y;
+  const int split = blockIdx.z;
+  const int tok_per_cta = AT_ROWS / G;
+  const int t0 = qb * tok_per_cta;
+  const int t_end = min(t0 + tok_per_cta, a.M);
+  const int p_max = a.rows[t_end - 1];
+  const int p_min = a.rows[t0];
+  const int k_lo = a.n_splits > 1 ? split * a.split_keys : 0;
+  int k_hi = p_max + 1;
+  if (a.n_splits > 1) k_hi = min(k_hi, (split + 1) * a.split_keys);
+  const int n_tiles = k_hi > k_lo ? (k_hi - k_lo + AT_KEYS - 1) / AT_KEYS : 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], 4);
+      mbar_init(&p_full[s], 4);
+    }
+    mbar_init(pv_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (n_tiles > 0 && elect_one()) {
+      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+      for (int at = 0; at < C::ATOMS; ++at)
+        tma_load_3d(sQ + at * (AT_ROWS * 128), &tmQ, q_full, at * 64, hk * G, t0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        const int key0 = k_lo + j * AT_KEYS;
+        mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
+#pragma unroll
+        for (int at = 0; at < C::ATOMS; ++at)
+          tma_load_2d(sK + st * C::KV_BYTES + at * (AT_KEYS * 128), &tmK, &k_full[st], hk * DH + at * 64, key0);
+        mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
+#pragma unroll
+        for (int at = 0; at < C::ATOMS; ++at)
+          tma_load_2d(sV + st * C::KV_BYTES + at * (AT_KEYS * 128), &tmV, &v_full[st], hk * DH + at * 64, key0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (n_tiles > 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(AT_ROWS, AT_KEYS, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(AT_ROWS, DH, 0, 1);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      const uint32_t q_base = smem_u32(sQ);
+      auto issue_pv = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&p_full[st], (j >> 1) & 1);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t p_base = smem_u32(sP + st * C::P_BYTES);
+          const uint32_t v_base = smem_u32(sV + st * C::KV_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < AT_KEYS / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(p_base + (kk >> 2) * (AT_ROWS * 128) + (kk & 3) * 32, 16, 1024);
+            // V tile [keys][64-dh atoms]: MN-major; K step = 16 key rows = 2048 B,
+            // next 64-wide dh atom at LBO = 128 keys * 128 B.
+            const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, AT_KEYS * 128, 1024);
+            umma_bf16_ss(tmem + C::TMEM_O, ad, bd, idesc_o, (j | kk) != 0);
+          }
+          umma_commit(&kv_empty[st]);
+          umma_commit(pv_done);
+        }
+        __syncwarp();
+      };
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&s_empty[st], ((j >> 1) - 1) & 1);
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t k_base = smem_u32(sK + st * C::KV_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * (AT_ROWS * 128) + (kk & 3) * 32;
+            const uint64_t ad = umma_desc_sw128(q_base + off, 16, 1024);
+            const uint64_t bd = umma_desc_sw128(k_base + off, 16, 1024);
+            umma_bf16_ss(tmem + (st ? C::TMEM_S1 : C::TMEM_S0), ad, bd, idesc_s, kk != 0);
+          }
+          umma_commit(&s_full[st]);
+        }
+        __syncwarp();
+        if (j >= 1) issue_pv(j - 1);
+      }
+      issue_pv(n_tiles - 1);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;  // query row of this thread = TMEM lane
+    const int tl = r / G;
+    const int tok = t0 + tl;
+    const int head = hk * G + r % G;
+    const bool live = tok < a.M;
+    const int prow = live ? a.rows[tok] : -1;
+    const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
+    const float c = a.scale * 1.4426950408889634f;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j & 1;
+      const int key0 = k_lo + j * AT_KEYS;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t s[AT_KEYS];
+#pragma unroll
+      for (int cc = 0; cc < AT_KEYS / 32; ++cc)
+        tmem_ld32(lane_base + (st ? C::TMEM_S1 : C::TMEM_S0) + cc * 32,
+                  *reinterpret_cast<uint32_t(*)[32]>(&s[cc * 32]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[st]);
+      // scale into log2 units + causal mask by position (keys > p_row or beyond the split)
+      const int lim = min(prow, k_hi - 1) - key0;  // last visible key index within the tile
+      const bool need_mask = (key0 + AT_KEYS - 1 > p_min) || (key0 + AT_KEYS > k_hi);
+      float mt = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < AT_KEYS; ++k) {
+        float v = __uint_as_float(s[k]) * c;
+        if (need_mask && k > lim) v = -INFINITY;
+        s[k] = __float_as_uint(v);
+        mt = fmaxf(mt, v);
+      }
+      // lazy rescale: only when the max grows by more than 2^8
+      const bool grow = mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt != -INFINITY);
+      const float m_new = grow ? fmaxf(mt, m_used) : m_used;
+      const float alpha = (grow && m_used != -INFINITY) ? exp2f(m_used - m_new) : 1.f;
+      if (__any_sync(0xffffffffu, grow && m_used != -INFINITY) && j > 0) {
+        // O of rows in this warp's lane quarter is rescaled in TMEM; PV_{j-1} must be done
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < DH / 32; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(lane_base + C::TMEM_O + cc * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(lane_base + C::TMEM_O + cc * 32, o);
+        }
+        tmem_st_wait();
+      }
+      l *= alpha;
+      m_used = m_new;
+      // P = exp2(s - m) -> bf16 -> swizzled K-major smem tile (row r, keys 0..127)
+      uint8_t* pbuf = sP + st * C::P_BYTES;
+      float rs = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < AT_KEYS / 8; ++ch) {
+        float p[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float v = __uint_as_float(s[ch * 8 + e]);
+          p[e] = (m_used == -INFINITY) ? 0.f : exp2f(v - m_used);
+          rs += p[e];
+        }
+        uint4 pk;
+        pk.x = pack_bf16(p[0], p[1]);
+        pk.y = pack_bf16(p[2], p[3]);
+        pk.z = pack_bf16(p[4], p[5]);
+        pk.w = pack_bf16(p[6], p[7]);
+        const int atom = ch >> 3, cin = ch & 7;
+        *reinterpret_cast<uint4*>(pbuf + atom * (AT_ROWS * 128) + r * 128 + ((cin ^ (r & 7)) << 4)) = pk;
+      }
+      l += rs;
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[st]);
+    }
+    // ---- epilogue
+    if (n_tiles > 0) {
+      mbar_wait(pv_done, (n_tiles - 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const size_t qi = (size_t)tok * a.Hq + head;
+#pragma unroll 1
+    for (int cc = 0; cc < DH / 32; ++cc) {
+      uint32_t o[32];
+      if (n_tiles > 0) {
+        tmem_ld32(lane_base + C::TMEM_O + cc * 32, o);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = 0u;
+      }
+      if (!live) continue;
+      if (a.n_splits > 1) {
+        float4* po = reinterpret_cast<float4*>(a.part_o + ((size_t)split * a.M * a.Hq + qi) * DH + cc * 32);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          po[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                              __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+      } else {
+        uint4* po = reinterpret_cast<uint4*>(a.out + qi * DH + cc * 32);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(o[8 * e + 0]) * inv, __uint_as_float(o[8 * e + 1]) * inv);
+          v.y = pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv);
+          v.z = pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv);
+          v.w = pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv);
+          po[e] = v;
+        }
+      }
+    }
+    if (live && a.n_splits > 1) {
+      // natural-log LSE of the scaled scores: m (log2 units) -> * ln2
+      a.part_lse[(size_t)split * a.M * a.Hq + qi] =
+          l > 0.f ? m_used * 0.6931471805599453f + __logf(l) : -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream) {
+  CUtensorMap tq, tk, tv;
+  // Q [M][Hq][dh] viewed as (dh, Hq, M); box (64, G, 128/G)
+  if (!make_tmap_3d(&tq, a.q, a.dh, a.Hq, a.M, a.dh, (uint64_t)a.Hq * a.dh, 64, G, AT_ROWS / G)) return -1;
+  // K/V layer [T][Hkv*dh]; box (64, 128 keys)
+  if (!make_tmap_2d(&tk, a.k, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
+  if (!make_tmap_2d(&tv, a.v, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
+  dim3 grid(n_qblocks, a.Hkv, a.n_splits);
+  if (a.dh == 128) {
+    cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AttCfg<128>::SMEM);
+    attn_tc_kernel<128><<<grid, AT_THREADS, AttCfg<128>::SMEM, stream>>>(tq, tk, tv, a, G, n_qblocks);
+  } else if (a.dh == 64) {
+    cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AttCfg<64>::SMEM);
+    attn_tc_kernel<64><<<grid, AT_THREADS, AttCfg<64>::SMEM, stream>>>(tq, tk, tv, a, G, n_qblocks);
+  } else {
+    return -1;
+  }
+  return 1;
+}
+
+}  // namespace fragk

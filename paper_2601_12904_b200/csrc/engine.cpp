@@ -175,7 +175,7 @@ static void validate_cfg(const frag_model_cfg& c) {
   req(c.layers >= 1, "layers >= 1");
   req(c.head_dim == 64 || c.head_dim == 128, "head_dim in {64, 128}");
   req(c.n_heads >= 1 && c.n_kv_heads >= 1 && c.n_heads % c.n_kv_heads == 0, "n_heads multiple of n_kv_heads");
-  req(64 % (c.n_heads / c.n_kv_heads) == 0, "GQA group divides 64");
+  req(128 % (c.n_heads / c.n_kv_heads) == 0, "GQA group divides 128");
   req(c.d_model % 64 == 0, "d_model % 64 == 0");
   req(c.ffn_dim % 64 == 0, "ffn_dim % 64 == 0");
   req(c.vocab % 64 == 0 && c.vocab >= 2, "vocab % 64 == 0");
@@ -313,7 +313,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
 
   // split-KV policy: enough CTAs for >= 2 waves, splits of >= 256 keys
   const int G = Hq / Hkv;
-  const int nqb = (M + (64 / G) - 1) / (64 / G);
+  const int nqb = (M + (128 / G) - 1) / (128 / G);
   const long ctas = (long)nqb * Hkv;
   int n_splits = 1, split_keys = 0;
   const int sms = fragk::num_sms();
@@ -321,7 +321,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     n_splits = (int)((2L * sms + ctas - 1) / ctas);
     const int max_splits = (T + 255) / 256;
     if (n_splits > max_splits) n_splits = max_splits;
-    split_keys = (int)align_up((size_t)((T + n_splits - 1) / n_splits), 64);
+    split_keys = (int)align_up((size_t)((T + n_splits - 1) / n_splits), 128);
     n_splits = (T + split_keys - 1) / split_keys;
     if (n_splits <= 1) n_splits = 1, split_keys = 0;
   }

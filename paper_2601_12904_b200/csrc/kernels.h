@@ -4,6 +4,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -44,6 +45,13 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
 int gemm_pick_bn(int M, int N, int K);
 int num_sms();
 
+// TMA descriptors (bf16, SWIZZLE_128B, 64-element inner box), encoded through the
+// driver entry point so the library needs no link-time libcuda.
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+                  uint32_t box_rows);
+bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_elems,
+                  uint64_t s2_elems, uint32_t b0, uint32_t b1, uint32_t b2);
+
 // ------------------------------------------------------------------ K1
 struct StitchChunk {
   const bf16* k_src;   // record K [L][n][Hkv][dh]
@@ -78,6 +86,7 @@ struct AttnArgs {
   float scale;           // 1/sqrt(dh)
 };
 int sparse_q_attention(const AttnArgs& a, cudaStream_t stream);  // returns launches
+int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream);
 
 // ------------------------------------------------------------------ K9/K10
 struct ScoreArgs {
