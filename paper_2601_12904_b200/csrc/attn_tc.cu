@@ -203,17 +203,26 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[st]);
-      // scale into log2 units + causal mask by position (keys > p_row or beyond the split)
+      // causal mask by position (keys > p_row or beyond the split), raw scores
       const int lim = min(prow, k_hi - 1) - key0;  // last visible key index within the tile
       const bool need_mask = (key0 + AT_KEYS - 1 > p_min) || (key0 + AT_KEYS > k_hi);
-      float mt = -INFINITY;
+      if (need_mask) {
 #pragma unroll
-      for (int k = 0; k < AT_KEYS; ++k) {
-        float v = __uint_as_float(s[k]) * c;
-        if (need_mask && k > lim) v = -INFINITY;
-        s[k] = __float_as_uint(v);
-        mt = fmaxf(mt, v);
+        for (int k = 0; k < AT_KEYS; ++k)
+          if (k > lim) s[k] = 0xff800000u;  // -inf
       }
+      // row max with 8 independent chains (one softmax warp per SMSP: latency, not
+      // throughput, bounds this loop), then into log2 units
+      float mx8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(s[e]);
+#pragma unroll
+      for (int k = 8; k < AT_KEYS; k += 8)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(mx8[e], __uint_as_float(s[k + e]));
+      const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float mt = mraw * c;
       // lazy rescale: only when the max grows by more than 2^8
       const bool grow = mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt != -INFINITY);
       const float m_new = grow ? fmaxf(mt, m_used) : m_used;
@@ -237,15 +246,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       m_used = m_new;
       // P = exp2(s - m) -> bf16 -> swizzled K-major smem tile (row r, keys 0..127)
       uint8_t* pbuf = sP + st * C::P_BYTES;
-      float rs = 0.f;
+      // p = 2^(s*c - m): one FFMA + MUFU.EX2 per element; masked s = -inf -> 0.
+      // A row with no visible key so far has every s = -inf, so m may be taken as 0.
+      const float mneg = m_used == -INFINITY ? 0.f : -m_used;
+      float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int ch = 0; ch < AT_KEYS / 8; ++ch) {
         float p[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float v = __uint_as_float(s[ch * 8 + e]);
-          p[e] = (m_used == -INFINITY) ? 0.f : exp2f(v - m_used);
-          rs += p[e];
+          p[e] = ex2_approx(__fmaf_rn(__uint_as_float(s[ch * 8 + e]), c, mneg));
+          rs8[e] += p[e];
         }
         uint4 pk;
         pk.x = pack_bf16(p[0], p[1]);
@@ -255,7 +266,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const int atom = ch >> 3, cin = ch & 7;
         *reinterpret_cast<uint4*>(pbuf + atom * (AT_ROWS * 128) + r * 128 + ((cin ^ (r & 7)) << 4)) = pk;
       }
-      l += rs;
+      l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
       fence_async_smem();
       tc_fence_before();
       __syncwarp();
