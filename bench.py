@@ -184,9 +184,6 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     # ---- timed region (device-resident inputs)
-    eng.profile(True)
-    for k in range(5):
-        eng.profile_read(k, reset=True)
     launches0 = F.launch_count()
     if world > 1:
         torch.distributed.barrier()
@@ -202,9 +199,19 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = F.launch_count() - launches0
+    crit = res.crit()
+
+    # ---- per-kernel-class device time: the same K requests again with CUDA
+    # events around every launch on the launching stream (kept out of the
+    # headline loop because the ~700 event records per request cost host time)
+    eng.profile(True)
+    for k in range(5):
+        eng.profile_read(k, reset=True)
+    for i in range(args.steps):
+        step_dev(args.warmup + i)
+    torch.cuda.synchronize()
     prof = {k: eng.profile_read(k) for k in range(5)}
     eng.profile(False)
-    crit = res.crit()
 
     # ---- stage breakdown (one extra request with per-stage events)
     step_dev(0, timing=True)

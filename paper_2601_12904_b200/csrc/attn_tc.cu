@@ -334,10 +334,10 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   if (!make_tmap_2d(&tv, a.v, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
   dim3 grid(n_qblocks, a.Hkv, a.n_splits);
   if (a.dh == 128) {
-    cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AttCfg<128>::SMEM);
+    smem_attr_once(attn_tc_kernel<128>, (int)AttCfg<128>::SMEM);
     attn_tc_kernel<128><<<grid, AT_THREADS, AttCfg<128>::SMEM, stream>>>(tq, tk, tv, a, G, n_qblocks);
   } else if (a.dh == 64) {
-    cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AttCfg<64>::SMEM);
+    smem_attr_once(attn_tc_kernel<64>, (int)AttCfg<64>::SMEM);
     attn_tc_kernel<64><<<grid, AT_THREADS, AttCfg<64>::SMEM, stream>>>(tq, tk, tv, a, G, n_qblocks);
   } else {
     return -1;

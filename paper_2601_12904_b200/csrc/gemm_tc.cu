@@ -332,7 +332,7 @@ namespace {
 template <int BN, int EPI>
 int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& ep, cudaStream_t stream) {
   using C = GemmCfg<BN>;
-  cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  smem_attr_once(gemm_tc_kernel<BN, EPI>, (int)C::SMEM);
   CUtensorMap ta, tb;
   if (!make_tmap_2d(&ta, A, M, K, K, BM)) return -1;
   if (!make_tmap_2d(&tb, B, N, K, K, BN)) return -1;
