@@ -3,6 +3,7 @@
 // C++ exception ever crosses the ABI.
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -437,8 +438,23 @@ FRAG_API frag_status frag_kernel_gemm(const void* a, const void* b, void* c, int
     } else {
       fail(FRAG_E_CONTRACT, "unknown epilogue");
     }
+    // split-K workspace for the small-M path (process-wide; this entry point is
+    // for kernel-level tests and is serialised by the mutex)
+    static std::mutex ws_mu;
+    static DevBuf ws, cnt;
+    std::lock_guard<std::mutex> g(ws_mu);
+    if (!ws.p) {
+      ws.alloc((size_t)32 << 20);
+      cnt.alloc(16384 * sizeof(int));
+      check_cuda(cudaMemset(cnt.p, 0, cnt.bytes), "counter init");
+    }
+    ep.ws = ws.as<float>();
+    ep.ws_bytes = ws.bytes;
+    ep.counters = cnt.as<int>();
+    ep.counters_cap = (int)(cnt.bytes / sizeof(int));
     const int n = fragk::gemm_bf16_tc(static_cast<const bf16*>(a), static_cast<const bf16*>(b), M, N, K, kind, ep,
                                       static_cast<cudaStream_t>(stream), force_bn);
+    check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "gemm");
     if (n < 0) fail(FRAG_E_CONTRACT, "unsupported GEMM shape (K % 64, N % 64 and N % BN required)");
     g_launches += n;
     check_cuda(cudaPeekAtLastError(), "gemm launch");

@@ -291,6 +291,10 @@ void result_init(Result* r, Engine* e, int max_tokens) {
   r->q_tok.alloc(M * sizeof(int));
   r->scores.alloc(M * sizeof(float));
   r->row_map.alloc(M * sizeof(int));
+  // split-K workspace (small-M GEMMs) + self-resetting tile counters
+  r->gemm_ws.alloc((size_t)32 << 20);
+  r->gemm_cnt.alloc(16384 * sizeof(int));
+  check_cuda(cudaMemset(r->gemm_cnt.p, 0, r->gemm_cnt.bytes), "counter init");
   for (auto& ev : r->ev) check_cuda(cudaEventCreate(&ev), "cudaEventCreate");
   e->ensure_rope(max_tokens);
 }
@@ -310,6 +314,12 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
   const int* ptok = r->plan_tok.as<int>();
   float* h = r->h.as<float>();
   bf16* x = r->x.as<bf16>();
+  auto with_ws = [&](fragk::EpiParams& ep) {
+    ep.ws = r->gemm_ws.as<float>();
+    ep.ws_bytes = r->gemm_ws.bytes;
+    ep.counters = r->gemm_cnt.as<int>();
+    ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
+  };
 
   // split-KV policy: enough CTAs for >= 2 waves, splits of >= 256 keys
   const int G = Hq / Hkv;
@@ -345,6 +355,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     }
     {
       fragk::EpiParams ep;
+      with_ws(ep);
       ep.rows = prow;
       ep.rope = e->rope.as<float2>();
       ep.q_out = r->q.as<bf16>();
@@ -380,6 +391,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     }
     {
       fragk::EpiParams ep;
+      with_ws(ep);
       ep.resid = h;
       ep.ldo = d;
       Scoped sc(P, s, KC_GEMM, 2.0 * M * d * qc, 2.0 * (qc * d + (double)M * qc) + 8.0 * M * d);
@@ -392,6 +404,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     }
     {
       fragk::EpiParams ep;
+      with_ws(ep);
       ep.out_bf16 = r->act.as<bf16>();
       ep.ldo = F;
       Scoped sc(P, s, KC_GEMM, 2.0 * M * 2.0 * F * d, 2.0 * (2.0 * F * d + (double)M * d + (double)M * F));
@@ -399,6 +412,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     }
     {
       fragk::EpiParams ep;
+      with_ws(ep);
       ep.resid = h;
       ep.ldo = d;
       Scoped sc(P, s, KC_GEMM, 2.0 * M * (double)d * F, 2.0 * ((double)F * d + (double)M * F) + 8.0 * M * d);
@@ -415,6 +429,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       sc.launched(1);
     }
     fragk::EpiParams ep;
+    with_ws(ep);
     ep.out_f32 = r->logits.as<float>();
     ep.ldo = c.vocab;
     Scoped sc(P, s, KC_GEMM, 2.0 * n_logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
@@ -742,6 +757,10 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
       sc.launched(1);
     }
     fragk::EpiParams ep;
+    ep.ws = r->gemm_ws.as<float>();
+    ep.ws_bytes = r->gemm_ws.bytes;
+    ep.counters = r->gemm_cnt.as<int>();
+    ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
     ep.out_f32 = r->logits.as<float>();
     ep.ldo = c.vocab;
     Scoped sc(e->prof, s, KC_GEMM, 2.0 * r->logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);

@@ -34,7 +34,9 @@ constexpr int GEMM_THREADS = 192;
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  // BN=64 is the small-M (weight-streaming) shape: 4 stages so two CTAs share an SM
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 4);
+  static constexpr int MIN_BLOCKS = BN == 64 ? 2 : 1;
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BN * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -143,7 +145,7 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
 }
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, const EpiParams ep) {
   using C = GemmCfg<BN>;
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -184,13 +187,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // work item = (tile, k-split); splits > 1 only for few-tile (small-M) GEMMs,
+  // reduced deterministically by the last-arriving CTA of each tile.
+  const int splits = ep.splits > 1 ? ep.splits : 1;
+  const int num_work = num_tiles * splits;
   if (warp == 0) {
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+        const int tile = w / splits, sp = w % splits;
         const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
@@ -208,11 +217,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+      const int sp = w % splits;
+      const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < nk; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
@@ -222,10 +233,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
-            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
-          if (kb == nk - 1) umma_commit(&tfull[acc]);
+          if (kb == kb1 - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -239,35 +250,104 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = q * 32 + lane;
+    const int ws_rows = m_tiles == 1 ? M : BM;  // rows kept per split partial
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+      const int tile = w / splits, sp = w % splits;
       const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * BM + row_in_tile;
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if constexpr (EPI == EPI_SWIGLU) {
+      if (splits == 1) {
+        if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; c += 2) {
-          uint32_t r[32], r2[32];
-          tmem_ld32(t_row + c * 32, r);
-          tmem_ld32(t_row + (c + 1) * 32, r2);
-          tmem_ld_wait();
-          if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+          for (int c = 0; c < BN / 32; c += 2) {
+            uint32_t r[32], r2[32];
+            tmem_ld32(t_row + c * 32, r);
+            tmem_ld32(t_row + (c + 1) * 32, r2);
+            tmem_ld_wait();
+            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(t_row + c * 32, r);
+            tmem_ld_wait();
+            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
       } else {
+        // split partial -> workspace (fp32), TMEM released right away
+        float* wsp = ep.ws + ((size_t)(tile * splits + sp) * ws_rows + row_in_tile) * BN;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
           tmem_ld32(t_row + c * 32, r);
           tmem_ld_wait();
-          if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
+          if (row_in_tile < ws_rows) {
+            float4* dst = reinterpret_cast<float4*>(wsp + c * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) {
+          const int old = atomicAdd(&ep.counters[tile], 1);
+          *last_flag = (old == splits - 1) ? 1 : 0;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (*last_flag) {
+          // deterministic reduction in split order, then the fused epilogue
+          __threadfence();
+          const float* base = ep.ws + ((size_t)tile * splits * ws_rows + row_in_tile) * BN;
+          const size_t sstride = (size_t)ws_rows * BN;
+          if (row_in_tile < ws_rows && row < M) {
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; c += (EPI == EPI_SWIGLU ? 2 : 1)) {
+              uint32_t r[32], r2[32];
+              const int nchunk = EPI == EPI_SWIGLU ? 2 : 1;
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                if (h2 >= nchunk) break;
+                float accv[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) accv[e] = 0.f;
+                for (int s2 = 0; s2 < splits; ++s2) {
+                  const float4* src = reinterpret_cast<const float4*>(base + s2 * sstride + (c + h2) * 32);
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) {
+                    const float4 v = __ldcg(src + j);
+                    accv[4 * j] += v.x;
+                    accv[4 * j + 1] += v.y;
+                    accv[4 * j + 2] += v.z;
+                    accv[4 * j + 3] += v.w;
+                  }
+                }
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                  if (h2 == 0) r[e] = __float_as_uint(accv[e]);
+                  else r2[e] = __float_as_uint(accv[e]);
+                }
+              }
+              epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+            }
+          }
+          if (warp == 2 && lane == 0) ep.counters[tile] = 0;  // self-reset for the next GEMM
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -336,8 +416,9 @@ int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& e
   CUtensorMap ta, tb;
   if (!make_tmap_2d(&ta, A, M, K, K, BM)) return -1;
   if (!make_tmap_2d(&tb, B, N, K, K, BN)) return -1;
-  const int tiles = ((M + BM - 1) / BM) * (N / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int work = ((M + BM - 1) / BM) * (N / BN) * (ep.splits > 1 ? ep.splits : 1);
+  const int slots = num_sms() * C::MIN_BLOCKS;
+  const int grid = work < slots ? work : slots;
   gemm_tc_kernel<BN, EPI><<<grid, GEMM_THREADS, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
   return 1;
 }
@@ -392,11 +473,27 @@ int gemm_pick_bn(int M, int N, int K) {
   return best_bn;
 }
 
-int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
+int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep0,
                  cudaStream_t stream, int force_bn) {
   if (M <= 0) return 0;
   if (K % BK != 0 || N % 64 != 0) return -1;
-  const int bn = force_bn ? force_bn : gemm_pick_bn(M, N, K);
+  EpiParams ep = ep0;
+  ep.splits = 1;
+  int bn = force_bn ? force_bn : gemm_pick_bn(M, N, K);
+  if (!force_bn && M <= BM && ep.ws && ep.counters) {
+    // Weight-streaming shape (one M tile): BN=64 tiles, two CTAs per SM, and a
+    // deterministic split-K so enough CTAs stream the weights.
+    bn = 64;
+    const long tiles = N / 64, slots = 2L * num_sms(), nk = K / BK;
+    long best = -1, best_s = 1;
+    for (long s = 1; s <= 8 && s * 4 <= nk; ++s) {
+      if (tiles > ep.counters_cap) break;
+      if ((size_t)(tiles * s * M * 64) * sizeof(float) > ep.ws_bytes) break;
+      const long cost = ((tiles * s + slots - 1) / slots) * ((nk + s - 1) / s);
+      if (best < 0 || cost < best) best = cost, best_s = s;
+    }
+    ep.splits = (int)best_s;
+  }
   if (N % bn != 0) return -1;
   switch (bn) {
     case 256: return dispatch_epi<256>(A, B, M, N, K, epi, ep, stream);

@@ -35,6 +35,13 @@ struct EpiParams {
   bf16* k_cache = nullptr;         // layer base, [T][Hkv][dh]
   bf16* v_cache = nullptr;
   int Hq = 0, Hkv = 0, dh = 0;
+  // split-K workspace for small-M GEMMs (owned by the caller's result; the
+  // counters must start at zero and are left at zero by the kernel)
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  int* counters = nullptr;
+  int counters_cap = 0;
+  int splits = 1;  // set by gemm_bf16_tc
 };
 
 struct GemmTimer;  // optional per-launch event hook (bench roofline)
