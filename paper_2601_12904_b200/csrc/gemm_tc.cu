@@ -20,6 +20,7 @@
 
 #include <cstdio>
 #include <mutex>
+#include <unordered_map>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -437,6 +438,17 @@ int dispatch_epi(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
 }
 
 }  // namespace
+
+bool smem_attr_needed(const void* fn, int dev) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, unsigned long long> done;
+  std::lock_guard<std::mutex> g(mu);
+  unsigned long long& m = done[fn];
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (m & bit) return false;
+  m |= bit;
+  return true;
+}
 
 int num_sms() {
   if (g_num_sms == 0) {

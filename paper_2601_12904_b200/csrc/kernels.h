@@ -128,14 +128,13 @@ void fill_bf16(bf16* dst, size_t n, float v, cudaStream_t stream);
 namespace fragk {
 // Raise a kernel's dynamic shared-memory limit once per device (the attribute is
 // per device context; setting it on every launch costs a driver round trip).
+// Keyed by the kernel's address (instantiations share a function type).
+bool smem_attr_needed(const void* fn, int dev);  // marks (fn, dev) as done
 template <class Kernel>
 inline void smem_attr_once(Kernel* fn, int bytes) {
-  static unsigned long long done = 0;  // bit per device ordinal
   int dev = 0;
   cudaGetDevice(&dev);
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit) return;
+  if (!smem_attr_needed(reinterpret_cast<const void*>(fn), dev)) return;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  __atomic_fetch_or(&done, bit, __ATOMIC_RELEASE);
 }
 }  // namespace fragk
