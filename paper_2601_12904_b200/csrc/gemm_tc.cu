@@ -35,9 +35,8 @@ constexpr int GEMM_THREADS = 192;
 
 template <int BN>
 struct GemmCfg {
-  // BN=64 is the small-M (weight-streaming) shape: 4 stages so two CTAs share an SM
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 4);
-  static constexpr int MIN_BLOCKS = BN == 64 ? 2 : 1;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int MIN_BLOCKS = 1;
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BN * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -492,11 +491,12 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
   EpiParams ep = ep0;
   ep.splits = 1;
   int bn = force_bn ? force_bn : gemm_pick_bn(M, N, K);
-  if (!force_bn && M <= BM && ep.ws && ep.counters) {
-    // Weight-streaming shape (one M tile): BN=64 tiles, two CTAs per SM, and a
-    // deterministic split-K so enough CTAs stream the weights.
+  if (!force_bn && M <= BM && K >= 8192 && N / 64 < num_sms() && ep.ws && ep.counters) {
+    // Long-K weight-streaming shape (one M tile, few N tiles, e.g. the FFN down
+    // projection of the question pass): deterministic split-K so more CTAs
+    // stream the weights.
     bn = 64;
-    const long tiles = N / 64, slots = 2L * num_sms(), nk = K / BK;
+    const long tiles = N / 64, slots = (long)num_sms(), nk = K / BK;
     long best = -1, best_s = 1;
     for (long s = 1; s <= 8 && s * 4 <= nk; ++s) {
       if (tiles > ep.counters_cap) break;
