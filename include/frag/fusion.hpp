@@ -1,0 +1,188 @@
+// frag::fusion — C++ API of the B200 reprocessing path (RAII over frag_c.h).
+//
+// Mirrors the reference's operation surface for the online stage:
+//   ChunkStore::put_record / fetch
+//   Engine::preprocess_isolated             SPEC.md:344-352 (Eq. 5)
+//   Engine::reprocess                        stitch_full_reuse + select_query_guided +
+//                                            sparse_prefill_and_decode to the first token
+//
+//   Engine::full_prefill                     Eq. 2 Full Attention with the same kernels
+// Status codes from the C ABI are re-thrown as the reference's exception
+// classes (common.hpp:17-40): ContractError, StoreError, FormatError.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "frag/core.hpp"
+#include "frag/frag_c.h"
+
+namespace frag {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(frag_status s) {
+  if (s == FRAG_OK) return;
+  const std::string m = frag_last_error();
+  switch (s) {
+    case FRAG_E_CONTRACT: throw ContractError(m);
+    case FRAG_E_STORE: throw StoreError(m);
+    case FRAG_E_FORMAT: throw FormatError(FormatError::Kind::Malformed, m);
+    case FRAG_E_OOM: throw std::bad_alloc();
+    default: throw CudaError(m);
+  }
+}
+
+inline frag_chunk_id to_c(const ChunkId& id) {
+  frag_chunk_id c;
+  std::memcpy(c.bytes, id.bytes.data(), 16);
+  return c;
+}
+inline ChunkId from_c(const frag_chunk_id& c) {
+  ChunkId id;
+  std::memcpy(id.bytes.data(), c.bytes, 16);
+  return id;
+}
+
+inline frag_model_cfg preset(const std::string& name) {
+  frag_model_cfg c{};
+  check(frag_model_preset(name.c_str(), &c));
+  return c;
+}
+
+class ChunkStore {
+ public:
+  ChunkStore(const frag_model_cfg& cfg, int device = 0, size_t hbm_bytes = 0) {
+    check(frag_store_create(&cfg, device, hbm_bytes, &h_));
+  }
+  ~ChunkStore() { frag_store_destroy(h_); }
+  ChunkStore(const ChunkStore&) = delete;
+  ChunkStore& operator=(const ChunkStore&) = delete;
+
+  // put_record: k/v host or device [L][n][Hkv][dh] bf16 bits.
+  void put_record(const ChunkId& id, std::span<const Token> tokens, Pos native_start, const void* k_bf16,
+                  const void* v_bf16, int variant = FRAG_VARIANT_ISOLATED, bool overwrite = false) {
+    const frag_chunk_id c = to_c(id);
+    check(frag_store_put(h_, &c, tokens.data(), static_cast<int32_t>(tokens.size()), native_start, variant, k_bf16,
+                         v_bf16, overwrite ? 1 : 0));
+  }
+  // fetch: heat++, pinned until release().
+  frag_record_view fetch(const ChunkId& id) {
+    const frag_chunk_id c = to_c(id);
+    frag_record_view v{};
+    check(frag_store_fetch(h_, &c, &v));
+    return v;
+  }
+  void release(const ChunkId& id) {
+    const frag_chunk_id c = to_c(id);
+    check(frag_store_release(h_, &c));
+  }
+  size_t size() const { return static_cast<size_t>(frag_store_count(h_)); }
+  uint64_t bytes_used() const { return frag_store_bytes_used(h_); }
+  frag_store* handle() const { return h_; }
+
+ private:
+  frag_store* h_ = nullptr;
+};
+
+class Engine;
+
+// Fused KV cache + first-token logits of one request; reusable.
+class Result {
+ public:
+  Result(Engine& e, int max_tokens);
+  ~Result() { frag_result_free(h_); }
+  Result(const Result&) = delete;
+  Result& operator=(const Result&) = delete;
+
+  std::vector<float> logits() const {
+    const float* p = nullptr;
+    int32_t rows = 0, vocab = 0;
+    check(frag_result_logits(h_, &p, &rows, &vocab, 0));
+    return std::vector<float>(p, p + static_cast<size_t>(rows) * vocab);
+  }
+  Token first_token() const {  // greedy argmax of the last question row
+    const float* p = nullptr;
+    int32_t rows = 0, vocab = 0;
+    check(frag_result_logits(h_, &p, &rows, &vocab, 0));
+    const float* last = p + static_cast<size_t>(rows - 1) * vocab;
+    int32_t best = 0;
+    for (int32_t i = 1; i < vocab; ++i)
+      if (last[i] > last[best]) best = i;
+    return best;
+  }
+  std::vector<Pos> critical_positions() const {
+    const int32_t k = frag_result_crit(h_, nullptr, 0);
+    std::vector<Pos> out(k > 0 ? k : 0);
+    if (k > 0) frag_result_crit(h_, out.data(), k);
+    return out;
+  }
+  frag_timing timing() const {
+    frag_timing t{};
+    check(frag_result_timing(h_, &t));
+    return t;
+  }
+  // device pointers [L][T][Hkv][dh] bf16
+  void fused_kv(const void** k, const void** v, int32_t* tokens) const { check(frag_result_fused_kv(h_, k, v, tokens)); }
+  frag_result* handle() const { return h_; }
+
+ private:
+  frag_result* h_ = nullptr;
+};
+
+class Engine {
+ public:
+  // init_model: seeded random weights, bf16 on `device`.
+  Engine(const frag_model_cfg& cfg, int device = 0, uint64_t seed = 1234) {
+    check(frag_engine_create(&cfg, device, seed, &h_));
+  }
+  ~Engine() { frag_engine_destroy(h_); }
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  frag_model_cfg config() const {
+    frag_model_cfg c{};
+    check(frag_engine_config(h_, &c));
+    return c;
+  }
+
+  ChunkId preprocess_isolated(ChunkStore& st, std::span<const Token> chunk, std::span<const Token> system = {},
+                              bool overwrite = false) {
+    frag_chunk_id id{};
+    check(frag_preprocess_isolated(h_, st.handle(), system.data(), static_cast<int32_t>(system.size()), chunk.data(),
+                                   static_cast<int32_t>(chunk.size()), overwrite ? 1 : 0, &id));
+    return from_c(id);
+  }
+
+  // reprocess(question, chunk_ids, recompute_ratio) -> fused KV + logits
+  void reprocess(ChunkStore& st, std::span<const Token> question, std::span<const ChunkId> chunk_ids, float ratio,
+                 Result& out, std::span<const Token> system = {}, const frag_reprocess_opts* opts = nullptr,
+                 void* cuda_stream = nullptr) {
+    std::vector<frag_chunk_id> ids;
+    ids.reserve(chunk_ids.size());
+    for (const auto& c : chunk_ids) ids.push_back(to_c(c));
+    check(frag_reprocess(h_, st.handle(), system.data(), static_cast<int32_t>(system.size()), question.data(),
+                         static_cast<int32_t>(question.size()), ids.data(), static_cast<int32_t>(ids.size()), ratio,
+                         opts, cuda_stream, out.handle()));
+  }
+
+  void full_prefill(std::span<const Token> tokens, Result& out, std::span<const Token> system = {},
+                    const frag_reprocess_opts* opts = nullptr, void* cuda_stream = nullptr) {
+    check(frag_full_prefill(h_, system.data(), static_cast<int32_t>(system.size()), tokens.data(),
+                            static_cast<int32_t>(tokens.size()), opts, cuda_stream, out.handle()));
+  }
+
+  frag_engine* handle() const { return h_; }
+
+ private:
+  frag_engine* h_ = nullptr;
+};
+
+inline Result::Result(Engine& e, int max_tokens) { check(frag_result_create(e.handle(), max_tokens, &h_)); }
+
+}  // namespace frag
