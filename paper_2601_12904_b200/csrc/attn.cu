@@ -9,7 +9,6 @@ namespace fragk {
 
 namespace {
 
-constexpr int ATT_ROWS = 128;  // query rows per CTA tile (128/G tokens x G heads)
 
 // Merge split partials: out = sum_s w_s O_s / sum_s w_s, w_s = exp(lse_s - max).
 template <int DH>
@@ -37,9 +36,10 @@ int sparse_q_attention(const AttnArgs& a0, cudaStream_t stream) {
   if (a.M <= 0) return 0;
   if (a.Hkv <= 0 || a.Hq % a.Hkv != 0) return -1;
   const int G = a.Hq / a.Hkv;
-  if (ATT_ROWS % G != 0) return -1;
+  if (128 % G != 0) return -1;
   if (a.dh != 64 && a.dh != 128) return -1;
-  const int n_qblocks = (a.M + ATT_ROWS / G - 1) / (ATT_ROWS / G);
+  const int tok_per_cta = attn_rows_per_cta() / G;  // query rows per CTA = tokens x G heads
+  const int n_qblocks = (a.M + tok_per_cta - 1) / tok_per_cta;
   if (a.split_keys <= 0 || a.n_splits <= 1) a.n_splits = 1;
   if (attn_tc_launch(a, G, n_qblocks, stream) < 0) return -1;
   if (a.n_splits == 1) return 1;

@@ -323,7 +323,8 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
 
   // split-KV policy: enough CTAs for >= 2 waves, splits of >= 256 keys
   const int G = Hq / Hkv;
-  const int nqb = (M + (128 / G) - 1) / (128 / G);
+  const int tpc = fragk::attn_rows_per_cta() / G;  // tokens per attention CTA
+  const int nqb = (M + tpc - 1) / tpc;
   const long ctas = (long)nqb * Hkv;
   int n_splits = 1, split_keys = 0;
   const int sms = fragk::num_sms();

@@ -94,6 +94,7 @@ struct AttnArgs {
 };
 int sparse_q_attention(const AttnArgs& a, cudaStream_t stream);  // returns launches
 int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream);
+int attn_rows_per_cta();
 
 // ------------------------------------------------------------------ K9/K10
 struct ScoreArgs {
