@@ -67,12 +67,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint64_t* q_full = bar + 0;
   uint64_t* k_full = bar + 1;      // [2]
   uint64_t* v_full = bar + 3;      // [2]
-  uint64_t* kv_empty = bar + 5;    // [2]
+  uint64_t* pv_done = bar + 5;     // [2] per K/V stage: PV_A(j), PV_B(j) complete
   uint64_t* s_full = bar + 7;      // [QT][2]
   uint64_t* s_empty = bar + 11;    // [QT][2]
   uint64_t* p_full = bar + 15;     // [QT][2]
-  uint64_t* pv_done = bar + 19;    // [QT]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 21);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
 
   const int warp = warp_id(), lane = lane_id();
   const int qb = n_qblocks - 1 - (int)blockIdx.x;  // heaviest (latest rows) first
@@ -96,14 +95,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&pv_done[s], 1);
     }
     for (int i = 0; i < AT_QT * 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
       mbar_init(&p_full[i], 4);
     }
-    for (int t = 0; t < AT_QT; ++t) mbar_init(&pv_done[t], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -123,7 +121,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                       t0 + t * tok_per_tile);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&pv_done[st], ((j >> 1) & 1) ^ 1);  // stage free once PV(j-2) is done
         const int key0 = k_lo + j * AT_KEYS;
         mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
 #pragma unroll
@@ -159,8 +157,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
               const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, C::KV_ATOM, 1024);
               umma_bf16_ss(tmem + t * C::T_TILE + C::T_O, ad, bd, idesc_o, (j | kk) != 0);
             }
-            umma_commit(&pv_done[t]);
-            if (t == n_qt - 1) umma_commit(&kv_empty[st]);
+            // one commit per PV pair: it frees the K/V stage and P buffers (j%2)
+            // and publishes O for the softmax rescale / epilogue
+            if (t == n_qt - 1) umma_commit(&pv_done[st]);
           }
           __syncwarp();
         }
@@ -240,7 +239,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const float alpha = (grow && m_used != -INFINITY) ? ex2_approx(m_used - m_new) : 1.f;
         if (__any_sync(0xffffffffu, grow && m_used != -INFINITY) && j > 0) {
           // rescale this lane quarter's O rows in TMEM; PV(j-1) must have landed
-          mbar_wait(&pv_done[t], (j - 1) & 1);
+          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int cc = 0; cc < DH / 32; ++cc) {
@@ -255,6 +254,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
         l *= alpha;
         m_used = m_new;
+        // P buffer j%2 was last read by PV(j-2): wait for it explicitly (do not rely
+        // on commit ordering between different accumulators)
+        if (j >= 2) mbar_wait(&pv_done[st], ((j >> 1) - 1) & 1);
         // p = 2^(s*c - m): one FFMA + MUFU.EX2 per element; masked s = -inf -> 0
         const float mneg = m_used == -INFINITY ? 0.f : -m_used;
         uint8_t* prow_smem = sP + (t * 2 + st) * C::P_BYTES + r * 128;
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       // ---- epilogue
       if (n_tiles > 0) {
-        mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
+        mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
         tc_fence_after();
       }
       const float inv = l > 0.f ? 1.f / l : 0.f;
