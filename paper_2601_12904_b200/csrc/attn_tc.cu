@@ -37,6 +37,7 @@ constexpr int AT_ROWS = 128;  // rows per query tile
 constexpr int AT_QT = 2;      // query tiles per CTA
 constexpr int AT_KEYS = 64;   // keys per K/V tile
 constexpr int AT_THREADS = 320;
+constexpr int KV_STAGES = 3;  // K/V ring depth (2 tiles of prefetch)
 constexpr float RESCALE_THRESH = 8.0f;  // log2 units
 
 template <int DH>
@@ -47,7 +48,7 @@ struct AttCfg {
   static constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;        // K (or V) per stage
   static constexpr uint32_t P_BYTES = AT_ROWS * AT_KEYS * 2;    // [128][64] one atom
   static constexpr size_t SMEM =
-      1024 + AT_QT * (size_t)Q_TILE + 4 * (size_t)KV_BYTES + AT_QT * 2 * (size_t)P_BYTES + 512;
+      1024 + AT_QT * (size_t)Q_TILE + 2 * KV_STAGES * (size_t)KV_BYTES + AT_QT * 2 * (size_t)P_BYTES + 512;
   // TMEM columns per query tile: S0, S1 (64 each), O (DH)
   static constexpr uint32_t T_S0 = 0, T_S1 = 64, T_O = 128, T_TILE = 256;
 };
@@ -61,17 +62,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                          // [QT][Q_TILE]
   uint8_t* sK = sQ + AT_QT * C::Q_TILE;        // [2 stages][KV_BYTES]
-  uint8_t* sV = sK + 2 * C::KV_BYTES;          // [2 stages][KV_BYTES]
-  uint8_t* sP = sV + 2 * C::KV_BYTES;          // [QT][2 buffers][P_BYTES]
+  uint8_t* sV = sK + KV_STAGES * C::KV_BYTES;  // [stages][KV_BYTES]
+  uint8_t* sP = sV + KV_STAGES * C::KV_BYTES;  // [QT][2 buffers][P_BYTES]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sP + AT_QT * 2 * C::P_BYTES);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;      // [2]
-  uint64_t* v_full = bar + 3;      // [2]
-  uint64_t* pv_done = bar + 5;     // [2] per K/V stage: PV_A(j), PV_B(j) complete
-  uint64_t* s_full = bar + 7;      // [QT][2]
-  uint64_t* s_empty = bar + 11;    // [QT][2]
-  uint64_t* p_full = bar + 15;     // [QT][2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
+  uint64_t* k_full = bar + 1;      // [KV_STAGES]
+  uint64_t* v_full = bar + 4;      // [KV_STAGES]
+  uint64_t* pv_done = bar + 7;     // [KV_STAGES]: PV_A(j), PV_B(j) of the tile in that stage complete
+  uint64_t* s_full = bar + 10;     // [QT][2]
+  uint64_t* s_empty = bar + 14;    // [QT][2]
+  uint64_t* p_full = bar + 18;     // [QT][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
 
   const int warp = warp_id(), lane = lane_id();
   const int qb = n_qblocks - 1 - (int)blockIdx.x;  // heaviest (latest rows) first
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < KV_STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&pv_done[s], 1);
@@ -120,8 +121,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           tma_load_3d(sQ + t * C::Q_TILE + at * (AT_ROWS * 128), &tmQ, q_full, at * 64, hk * G,
                       t0 + t * tok_per_tile);
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        mbar_wait(&pv_done[st], ((j >> 1) & 1) ^ 1);  // stage free once PV(j-2) is done
+        const int st = j % KV_STAGES;
+        const int use = j / KV_STAGES;
+        mbar_wait(&pv_done[st], (use & 1) ^ 1);  // stage free once PV(j - KV_STAGES) is done
         const int key0 = k_lo + j * AT_KEYS;
         mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
 #pragma unroll
@@ -141,13 +143,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       mbar_wait(q_full, 0);
       tc_fence_after();
       auto issue_pv = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&v_full[st], (j >> 1) & 1);
+        const int st = j % KV_STAGES, pb = j & 1;
+        mbar_wait(&v_full[st], (j / KV_STAGES) & 1);
         for (int t = 0; t < n_qt; ++t) {
-          mbar_wait(&p_full[t * 2 + st], (j >> 1) & 1);
+          mbar_wait(&p_full[t * 2 + pb], (j >> 1) & 1);
           tc_fence_after();
           if (elect_one()) {
-            const uint32_t p_base = smem_u32(sP + (t * 2 + st) * C::P_BYTES);
+            const uint32_t p_base = smem_u32(sP + (t * 2 + pb) * C::P_BYTES);
             const uint32_t v_base = smem_u32(sV + st * C::KV_BYTES);
 #pragma unroll
             for (int kk = 0; kk < AT_KEYS / 16; ++kk) {
@@ -165,10 +167,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         }
       };
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
+        const int st = j % KV_STAGES, sb = j & 1;
+        mbar_wait(&k_full[st], (j / KV_STAGES) & 1);
         for (int t = 0; t < n_qt; ++t) {
-          if (j >= 2) mbar_wait(&s_empty[t * 2 + st], ((j >> 1) - 1) & 1);
+          if (j >= 2) mbar_wait(&s_empty[t * 2 + sb], ((j >> 1) - 1) & 1);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t q_base = smem_u32(sQ + t * C::Q_TILE);
@@ -177,9 +179,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             for (int kk = 0; kk < DH / 16; ++kk) {
               const uint64_t ad = umma_desc_sw128(q_base + (kk >> 2) * (AT_ROWS * 128) + (kk & 3) * 32, 16, 1024);
               const uint64_t bd = umma_desc_sw128(k_base + (kk >> 2) * C::KV_ATOM + (kk & 3) * 32, 16, 1024);
-              umma_bf16_ss(tmem + t * C::T_TILE + (st ? C::T_S1 : C::T_S0), ad, bd, idesc_s, kk != 0);
+              umma_bf16_ss(tmem + t * C::T_TILE + (sb ? C::T_S1 : C::T_S0), ad, bd, idesc_s, kk != 0);
             }
-            umma_commit(&s_full[t * 2 + st]);
+            umma_commit(&s_full[t * 2 + sb]);
           }
           __syncwarp();
         }
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const float alpha = (grow && m_used != -INFINITY) ? ex2_approx(m_used - m_new) : 1.f;
         if (__any_sync(0xffffffffu, grow && m_used != -INFINITY) && j > 0) {
           // rescale this lane quarter's O rows in TMEM; PV(j-1) must have landed
-          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          mbar_wait(&pv_done[(j - 1) % KV_STAGES], ((j - 1) / KV_STAGES) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int cc = 0; cc < DH / 32; ++cc) {
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         m_used = m_new;
         // P buffer j%2 was last read by PV(j-2): wait for it explicitly (do not rely
         // on commit ordering between different accumulators)
-        if (j >= 2) mbar_wait(&pv_done[st], ((j >> 1) - 1) & 1);
+        if (j >= 2) mbar_wait(&pv_done[(j - 2) % KV_STAGES], ((j - 2) / KV_STAGES) & 1);
         // p = 2^(s*c - m): one FFMA + MUFU.EX2 per element; masked s = -inf -> 0
         const float mneg = m_used == -INFINITY ? 0.f : -m_used;
         uint8_t* prow_smem = sP + (t * 2 + st) * C::P_BYTES + r * 128;
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       // ---- epilogue
       if (n_tiles > 0) {
-        mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+        mbar_wait(&pv_done[(n_tiles - 1) % KV_STAGES], ((n_tiles - 1) / KV_STAGES) & 1);
         tc_fence_after();
       }
       const float inv = l > 0.f ? 1.f / l : 0.f;
