@@ -7,19 +7,22 @@
 // GEMM epilogue), so stale entries are replaced and earlier critical tokens'
 // fresh K/V are visible in the same pass.
 //
-// One CTA = two 128-row query tiles (each 128/G tokens x G heads of one GQA
-// group; both share every K/V tile) x one key split. 10 warps:
-//   warp 0      TMA: both Q tiles once; K and V tiles (64 keys x dh, SW128)
+// One CTA = two 128-row query tiles A, B (each 128/G tokens x G heads of one
+// GQA group; both share every K/V tile) x one key split. 10 warps:
+//   warp 0      TMA: both Q tiles once; K and V tiles (128 keys x dh, SW128)
 //               into a 2-stage ring.
-//   warp 1      TMEM alloc (512 cols) + single-thread tcgen05.mma issue, per
-//               K/V tile j:  S_A(j), S_B(j)   = Q_t K_j^T   (M=128, N=64, K=dh)
-//                            O_A += P_A(j-1) V_{j-1},  O_B += P_B(j-1) V_{j-1}
-//               S is double-buffered per tile so S(j+1) overlaps softmax(j).
-//   warps 2-5   softmax of tile A, warps 6-9 softmax of tile B: one thread per
-//               query row (TMEM lane) -> two softmax warps per SM sub-partition.
-//               Online softmax in log2 units with lazy O rescale (> 2^8), P ->
-//               bf16 -> swizzled smem (K-major UMMA A operand); V is the
-//               MN-major B operand straight from its TMA tile.
+//   warp 1      TMEM alloc (512 cols) + single-thread tcgen05.mma issue in a
+//               ping-pong order so one tile's softmax overlaps the other
+//               tile's MMAs:
+//                 S_A(0) S_B(0) | PV_A(0) S_A(1) | PV_B(0) S_B(1) | PV_A(1) ...
+//               S_t = Q_t K^T (M=128, N=128 keys, K=dh, both operands from smem)
+//               O_t += P_t V  (M=128, N=dh, K=128 keys, P from TMEM, V MN-major smem)
+//   warps 2-5   softmax of tile A, warps 6-9 of tile B: one thread per query
+//               row (TMEM lane). tcgen05.ld S, causal mask by position, online
+//               softmax in log2 units (lazy O rescale when the max grows > 2^8),
+//               P packed bf16 and tcgen05.st back over the S columns.
+// TMEM per tile: [S | P aliased](128 cols) + O (128 cols); the in-order tensor
+// pipe orders PV_t(j)'s read of P before S_t(j+1) overwrites those columns.
 // Split-KV partials (O normalised per split + LSE) are merged by
 // attn_combine_kernel (attn.cu).
 #include <cuda.h>
@@ -35,22 +38,18 @@ namespace {
 
 constexpr int AT_ROWS = 128;  // rows per query tile
 constexpr int AT_QT = 2;      // query tiles per CTA
-constexpr int AT_KEYS = 64;   // keys per K/V tile
+constexpr int AT_KEYS = 128;  // keys per K/V tile
 constexpr int AT_THREADS = 320;
-constexpr int KV_STAGES = 3;  // K/V ring depth (2 tiles of prefetch)
 constexpr float RESCALE_THRESH = 8.0f;  // log2 units
 
 template <int DH>
 struct AttCfg {
-  static constexpr int ATOMS = DH / 64;                         // 64-column swizzle atoms per row
-  static constexpr uint32_t Q_TILE = AT_ROWS * DH * 2;          // [ATOMS][128][64]
-  static constexpr uint32_t KV_ATOM = AT_KEYS * 128;            // [64 keys][64 cols] bf16
-  static constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;        // K (or V) per stage
-  static constexpr uint32_t P_BYTES = AT_ROWS * AT_KEYS * 2;    // [128][64] one atom
-  static constexpr size_t SMEM =
-      1024 + AT_QT * (size_t)Q_TILE + 2 * KV_STAGES * (size_t)KV_BYTES + AT_QT * 2 * (size_t)P_BYTES + 512;
-  // TMEM columns per query tile: S0, S1 (64 each), O (DH)
-  static constexpr uint32_t T_S0 = 0, T_S1 = 64, T_O = 128, T_TILE = 256;
+  static constexpr int ATOMS = DH / 64;                    // 64-column swizzle atoms per row
+  static constexpr uint32_t Q_TILE = AT_ROWS * DH * 2;     // [ATOMS][128][64]
+  static constexpr uint32_t KV_ATOM = AT_KEYS * 128;       // [128 keys][64 cols] bf16
+  static constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;   // K (or V) per stage
+  static constexpr size_t SMEM = 1024 + AT_QT * (size_t)Q_TILE + 4 * (size_t)KV_BYTES + 256;
+  static constexpr uint32_t T_S = 0, T_O = 128, T_TILE = 256;  // TMEM columns per tile
 };
 
 template <int DH>
@@ -60,19 +59,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   using C = AttCfg<DH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                          // [QT][Q_TILE]
-  uint8_t* sK = sQ + AT_QT * C::Q_TILE;        // [2 stages][KV_BYTES]
-  uint8_t* sV = sK + KV_STAGES * C::KV_BYTES;  // [stages][KV_BYTES]
-  uint8_t* sP = sV + KV_STAGES * C::KV_BYTES;  // [QT][2 buffers][P_BYTES]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + AT_QT * 2 * C::P_BYTES);
+  uint8_t* sQ = smem;                       // [QT][Q_TILE]
+  uint8_t* sK = sQ + AT_QT * C::Q_TILE;     // [2 stages][KV_BYTES]
+  uint8_t* sV = sK + 2 * C::KV_BYTES;       // [2 stages][KV_BYTES]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * C::KV_BYTES);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;      // [KV_STAGES]
-  uint64_t* v_full = bar + 4;      // [KV_STAGES]
-  uint64_t* pv_done = bar + 7;     // [KV_STAGES]: PV_A(j), PV_B(j) of the tile in that stage complete
-  uint64_t* s_full = bar + 10;     // [QT][2]
-  uint64_t* s_empty = bar + 14;    // [QT][2]
-  uint64_t* p_full = bar + 18;     // [QT][2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* v_full = bar + 3;    // [2]
+  uint64_t* kv_empty = bar + 5;  // [2]
+  uint64_t* s_full = bar + 7;    // [QT]
+  uint64_t* p_full = bar + 9;    // [QT]
+  uint64_t* pv_done = bar + 11;  // [QT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
   const int warp = warp_id(), lane = lane_id();
   const int qb = n_qblocks - 1 - (int)blockIdx.x;  // heaviest (latest rows) first
@@ -93,15 +91,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < KV_STAGES; ++s) {
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
-      mbar_init(&pv_done[s], 1);
+      mbar_init(&kv_empty[s], 1);
     }
-    for (int i = 0; i < AT_QT * 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-      mbar_init(&p_full[i], 4);
+    for (int t = 0; t < AT_QT; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 4);
+      mbar_init(&pv_done[t], 1);
     }
     fence_mbar_init();
   }
@@ -121,9 +119,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           tma_load_3d(sQ + t * C::Q_TILE + at * (AT_ROWS * 128), &tmQ, q_full, at * 64, hk * G,
                       t0 + t * tok_per_tile);
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % KV_STAGES;
-        const int use = j / KV_STAGES;
-        mbar_wait(&pv_done[st], (use & 1) ^ 1);  // stage free once PV(j - KV_STAGES) is done
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);  // PV(j-2) done with this stage
         const int key0 = k_lo + j * AT_KEYS;
         mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
 #pragma unroll
@@ -141,53 +138,49 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       constexpr uint32_t idesc_s = umma_idesc_bf16(AT_ROWS, AT_KEYS, 0, 0);
       constexpr uint32_t idesc_o = umma_idesc_bf16(AT_ROWS, DH, 0, 1);
       mbar_wait(q_full, 0);
-      tc_fence_after();
-      auto issue_pv = [&](int j) {
-        const int st = j % KV_STAGES, pb = j & 1;
-        mbar_wait(&v_full[st], (j / KV_STAGES) & 1);
-        for (int t = 0; t < n_qt; ++t) {
-          mbar_wait(&p_full[t * 2 + pb], (j >> 1) & 1);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t p_base = smem_u32(sP + (t * 2 + pb) * C::P_BYTES);
-            const uint32_t v_base = smem_u32(sV + st * C::KV_BYTES);
+      auto issue_s = [&](int t, int j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t q_base = smem_u32(sQ + t * C::Q_TILE);
+          const uint32_t k_base = smem_u32(sK + st * C::KV_BYTES);
 #pragma unroll
-            for (int kk = 0; kk < AT_KEYS / 16; ++kk) {
-              const uint64_t ad = umma_desc_sw128(p_base + kk * 32, 16, 1024);
-              // V tile [64 keys][64-dh atoms], MN-major: K step = 16 key rows = 2048 B,
-              // next 64-wide dh atom at LBO = 64 keys * 128 B.
-              const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, C::KV_ATOM, 1024);
-              umma_bf16_ss(tmem + t * C::T_TILE + C::T_O, ad, bd, idesc_o, (j | kk) != 0);
-            }
-            // one commit per PV pair: it frees the K/V stage and P buffers (j%2)
-            // and publishes O for the softmax rescale / epilogue
-            if (t == n_qt - 1) umma_commit(&pv_done[st]);
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * (AT_ROWS * 128) + (kk & 3) * 32;  // Q/K atoms are 128 rows
+            umma_bf16_ss(tmem + t * C::T_TILE + C::T_S, umma_desc_sw128(q_base + off, 16, 1024),
+                         umma_desc_sw128(k_base + off, 16, 1024), idesc_s, kk != 0);
           }
-          __syncwarp();
+          umma_commit(&s_full[t]);
         }
+        __syncwarp();
       };
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % KV_STAGES, sb = j & 1;
-        mbar_wait(&k_full[st], (j / KV_STAGES) & 1);
-        for (int t = 0; t < n_qt; ++t) {
-          if (j >= 2) mbar_wait(&s_empty[t * 2 + sb], ((j >> 1) - 1) & 1);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t q_base = smem_u32(sQ + t * C::Q_TILE);
-            const uint32_t k_base = smem_u32(sK + st * C::KV_BYTES);
+      auto issue_pv = [&](int t, int j) {
+        const int st = j & 1;
+        mbar_wait(&p_full[t], j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t v_base = smem_u32(sV + st * C::KV_BYTES);
 #pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk) {
-              const uint64_t ad = umma_desc_sw128(q_base + (kk >> 2) * (AT_ROWS * 128) + (kk & 3) * 32, 16, 1024);
-              const uint64_t bd = umma_desc_sw128(k_base + (kk >> 2) * C::KV_ATOM + (kk & 3) * 32, 16, 1024);
-              umma_bf16_ss(tmem + t * C::T_TILE + (sb ? C::T_S1 : C::T_S0), ad, bd, idesc_s, kk != 0);
-            }
-            umma_commit(&s_full[t * 2 + sb]);
+          for (int kk = 0; kk < AT_KEYS / 16; ++kk) {
+            // P: 16 keys = 8 packed bf16x2 TMEM columns; V: 16 key rows = 2048 B,
+            // MN-major, next 64-wide dh atom at LBO = 128 keys * 128 B
+            umma_bf16_ts(tmem + t * C::T_TILE + C::T_O, tmem + t * C::T_TILE + C::T_S + kk * 8,
+                         umma_desc_sw128(v_base + kk * 2048, C::KV_ATOM, 1024), idesc_o, (j | kk) != 0);
           }
-          __syncwarp();
+          umma_commit(&pv_done[t]);
+          if (t == n_qt - 1) umma_commit(&kv_empty[st]);
         }
-        if (j >= 1) issue_pv(j - 1);
+        __syncwarp();
+      };
+      for (int t = 0; t < n_qt; ++t) issue_s(t, 0);
+      for (int j = 0; j < n_tiles; ++j) {
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        for (int t = 0; t < n_qt; ++t) {
+          issue_pv(t, j);
+          if (j + 1 < n_tiles) issue_s(t, j + 1);
+        }
       }
-      issue_pv(n_tiles - 1);
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
@@ -203,22 +196,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const int p_min = a.rows[t0 + t * tok_per_tile];
       const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16) + t * C::T_TILE;
       const float c = a.scale * 1.4426950408889634f;
-      uint64_t* sf = s_full + t * 2;
-      uint64_t* se = s_empty + t * 2;
-      uint64_t* pf = p_full + t * 2;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
         const int key0 = k_lo + j * AT_KEYS;
-        mbar_wait(&sf[st], (j >> 1) & 1);
+        mbar_wait(&s_full[t], j & 1);
         tc_fence_after();
         uint32_t s[AT_KEYS];
-        tmem_ld32(lane_base + (st ? C::T_S1 : C::T_S0), *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        tmem_ld32(lane_base + (st ? C::T_S1 : C::T_S0) + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+#pragma unroll
+        for (int cc = 0; cc < AT_KEYS / 32; ++cc)
+          tmem_ld32(lane_base + C::T_S + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[cc * 32]));
         tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&se[st]);
         // causal mask by position (keys > p_row or beyond the split), raw scores
         const int lim = min(prow, k_hi - 1) - key0;
         if ((key0 + AT_KEYS - 1 > p_min) || (key0 + AT_KEYS > k_hi)) {
@@ -240,8 +227,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const float m_new = grow ? fmaxf(mt, m_used) : m_used;
         const float alpha = (grow && m_used != -INFINITY) ? ex2_approx(m_used - m_new) : 1.f;
         if (__any_sync(0xffffffffu, grow && m_used != -INFINITY) && j > 0) {
-          // rescale this lane quarter's O rows in TMEM; PV(j-1) must have landed
-          mbar_wait(&pv_done[(j - 1) % KV_STAGES], ((j - 1) / KV_STAGES) & 1);
+          // rescale this lane quarter's O rows in TMEM; PV_t(j-1) must have landed
+          mbar_wait(&pv_done[t], (j - 1) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int cc = 0; cc < DH / 32; ++cc) {
@@ -252,41 +239,36 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
             tmem_st32(lane_base + C::T_O + cc * 32, o);
           }
-          tmem_st_wait();
         }
         l *= alpha;
         m_used = m_new;
-        // P buffer j%2 was last read by PV(j-2): wait for it explicitly (do not rely
-        // on commit ordering between different accumulators)
-        if (j >= 2) mbar_wait(&pv_done[(j - 2) % KV_STAGES], ((j - 2) / KV_STAGES) & 1);
-        // p = 2^(s*c - m): one FFMA + MUFU.EX2 per element; masked s = -inf -> 0
+        // p = 2^(s*c - m): one FFMA + MUFU.EX2 per element; masked s = -inf -> 0.
+        // P (bf16 pairs) overwrites the first 64 S columns of this tile.
         const float mneg = m_used == -INFINITY ? 0.f : -m_used;
-        uint8_t* prow_smem = sP + (t * 2 + st) * C::P_BYTES + r * 128;
         float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int ch = 0; ch < AT_KEYS / 8; ++ch) {
-          float p[8];
+        for (int half = 0; half < 2; ++half) {
+          uint32_t pk[32];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = ex2_approx(__fmaf_rn(__uint_as_float(s[ch * 8 + e]), c, mneg));
-            rs8[e] += p[e];
+          for (int e = 0; e < 32; ++e) {
+            const int k = half * 64 + 2 * e;
+            const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(s[k]), c, mneg));
+            const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(s[k + 1]), c, mneg));
+            rs8[(2 * e) & 7] += p0;
+            rs8[(2 * e + 1) & 7] += p1;
+            pk[e] = pack_bf16(p0, p1);
           }
-          uint4 pk;
-          pk.x = pack_bf16(p[0], p[1]);
-          pk.y = pack_bf16(p[2], p[3]);
-          pk.z = pack_bf16(p[4], p[5]);
-          pk.w = pack_bf16(p[6], p[7]);
-          *reinterpret_cast<uint4*>(prow_smem + ((ch ^ (r & 7)) << 4)) = pk;
+          tmem_st32(lane_base + C::T_S + half * 32, pk);
         }
         l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-        fence_async_smem();
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&pf[st]);
+        if (lane == 0) mbar_arrive(&p_full[t]);
       }
       // ---- epilogue
       if (n_tiles > 0) {
-        mbar_wait(&pv_done[(n_tiles - 1) % KV_STAGES], ((n_tiles - 1) / KV_STAGES) & 1);
+        mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
         tc_fence_after();
       }
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -344,7 +326,7 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   CUtensorMap tq, tk, tv;
   // Q [M][Hq][dh] viewed as (dh, Hq, M); box (64, G, 128/G)
   if (!make_tmap_3d(&tq, a.q, a.dh, a.Hq, a.M, a.dh, (uint64_t)a.Hq * a.dh, 64, G, AT_ROWS / G)) return -1;
-  // K/V layer [T][Hkv*dh]; box (64, 64 keys)
+  // K/V layer [T][Hkv*dh]; box (64, 128 keys)
   if (!make_tmap_2d(&tk, a.k, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
   if (!make_tmap_2d(&tv, a.v, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
   dim3 grid(n_qblocks, a.Hkv, a.n_splits);
