@@ -187,18 +187,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // work item = (tile, k-split); splits > 1 only for few-tile (small-M) GEMMs,
-  // reduced deterministically by the last-arriving CTA of each tile.
+  // work items: the first `full` tiles whole, then the remaining (tail) tiles
+  // each cut into `splits` K ranges, reduced deterministically by the
+  // last-arriving CTA of each tail tile (split-K for the last partial wave and
+  // for few-tile small-M GEMMs).
   const int splits = ep.splits > 1 ? ep.splits : 1;
-  const int num_work = num_tiles * splits;
+  const int n_full = splits > 1 ? ep.full_tiles : num_tiles;
+  const int num_work = n_full + (num_tiles - n_full) * splits;
+  auto decode = [&](int w, int& tile, int& sp, int& S) {
+    if (w < n_full) {
+      tile = w, sp = 0, S = 1;
+    } else {
+      const int u = w - n_full;
+      tile = n_full + u / splits, sp = u % splits, S = splits;
+    }
+  };
   if (warp == 0) {
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
-        const int tile = w / splits, sp = w % splits;
+        int tile, sp, S;
+        decode(w, tile, sp, S);
         const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
-        const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
+        const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -218,8 +230,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
-      const int sp = w % splits;
-      const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
+      int tile, sp, S;
+      decode(w, tile, sp, S);
+      const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -254,13 +267,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
-      const int tile = w / splits, sp = w % splits;
+      int tile, sp, S;
+      decode(w, tile, sp, S);
       const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
+      const int ti = tile - n_full;  // tail index (workspace / counter slot)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * BM + row_in_tile;
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (splits == 1) {
+      if (S == 1) {
         if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
           for (int c = 0; c < BN / 32; c += 2) {
@@ -284,7 +299,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
         if (lane == 0) mbar_arrive(&tempty[acc]);
       } else {
         // split partial -> workspace (fp32), TMEM released right away
-        float* wsp = ep.ws + ((size_t)(tile * splits + sp) * ws_rows + row_in_tile) * BN;
+        float* wsp = ep.ws + ((size_t)(ti * S + sp) * ws_rows + row_in_tile) * BN;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
@@ -304,14 +319,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (warp == 2 && lane == 0) {
-          const int old = atomicAdd(&ep.counters[tile], 1);
-          *last_flag = (old == splits - 1) ? 1 : 0;
+          const int old = atomicAdd(&ep.counters[ti], 1);
+          *last_flag = (old == S - 1) ? 1 : 0;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (*last_flag) {
           // deterministic reduction in split order, then the fused epilogue
           __threadfence();
-          const float* base = ep.ws + ((size_t)tile * splits * ws_rows + row_in_tile) * BN;
+          const float* base = ep.ws + ((size_t)ti * S * ws_rows + row_in_tile) * BN;
           const size_t sstride = (size_t)ws_rows * BN;
           if (row_in_tile < ws_rows && row < M) {
 #pragma unroll 1
@@ -324,7 +339,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
                 float accv[32];
 #pragma unroll
                 for (int e = 0; e < 32; ++e) accv[e] = 0.f;
-                for (int s2 = 0; s2 < splits; ++s2) {
+                for (int s2 = 0; s2 < S; ++s2) {
                   const float4* src = reinterpret_cast<const float4*>(base + s2 * sstride + (c + h2) * 32);
 #pragma unroll
                   for (int j = 0; j < 8; ++j) {
@@ -344,7 +359,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
               epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
             }
           }
-          if (warp == 2 && lane == 0) ep.counters[tile] = 0;  // self-reset for the next GEMM
+          if (warp == 2 && lane == 0) ep.counters[ti] = 0;  // self-reset for the next GEMM
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
@@ -416,7 +431,8 @@ int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& e
   CUtensorMap ta, tb;
   if (!make_tmap_2d(&ta, A, M, K, K, BM)) return -1;
   if (!make_tmap_2d(&tb, B, N, K, K, BN)) return -1;
-  const int work = ((M + BM - 1) / BM) * (N / BN) * (ep.splits > 1 ? ep.splits : 1);
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int slots = num_sms() * C::MIN_BLOCKS;
   const int grid = work < slots ? work : slots;
   gemm_tc_kernel<BN, EPI><<<grid, GEMM_THREADS, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
@@ -462,30 +478,42 @@ int num_sms() {
 // Pick the N tile: maximise useful MMA work per wave while keeping tiles wide
 // enough to stay under the shared-memory bandwidth bound (BN=256 moves 96 B/clk
 // per SM at full MMA rate, BN=128 128 B/clk, BN=64 192 B/clk).
+namespace {
+// Tail split for the last partial wave: S K-ranges per leftover tile so the
+// leftover tiles occupy (about) one full wave of SMs.
+int tail_splits(long tiles, long sms, long nk) {
+  const long rem = tiles % sms;
+  if (rem == 0) return 1;
+  long s = sms / rem;
+  if (s > 8) s = 8;
+  while (s > 1 && nk / s < 4) --s;
+  return (int)(s < 1 ? 1 : s);
+}
+}  // namespace
+
+// Pick the N tile. Policy measured on B200 with tools/gemm_tune.py
+// (profiles/gemm_tune_r01.txt): weight-streaming small-M GEMMs want many CTAs
+// (BN=64, BN=128 for very wide N); at M~2.5k BN=128 wins for the N=4k/6k
+// projections and BN=256 for the wide gate/up; long-K (down projection) wants
+// BN=128 with the tail wave split along K; large M (full prefill) wants BN=256.
 int gemm_pick_bn(int M, int N, int K) {
-  (void)K;
-  const int sms = num_sms();
   const int m_tiles = (M + BM - 1) / BM;
-  double best = 1e30;
-  int best_bn = 64;
-  const int cands[3] = {256, 128, 64};
-  const double eff[3] = {1.0, 0.92, 0.70};
-  for (int i = 0; i < 3; ++i) {
-    const int bn = cands[i];
-    if (N % bn) continue;
-    const long tiles = (long)m_tiles * (N / bn);
-    const long waves = (tiles + sms - 1) / sms;
-    const double t = (double)waves * bn / eff[i];
-    if (t < best - 1e-9) {
-      best = t;
-      best_bn = bn;
-    }
-  }
-  return best_bn;
+  int bn;
+  if (M <= BM) bn = N >= 16384 ? 128 : 64;
+  else if (m_tiles >= 64) bn = 256;
+  else if (K >= 8192) bn = 128;
+  else if (N >= 16384) bn = 256;
+  else bn = 128;
+  while (bn > 64 && N % bn) bn >>= 1;
+  return bn;
 }
 
 int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep0,
-                 cudaStream_t stream, int force_bn) {
+                 cudaStream_t stream, int force_bn_flags) {
+  // force_bn_flags: 0 = automatic; else BN in the low 16 bits (64/128/256),
+  // bit 16 = still allow the tail split-K, bit 17 = forbid it (tuning only)
+  const int force_bn = force_bn_flags & 0xffff;
+  const bool tail_ok = force_bn ? (force_bn_flags & 0x10000) != 0 : (force_bn_flags & 0x20000) == 0;
   if (M <= 0) return 0;
   if (K % BK != 0 || N % 64 != 0) return -1;
   EpiParams ep = ep0;
@@ -505,8 +533,20 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
       if (best < 0 || cost < best) best = cost, best_s = s;
     }
     ep.splits = (int)best_s;
+    ep.full_tiles = 0;
   }
   if (N % bn != 0) return -1;
+  if (ep.splits == 1 && tail_ok && M > BM && (M + BM - 1) / BM < 64 && K >= 8192 && ep.ws && ep.counters) {
+    // split-K only the last partial wave (deterministic last-CTA reduction)
+    const long tiles = (long)((M + BM - 1) / BM) * (N / bn), sms = num_sms();
+    const int s = tail_splits(tiles, sms, K / BK);
+    const long tail = tiles % sms;
+    if (s > 1 && tail <= ep.counters_cap &&
+        (size_t)tail * s * BM * bn * sizeof(float) <= ep.ws_bytes) {
+      ep.splits = s;
+      ep.full_tiles = (int)(tiles - tail);
+    }
+  }
   switch (bn) {
     case 256: return dispatch_epi<256>(A, B, M, N, K, epi, ep, stream);
     case 128: return dispatch_epi<128>(A, B, M, N, K, epi, ep, stream);

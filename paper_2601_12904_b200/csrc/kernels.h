@@ -41,7 +41,8 @@ struct EpiParams {
   size_t ws_bytes = 0;
   int* counters = nullptr;
   int counters_cap = 0;
-  int splits = 1;  // set by gemm_bf16_tc
+  int splits = 1;      // set by gemm_bf16_tc: K splits of each tail tile
+  int full_tiles = 0;  // tiles before the split tail
 };
 
 struct GemmTimer;  // optional per-launch event hook (bench roofline)
