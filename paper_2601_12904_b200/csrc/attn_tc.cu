@@ -41,8 +41,6 @@ constexpr int AT_QT = 2;      // query tiles per CTA
 constexpr int AT_KEYS = 128;  // keys per K/V tile
 constexpr int AT_THREADS = 320;
 constexpr float RESCALE_THRESH = 8.0f;  // log2 units
-constexpr int K_STAGES = 3;  // K ring: S MMAs run a tile ahead of PV, so K is prefetched deeper
-constexpr int V_STAGES = 2;
 
 template <int DH>
 struct AttCfg {
@@ -50,8 +48,9 @@ struct AttCfg {
   static constexpr uint32_t Q_TILE = AT_ROWS * DH * 2;     // [ATOMS][128][64]
   static constexpr uint32_t KV_ATOM = AT_KEYS * 128;       // [128 keys][64 cols] bf16
   static constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;   // K (or V) per stage
-  static constexpr size_t SMEM = 1024 + AT_QT * (size_t)Q_TILE + (K_STAGES + V_STAGES) * (size_t)KV_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + AT_QT * (size_t)Q_TILE + 4 * (size_t)KV_BYTES + 256;
   static constexpr uint32_t T_S = 0, T_O = 128, T_TILE = 256;  // TMEM columns per tile
+  static_assert(SMEM <= 232448, "attention tile exceeds the 227 KB shared-memory limit");
 };
 
 template <int DH>
@@ -62,19 +61,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                       // [QT][Q_TILE]
-  uint8_t* sK = sQ + AT_QT * C::Q_TILE;     // [K_STAGES][KV_BYTES]
-  uint8_t* sV = sK + K_STAGES * C::KV_BYTES;  // [V_STAGES][KV_BYTES]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + V_STAGES * C::KV_BYTES);
+  uint8_t* sK = sQ + AT_QT * C::Q_TILE;     // [2 stages][KV_BYTES]
+  uint8_t* sV = sK + 2 * C::KV_BYTES;       // [2 stages][KV_BYTES]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * C::KV_BYTES);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;    // [K_STAGES]
-  uint64_t* k_empty = bar + 4;   // [K_STAGES]
-  uint64_t* v_full = bar + 7;    // [V_STAGES]
-  uint64_t* v_empty = bar + 9;   // [V_STAGES]
-  uint64_t* s_full = bar + 11;   // [QT]
-  uint64_t* p_full = bar + 13;   // [QT]
-  uint64_t* pv_done = bar + 15;  // [QT]
-  uint64_t* turn = bar + 17;     // [QT] softmax ping-pong: turn[t] completes when the other tile's softmax is done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* v_full = bar + 3;    // [2]
+  uint64_t* kv_empty = bar + 5;  // [2]
+  uint64_t* s_full = bar + 7;    // [QT]
+  uint64_t* p_full = bar + 9;    // [QT]
+  uint64_t* pv_done = bar + 11;  // [QT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
   const int warp = warp_id(), lane = lane_id();
   const int qb = n_qblocks - 1 - (int)blockIdx.x;  // heaviest (latest rows) first
@@ -99,19 +96,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < K_STAGES; ++s) {
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < V_STAGES; ++s) {
       mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
+      mbar_init(&kv_empty[s], 1);
     }
     for (int t = 0; t < AT_QT; ++t) {
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 4);
       mbar_init(&pv_done[t], 1);
-      mbar_init(&turn[t], 4);
     }
     fence_mbar_init();
   }
@@ -123,8 +116,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 
   if (warp == W_TMA) {
     // ------------------------------------------------------------ TMA producer
-    // lane 0 streams Q and the K ring, lane 1 the V ring (independent queues)
-    if (n_tiles > 0 && lane == 0) {
+    if (n_tiles > 0 && elect_one()) {
       mbar_arrive_expect_tx(q_full, n_qt * C::Q_TILE);
       for (int t = 0; t < n_qt; ++t)
 #pragma unroll
@@ -132,23 +124,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           tma_load_3d(sQ + t * C::Q_TILE + at * (AT_ROWS * 128), &tmQ, q_full, at * 64, hk * G,
                       t0 + t * tok_per_tile);
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % K_STAGES;
-        mbar_wait(&k_empty[st], ((j / K_STAGES) & 1) ^ 1);  // S(j - K_STAGES) done with this slot
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);  // PV(j-2) done with this stage
+        const int key0 = k_lo + j * AT_KEYS;
         mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
 #pragma unroll
         for (int at = 0; at < C::ATOMS; ++at)
-          tma_load_2d(sK + st * C::KV_BYTES + at * C::KV_ATOM, &tmK, &k_full[st], hk * DH + at * 64,
-                      k_lo + j * AT_KEYS);
-      }
-    } else if (n_tiles > 0 && lane == 1) {
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % V_STAGES;
-        mbar_wait(&v_empty[st], ((j / V_STAGES) & 1) ^ 1);  // PV(j - V_STAGES) done with this slot
+          tma_load_2d(sK + st * C::KV_BYTES + at * C::KV_ATOM, &tmK, &k_full[st], hk * DH + at * 64, key0);
         mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
 #pragma unroll
         for (int at = 0; at < C::ATOMS; ++at)
-          tma_load_2d(sV + st * C::KV_BYTES + at * C::KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64,
-                      k_lo + j * AT_KEYS);
+          tma_load_2d(sV + st * C::KV_BYTES + at * C::KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64, key0);
       }
     }
   } else if (warp == W_MMA) {
@@ -162,8 +148,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const uint64_t dk = umma_desc_sw128(smem_u32(sK), 16, 1024);
       const uint64_t dv = umma_desc_sw128(smem_u32(sV), C::KV_ATOM, 1024);
       auto issue_s = [&](int t, int j) {
-        const int st = j % K_STAGES;
-        mbar_wait(&k_full[st], (j / K_STAGES) & 1);
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t q0 = dq + ((t * C::Q_TILE) >> 4);
@@ -175,12 +161,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             umma_bf16_ss(d_tmem, q0 + off, k0 + off, idesc_s, kk != 0);
           }
           umma_commit(&s_full[t]);
-          if (t == n_qt - 1) umma_commit(&k_empty[st]);
         }
         __syncwarp();
       };
       auto issue_pv = [&](int t, int j) {
-        const int st = j % V_STAGES;
+        const int st = j & 1;
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
         if (elect_one()) {
@@ -194,13 +179,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             umma_bf16_ts(d_tmem, p_tmem + kk * 8, v0 + ((kk * 2048) >> 4), idesc_o, (j | kk) != 0);
           }
           umma_commit(&pv_done[t]);
-          if (t == n_qt - 1) umma_commit(&v_empty[st]);
+          if (t == n_qt - 1) umma_commit(&kv_empty[st]);
         }
         __syncwarp();
       };
       for (int t = 0; t < n_qt; ++t) issue_s(t, 0);
       for (int j = 0; j < n_tiles; ++j) {
-        mbar_wait(&v_full[j % V_STAGES], (j / V_STAGES) & 1);
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
         for (int t = 0; t < n_qt; ++t) {
           issue_pv(t, j);
           if (j + 1 < n_tiles) issue_s(t, j + 1);
@@ -247,9 +232,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(mx8[e], __uint_as_float(s[k + e]));
         const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * c;
-        // Strict ping-pong of the two softmax groups (A(0) B(0) A(1) B(1) ...): each
-        // runs alone on the SFUs while the tensor pipe works on the other tile.
-        if (n_qt == 2 && (t == 1 || j > 0)) mbar_wait(&turn[t], (t == 0 ? j - 1 : j) & 1);
         // lazy rescale: only when the max grows by more than 2^8
         const bool grow = mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt != -INFINITY);
         const float m_new = grow ? fmaxf(mt, m_used) : m_used;
@@ -292,10 +274,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&p_full[t]);
-          if (n_qt == 2) mbar_arrive(&turn[t ^ 1]);
-        }
+        if (lane == 0) mbar_arrive(&p_full[t]);
       }
       // ---- epilogue
       if (n_tiles > 0) {
@@ -370,7 +349,7 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   } else {
     return -1;
   }
-  return 1;
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace fragk

@@ -42,6 +42,7 @@ struct GemmCfg {
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static_assert(SMEM <= 232448, "GEMM pipeline exceeds the 227 KB shared-memory limit");
 };
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
@@ -436,7 +437,7 @@ int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& e
   const int slots = num_sms() * C::MIN_BLOCKS;
   const int grid = work < slots ? work : slots;
   gemm_tc_kernel<BN, EPI><<<grid, GEMM_THREADS, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
-  return 1;
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 template <int BN>

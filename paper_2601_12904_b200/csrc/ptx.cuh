@@ -179,6 +179,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------- bf16 / misc
@@ -194,6 +202,22 @@ __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe: round-to-nearest split x = i + f (f in [-0.5, 0.5]) via
+// the 1.5*2^23 magic constant, cubic for 2^f (rel. error < 1e-4, below bf16
+// resolution of P), exponent added in the integer domain. x <= 0 expected;
+// clamped at -126 (2^-126 ~ 1e-38 stands in for 0 of masked keys).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: low mantissa bits = round(x)
+  const float xi = t - 12582912.0f;
+  const float f = x - xi;
+  float p = __fmaf_rn(0.05550411f, f, 0.24022652f);
+  p = __fmaf_rn(p, f, 0.69314718f);
+  p = __fmaf_rn(p, f, 1.0f);
+  const int i = __float_as_int(t) - 0x4B400000;
+  return __int_as_float(__float_as_int(p) + (i << 23));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
