@@ -134,3 +134,26 @@ def test_rope_shift_bit_exact(cuda, delta):
     got = dst.cpu().numpy().view(np.uint16)
     exp = kbits if delta == 0 else _rope_shift_ref(kbits, float(delta), 1e4)
     assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 512, 256), (2490, 1024, 4096), (1000, 768, 512)])
+@pytest.mark.parametrize("bn", [128, 256])
+def test_gemm_cta_pair_vs_torch(cuda, M, N, K, bn):
+    """cta_group::2 GEMM (256-row tiles shared by a CTA pair)."""
+    import torch
+    if N % bn:
+        pytest.skip("N not a multiple of BN")
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + bn)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device=cuda, generator=g).to(torch.bfloat16)
+    ref = a.double() @ b.double().T
+    c = torch.empty(M, N, device=cuda, dtype=torch.float32)
+    _gemm(a, b, c, 1, bn | 0x40000)
+    torch.cuda.synchronize()
+    err = (c.double() - ref).abs().max().item()
+    assert err <= 2e-5 * math.sqrt(K) * ref.abs().max().item() + 1e-4, err
+    r0 = torch.randn(M, N, device=cuda, generator=g)
+    r = r0.clone()
+    _gemm(a, b, r, 2, bn | 0x40000)
+    torch.cuda.synchronize()
+    assert torch.allclose(r, r0 + c, rtol=0, atol=1e-4 * ref.abs().max().item() + 1e-5)
