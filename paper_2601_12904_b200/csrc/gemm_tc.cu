@@ -106,18 +106,37 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
   };
   if (warp == 0) {
     if (elect_one()) {
-      int stage = 0;
+      pdl_launch_dependents();
+      // Weights (B) do not depend on the preceding kernel: issue the first
+      // stages' B loads before waiting on it (programmatic dependent launch),
+      // then the activation (A) loads once its output is visible.
+      int npre = 0;
+      if ((int)blockIdx.x < num_work) {
+        int tile, sp, S;
+        decode(blockIdx.x, tile, sp, S);
+        const int n_blk = tile / m_tiles;
+        const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
+        npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
+        for (int i = 0; i < npre; ++i) {
+          mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+          tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
+        }
+      }
+      pdl_wait();
+      int stage = 0, it = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
         int tile, sp, S;
         decode(w, tile, sp, S);
         const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
         const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          if (it >= npre) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+          }
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -163,6 +182,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
       if (acc == 0) acc_phase ^= 1;
     }
   } else {
+    pdl_wait();  // the epilogue reads/writes buffers of the preceding kernels
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = q * 32 + lane;
     const int ws_rows = m_tiles == 1 ? M : BM;  // rows kept per split partial
@@ -337,7 +357,7 @@ int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& e
   const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int slots = num_sms() * C::MIN_BLOCKS;
   const int grid = work < slots ? work : slots;
-  gemm_tc_kernel<BN, EPI><<<grid, GEMM_THREADS, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
+  launch_pdl(gemm_tc_kernel<BN, EPI>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -133,19 +133,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      int stage = 0;
+      pdl_launch_dependents();
+      // weight (B) loads of the first stages go out before the dependency wait
+      int npre = 0;
+      if (pair < num_tiles) {
+        const int n_blk = pair / m_tiles;
+        npre = nk < STAGES ? nk : STAGES;
+        for (int i = 0; i < npre; ++i) {
+          const uint32_t fb = smem_u32(&full[i]) & PEER_MASK;
+          if (leader)
+            mbar_arrive_expect_tx(&full[i], 2 * C::STAGE_BYTES);
+          else
+            mbar_arrive_cluster(fb);
+          tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, fb, i * BK2, n_blk * BN + rank * (BN / 2));
+        }
+      }
+      pdl_wait();
+      int stage = 0, it = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < num_tiles; tile += n_pairs) {
         const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
-          if (leader)
-            mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          else
-            mbar_arrive_cluster(fb);
+          if (it >= npre) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            else
+              mbar_arrive_cluster(fb);
+            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK2, n_blk * BN + rank * (BN / 2));
+          }
           tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK2, m_blk * BM2 + rank * 128);
-          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK2, n_blk * BN + rank * (BN / 2));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -188,6 +206,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
       }
     }
   } else {
+    pdl_wait();  // the epilogue reads/writes buffers of the preceding kernels
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = q * 32 + lane;
     const uint32_t te_leader = smem_u32(tempty) & PEER_MASK;
@@ -242,7 +261,7 @@ int launch2(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& 
   const int tiles = ((M + BM2 - 1) / BM2) * (N / BN);
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  gemm_tc2_kernel<BN, EPI><<<grid, GEMM2_THREADS, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
+  launch_pdl(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(GEMM2_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -3,6 +3,7 @@
 // never synchronises. Kernel numbering (K1..K11) follows SURVEY.md §2.2.
 #pragma once
 #include <cstddef>
+#include <utility>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -131,6 +132,25 @@ void fill_bf16(bf16* dst, size_t n, float v, cudaStream_t stream);
 }  // namespace fragk
 
 namespace fragk {
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while the previous one drains; it must griddepcontrol.wait before touching
+// that kernel's outputs.
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // Raise a kernel's dynamic shared-memory limit once per device (the attribute is
 // per device context; setting it on every launch costs a driver round trip).
 // Keyed by the kernel's address (instantiations share a function type).
