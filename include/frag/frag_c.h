@@ -99,6 +99,7 @@ typedef struct {
   float sparse_ms;   /* selective-recompute prefill, all layers */
   float lm_head_ms;  /* final norm + K11 + logits copy */
   float total_ms;
+  float host_prep_ms; /* host work before the first device launch (always measured) */
 } frag_timing;
 
 /* ------------------------------------------------------------------ misc */
@@ -184,6 +185,8 @@ FRAG_API frag_status frag_result_logits(const frag_result* res, const float** lo
                                         int32_t* vocab, int32_t on_device);
 /* Critical positions (1-based, ascending) chosen for the last request. */
 FRAG_API int32_t frag_result_crit(const frag_result* res, int32_t* host_out, int32_t cap);
+/* Stage times of the last call (0 unless it set opts.timing; timed calls run
+ * eagerly, untimed ones replay a CUDA graph) and its host prep time. */
 FRAG_API frag_status frag_result_timing(const frag_result* res, frag_timing* out);
 /* Debug views for parity tests: final-layer question queries fp32 [n_q][Hq][dh]
  * and the per-token query-guided scores fp32 [N] (device pointers). */

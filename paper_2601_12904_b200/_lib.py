@@ -51,7 +51,8 @@ class ReprocessOpts(C.Structure):
 
 class Timing(C.Structure):
     _fields_ = [("stitch_ms", C.c_float), ("question_ms", C.c_float), ("select_ms", C.c_float),
-                ("sparse_ms", C.c_float), ("lm_head_ms", C.c_float), ("total_ms", C.c_float)]
+                ("sparse_ms", C.c_float), ("lm_head_ms", C.c_float), ("total_ms", C.c_float),
+                ("host_prep_ms", C.c_float)]
 
     def as_dict(self):
         return {f: float(getattr(self, f)) for f, _ in self._fields_}

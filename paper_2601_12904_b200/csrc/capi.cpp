@@ -397,8 +397,12 @@ FRAG_API int32_t frag_result_crit(const frag_result* res, int32_t* host_out, int
 FRAG_API frag_status frag_result_timing(const frag_result* res, frag_timing* out) {
   return guard([&] {
     need(res && out, "null argument");
-    need(res->r->timing_valid, "timing was not requested for the last call");
-    *out = res->r->timing;
+    *out = res->r->timing;  // stage fields are 0 unless the last call asked for timing
+    if (!res->r->timing_valid) {
+      const float hp = out->host_prep_ms;
+      *out = frag_timing{};
+      out->host_prep_ms = hp;
+    }
   });
 }
 

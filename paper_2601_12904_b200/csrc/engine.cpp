@@ -3,6 +3,7 @@
 //   -> select_query_guided (K9, K10) -> sparse prefill (K2..K8 per layer) -> lm_head (K11).
 // The whole request is stream-ordered; the only host synchronisation is the
 // final one that makes the first-token logits visible (the TTFT end).
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -12,6 +13,7 @@
 namespace fragimpl {
 
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_alloc_epoch{0};
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
@@ -22,6 +24,7 @@ void check_cuda(cudaError_t e, const char* what) {
 
 void DevBuf::alloc(size_t n) {
   release();
+  g_alloc_epoch++;  // invalidates captured request graphs
   if (n == 0) return;
   cudaError_t e = cudaMalloc(&p, n);
   if (e != cudaSuccess) {
@@ -40,6 +43,7 @@ void PinnedBuf::ensure(size_t n) {
   p = nullptr;
   bytes = 0;
   check_cuda(cudaMallocHost(&p, n), "cudaMallocHost");
+  g_alloc_epoch++;  // captured graphs may copy from/to pinned buffers
   bytes = n;
 }
 
@@ -266,6 +270,9 @@ Engine* engine_create(const frag_model_cfg& cfg, int device, uint64_t seed) {
 }
 
 Result::~Result() {
+  for (auto& g : graphs)
+    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+  if (cap_stream) cudaStreamDestroy(cap_stream);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
 }
@@ -471,19 +478,22 @@ struct Stage {
   }
 };
 
-void stitch(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys,
-            const std::vector<Record*>& recs, int S) {
+// K1 host side: per-chunk descriptors and cos/sin(delta*theta) tables staged and
+// copied to the device (per request); the kernel launch is part of the body.
+StitchPlan stitch_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys,
+                          const std::vector<Record*>& recs, int S) {
   const auto& c = e->cfg;
   const int half = c.head_dim / 2;
-  const int n_desc = (sys && sys->n > 0 ? 1 : 0) + (int)recs.size();
-  if (n_desc == 0) return;
-  auto* desc = stg.take<fragk::StitchChunk>(n_desc);
+  StitchPlan p;
+  p.n_desc = (sys && sys->n > 0 ? 1 : 0) + (int)recs.size();
+  if (p.n_desc == 0) return p;
+  auto* desc = stg.take<fragk::StitchChunk>(p.n_desc);
   std::vector<float2> tabs;
-  int nd = 0, max_rows = 0, n_tab = 0;
+  int nd = 0, n_tab = 0;
   const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
   if (sys && sys->n > 0) {
     desc[nd++] = {sys->kv.as<bf16>(), sys->kv.as<bf16>() + (size_t)c.layers * sys->n * kvc, sys->n, 0, -1};
-    max_rows = sys->n;
+    p.max_rows = sys->n;
   }
   int row = S;
   for (Record* rec : recs) {
@@ -499,26 +509,94 @@ void stitch(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys,
       }
     }
     desc[nd++] = {rec->k(), rec->v(), rec->n_tok, row, table};
-    if (rec->n_tok > max_rows) max_rows = rec->n_tok;
+    if (rec->n_tok > p.max_rows) p.max_rows = rec->n_tok;
     row += rec->n_tok;
   }
   float2* tab_h = stg.take<float2>(tabs.size() > 0 ? tabs.size() : 1);
   if (!tabs.empty()) std::memcpy(tab_h, tabs.data(), tabs.size() * sizeof(float2));
-  r->stitch_desc.ensure(n_desc * sizeof(fragk::StitchChunk));
+  r->stitch_desc.ensure(p.n_desc * sizeof(fragk::StitchChunk));
   r->stitch_tab.ensure(std::max<size_t>(tabs.size(), 1) * sizeof(float2));
-  check_cuda(cudaMemcpyAsync(r->stitch_desc.p, desc, n_desc * sizeof(fragk::StitchChunk), cudaMemcpyHostToDevice, s),
+  check_cuda(cudaMemcpyAsync(r->stitch_desc.p, desc, p.n_desc * sizeof(fragk::StitchChunk), cudaMemcpyHostToDevice,
+                             s),
              "stitch desc");
   if (!tabs.empty())
     check_cuda(cudaMemcpyAsync(r->stitch_tab.p, tab_h, tabs.size() * sizeof(float2), cudaMemcpyHostToDevice, s),
                "stitch tab");
-  double bytes = 0;
-  for (int i = 0; i < n_desc; ++i) bytes += 4.0 * c.layers * desc[i].n_tok * kvc * sizeof(bf16);
-  Scoped sc(e->prof, s, KC_STITCH, 0, bytes);
-  fragk::rope_shift_assemble(r->stitch_desc.as<fragk::StitchChunk>(), n_desc, max_rows,
+  for (int i = 0; i < p.n_desc; ++i) p.bytes += 4.0 * c.layers * desc[i].n_tok * kvc * sizeof(bf16);
+  return p;
+}
+
+void stitch_launch(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p) {
+  if (p.n_desc == 0) return;
+  const auto& c = e->cfg;
+  Scoped sc(e->prof, s, KC_STITCH, 0, p.bytes);
+  fragk::rope_shift_assemble(r->stitch_desc.as<fragk::StitchChunk>(), p.n_desc, p.max_rows,
                              r->stitch_tab.as<float2>(), r->k_fused.as<bf16>(), r->v_fused.as<bf16>(), c.layers,
                              r->max_tokens, c.n_kv_heads, c.head_dim, s);
   sc.launched(1);
   peek("stitch");
+}
+
+void stitch(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys, const std::vector<Record*>& recs,
+            int S) {
+  stitch_launch(e, r, s, stitch_prepare(e, r, s, stg, sys, recs, S));
+}
+
+// Replay the request body from a CUDA graph when its shape was seen before
+// and no device buffer was (re)allocated since the capture; otherwise run it
+// eagerly (first sighting, per-stage timing, or profiling).
+template <class Body>
+void run_graphed(Result* r, cudaStream_t s, bool graphable, const GraphKey& key, Body&& body) {
+  if (!graphable) {
+    body(s);
+    return;
+  }
+  const uint64_t epoch = g_alloc_epoch.load();
+  auto it = r->graphs.find(key);
+  if (it != r->graphs.end() && it->second.epoch == epoch) {
+    g_launches += it->second.launches;
+    check_cuda(cudaGraphLaunch(it->second.exec, s), "cudaGraphLaunch");
+    return;
+  }
+  if (it != r->graphs.end()) {
+    cudaGraphExecDestroy(it->second.exec);
+    r->graphs.erase(it);
+  }
+  if (r->graphs.size() >= 64) {  // bound the cache: many distinct shapes -> start over
+    for (auto& g : r->graphs) cudaGraphExecDestroy(g.second.exec);
+    r->graphs.clear();
+    r->seen.clear();
+  }
+  if (!r->seen.count(key)) {  // first sighting: run eagerly so every buffer reaches its final size
+    body(s);
+    r->seen.insert(key);
+    return;
+  }
+  // capture on a private stream: the caller's may be the legacy default
+  // stream, which cannot be captured; the graph is then launched on `s`
+  if (!r->cap_stream) check_cuda(cudaStreamCreateWithFlags(&r->cap_stream, cudaStreamNonBlocking), "capture stream");
+  cudaStream_t cs = r->cap_stream;
+  cudaGraph_t g = nullptr;
+  const uint64_t l0 = g_launches.load();
+  check_cuda(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+  try {
+    body(cs);
+  } catch (...) {
+    cudaStreamEndCapture(cs, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  check_cuda(cudaStreamEndCapture(cs, &g), "end capture");
+  GraphEntry ent;
+  ent.launches = g_launches.load() - l0;
+  g_launches -= ent.launches;  // counted when the graph is launched
+  cudaError_t err = cudaGraphInstantiate(&ent.exec, g, 0);
+  cudaGraphDestroy(g);
+  check_cuda(err, "cudaGraphInstantiate");
+  ent.epoch = g_alloc_epoch.load();
+  r->graphs.emplace(key, ent);
+  g_launches += ent.launches;
+  check_cuda(cudaGraphLaunch(ent.exec, s), "cudaGraphLaunch");
 }
 
 Result* scratch_for(Engine* e, int tokens) {
@@ -564,16 +642,15 @@ void ev_record(Result* r, bool on, int i, cudaStream_t s) {
   if (on) cudaEventRecord(r->ev[i], s);
 }
 
-void finish(Result* r, bool timing, cudaStream_t s, const frag_reprocess_opts* o) {
+void logits_d2h(Result* r, cudaStream_t s) {
+  if (r->logits_on_device || r->logit_rows == 0) return;
+  const size_t n = (size_t)r->logit_rows * r->eng->cfg.vocab;
+  check_cuda(cudaMemcpyAsync(r->logits_host.p, r->logits.p, n * sizeof(float), cudaMemcpyDeviceToHost, s),
+             "logits D2H");
+}
+
+void finish(Result* r, bool timing, cudaStream_t s) {
   Engine* e = r->eng;
-  const auto& c = e->cfg;
-  r->logits_on_device = o && o->logits_on_device;
-  if (!r->logits_on_device && r->logit_rows > 0) {
-    const size_t n = (size_t)r->logit_rows * c.vocab;
-    r->logits_host.ensure(n * sizeof(float));
-    check_cuda(cudaMemcpyAsync(r->logits_host.p, r->logits.p, n * sizeof(float), cudaMemcpyDeviceToHost, s),
-               "logits D2H");
-  }
   ev_record(r, timing, 6, s);
   r->last_stream = s;
   check_cuda(cudaStreamSynchronize(s), "reprocess");
@@ -594,10 +671,15 @@ void finish(Result* r, bool timing, cudaStream_t s, const frag_reprocess_opts* o
 }  // namespace
 
 // ---------------------------------------------------------------- reprocess
+// Host prep (record fetch, RoPE/stitch tables, staging + H2D of the small
+// per-request inputs) runs every call; the device body (K1 -> question pass ->
+// K9/K10 -> sparse pass -> lm_head -> logits D2H) is captured once per request
+// shape into a CUDA graph and replayed, so ~500 launches cost one.
 void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
                bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio,
                const frag_reprocess_opts* o, cudaStream_t s, Result* r) {
   const auto& c = e->cfg;
+  const auto t_entry = std::chrono::steady_clock::now();
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (!st) fail(FRAG_E_CONTRACT, "store is null");
   if (st->device != e->device) fail(FRAG_E_CONTRACT, "store and engine are on different devices");
@@ -647,17 +729,20 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   r->k_sel = k;
   r->M = M;
   const bool all_logits = o && o->all_logits;
+  const bool raw = o && o->raw_scores;
   r->logit_rows = all_logits ? n_q : 1;
+  r->logits_on_device = o && o->logits_on_device;
 
+  // ---- host prep: everything that depends on this request's chunks / tokens
   r->staging.ensure(64 * 1024 + (size_t)(n_chunks + 2) * (64 + c.head_dim * 4) + (size_t)(4 * T + 4 * M + 4 * n_q) * 4);
   Stage stg(r->staging);
-
-  ev_record(r, timing, 0, s);
-  // ---- K1: stitch_full_reuse
-  stitch(e, r, s, stg, skv, recs, S);
-  // chunk token ids in prompt order (needed by the recompute gather, K2)
+  // injected plan first: the captured body copies from these staging slots,
+  // so their offsets must depend only on the graph key
+  int* inj_rows = inject ? stg.take<int>(M) : nullptr;
+  int* inj_tok = inject ? stg.take<int>(M) : nullptr;
+  StitchPlan sp = stitch_prepare(e, r, s, stg, skv, recs, S);
   {
-    int off = 0;
+    int off = 0;  // chunk token ids in prompt order (the recompute gather, K2)
     for (Record* rec : recs) {
       check_cuda(cudaMemcpyAsync(r->chunk_tok.as<int>() + off, rec->tok.p, rec->n_tok * sizeof(int),
                                  cudaMemcpyDeviceToDevice, s),
@@ -672,25 +757,17 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     std::memcpy(qh, q_tokens, n_q * sizeof(int));
     check_cuda(cudaMemcpyAsync(r->q_tok.p, qh, n_q * sizeof(int), cudaMemcpyHostToDevice, s), "q tok");
   }
-  ev_record(r, timing, 1, s);
-  // ---- question pass (last_layer_query_states against the stitched cache)
   {
-    int* rows_h = stg.take<int>(n_q);
+    int* rows_h = stg.take<int>(n_q);  // question-pass plan: the last n_q rows
     for (int i = 0; i < n_q; ++i) rows_h[i] = T - n_q + i;
     check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, n_q * sizeof(int), cudaMemcpyHostToDevice, s), "q rows");
     check_cuda(cudaMemcpyAsync(r->plan_tok.p, r->q_tok.p, n_q * sizeof(int), cudaMemcpyDeviceToDevice, s), "q plan");
-    run_rows(e, r, s, n_q, T, PASS_QUESTION, nullptr, 0);
   }
-  ev_record(r, timing, 2, s);
-  // ---- select_query_guided (K9 + K10) -> QIndexPlan on device
-  if (inject) {
-    int* rows_h = stg.take<int>(M);
-    int* tok_h = stg.take<int>(M);
+  if (inject) {  // written now, copied inside the body after the question pass
     for (int i = 0; i < k; ++i) {
       const int row = o->inject_crit[i] - 1;
-      rows_h[i] = row;
-      int j = row - S;
-      int t = 0;
+      inj_rows[i] = row;
+      int j = row - S, t = 0;
       for (Record* rec : recs) {
         if (j < rec->n_tok) {
           t = rec->tok_host[j];
@@ -698,44 +775,13 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
         }
         j -= rec->n_tok;
       }
-      tok_h[i] = t;
+      inj_tok[i] = t;
     }
     for (int i = 0; i < n_q; ++i) {
-      rows_h[k + i] = T - n_q + i;
-      tok_h[k + i] = q_tokens[i];
+      inj_rows[k + i] = T - n_q + i;
+      inj_tok[k + i] = q_tokens[i];
     }
-    check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, M * sizeof(int), cudaMemcpyHostToDevice, s), "plan rows");
-    check_cuda(cudaMemcpyAsync(r->plan_tok.p, tok_h, M * sizeof(int), cudaMemcpyHostToDevice, s), "plan tok");
-  } else {
-    if (N > 0) {
-      const int nblk = (N + 31) / 32;
-      r->part_ms.ensure((size_t)nblk * n_q * c.n_heads * sizeof(float2));
-      r->row_ms.ensure((size_t)n_q * c.n_heads * sizeof(float2));
-      fragk::ScoreArgs a{};
-      a.q = r->q_final.as<float>();
-      a.k = r->k_fused.as<bf16>() + (size_t)(c.layers - 1) * r->max_tokens * c.n_kv_heads * c.head_dim;
-      a.nq = n_q;
-      a.Hq = c.n_heads;
-      a.Hkv = c.n_kv_heads;
-      a.dh = c.head_dim;
-      a.key_row0 = S;
-      a.n_keys = N;
-      a.scale = 1.0f / std::sqrt((float)c.head_dim);
-      a.part_ms = r->part_ms.as<float2>();
-      a.row_ms = r->row_ms.as<float2>();
-      a.scores = r->scores.as<float>();
-      a.raw = o && o->raw_scores;
-      Scoped sc(e->prof, s, KC_SELECT, 4.0 * n_q * c.n_heads * (double)N * c.head_dim,
-                2.0 * N * (double)c.n_kv_heads * c.head_dim * 2);
-      sc.launched(fragk::qg_score(a, s));
-    }
-    Scoped sc(e->prof, s, KC_SELECT, 0, 4.0 * N * 6);
-    sc.launched(fragk::topk_plan(r->scores.as<float>(), N, k, S, r->chunk_tok.as<int>(), r->q_tok.as<int>(), n_q,
-                                 T - n_q, r->plan_rows.as<int>(), r->plan_tok.as<int>(), s));
   }
-  peek("select");
-  ev_record(r, timing, 3, s);
-  // ---- sparse_prefill (Eq. 9) to the first-token logits
   {
     int* map_h = stg.take<int>(r->logit_rows);
     if (all_logits)
@@ -743,34 +789,88 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     else
       map_h[0] = M - 1;
     check_cuda(cudaMemcpyAsync(r->row_map.p, map_h, r->logit_rows * sizeof(int), cudaMemcpyHostToDevice, s), "map");
-    run_rows(e, r, s, M, T, PASS_FULL, nullptr, 0);  // logits below, timed as their own stage
   }
-  ev_record(r, timing, 4, s);
-  {
-    // final norm + lm_head on the logit rows (K3 + K11)
-    const int d = c.d_model;
-    r->lm_x.ensure((size_t)r->logit_rows * d * sizeof(bf16));
-    r->logits.ensure((size_t)r->logit_rows * c.vocab * sizeof(float));
-    {
-      Scoped sc(e->prof, s, KC_NORM, 0, (double)r->logit_rows * d * 6);
-      fragk::rmsnorm(r->h.as<float>(), r->logit_rows, d, e->final_norm, c.norm_eps, r->lm_x.as<bf16>(), s,
-                     r->row_map.as<int>());
-      sc.launched(1);
+  if (N > 0 && !inject) {
+    r->part_ms.ensure((size_t)((N + 31) / 32) * n_q * c.n_heads * sizeof(float2));
+    r->row_ms.ensure((size_t)n_q * c.n_heads * sizeof(float2));
+  }
+  r->lm_x.ensure((size_t)r->logit_rows * c.d_model * sizeof(bf16));
+  r->logits.ensure((size_t)r->logit_rows * c.vocab * sizeof(float));
+  if (!r->logits_on_device) r->logits_host.ensure((size_t)r->logit_rows * c.vocab * sizeof(float));
+
+  // ---- device body
+  auto body = [&](cudaStream_t bs) {
+    ev_record(r, timing, 0, bs);
+    stitch_launch(e, r, bs, sp);  // K1: stitch_full_reuse
+    ev_record(r, timing, 1, bs);
+    // question pass: last_layer_query_states against the stitched cache
+    run_rows(e, r, bs, n_q, T, PASS_QUESTION, nullptr, 0);
+    ev_record(r, timing, 2, bs);
+    // select_query_guided (K9 + K10) -> QIndexPlan on device
+    if (inject) {
+      check_cuda(cudaMemcpyAsync(r->plan_rows.p, inj_rows, M * sizeof(int), cudaMemcpyHostToDevice, bs), "plan rows");
+      check_cuda(cudaMemcpyAsync(r->plan_tok.p, inj_tok, M * sizeof(int), cudaMemcpyHostToDevice, bs), "plan tok");
+    } else {
+      if (N > 0) {
+        fragk::ScoreArgs a{};
+        a.q = r->q_final.as<float>();
+        a.k = r->k_fused.as<bf16>() + (size_t)(c.layers - 1) * r->max_tokens * c.n_kv_heads * c.head_dim;
+        a.nq = n_q;
+        a.Hq = c.n_heads;
+        a.Hkv = c.n_kv_heads;
+        a.dh = c.head_dim;
+        a.key_row0 = S;
+        a.n_keys = N;
+        a.scale = 1.0f / std::sqrt((float)c.head_dim);
+        a.part_ms = r->part_ms.as<float2>();
+        a.row_ms = r->row_ms.as<float2>();
+        a.scores = r->scores.as<float>();
+        a.raw = raw;
+        Scoped sc(e->prof, bs, KC_SELECT, 4.0 * n_q * c.n_heads * (double)N * c.head_dim,
+                  2.0 * N * (double)c.n_kv_heads * c.head_dim * 2);
+        sc.launched(fragk::qg_score(a, bs));
+      }
+      Scoped sc(e->prof, bs, KC_SELECT, 0, 4.0 * N * 6);
+      sc.launched(fragk::topk_plan(r->scores.as<float>(), N, k, S, r->chunk_tok.as<int>(), r->q_tok.as<int>(), n_q,
+                                   T - n_q, r->plan_rows.as<int>(), r->plan_tok.as<int>(), bs));
     }
-    fragk::EpiParams ep;
-    ep.ws = r->gemm_ws.as<float>();
-    ep.ws_bytes = r->gemm_ws.bytes;
-    ep.counters = r->gemm_cnt.as<int>();
-    ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
-    ep.out_f32 = r->logits.as<float>();
-    ep.ldo = c.vocab;
-    Scoped sc(e->prof, s, KC_GEMM, 2.0 * r->logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
-    sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, r->logit_rows, c.vocab, d, fragk::EPI_STORE_F32,
-                                    ep, s));
-  }
-  peek("lm_head");
-  ev_record(r, timing, 5, s);
-  finish(r, timing, s, o);
+    peek("select");
+    ev_record(r, timing, 3, bs);
+    // sparse_prefill (Eq. 9) to the first-token logits
+    run_rows(e, r, bs, M, T, PASS_FULL, nullptr, 0);
+    ev_record(r, timing, 4, bs);
+    {
+      // final norm + lm_head on the logit rows (K3 + K11)
+      const int d = c.d_model;
+      {
+        Scoped sc(e->prof, bs, KC_NORM, 0, (double)r->logit_rows * d * 6);
+        fragk::rmsnorm(r->h.as<float>(), r->logit_rows, d, e->final_norm, c.norm_eps, r->lm_x.as<bf16>(), bs,
+                       r->row_map.as<int>());
+        sc.launched(1);
+      }
+      fragk::EpiParams ep;
+      ep.ws = r->gemm_ws.as<float>();
+      ep.ws_bytes = r->gemm_ws.bytes;
+      ep.counters = r->gemm_cnt.as<int>();
+      ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
+      ep.out_f32 = r->logits.as<float>();
+      ep.ldo = c.vocab;
+      Scoped sc(e->prof, bs, KC_GEMM, 2.0 * r->logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
+      sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, r->logit_rows, c.vocab, d,
+                                      fragk::EPI_STORE_F32, ep, bs));
+    }
+    peek("lm_head");
+    ev_record(r, timing, 5, bs);
+    logits_d2h(r, bs);
+  };
+
+  const bool graphable = !timing && !e->prof.on;
+  GraphKey key{T, S, N, n_q, k, (int)inject, (int)all_logits, (int)raw, (int)r->logits_on_device, sp.n_desc,
+               sp.max_rows, (uint64_t)(uintptr_t)e->rope.p};
+  r->timing.host_prep_ms =
+      std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
+  run_graphed(r, s, graphable, key, body);
+  finish(r, timing, s);
 }
 
 void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
@@ -811,7 +911,10 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
   run_rows(e, r, s, n_tok, T, PASS_FULL, r->row_map.as<int>(), 1);
   ev_record(r, timing, 4, s);
   ev_record(r, timing, 5, s);
-  finish(r, timing, s, o);
+  r->logits_on_device = o && o->logits_on_device;
+  if (!r->logits_on_device) r->logits_host.ensure((size_t)c.vocab * sizeof(float));
+  logits_d2h(r, s);
+  finish(r, timing, s);
 }
 
 void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,

@@ -10,7 +10,9 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <shared_mutex>
+#include <tuple>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -32,6 +34,7 @@ void check_cuda(cudaError_t e, const char* what);
 void set_last_error(const std::string& m);
 
 extern std::atomic<uint64_t> g_launches;
+extern std::atomic<uint64_t> g_alloc_epoch;  // bumped on every device (re)allocation
 
 // Device memory helper (RAII).
 struct DevBuf {
@@ -163,8 +166,31 @@ struct Engine {
   size_t qkv_cols() const { return (size_t)(cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim; }
 };
 
+// Shape of a request body; a captured CUDA graph is valid for one key.
+struct GraphKey {
+  int T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows;
+  uint64_t rope;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows, rope) <
+           std::tie(o.T, o.S, o.N, o.nq, o.k, o.inject, o.all_logits, o.raw, o.logits_on_device, o.n_desc,
+                    o.max_rows, o.rope);
+  }
+};
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t epoch = 0;
+  uint64_t launches = 0;
+};
+struct StitchPlan {
+  int n_desc = 0, max_rows = 0;
+  double bytes = 0;
+};
+
 struct Result {
   Engine* eng = nullptr;
+  std::map<GraphKey, GraphEntry> graphs;
+  std::set<GraphKey> seen;
+  cudaStream_t cap_stream = nullptr;
   int max_tokens = 0;
   // fused cache [L][max_tokens][Hkv][dh]
   DevBuf k_fused, v_fused;

@@ -87,3 +87,24 @@ def test_single_chunk_native_offset_is_bit_copy(tiny):
     L_ = eng.cfg.layers
     # rows S..S+n-1 hold the record untouched (r=0: nothing recomputed there)
     assert np.array_equal(k[:, 8:8 + 256], rk) and np.array_equal(v[:, 8:8 + 256], rv)
+
+
+def test_graph_replay_matches_eager(tiny):
+    """The request body is replayed from a CUDA graph from the second request of
+    a shape on; replays must reproduce the eager (timing=True) run bit for bit,
+    including when a same-shape request brings different chunks / RoPE deltas /
+    question tokens (the graph reads them from the per-request staging)."""
+    eng, store, res, ids = tiny["eng"], tiny["store"], tiny["res"], tiny["ids"]
+    q2 = list(reversed(tiny["question"]))
+    order_b = ids[4:] + ids[:4]  # same shape, different deltas per chunk
+    outs = {}
+    for name, q, order in (("a", tiny["question"], ids), ("b", q2, order_b)):
+        eng.reprocess(store, q, order, 0.2, res, system=tiny["system"], timing=True)
+        outs[name] = (res.logits().copy(), res.crit().copy())
+    for rep in range(3):
+        for name, q, order in (("a", tiny["question"], ids), ("b", q2, order_b)):
+            eng.reprocess(store, q, order, 0.2, res, system=tiny["system"])
+            lg, crit = res.logits(), res.crit()
+            assert np.array_equal(crit, outs[name][1]), (rep, name)
+            assert np.array_equal(lg, outs[name][0]), (rep, name)
+    assert not np.array_equal(outs["a"][0], outs["b"][0])
