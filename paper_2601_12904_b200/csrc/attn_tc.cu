@@ -29,6 +29,8 @@
 
 #include <cfloat>
 
+#include <cstdlib>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -41,6 +43,7 @@ constexpr int AT_QT = 2;      // query tiles per CTA
 constexpr int AT_KEYS = 128;  // keys per K/V tile
 constexpr int AT_THREADS = 320;
 constexpr float RESCALE_THRESH = 8.0f;  // log2 units
+constexpr int kDefaultPoly = 0;  // measured: MUFU-only is fastest at dh=128 (tools/attn_bench.py)
 
 template <int DH>
 struct AttCfg {
@@ -53,7 +56,9 @@ struct AttCfg {
   static_assert(SMEM <= 232448, "attention tile exceeds the 227 KB shared-memory limit");
 };
 
-template <int DH>
+// POLY: every POLY-th pair of P elements takes the FMA-pipe 2^x (ex2_poly)
+// instead of MUFU.EX2, balancing the two pipes (0 = all MUFU).
+template <int DH, int POLY>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int G, int n_qblocks) {
@@ -74,8 +79,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
   const int warp = warp_id(), lane = lane_id();
-  const int qb = n_qblocks - 1 - (int)blockIdx.x;  // heaviest (latest rows) first
-  const int hk = blockIdx.y;
+  // global longest-first order: q-block work grows with its row positions, so
+  // dispatch (q-block desc) x (kv head) makes the hardware's greedy CTA
+  // scheduler an LPT schedule across all heads (the tail wave is the lightest)
+  const int qb = n_qblocks - 1 - (int)blockIdx.x / a.Hkv;
+  const int hk = (int)blockIdx.x % a.Hkv;
   const int split = blockIdx.z;
   const int tok_per_tile = AT_ROWS / G;
   const int t0 = qb * AT_QT * tok_per_tile;
@@ -227,11 +235,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(s[e]);
 #pragma unroll
-        for (int k = 8; k < AT_KEYS; k += 8)
+        for (int k = 8; k < AT_KEYS - 8; k += 16)
 #pragma unroll
-          for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(mx8[e], __uint_as_float(s[k + e]));
-        const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * c;
+          for (int e = 0; e < 8; ++e) mx8[e] = fmax3(mx8[e], __uint_as_float(s[k + e]), __uint_as_float(s[k + 8 + e]));
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(mx8[e], __uint_as_float(s[AT_KEYS - 8 + e]));
+        const float mt = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])) * c;
         // lazy rescale: only when the max grows by more than 2^8
         const bool grow = mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt != -INFINITY);
         const float m_new = grow ? fmaxf(mt, m_used) : m_used;
@@ -262,8 +271,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const int k = half * 64 + 2 * e;
-            const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(s[k]), c, mneg));
-            const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(s[k + 1]), c, mneg));
+            const float x0 = __fmaf_rn(__uint_as_float(s[k]), c, mneg);
+            const float x1 = __fmaf_rn(__uint_as_float(s[k + 1]), c, mneg);
+            const bool poly = POLY > 0 && (e % (POLY > 0 ? POLY : 1)) == POLY - 1;
+            const float p0 = poly ? ex2_poly(x0) : ex2_approx(x0);
+            const float p1 = poly ? ex2_poly(x1) : ex2_approx(x1);
             rs8[(2 * e) & 7] += p0;
             rs8[(2 * e + 1) & 7] += p1;
             pk[e] = pack_bf16(p0, p1);
@@ -339,13 +351,24 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   // K/V layer [T][Hkv*dh]; box (64, 128 keys)
   if (!make_tmap_2d(&tk, a.k, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
   if (!make_tmap_2d(&tv, a.v, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
-  dim3 grid(n_qblocks, a.Hkv, a.n_splits);
+  dim3 grid(n_qblocks * a.Hkv, 1, a.n_splits);
+  // FRAG_ATTN_POLY: tuning knob for the MUFU/FMA exp split (default below)
+  static const int poly = [] {
+    const char* v = std::getenv("FRAG_ATTN_POLY");
+    return v ? std::atoi(v) : kDefaultPoly;
+  }();
+  auto go = [&](auto kern, int smem) {
+    smem_attr_once(kern, smem);
+    kern<<<grid, AT_THREADS, smem, stream>>>(tq, tk, tv, a, G, n_qblocks);
+  };
   if (a.dh == 128) {
-    smem_attr_once(attn_tc_kernel<128>, (int)AttCfg<128>::SMEM);
-    attn_tc_kernel<128><<<grid, AT_THREADS, AttCfg<128>::SMEM, stream>>>(tq, tk, tv, a, G, n_qblocks);
+    constexpr int SM = (int)AttCfg<128>::SMEM;
+    switch (poly) {
+      case 4: go(attn_tc_kernel<128, 4>, SM); break;
+      default: go(attn_tc_kernel<128, kDefaultPoly>, SM); break;
+    }
   } else if (a.dh == 64) {
-    smem_attr_once(attn_tc_kernel<64>, (int)AttCfg<64>::SMEM);
-    attn_tc_kernel<64><<<grid, AT_THREADS, AttCfg<64>::SMEM, stream>>>(tq, tk, tv, a, G, n_qblocks);
+    go(attn_tc_kernel<64, kDefaultPoly>, (int)AttCfg<64>::SMEM);
   } else {
     return -1;
   }

@@ -215,15 +215,21 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // resolution of P), exponent added in the integer domain. x <= 0 expected;
 // clamped at -126 (2^-126 ~ 1e-38 stands in for 0 of masked keys).
 __device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.0f);
+  x = fmaxf(x, -127.0f);  // -inf (masked) -> exactly +0 below
   const float t = x + 12582912.0f;  // 1.5 * 2^23: low mantissa bits = round(x)
-  const float xi = t - 12582912.0f;
-  const float f = x - xi;
+  const float f = x - (t - 12582912.0f);
   float p = __fmaf_rn(0.05550411f, f, 0.24022652f);
   p = __fmaf_rn(p, f, 0.69314718f);
   p = __fmaf_rn(p, f, 1.0f);
-  const int i = __float_as_int(t) - 0x4B400000;
-  return __int_as_float(__float_as_int(p) + (i << 23));
+  // bits(t) << 23 == round(x) << 23 (mod 2^32): one shift-add on the exponent
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// three-input max (sm_100+ max.f32 with three sources)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
