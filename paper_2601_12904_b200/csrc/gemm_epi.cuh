@@ -108,5 +108,85 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
   }
 }
 
+
+// ---------------------------------------------------------------- split-K fixup
+// Cooperative, deterministic reduction of one split-K tile slot. Every split
+// CTA has written its fp32 partial (ws_rows x BN, row-major, one row per TMEM
+// lane) to ep.ws slot (slot*S + sp). All S split CTAs of the slot are
+// co-resident (persistent grid), so instead of one last-arriving CTA reducing
+// the whole tile, each waits for all S partials and then reduces and runs the
+// fused epilogue on its own share of the 32-column chunks (round-robin by
+// split index), summing the partials in split order -> bit-identical results
+// whatever the arrival order. Called by the 4 epilogue warps (128 threads,
+// named barrier 1); `warp2_lane0` does the counter traffic.
+template <int BN, int EPI>
+__device__ __forceinline__ void split_fixup(const EpiParams& ep, int slot, int S, int sp, int ws_rows,
+                                            int row_in_tile, int row, int M, int col0, bool warp2_lane0) {
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  int* cnt = ep.counters + slot;
+  if (warp2_lane0) {
+    atomicAdd(cnt, 1);
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+      if (v < S) __nanosleep(64);
+    } while (v < S);
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  constexpr int CW = EPI == EPI_SWIGLU ? 2 : 1;  // 32-col chunks per epilogue unit
+  constexpr int UNITS = BN / 32 / CW;
+  const float* base = ep.ws + ((size_t)slot * S * ws_rows + row_in_tile) * BN;
+  const size_t sstride = (size_t)ws_rows * BN;
+  if (row_in_tile < ws_rows && row < M) {
+#pragma unroll 1
+    for (int u = sp; u < UNITS; u += S) {
+      uint32_t r[2][32];
+#pragma unroll
+      for (int h2 = 0; h2 < CW; ++h2) {
+        const int c = u * CW + h2;
+        float4 acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int s2 = 0;
+        for (; s2 + 1 < S; s2 += 2) {  // two partials in flight per step
+          const float4* a = reinterpret_cast<const float4*>(base + s2 * sstride + c * 32);
+          const float4* b = reinterpret_cast<const float4*>(base + (s2 + 1) * sstride + c * 32);
+          float4 va[8], vb[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) va[j] = __ldcg(a + j), vb[j] = __ldcg(b + j);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            acc[j].x += va[j].x, acc[j].y += va[j].y, acc[j].z += va[j].z, acc[j].w += va[j].w;
+            acc[j].x += vb[j].x, acc[j].y += vb[j].y, acc[j].z += vb[j].z, acc[j].w += vb[j].w;
+          }
+        }
+        if (s2 < S) {
+          const float4* a = reinterpret_cast<const float4*>(base + s2 * sstride + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 v = __ldcg(a + j);
+            acc[j].x += v.x, acc[j].y += v.y, acc[j].z += v.z, acc[j].w += v.w;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          r[h2][4 * j] = __float_as_uint(acc[j].x);
+          r[h2][4 * j + 1] = __float_as_uint(acc[j].y);
+          r[h2][4 * j + 2] = __float_as_uint(acc[j].z);
+          r[h2][4 * j + 3] = __float_as_uint(acc[j].w);
+        }
+      }
+      epi_chunk<EPI>(ep, row, col0 + u * CW * 32, r[0], r[CW - 1]);
+    }
+  }
+  // second round of arrivals: the last CTA out resets the counter for the next GEMM
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (warp2_lane0) {
+    const int old = atomicAdd(cnt, 1);
+    if (old == 2 * S - 1) *cnt = 0;
+  }
+}
+
 }  // namespace
 }  // namespace fragk

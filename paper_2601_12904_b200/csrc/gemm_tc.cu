@@ -61,7 +61,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -90,9 +89,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
   const uint32_t tmem_base = *tmem_slot;
 
   // work items: the first `full` tiles whole, then the remaining (tail) tiles
-  // each cut into `splits` K ranges, reduced deterministically by the
-  // last-arriving CTA of each tail tile (split-K for the last partial wave and
-  // for few-tile small-M GEMMs).
+  // each cut into `splits` K ranges, reduced deterministically and
+  // cooperatively by the tile's split CTAs (split_fixup; split-K for the last
+  // partial wave and for few-tile small-M GEMMs).
   const int splits = ep.splits > 1 ? ep.splits : 1;
   const int n_full = splits > 1 ? ep.full_tiles : num_tiles;
   const int num_work = n_full + (num_tiles - n_full) * splits;
@@ -238,52 +237,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && lane == 0) {
-          const int old = atomicAdd(&ep.counters[ti], 1);
-          *last_flag = (old == S - 1) ? 1 : 0;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (*last_flag) {
-          // deterministic reduction in split order, then the fused epilogue
-          __threadfence();
-          const float* base = ep.ws + ((size_t)ti * S * ws_rows + row_in_tile) * BN;
-          const size_t sstride = (size_t)ws_rows * BN;
-          if (row_in_tile < ws_rows && row < M) {
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; c += (EPI == EPI_SWIGLU ? 2 : 1)) {
-              uint32_t r[32], r2[32];
-              const int nchunk = EPI == EPI_SWIGLU ? 2 : 1;
-#pragma unroll
-              for (int h2 = 0; h2 < 2; ++h2) {
-                if (h2 >= nchunk) break;
-                float accv[32];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) accv[e] = 0.f;
-                for (int s2 = 0; s2 < S; ++s2) {
-                  const float4* src = reinterpret_cast<const float4*>(base + s2 * sstride + (c + h2) * 32);
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) {
-                    const float4 v = __ldcg(src + j);
-                    accv[4 * j] += v.x;
-                    accv[4 * j + 1] += v.y;
-                    accv[4 * j + 2] += v.z;
-                    accv[4 * j + 3] += v.w;
-                  }
-                }
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                  if (h2 == 0) r[e] = __float_as_uint(accv[e]);
-                  else r2[e] = __float_as_uint(accv[e]);
-                }
-              }
-              epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
-            }
-          }
-          if (warp == 2 && lane == 0) ep.counters[ti] = 0;  // self-reset for the next GEMM
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        split_fixup<BN, EPI>(ep, ti, S, sp, ws_rows, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -435,7 +389,9 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
   // force_bn_flags: 0 = automatic; else BN in the low 16 bits (64/128/256),
   // bit 16 = still allow the tail split-K, bit 17 = forbid it (tuning only)
   const int force_bn = force_bn_flags & 0xffff;
-  if (force_bn_flags & 0x40000) return gemm_bf16_tc_pair(A, B, M, N, K, epi, ep0, stream, force_bn ? force_bn : 256);
+  if (force_bn_flags & 0x40000)
+    return gemm_bf16_tc_pair(A, B, M, N, K, epi, ep0, stream, force_bn ? force_bn : 256,
+                             (force_bn_flags & 0x10000) != 0);
   const bool tail_ok = force_bn ? (force_bn_flags & 0x10000) != 0 : (force_bn_flags & 0x20000) == 0;
   if (M <= 0) return 0;
   if (K % BK != 0 || N % 64 != 0) return -1;
@@ -462,7 +418,9 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
   // Large M: CTA-pair tiles (256 x 256, cta_group::2) beat every 1-CTA shape in
   // the B200 sweep (profiles/gemm_tune_r01.txt) for the projection shapes.
   if (!force_bn && M >= 256 && N % 256 == 0 && ep.splits == 1)
-    return gemm_bf16_tc_pair(A, B, M, N, K, epi, ep, stream, 256);
+    // tail split-K only pays for long K (the FFN down projection): at K=4096 the
+    // partial write + fixup cost what the shorter last wave saves (gemm_tune)
+    return gemm_bf16_tc_pair(A, B, M, N, K, epi, ep, stream, 256, (force_bn_flags & 0x20000) == 0 && K >= 8192);
   if (ep.splits == 1 && tail_ok && M > BM && (M + BM - 1) / BM < 64 && K >= 8192 && ep.ws && ep.counters) {
     // split-K only the last partial wave (deterministic last-CTA reduction)
     const long tiles = (long)((M + BM - 1) / BM) * (N / bn), sms = num_sms();

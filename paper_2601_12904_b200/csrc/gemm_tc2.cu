@@ -83,7 +83,7 @@ struct Gemm2Cfg {
   static constexpr uint32_t B_BYTES = (BN / 2) * BK2 * 2;  // this CTA's BN/2 rows of B
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;  // + barriers, TMEM slot, flag
   static_assert(SMEM <= 232448, "GEMM pipeline exceeds the 227 KB shared-memory limit");
 };
 
@@ -111,6 +111,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
   const int n_tiles = N / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int nk = K / BK2;
+  // work items: the first n_full tiles whole, then each tail tile cut into
+  // `splits` K ranges (split-K of the last partial wave); the split CTAs of
+  // each 128-row half-tile reduce it cooperatively (split_fixup)
+  const int splits = ep.splits > 1 ? ep.splits : 1;
+  const int n_full = splits > 1 ? ep.full_tiles : num_tiles;
+  const int num_work = n_full + (num_tiles - n_full) * splits;
+  auto decode = [&](int w, int& tile, int& sp, int& S) {
+    if (w < n_full) {
+      tile = w, sp = 0, S = 1;
+    } else {
+      const int u = w - n_full;
+      tile = n_full + u / splits, sp = u % splits, S = splits;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -136,24 +150,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
       pdl_launch_dependents();
       // weight (B) loads of the first stages go out before the dependency wait
       int npre = 0;
-      if (pair < num_tiles) {
-        const int n_blk = pair / m_tiles;
-        npre = nk < STAGES ? nk : STAGES;
+      if (pair < num_work) {
+        int tile, sp, S;
+        decode(pair, tile, sp, S);
+        const int n_blk = tile / m_tiles;
+        const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
+        npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
         for (int i = 0; i < npre; ++i) {
           const uint32_t fb = smem_u32(&full[i]) & PEER_MASK;
           if (leader)
             mbar_arrive_expect_tx(&full[i], 2 * C::STAGE_BYTES);
           else
             mbar_arrive_cluster(fb);
-          tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, fb, i * BK2, n_blk * BN + rank * (BN / 2));
+          tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, fb, (kb0 + i) * BK2, n_blk * BN + rank * (BN / 2));
         }
       }
       pdl_wait();
       int stage = 0, it = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+      for (int w = pair; w < num_work; w += n_pairs) {
+        int tile, sp, S;
+        decode(w, tile, sp, S);
         const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
           if (it >= npre) {
             mbar_wait(&empty[stage], phase ^ 1);
@@ -180,20 +200,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+      for (int w = pair; w < num_work; w += n_pairs) {
+        int tile, sp, S;
+        decode(w, tile, sp, S);
+        const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
             const uint64_t a0 = da + ((stage * C::A_BYTES) >> 4);
             const uint64_t b0 = db + ((stage * C::B_BYTES) >> 4);
 #pragma unroll
-            for (int k = 0; k < BK2 / 16; ++k) umma_bf16_pair(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < BK2 / 16; ++k)
+              umma_bf16_pair(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
             umma_commit_pair(&empty[stage]);
-            if (kb == nk - 1) umma_commit_pair(&tfull[acc]);
+            if (kb == kb1 - 1) umma_commit_pair(&tfull[acc]);
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -212,33 +236,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
     const uint32_t te_leader = smem_u32(tempty) & PEER_MASK;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+    for (int w = pair; w < num_work; w += n_pairs) {
+      int tile, sp, S;
+      decode(w, tile, sp, S);
       const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * BM2 + rank * 128 + row_in_tile;
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if constexpr (EPI == EPI_SWIGLU) {
+      if (S == 1) {
+        if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; c += 2) {
-          uint32_t r[32], r2[32];
-          tmem_ld32(t_row + c * 32, r);
-          tmem_ld32(t_row + (c + 1) * 32, r2);
-          tmem_ld_wait();
-          if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+          for (int c = 0; c < BN / 32; c += 2) {
+            uint32_t r[32], r2[32];
+            tmem_ld32(t_row + c * 32, r);
+            tmem_ld32(t_row + (c + 1) * 32, r2);
+            tmem_ld_wait();
+            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(t_row + c * 32, r);
+            tmem_ld_wait();
+            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
       } else {
+        // split partial of this CTA's 128 rows -> workspace (fp32); TMEM freed at once
+        const int slot = (tile - n_full) * 2 + (int)rank;  // counter / workspace half-tile slot
+        float* wsp = ep.ws + ((size_t)(slot * S + sp) * 128 + row_in_tile) * BN;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
           tmem_ld32(t_row + c * 32, r);
           tmem_ld_wait();
-          if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
+          float4* dst = reinterpret_cast<float4*>(wsp + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+        split_fixup<BN, EPI>(ep, slot, S, sp, 128, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -259,8 +306,9 @@ int launch2(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& 
   if (!make_tmap_2d(&ta, A, M, K, K, 128)) return -1;
   if (!make_tmap_2d(&tb, B, N, K, K, BN / 2)) return -1;
   const int tiles = ((M + BM2 - 1) / BM2) * (N / BN);
+  const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int pairs = num_sms() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  const int grid = 2 * (work < pairs ? work : pairs);
   launch_pdl(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(GEMM2_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
@@ -268,9 +316,35 @@ int launch2(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& 
 }  // namespace
 
 // Large-M GEMM on CTA pairs (BN = 256 or 128 per pair). Returns launches or -1.
+namespace {
+int pair_dispatch(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
+                  cudaStream_t s, int bn);
+}
+
 int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
-                      cudaStream_t s, int bn) {
+                      cudaStream_t s, int bn, bool tail_split) {
   if (K % BK2 != 0 || N % bn != 0) return -1;
+  EpiParams ep2 = ep;
+  ep2.splits = 1;
+  if (tail_split && ep.ws && ep.counters) {
+    // split-K only the last partial wave of CTA pairs (deterministic reduction
+    // per 128-row half by the last-arriving CTA)
+    const long tiles = (long)((M + BM2 - 1) / BM2) * (N / bn), pairs = num_sms() / 2, nk = K / BK2;
+    const long rem = tiles % pairs;
+    long sp = rem ? pairs / rem : 1;
+    if (sp > 8) sp = 8;
+    while (sp > 1 && nk / sp < 4) --sp;
+    if (sp > 1 && 2 * rem <= ep.counters_cap && (size_t)rem * 2 * sp * 128 * bn * sizeof(float) <= ep.ws_bytes) {
+      ep2.splits = (int)sp;
+      ep2.full_tiles = (int)(tiles - rem);
+    }
+  }
+  return pair_dispatch(A, B, M, N, K, epi, ep2, s, bn);
+}
+
+namespace {
+int pair_dispatch(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
+                  cudaStream_t s, int bn) {
   if (bn == 256) {
     switch (epi) {
       case EPI_STORE_BF16: return launch2<256, EPI_STORE_BF16>(A, B, M, N, K, ep, s);
@@ -290,5 +364,6 @@ int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind
   }
   return -1;
 }
+}  // namespace
 
 }  // namespace fragk

@@ -52,9 +52,10 @@ struct GemmTimer;  // optional per-launch event hook (bench roofline)
 int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
                  cudaStream_t stream, int force_bn = 0);
 int gemm_pick_bn(int M, int N, int K);
-// CTA-pair (cta_group::2) variant: 256 x bn tiles (bn = 128 or 256), no split-K.
+// CTA-pair (cta_group::2) variant: 256 x bn tiles (bn = 128 or 256); the last
+// partial wave split along K unless tail_split is false.
 int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
-                      cudaStream_t stream, int bn);
+                      cudaStream_t stream, int bn, bool tail_split = true);
 int num_sms();
 
 // TMA descriptors (bf16, SWIZZLE_128B, 64-element inner box), encoded through the

@@ -136,10 +136,13 @@ def test_rope_shift_bit_exact(cuda, delta):
     assert np.array_equal(got, exp)
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 512, 256), (2490, 1024, 4096), (1000, 768, 512)])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 512, 256), (2490, 1024, 4096), (1000, 768, 512),
+                                   (2490, 4096, 4096), (1000, 6144, 512)])
 @pytest.mark.parametrize("bn", [128, 256])
-def test_gemm_cta_pair_vs_torch(cuda, M, N, K, bn):
-    """cta_group::2 GEMM (256-row tiles shared by a CTA pair)."""
+@pytest.mark.parametrize("tail", [0, 1])
+def test_gemm_cta_pair_vs_torch(cuda, M, N, K, bn, tail):
+    """cta_group::2 GEMM (256-row tiles shared by a CTA pair); tail=1 splits the
+    last partial wave of pairs along K (deterministic last-CTA reduction)."""
     import torch
     if N % bn:
         pytest.skip("N not a multiple of BN")
@@ -148,12 +151,17 @@ def test_gemm_cta_pair_vs_torch(cuda, M, N, K, bn):
     b = torch.randn(N, K, device=cuda, generator=g).to(torch.bfloat16)
     ref = a.double() @ b.double().T
     c = torch.empty(M, N, device=cuda, dtype=torch.float32)
-    _gemm(a, b, c, 1, bn | 0x40000)
+    flags = bn | 0x40000 | (0x10000 if tail else 0)
+    _gemm(a, b, c, 1, flags)
     torch.cuda.synchronize()
     err = (c.double() - ref).abs().max().item()
     assert err <= 2e-5 * math.sqrt(K) * ref.abs().max().item() + 1e-4, err
+    c2 = torch.empty_like(c)
+    _gemm(a, b, c2, 1, flags)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)  # deterministic (split reduction in split order)
     r0 = torch.randn(M, N, device=cuda, generator=g)
     r = r0.clone()
-    _gemm(a, b, r, 2, bn | 0x40000)
+    _gemm(a, b, r, 2, flags)
     torch.cuda.synchronize()
     assert torch.allclose(r, r0 + c, rtol=0, atol=1e-4 * ref.abs().max().item() + 1e-5)

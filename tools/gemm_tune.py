@@ -18,8 +18,8 @@ for M in Ms:
         c = torch.zeros(M, N, device=dev, dtype=torch.float32)
         res = []
         for bn in (0, 64, 128, 256, 1128, 1256):
-            for tail in ((0,) if bn == 0 or bn > 1000 else (0, 1)):
-                flags = (bn | (tail << 16) if bn < 1000 else (bn - 1000) | 0x40000) if bn else 0
+            for tail in ((0,) if bn == 0 else (0, 1)):
+                flags = (bn | (tail << 16) if bn < 1000 else (bn - 1000) | 0x40000 | (tail << 16)) if bn else 0
                 try:
                     for _ in range(3):
                         L.check(L.lib.frag_kernel_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), M, N, K, 2, flags, None))
@@ -31,7 +31,7 @@ for M in Ms:
                     e1.record()
                     torch.cuda.synchronize()
                     us = e0.elapsed_time(e1) / 20 * 1e3
-                    nm = f"pair{bn - 1000}" if bn > 1000 else f"bn{bn or 'auto'}{'+tail' if tail else ''}"
+                    nm = (f"pair{bn - 1000}" if bn > 1000 else f"bn{bn or 'auto'}") + ("+tail" if tail else "")
                     res.append((nm, round(us, 1), round(2 * M * N * K / us / 1e6, 0)))
                 except Exception as ex:
                     res.append((f"bn{bn}", "err", str(ex)[:40]))
