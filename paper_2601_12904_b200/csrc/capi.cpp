@@ -458,7 +458,9 @@ FRAG_API frag_status frag_kernel_gemm(const void* a, const void* b, void* c, int
     ep.counters_cap = (int)(cnt.bytes / sizeof(int));
     const int n = fragk::gemm_bf16_tc(static_cast<const bf16*>(a), static_cast<const bf16*>(b), M, N, K, kind, ep,
                                       static_cast<cudaStream_t>(stream), force_bn);
-    check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "gemm");
+    // flag 0x80000 (tuning tools): no synchronise, so back-to-back launches can
+    // be timed; the caller keeps them on one stream
+    if (!(force_bn & 0x80000)) check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "gemm");
     if (n < 0) fail(FRAG_E_CONTRACT, "unsupported GEMM shape (K % 64, N % 64 and N % BN required)");
     g_launches += n;
     check_cuda(cudaPeekAtLastError(), "gemm launch");

@@ -109,6 +109,56 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
 }
 
 
+// Sum n fp32 partials (row-major rows of BN, `sstride` floats apart) of this
+// thread's row in partial order and run the fused epilogue on 32-column
+// chunk units u = u0, u0 + du, ... (a unit is 2 chunks for SwiGLU).
+template <int BN, int EPI>
+__device__ __forceinline__ void reduce_partials(const EpiParams& ep, const float* base, size_t sstride, int n,
+                                                int u0, int du, int row, int col0) {
+  constexpr int CW = EPI == EPI_SWIGLU ? 2 : 1;
+  constexpr int UNITS = BN / 32 / CW;
+#pragma unroll 1
+  for (int u = u0; u < UNITS; u += du) {
+    uint32_t r[2][32];
+#pragma unroll
+    for (int h2 = 0; h2 < CW; ++h2) {
+      const int c = u * CW + h2;
+      float4 acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      int s2 = 0;
+      for (; s2 + 1 < n; s2 += 2) {  // two partials in flight per step
+        const float4* a = reinterpret_cast<const float4*>(base + s2 * sstride + c * 32);
+        const float4* b = reinterpret_cast<const float4*>(base + (s2 + 1) * sstride + c * 32);
+        float4 va[8], vb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) va[j] = __ldcg(a + j), vb[j] = __ldcg(b + j);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc[j].x += va[j].x, acc[j].y += va[j].y, acc[j].z += va[j].z, acc[j].w += va[j].w;
+          acc[j].x += vb[j].x, acc[j].y += vb[j].y, acc[j].z += vb[j].z, acc[j].w += vb[j].w;
+        }
+      }
+      if (s2 < n) {
+        const float4* a = reinterpret_cast<const float4*>(base + s2 * sstride + c * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v = __ldcg(a + j);
+          acc[j].x += v.x, acc[j].y += v.y, acc[j].z += v.z, acc[j].w += v.w;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        r[h2][4 * j] = __float_as_uint(acc[j].x);
+        r[h2][4 * j + 1] = __float_as_uint(acc[j].y);
+        r[h2][4 * j + 2] = __float_as_uint(acc[j].z);
+        r[h2][4 * j + 3] = __float_as_uint(acc[j].w);
+      }
+    }
+    epi_chunk<EPI>(ep, row, col0 + u * CW * 32, r[0], r[CW - 1]);
+  }
+}
+
 // ---------------------------------------------------------------- split-K fixup
 // Cooperative, deterministic reduction of one split-K tile slot. Every split
 // CTA has written its fp32 partial (ws_rows x BN, row-major, one row per TMEM
@@ -134,58 +184,52 @@ __device__ __forceinline__ void split_fixup(const EpiParams& ep, int slot, int S
     } while (v < S);
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
-  constexpr int CW = EPI == EPI_SWIGLU ? 2 : 1;  // 32-col chunks per epilogue unit
-  constexpr int UNITS = BN / 32 / CW;
   const float* base = ep.ws + ((size_t)slot * S * ws_rows + row_in_tile) * BN;
-  const size_t sstride = (size_t)ws_rows * BN;
-  if (row_in_tile < ws_rows && row < M) {
-#pragma unroll 1
-    for (int u = sp; u < UNITS; u += S) {
-      uint32_t r[2][32];
-#pragma unroll
-      for (int h2 = 0; h2 < CW; ++h2) {
-        const int c = u * CW + h2;
-        float4 acc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        int s2 = 0;
-        for (; s2 + 1 < S; s2 += 2) {  // two partials in flight per step
-          const float4* a = reinterpret_cast<const float4*>(base + s2 * sstride + c * 32);
-          const float4* b = reinterpret_cast<const float4*>(base + (s2 + 1) * sstride + c * 32);
-          float4 va[8], vb[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) va[j] = __ldcg(a + j), vb[j] = __ldcg(b + j);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            acc[j].x += va[j].x, acc[j].y += va[j].y, acc[j].z += va[j].z, acc[j].w += va[j].w;
-            acc[j].x += vb[j].x, acc[j].y += vb[j].y, acc[j].z += vb[j].z, acc[j].w += vb[j].w;
-          }
-        }
-        if (s2 < S) {
-          const float4* a = reinterpret_cast<const float4*>(base + s2 * sstride + c * 32);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 v = __ldcg(a + j);
-            acc[j].x += v.x, acc[j].y += v.y, acc[j].z += v.z, acc[j].w += v.w;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          r[h2][4 * j] = __float_as_uint(acc[j].x);
-          r[h2][4 * j + 1] = __float_as_uint(acc[j].y);
-          r[h2][4 * j + 2] = __float_as_uint(acc[j].z);
-          r[h2][4 * j + 3] = __float_as_uint(acc[j].w);
-        }
-      }
-      epi_chunk<EPI>(ep, row, col0 + u * CW * 32, r[0], r[CW - 1]);
-    }
-  }
+  if (row_in_tile < ws_rows && row < M)
+    reduce_partials<BN, EPI>(ep, base, (size_t)ws_rows * BN, S, sp, S, row, col0);
   // second round of arrivals: the last CTA out resets the counter for the next GEMM
   asm volatile("bar.sync 1, 128;" ::: "memory");
   if (warp2_lane0) {
     const int old = atomicAdd(cnt, 1);
     if (old == 2 * S - 1) *cnt = 0;
   }
+}
+
+// ---------------------------------------------------------------- stream-K
+// CTA whose k-block range [c*I/G, (c+1)*I/G) holds flattened k-block pos.
+__device__ __forceinline__ int sk_cta_of(long long pos, long long I, int G) {
+  int c = (int)(pos * G / I);
+  while (c + 1 < G && I * (c + 1) / G <= pos) ++c;
+  while (c > 0 && I * c / G > pos) --c;
+  return c;
+}
+
+// Finish one stream-K part of a tile shared by n CTAs (this one is the j-th,
+// counted from the owner; its partial is already in workspace slot j).
+// Contributors (j > 0) publish and leave; the owner (j = 0, whose part is its
+// last) waits for the n-1 others, sums slots 0..n-1 in order and runs the
+// fused epilogue. 4 epilogue warps, named barrier 1.
+template <int BN, int EPI>
+__device__ __forceinline__ void sk_finish(const EpiParams& ep, int tile, int j, int n, int ws_rows, int row_in_tile,
+                                          int row, int M, int col0, bool leader) {
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  int* cnt = ep.counters + tile;
+  if (j > 0) {
+    if (leader) atomicAdd(cnt, 1);
+    return;
+  }
+  if (leader) {
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+      if (v < n - 1) __nanosleep(32);
+    } while (v < n - 1);
+    *cnt = 0;  // every contributor has arrived: reset for the next GEMM
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const float* base = ep.ws + ((size_t)tile * ep.sk_maxc * ws_rows + row_in_tile) * BN;
+  if (row_in_tile < ws_rows && row < M) reduce_partials<BN, EPI>(ep, base, (size_t)ws_rows * BN, n, 0, 1, row, col0);
 }
 
 }  // namespace

@@ -88,20 +88,47 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // work items: the first `full` tiles whole, then the remaining (tail) tiles
-  // each cut into `splits` K ranges, reduced deterministically and
-  // cooperatively by the tile's split CTAs (split_fixup; split-K for the last
-  // partial wave and for few-tile small-M GEMMs).
+  // Work decomposition, one of:
+  //  * units: the first `full_tiles` tiles whole, then each tail tile cut into
+  //    `splits` K ranges reduced cooperatively by its split CTAs (split_fixup);
+  //  * stream-K (ep.streamk, one M tile): CTA c owns k-blocks
+  //    [c*I/G, (c+1)*I/G) of the flattened (tile, k-block) space, I = tiles*nk,
+  //    cut at tile boundaries into parts. A tile spread over several CTAs is
+  //    finished by the CTA holding its first k-block (the "owner"): that part
+  //    is the owner's last, while the other contributors' parts are their
+  //    first, so the owner never waits on work that has not started; it sums
+  //    the partials in CTA order (deterministic) and runs the epilogue.
+  const bool sk = ep.streamk != 0;
   const int splits = ep.splits > 1 ? ep.splits : 1;
   const int n_full = splits > 1 ? ep.full_tiles : num_tiles;
   const int num_work = n_full + (num_tiles - n_full) * splits;
-  auto decode = [&](int w, int& tile, int& sp, int& S) {
+  const long long I = (long long)num_tiles * nk;
+  const int G = gridDim.x;
+  const long long sk_hi = sk ? I * (blockIdx.x + 1) / G : 0;
+  auto first = [&]() -> long long { return sk ? I * blockIdx.x / G : (long long)blockIdx.x; };
+  // next part: tile, [kb0, kb1), split sp of S (S = 0 marks a stream-K part)
+  auto next = [&](long long& st, int& tile, int& kb0, int& kb1, int& sp, int& S) -> bool {
+    if (sk) {
+      if (st >= sk_hi) return false;
+      tile = (int)(st / nk);
+      kb0 = (int)(st % nk);
+      const long long left = sk_hi - st;
+      kb1 = left < nk - kb0 ? kb0 + (int)left : nk;
+      sp = 0, S = 0;
+      st += kb1 - kb0;
+      return true;
+    }
+    if (st >= num_work) return false;
+    const int w = (int)st;
     if (w < n_full) {
       tile = w, sp = 0, S = 1;
     } else {
       const int u = w - n_full;
       tile = n_full + u / splits, sp = u % splits, S = splits;
     }
+    kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
+    st += G;
+    return true;
   };
   if (warp == 0) {
     if (elect_one()) {
@@ -110,25 +137,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
       // stages' B loads before waiting on it (programmatic dependent launch),
       // then the activation (A) loads once its output is visible.
       int npre = 0;
-      if ((int)blockIdx.x < num_work) {
-        int tile, sp, S;
-        decode(blockIdx.x, tile, sp, S);
-        const int n_blk = tile / m_tiles;
-        const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
-        npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
-        for (int i = 0; i < npre; ++i) {
-          mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
-          tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
+      {
+        long long st = first();
+        int tile, kb0, kb1, sp, S;
+        if (next(st, tile, kb0, kb1, sp, S)) {
+          const int n_blk = tile / m_tiles;
+          npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
+          for (int i = 0; i < npre; ++i) {
+            mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+            tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
+          }
         }
       }
       pdl_wait();
       int stage = 0, it = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
-        int tile, sp, S;
-        decode(w, tile, sp, S);
+      long long st = first();
+      int tile, kb0, kb1, sp, S;
+      while (next(st, tile, kb0, kb1, sp, S)) {
         const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
-        const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           if (it >= npre) {
             mbar_wait(&empty[stage], phase ^ 1);
@@ -149,10 +176,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
-      int tile, sp, S;
-      decode(w, tile, sp, S);
-      const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
+    long long st = first();
+    int tile, kb0, kb1, sp, S;
+    while (next(st, tile, kb0, kb1, sp, S)) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -184,19 +210,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
     pdl_wait();  // the epilogue reads/writes buffers of the preceding kernels
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = q * 32 + lane;
-    const int ws_rows = m_tiles == 1 ? M : BM;  // rows kept per split partial
+    const int ws_rows = m_tiles == 1 ? M : BM;  // rows kept per split / stream-K partial
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
-      int tile, sp, S;
-      decode(w, tile, sp, S);
+    long long st = first();
+    int tile, kb0, kb1, sp, S;
+    while (next(st, tile, kb0, kb1, sp, S)) {
       const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
       const int ti = tile - n_full;  // tail index (workspace / counter slot)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * BM + row_in_tile;
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (S == 1) {
+      if (S == 0 && !(kb0 == 0 && kb1 == nk)) {
+        // stream-K part of a tile shared by several CTAs: partial -> workspace
+        // slot (tile, CTA offset from the owner), TMEM released right away
+        const long long p0 = (long long)tile * nk;
+        const int c_own = sk_cta_of(p0, I, G);
+        const int j = (int)blockIdx.x - c_own;
+        float* wsp = ep.ws + (((size_t)tile * ep.sk_maxc + j) * ws_rows + row_in_tile) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(t_row + c * 32, r);
+          tmem_ld_wait();
+          if (row_in_tile < ws_rows) {
+            float4* dst = reinterpret_cast<float4*>(wsp + c * 32);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              __stcg(dst + e, make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                          __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3])));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        const int n_contrib = sk_cta_of(p0 + nk - 1, I, G) - c_own + 1;
+        sk_finish<BN, EPI>(ep, tile, j, n_contrib, ws_rows, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0);
+      } else if (S <= 1) {
         if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
           for (int c = 0; c < BN / 32; c += 2) {
@@ -310,7 +361,7 @@ int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& e
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int slots = num_sms() * C::MIN_BLOCKS;
-  const int grid = work < slots ? work : slots;
+  const int grid = ep.streamk ? ep.streamk : (work < slots ? work : slots);
   launch_pdl(gemm_tc_kernel<BN, EPI>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
@@ -398,23 +449,38 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
   EpiParams ep = ep0;
   ep.splits = 1;
   int bn = force_bn ? force_bn : gemm_pick_bn(M, N, K);
-  if (!force_bn && M <= BM && K >= 8192 && N / 64 < num_sms() && ep.ws && ep.counters) {
-    // Long-K weight-streaming shape (one M tile, few N tiles, e.g. the FFN down
-    // projection of the question pass): deterministic split-K so more CTAs
-    // stream the weights.
-    bn = 64;
-    const long tiles = N / 64, slots = (long)num_sms(), nk = K / BK;
-    long best = -1, best_s = 1;
-    for (long s = 1; s <= 8 && s * 4 <= nk; ++s) {
-      if (tiles > ep.counters_cap) break;
-      if ((size_t)(tiles * s * M * 64) * sizeof(float) > ep.ws_bytes) break;
-      const long cost = ((tiles * s + slots - 1) / slots) * ((nk + s - 1) / s);
-      if (best < 0 || cost < best) best = cost, best_s = s;
-    }
-    ep.splits = (int)best_s;
+  const int force_splits = (force_bn_flags >> 20) & 0xf;  // tuning: fixed small-M split count
+  if (M <= BM && ep.ws && ep.counters) {
+    // One M tile (question pass, lm_head rows): a pure weight stream. BN=128
+    // and deterministic split-K up to one full wave of CTAs (a second partial
+    // round or a fixup per extra split costs more than it saves; measured with
+    // tools/gemm_small.py, profiles/gemm_small_r01.txt).
+    if (!force_bn) bn = N % 128 == 0 ? 128 : 64;
+    const long tiles = N / bn, sms = (long)num_sms(), nk = K / BK;
+    long s = 1;
+    while (s < 8 && tiles * (s + 1) <= sms && nk / (s + 1) >= 4) ++s;
+    if (force_splits > 0) s = force_splits;
+    if (s > nk) s = nk;  // every split needs at least one K block
+    if (tiles > ep.counters_cap || (size_t)(tiles * s * M * bn) * sizeof(float) > ep.ws_bytes) s = 1;
+    ep.splits = (int)s;
     ep.full_tiles = 0;
   }
   if (N % bn != 0) return -1;
+  const bool want_sk = (force_bn_flags & 0x2000000) != 0;  // tuning: force stream-K
+  if (M <= BM && want_sk && ep.ws && ep.counters) {
+    // stream-K over the flattened (N tile, k-block) space: every SM streams the
+    // same number of weight k-blocks whatever the tile count
+    const long long tiles = N / bn, nk = K / BK, I = tiles * nk;
+    long long G = num_sms();
+    if (I / G < 4) G = I / 4 > 0 ? I / 4 : 1;
+    const long long q = I / G;
+    const long long maxc = (nk + q - 1) / q + 1;
+    if (tiles <= ep.counters_cap && (size_t)(tiles * maxc * M * bn) * sizeof(float) <= ep.ws_bytes) {
+      ep.splits = 1;
+      ep.streamk = (int)G;
+      ep.sk_maxc = (int)maxc;
+    }
+  }
   // Large M: CTA-pair tiles (256 x 256, cta_group::2) beat every 1-CTA shape in
   // the B200 sweep (profiles/gemm_tune_r01.txt) for the projection shapes.
   if (!force_bn && M >= 256 && N % 256 == 0 && ep.splits == 1)

@@ -44,6 +44,8 @@ struct EpiParams {
   int counters_cap = 0;
   int splits = 1;      // set by gemm_bf16_tc: K splits of each tail tile
   int full_tiles = 0;  // tiles before the split tail
+  int streamk = 0;     // set by gemm_bf16_tc: stream-K decomposition (one M tile)
+  int sk_maxc = 0;     // stream-K: max CTAs sharing one tile (workspace slots per tile)
 };
 
 struct GemmTimer;  // optional per-launch event hook (bench roofline)

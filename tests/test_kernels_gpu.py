@@ -165,3 +165,40 @@ def test_gemm_cta_pair_vs_torch(cuda, M, N, K, bn, tail):
     _gemm(a, b, r, 2, flags)
     torch.cuda.synchronize()
     assert torch.allclose(r, r0 + c, rtol=0, atol=1e-4 * ref.abs().max().item() + 1e-5)
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 6144, 4096), (1, 4096, 14336), (100, 1280, 512), (128, 512, 256),
+                                   (32, 28672, 4096)])
+@pytest.mark.parametrize("bn", [64, 128])
+def test_gemm_stream_k_vs_torch(cuda, M, N, K, bn):
+    """Stream-K decomposition of the one-M-tile (question pass) GEMM: tiles
+    shared by several CTAs finished by their owner in CTA order."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + bn)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device=cuda, generator=g).to(torch.bfloat16)
+    ref = a.double() @ b.double().T
+    flags = bn | 0x2000000
+    c = torch.empty(M, N, device=cuda, dtype=torch.float32)
+    _gemm(a, b, c, 1, flags)
+    torch.cuda.synchronize()
+    err = (c.double() - ref).abs().max().item()
+    assert err <= 2e-5 * math.sqrt(K) * ref.abs().max().item() + 1e-4, err
+    c2 = torch.empty_like(c)
+    _gemm(a, b, c2, 1, flags)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+    r0 = torch.randn(M, N, device=cuda, generator=g)
+    r = r0.clone()
+    _gemm(a, b, r, 2, flags)
+    torch.cuda.synchronize()
+    assert torch.equal(r, r0 + c)
+    F = N // 2
+    out = torch.empty(M, F, device=cuda, dtype=torch.bfloat16)
+    _gemm(a, b, out, 3, flags)
+    torch.cuda.synchronize()
+    idx = torch.arange(F, device=cuda)
+    gg = c[:, (idx // 32) * 64 + idx % 32]
+    uu = c[:, (idx // 32) * 64 + 32 + idx % 32]
+    want = torch.nn.functional.silu(gg) * uu
+    assert (out.float() - want).abs().max().item() <= 1e-2 * want.abs().max().item() + 1e-3

@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_kernels_gpu.py -q -x -k "gemm" 2>&1 | tail -3
-python tools/gemm_tune.py 2490,16416 2>&1 | tail -8
+timeout 300 python -m pytest tests/test_kernels_gpu.py -q -x -k "stream_k or small_m" 2>&1 | tail -5
+timeout 300 python tools/gemm_small.py 32 tiny,small,qkv,o,gu,down > gpurun_out/gs.log 2>&1; cut -c1-400 gpurun_out/gs.log
