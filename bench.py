@@ -36,6 +36,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+N_CLASSES = 6  # frag_engine_profile_read classes (frag_c.h)
+CLASS_NAMES = ["gemm", "attention", "stitch", "norm", "select", "gemm_stream"]
 METRIC = "TTFT ms at 16k-token RAG prompt, 15% recompute vs full prefill; prefill tok/s"
 CONFIGS = {
     "llama3-8b": dict(preset="llama3-8b", chunks=8, chunk_len=2048, qlen=32, ratio=0.15),
@@ -58,6 +60,22 @@ def parse():
     p.add_argument("--cpu-layers", type=int, default=1)
     p.add_argument("--sweep", default="", help="comma list of extra ratios to time (e.g. 0,0.05,0.3)")
     return p.parse_args()
+
+
+# ---------------------------------------------------------------- multi-rank
+def max_over_ranks(vals, device):
+    """Element-wise max of per-rank device times (one process per GPU; no
+    collective touches the data path -- requests are independent)."""
+    import torch
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return t.tolist()
+
+
+def job_throughput(world, steps, tokens_per_request, max_ms):
+    """Whole-job tok/s: every rank served `steps` requests of `tokens_per_request`
+    prompt tokens; the job took the slowest rank's time (weak scaling)."""
+    return world * steps * tokens_per_request / (max_ms / 1e3)
 
 
 # ---------------------------------------------------------------- clocks
@@ -205,12 +223,12 @@ def run_ours(args, rank, world, local_rank):
     # events around every launch on the launching stream (kept out of the
     # headline loop because the ~700 event records per request cost host time)
     eng.profile(True)
-    for k in range(5):
+    for k in range(N_CLASSES):
         eng.profile_read(k, reset=True)
     for i in range(args.steps):
         step_dev(args.warmup + i)
     torch.cuda.synchronize()
-    prof = {k: eng.profile_read(k) for k in range(5)}
+    prof = {k: eng.profile_read(k) for k in range(N_CLASSES)}
     eng.profile(False)
 
     # ---- stage breakdown (one extra request with per-stage events)
@@ -301,13 +319,11 @@ def main():
     import torch
     ms, e2e_ms, full_ms = r["ms"], r["e2e_ms"], r["full_ms"]
     if world > 1:
-        t = torch.tensor([ms, e2e_ms, full_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms, e2e_ms, full_ms = t.tolist()
+        ms, e2e_ms, full_ms = max_over_ranks([ms, e2e_ms, full_ms], torch.device("cuda", local_rank))
     T = r["T"]
     ttft = ms / args.steps
-    value = world * args.steps * T / (ms / 1e3)
-    e2e_value = world * args.steps * T / (e2e_ms / 1e3)
+    value = job_throughput(world, args.steps, T, ms)
+    e2e_value = job_throughput(world, args.steps, T, e2e_ms)
     sus, burst, hbm, src = peaks()
     g = r["prof"][0]
     gemm_tflops = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
@@ -315,7 +331,8 @@ def main():
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get("gemm_tc_kernel_bytes_per_launch")
+            js = json.loads(tf.read_text())
+            traffic = js.get("gemm_tc2_kernel_bytes_per_launch", js.get("gemm_tc_kernel_bytes_per_launch"))
         except Exception:
             traffic = None
     c = r["cfg"]
@@ -335,18 +352,21 @@ def main():
         "e2e": {"value": e2e_value, "unit": "tok/s", "ttft_ms": e2e_ms / args.steps,
                 "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"],
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05, K4/K7/K8/K11)",
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc2_kernel / gemm_tc_kernel (tcgen05, K4/K7/K8 at M>128)",
                      "achieved": gemm_tflops, "peak": sus, "unit": "TFLOP/s",
                      "frac": (gemm_tflops / sus) if gemm_tflops else None, "traffic": traffic,
                      "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside the long step)",
                      "gemm_share_of_step": g["ms"] / ms if ms else None},
         "kernels": {name: {"ms_per_step": r["prof"][k]["ms"] / args.steps,
                            "launches_per_step": r["prof"][k]["launches"] / args.steps}
-                    for k, name in enumerate(["gemm", "attention", "stitch", "norm", "select"])},
+                    for k, name in enumerate(CLASS_NAMES)},
         "attention": {"achieved_tflops": attn_flops / (a["ms"] / args.steps / 1e3) / 1e12 if a["ms"] else None,
                       "flops_per_step": attn_flops},
         "stitch": {"achieved_gbs": (r["prof"][2]["bytes"] / (r["prof"][2]["ms"] / 1e3) / 1e9)
                    if r["prof"][2]["ms"] else None, "peak_gbs": hbm},
+        "gemm_stream": {"achieved_gbs": (r["prof"][5]["bytes"] / (r["prof"][5]["ms"] / 1e3) / 1e9)
+                        if r["prof"][5]["ms"] else None, "peak_gbs": hbm,
+                        "note": "one-M-tile GEMMs (question pass, lm_head): algorithmic bytes = weights + rows"},
         "clocks": r["clocks"],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -373,7 +373,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       ep.Hq = Hq;
       ep.Hkv = Hkv;
       ep.dh = dh;
-      Scoped sc(P, s, KC_GEMM, 2.0 * M * qkv * d, 2.0 * (qkv * d + (double)M * (d + qkv)));
+      Scoped sc(P, s, gemm_class(M), 2.0 * M * qkv * d, 2.0 * (qkv * d + (double)M * (d + qkv)));
       sc.launched(fragk::gemm_bf16_tc(x, W.wqkv, M, (int)qkv, d, fragk::EPI_QKV, ep, s));
     }
     if (mode != PASS_FULL && l == c.layers - 1) break;
@@ -402,7 +402,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       with_ws(ep);
       ep.resid = h;
       ep.ldo = d;
-      Scoped sc(P, s, KC_GEMM, 2.0 * M * d * qc, 2.0 * (qc * d + (double)M * qc) + 8.0 * M * d);
+      Scoped sc(P, s, gemm_class(M), 2.0 * M * d * qc, 2.0 * (qc * d + (double)M * qc) + 8.0 * M * d);
       sc.launched(fragk::gemm_bf16_tc(r->attn.as<bf16>(), W.wo, M, d, (int)qc, fragk::EPI_RESID, ep, s));
     }
     {
@@ -415,7 +415,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       with_ws(ep);
       ep.out_bf16 = r->act.as<bf16>();
       ep.ldo = F;
-      Scoped sc(P, s, KC_GEMM, 2.0 * M * 2.0 * F * d, 2.0 * (2.0 * F * d + (double)M * d + (double)M * F));
+      Scoped sc(P, s, gemm_class(M), 2.0 * M * 2.0 * F * d, 2.0 * (2.0 * F * d + (double)M * d + (double)M * F));
       sc.launched(fragk::gemm_bf16_tc(x, W.wgu, M, 2 * F, d, fragk::EPI_SWIGLU, ep, s));
     }
     {
@@ -423,7 +423,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       with_ws(ep);
       ep.resid = h;
       ep.ldo = d;
-      Scoped sc(P, s, KC_GEMM, 2.0 * M * (double)d * F, 2.0 * ((double)F * d + (double)M * F) + 8.0 * M * d);
+      Scoped sc(P, s, gemm_class(M), 2.0 * M * (double)d * F, 2.0 * ((double)F * d + (double)M * F) + 8.0 * M * d);
       sc.launched(fragk::gemm_bf16_tc(r->act.as<bf16>(), W.wd, M, d, F, fragk::EPI_RESID, ep, s));
     }
     peek("layer");
@@ -440,7 +440,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     with_ws(ep);
     ep.out_f32 = r->logits.as<float>();
     ep.ldo = c.vocab;
-    Scoped sc(P, s, KC_GEMM, 2.0 * n_logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
+    Scoped sc(P, s, gemm_class(n_logit_rows), 2.0 * n_logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
     sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, n_logit_rows, c.vocab, d,
                                     fragk::EPI_STORE_F32, ep, s));
   }
@@ -855,7 +855,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
       ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
       ep.out_f32 = r->logits.as<float>();
       ep.ldo = c.vocab;
-      Scoped sc(e->prof, bs, KC_GEMM, 2.0 * r->logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
+      Scoped sc(e->prof, bs, gemm_class(r->logit_rows), 2.0 * r->logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
       sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, r->logit_rows, c.vocab, d,
                                       fragk::EPI_STORE_F32, ep, bs));
     }

@@ -73,7 +73,10 @@ struct DeviceGuard {
 };
 
 // ---------------------------------------------------------------- profiling
-enum KClass { KC_GEMM = 0, KC_ATTN = 1, KC_STITCH = 2, KC_NORM = 3, KC_SELECT = 4, KC_N = 5 };
+// KC_GEMM: tensor-bound GEMMs (M > 128 rows); KC_GEMM_STREAM: one-M-tile
+// GEMMs (question pass, lm_head rows), bound by the weight stream from HBM.
+enum KClass { KC_GEMM = 0, KC_ATTN = 1, KC_STITCH = 2, KC_NORM = 3, KC_SELECT = 4, KC_GEMM_STREAM = 5, KC_N = 6 };
+inline int gemm_class(int M) { return M <= 128 ? KC_GEMM_STREAM : KC_GEMM; }
 struct Profiler {
   bool on = false;
   struct Rec {
