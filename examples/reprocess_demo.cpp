@@ -40,7 +40,7 @@ int main(int argc, char** argv) {
     }
     std::vector<frag::Token> q(32);
     for (auto& t : q) t = static_cast<frag::Token>(rng.below(cfg.vocab));
-    frag::Result res(eng, n_chunks * chunk_len + 32);
+    frag::Result res(eng, n_chunks * chunk_len + 32 + 16);  // + room for 16 decoded tokens
     frag_reprocess_opts opts{};
     opts.timing = 1;
     eng.reprocess(store, q, ids, ratio, res, {}, &opts);
@@ -49,6 +49,11 @@ int main(int argc, char** argv) {
                 "sparse %.3f, lm_head %.3f)\n",
                 preset.c_str(), n_chunks * chunk_len + 32, res.critical_positions().size(), res.first_token(),
                 t.total_ms, t.stitch_ms, t.question_ms, t.select_ms, t.sparse_ms, t.lm_head_ms);
+    // sparse_prefill_and_decode: greedy answer over the fused cache
+    const auto answer = eng.decode(res, 16);
+    std::printf("answer:");
+    for (auto tok : answer) std::printf(" %d", tok);
+    std::printf("\n");
     return 0;
   } catch (const frag::CudaError& e) {
     std::fprintf(stderr, "CudaError: %s\n", e.what());

@@ -176,6 +176,15 @@ FRAG_API frag_status frag_full_prefill(frag_engine* eng, const int32_t* sys, int
                                        int32_t n_tok, const frag_reprocess_opts* opts, void* stream,
                                        frag_result* res);
 
+/* sparse_prefill_and_decode, decode half: greedy decoding
+ * continuing the last frag_reprocess / frag_full_prefill of `res`. Token 0 is
+ * the argmax of the last logits row (lowest index on ties); each further token
+ * is one single-row step at the next position whose K/V are appended to the
+ * result's fused cache (the request's exclusive pages; records untouched).
+ * Needs result capacity >= T + max_new_tokens - 1. Writes max_new_tokens ids
+ * to host tokens_out; afterwards the result holds the last step's logits. */
+FRAG_API frag_status frag_decode(frag_engine* eng, frag_result* res, int32_t max_new_tokens, void* stream,
+                                 int32_t* tokens_out);
 FRAG_API frag_status frag_result_sync(frag_result* res);
 /* Fused cache: device pointers [L][T][Hkv][dh] bf16, T = tokens in the prompt. */
 FRAG_API frag_status frag_result_fused_kv(const frag_result* res, const void** k_dev, const void** v_dev,

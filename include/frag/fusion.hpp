@@ -7,6 +7,7 @@
 //                                            sparse_prefill_and_decode to the first token
 //
 //   Engine::full_prefill                     Eq. 2 Full Attention with the same kernels
+//   Engine::decode                           greedy decoding over the fused cache
 // Status codes from the C ABI are re-thrown as the reference's exception
 // classes (common.hpp:17-40): ContractError, StoreError, FormatError.
 #pragma once
@@ -175,6 +176,14 @@ class Engine {
                     const frag_reprocess_opts* opts = nullptr, void* cuda_stream = nullptr) {
     check(frag_full_prefill(h_, system.data(), static_cast<int32_t>(system.size()), tokens.data(),
                             static_cast<int32_t>(tokens.size()), opts, cuda_stream, out.handle()));
+  }
+
+  // Greedy decoding after reprocess / full_prefill (sparse_prefill_and_decode,
+  // SPEC.md:435-438): max_new_tokens ids; decoded K/V appended to `res`.
+  std::vector<Token> decode(Result& res, int max_new_tokens, void* cuda_stream = nullptr) {
+    std::vector<Token> out(max_new_tokens > 0 ? max_new_tokens : 0);
+    check(frag_decode(h_, res.handle(), max_new_tokens, cuda_stream, out.data()));
+    return out;
   }
 
   frag_engine* handle() const { return h_; }

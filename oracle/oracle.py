@@ -225,7 +225,38 @@ class Model:
             raise ValueError(f"orc_reprocess failed ({rc})")
         k = kk.value
         return {"k": kc[:, :T], "v": vc[:, :T], "logits": logits, "crit": crit[:k].copy(), "q_final": qf,
-                "scores": scores[:N], "stage_seconds": stages, "T": T}
+                "scores": scores[:N], "stage_seconds": stages, "T": T, "k_cache": kc, "v_cache": vc}
+
+    # ------------------------------------------------------------ decode
+    def decode_forced(self, cache_k, cache_v, T, tokens, emulate_bf16=True):
+        """Decode steps of sparse_prefill_and_decode with given inputs: token i
+        is fed at position T+i+1 (cache slot T+i) against the fused cache, its
+        K/V appended (exclusive pages); returns the logits after each step
+        [len(tokens)][V]. Greedy decoding = feeding back the argmax."""
+        cap = cache_k.shape[1]
+        assert T + len(tokens) <= cap
+        pos = np.zeros(cap, np.int32)
+        pos[:T] = np.arange(1, T + 1, dtype=np.int32)
+        out = []
+        for i, t in enumerate(tokens):
+            lg, _ = self.forward([int(t)], [T + i + 1], [T + i], cache_k, cache_v, pos, logit_rows=[0],
+                                 emulate_bf16=emulate_bf16)
+            out.append(lg[0].copy())
+        return np.array(out)
+
+    def greedy_decode(self, cache_k, cache_v, T, first_logits, n, emulate_bf16=True):
+        """Greedy decoding of n tokens (token 0 = argmax(first_logits), lowest
+        index on ties)."""
+        toks = [int(np.argmax(first_logits))]
+        for i in range(n - 1):
+            pos_T = T + i
+            cap = cache_k.shape[1]
+            pos = np.zeros(cap, np.int32)
+            pos[:pos_T] = np.arange(1, pos_T + 1, dtype=np.int32)
+            lg, _ = self.forward([toks[-1]], [pos_T + 1], [pos_T], cache_k, cache_v, pos, logit_rows=[0],
+                                 emulate_bf16=emulate_bf16)
+            toks.append(int(np.argmax(lg[0])))
+        return np.array(toks, np.int32)
 
 
 def stitch(cfg, chunks, cap, round_bf16=True):

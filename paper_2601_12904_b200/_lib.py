@@ -93,6 +93,7 @@ _SIGS = {
     "frag_reprocess_dev": (C.c_int, [_P, _P, _I32P, C.c_int32, _P, C.c_int32, C.POINTER(ChunkId), C.c_int32,
                                      C.c_float, C.POINTER(ReprocessOpts), _P, _P]),
     "frag_full_prefill": (C.c_int, [_P, _I32P, C.c_int32, _I32P, C.c_int32, C.POINTER(ReprocessOpts), _P, _P]),
+    "frag_decode": (C.c_int, [_P, _P, C.c_int32, _P, _I32P]),
     "frag_result_sync": (C.c_int, [_P]),
     "frag_result_fused_kv": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), _I32P]),
     "frag_result_logits": (C.c_int, [_P, C.POINTER(C.POINTER(C.c_float)), _I32P, _I32P, C.c_int32]),

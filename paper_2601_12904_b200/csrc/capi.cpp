@@ -346,6 +346,14 @@ FRAG_API frag_status frag_full_prefill(frag_engine* eng, const int32_t* sys, int
   });
 }
 
+FRAG_API frag_status frag_decode(frag_engine* eng, frag_result* res, int32_t max_new_tokens, void* stream,
+                                 int32_t* tokens_out) {
+  return guard([&] {
+    need(eng && res && tokens_out, "null argument");
+    decode(eng->e, res->r, max_new_tokens, static_cast<cudaStream_t>(stream), tokens_out);
+  });
+}
+
 FRAG_API frag_status frag_result_sync(frag_result* res) {
   return guard([&] {
     need(res, "null result");

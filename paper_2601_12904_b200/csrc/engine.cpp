@@ -917,6 +917,50 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
   finish(r, timing, s);
 }
 
+void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) {
+  const auto& c = e->cfg;
+  if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
+  if (n_new < 1) fail(FRAG_E_CONTRACT, "max_new_tokens must be >= 1");
+  if (!out_host) fail(FRAG_E_CONTRACT, "tokens_out is null");
+  if (r->T <= 0 || r->logit_rows < 1) fail(FRAG_E_CONTRACT, "decode needs a preceding reprocess or full prefill");
+  const int T0 = r->T;
+  if (T0 + n_new - 1 > r->max_tokens)
+    fail(FRAG_E_CONTRACT, "decoded tokens exceed the result capacity (" + std::to_string(r->max_tokens) + ")");
+  DeviceGuard dg(e->device);
+  e->ensure_rope(T0 + n_new);
+  r->dec_tok.ensure((size_t)n_new * sizeof(int));
+  r->staging.ensure((size_t)n_new * sizeof(int) + 64);
+  int* stage = r->staging.as<int>();
+  stage[0] = 0;  // the single decode row is logits row 0
+  check_cuda(cudaMemcpyAsync(r->row_map.p, stage, sizeof(int), cudaMemcpyHostToDevice, s), "row map");
+  const float* last = r->logits.as<float>() + (size_t)(r->logit_rows - 1) * c.vocab;
+  for (int i = 0; i < n_new; ++i) {
+    // token i = argmax(logits of the previous position); it becomes the next row's input
+    {
+      Scoped sc(e->prof, s, KC_SELECT, 0, 4.0 * c.vocab);
+      sc.launched(fragk::greedy_argmax(last, c.vocab, r->dec_tok.as<int>() + i, r->plan_tok.as<int>(),
+                                       r->plan_rows.as<int>(), T0 + i, s));
+    }
+    if (i == n_new - 1) break;
+    run_rows(e, r, s, 1, T0 + i + 1, PASS_FULL, r->row_map.as<int>(), 1);
+    last = r->logits.as<float>();
+  }
+  peek("decode");
+  check_cuda(cudaMemcpyAsync(stage, r->dec_tok.p, (size_t)n_new * sizeof(int), cudaMemcpyDeviceToHost, s), "tokens");
+  if (n_new > 1) {
+    r->logit_rows = 1;
+    if (!r->logits_on_device) {
+      r->logits_host.ensure((size_t)c.vocab * sizeof(float));
+      logits_d2h(r, s);
+    }
+  }
+  r->last_stream = s;
+  check_cuda(cudaStreamSynchronize(s), "decode");
+  std::memcpy(out_host, stage, (size_t)n_new * sizeof(int));
+  r->T = T0 + n_new - 1;  // the fused cache now also holds the decoded tokens' K/V
+  r->timing_valid = false;
+}
+
 void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                          bool overwrite, frag_chunk_id* id_out) {
   const auto& c = e->cfg;

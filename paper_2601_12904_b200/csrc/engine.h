@@ -200,7 +200,7 @@ struct Result {
   int T = 0, S = 0, N = 0, nq = 0, k_sel = 0, M = 0, logit_rows = 0;
   // workspace
   DevBuf h, x, q, attn, act, plan_rows, plan_tok, chunk_tok, q_tok, q_final, scores, part_ms, row_ms, part_o,
-      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt;
+      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok;
   PinnedBuf staging, logits_host;
   // timing
   cudaEvent_t ev[7] = {};
@@ -228,6 +228,11 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
                cudaStream_t s, Result* r);
 void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                   const frag_reprocess_opts* o, cudaStream_t s, Result* r);
+// Greedy decoding after a reprocess / full prefill: token 0 =
+// argmax of the last logits row, then n_new-1 single-row steps at positions
+// T+1.. whose K/V are appended to the result's own fused cache (its exclusive
+// pages); the shared records are never touched.
+void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host);
 void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                          bool overwrite, frag_chunk_id* id_out);
 

@@ -122,6 +122,10 @@ int qg_score(const ScoreArgs& a, cudaStream_t stream);
 // then the question rows appended. Writes plan_rows[k + nq] and plan_tok.
 int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* chunk_tok, const int* q_tok,
               int nq, int q_row0, int* plan_rows, int* plan_tok, cudaStream_t stream);
+// Greedy decoding step: out[0] = argmax(logits[0..V)) (lowest index on ties),
+// also stored as the next step's plan token / row when the pointers are set.
+int greedy_argmax(const float* logits, int V, int* out, int* plan_tok, int* plan_rows, int next_row,
+                  cudaStream_t stream);
 
 // ------------------------------------------------------------------ weights
 // Fill dst[i] = bf16(normal_f(sigma)) from the counter form of the splitmix64

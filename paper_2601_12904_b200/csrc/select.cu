@@ -304,4 +304,53 @@ int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* c
   return 1;
 }
 
+// ------------------------------------------------------------------ greedy step
+// argmax over one logits row (lowest index on ties: the greedy decoding rule of
+// SPEC.md:137 / 438); the winner is written to out[0] and, for the next decode
+// step, to plan_tok[0] with plan_rows[0] = next_row.
+namespace {
+constexpr int AM_THREADS = 1024;
+__global__ void __launch_bounds__(AM_THREADS) argmax_kernel(const float* __restrict__ logits, int V, int* out,
+                                                            int* plan_tok, int* plan_rows, int next_row) {
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += AM_THREADS) {
+    const float v = logits[i];
+    if (v > best) best = v, bi = i;  // strided scan: first hit of a value is its lowest index here
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) best = ov, bi = oi;
+  }
+  __shared__ float sv[AM_THREADS / 32];
+  __shared__ int si[AM_THREADS / 32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sv[w] = best, si[w] = bi;
+  __syncthreads();
+  if (w == 0) {
+    best = sv[l], bi = si[l];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) best = ov, bi = oi;
+    }
+    if (l == 0) {
+      if (bi == 0x7fffffff) bi = 0;  // all-NaN row: token 0
+      out[0] = bi;
+      if (plan_tok) plan_tok[0] = bi;
+      if (plan_rows) plan_rows[0] = next_row;
+    }
+  }
+}
+}  // namespace
+
+int greedy_argmax(const float* logits, int V, int* out, int* plan_tok, int* plan_rows, int next_row,
+                  cudaStream_t stream) {
+  argmax_kernel<<<1, AM_THREADS, 0, stream>>>(logits, V, out, plan_tok, plan_rows, next_row);
+  return 1;
+}
+
 }  // namespace fragk

@@ -152,6 +152,15 @@ class Engine:
                                     result._h))
         return result
 
+    def decode(self, result: "Result", max_new_tokens: int, *, stream=None) -> np.ndarray:
+        """Greedy decoding continuing the last reprocess / full prefill of
+        `result` (sparse_prefill_and_decode): max_new_tokens ids,
+        the first one from the prefill logits; decoded tokens' K/V are appended
+        to the result's fused cache."""
+        out = np.empty(max(int(max_new_tokens), 1), dtype=np.int32)
+        check(lib.frag_decode(self._h, result._h, int(max_new_tokens), _stream_ptr(stream), _i32p(out)))
+        return out[:max_new_tokens]
+
 
 @dataclass
 class Record:

@@ -27,3 +27,7 @@ def test_cpp_demo_runs_on_device(cuda, tmp_path):
     assert m, r.stdout
     assert int(m.group(1)) == 8 * 256 + 32 and int(m.group(2)) == 307
     assert 0 <= int(m.group(3)) < 256 and float(m.group(4)) > 0
+    ans = re.search(r"answer:((?: \d+)+)", r.stdout)
+    assert ans, r.stdout
+    toks = [int(x) for x in ans.group(1).split()]
+    assert len(toks) == 16 and toks[0] == int(m.group(3)) and all(0 <= t < 256 for t in toks)

@@ -321,3 +321,30 @@ def test_reprocess_selection_never_touches_system_or_question(small):
         assert len(crit) == int(np.floor(r * 80 + 0.5))
         assert np.all(crit >= S + 1) and np.all(crit <= S + 80)
         assert np.all(np.diff(crit) > 0)
+
+
+def test_oracle_decode_equals_prefill_of_extended_prompt():
+    """Prefill/decode equivalence: decoding tokens one by one over
+    a prefilled cache gives the logits of a full prefill of the longer prompt."""
+    from oracle import oracle as O
+    cfg = dict(vocab=64, d_model=32, n_heads=4, n_kv_heads=2, head_dim=8, ffn_dim=64, layers=2,
+               rope_base=1e4, norm_eps=1e-5)
+    m = O.Model(cfg).init_seed(3)
+    rng = np.random.default_rng(0)
+    prompt = rng.integers(0, 64, 12).tolist()
+    extra = rng.integers(0, 64, 4).tolist()
+    T = len(prompt)
+    k, v, pos = m.new_cache(T + len(extra))
+    m.forward(prompt, list(range(1, T + 1)), list(range(T)), k, v, pos)
+    step_logits = m.decode_forced(k, v, T, extra, emulate_bf16=False)
+    full = prompt + extra
+    k2, v2, pos2 = m.new_cache(len(full))
+    ref, _ = m.forward(full, list(range(1, len(full) + 1)), list(range(len(full))), k2, v2, pos2,
+                       logit_rows=list(range(T, len(full))))
+    assert np.allclose(step_logits, ref, rtol=1e-4, atol=1e-5)
+    assert np.allclose(k, k2, rtol=1e-5, atol=1e-6)
+    # greedy decoding feeds back the argmax
+    k3, v3, pos3 = m.new_cache(T + 4)
+    lg, _ = m.forward(prompt, list(range(1, T + 1)), list(range(T)), k3, v3, pos3, logit_rows=[T - 1])
+    toks = m.greedy_decode(k3, v3, T, lg[0], 4, emulate_bf16=False)
+    assert toks[0] == int(np.argmax(lg[0])) and len(toks) == 4

@@ -179,3 +179,33 @@ def test_llama8b_width_two_layer_parity(cuda):
     tau = np.sort(scores)[::-1][len(sel) - 1]
     diff = set((g["crit"] - 1).tolist()) ^ set(sel.tolist())
     assert all(abs(scores[j] - tau) <= 1e-4 * scores.mean() for j in diff)
+
+
+def test_decode_parity_teacher_forced(tiny):
+    """Greedy decode after a 15% reprocess vs the oracle fed the same tokens
+    over its own (selection-injected, bf16-emulating) fused cache: decoded K/V
+    rows and final logits within the reprocess tolerances, and every greedy
+    choice equal to the oracle's argmax unless its top-2 gap < 1e-2."""
+    F, O, S, eng = tiny["F"], tiny["O"], tiny["S"], tiny["eng"]
+    T = S + 8 * 256 + 32
+    n = 6
+    res = F.Result(eng, T + n)
+    eng.reprocess(tiny["store"], tiny["question"], tiny["ids"], 0.15, res, system=tiny["system"])
+    crit = res.crit()
+    k0, v0 = res.fused_kv()
+    toks = eng.decode(res, n)
+    kd, vd = res.fused_kv()
+    last = res.logits()[0]
+    sys_kv = (O.bf16_bits_to_f32(k0[:, :S]), O.bf16_bits_to_f32(v0[:, :S]))
+    out = tiny["om"].reprocess(sys_kv, tiny["recs"], tiny["question"], 0.15, inject=crit, emulate_bf16=True,
+                               cap=T + n)
+    steps = tiny["om"].decode_forced(out["k_cache"], out["v_cache"], T, toks[:-1], emulate_bf16=True)
+    prev = [out["logits"]] + list(steps[:-1])
+    for i, lg in enumerate(prev):
+        top = np.sort(lg)[::-1]
+        if top[0] - top[1] >= 1e-2:
+            assert int(toks[i]) == int(np.argmax(lg)), i
+    assert _rel_l2(last, steps[-1]) <= 2e-2 and _cos(last, steps[-1]) >= 0.999
+    gk = O.bf16_bits_to_f32(kd[:, T:T + n - 1])
+    rk = O.bf16_bits_to_f32(O.f32_to_bf16_bits(out["k_cache"][:, T:T + n - 1]))
+    assert _rel_l2(gk, rk) <= 2e-2 and _cos(gk, rk) >= 0.999

@@ -108,3 +108,42 @@ def test_graph_replay_matches_eager(tiny):
             assert np.array_equal(crit, outs[name][1]), (rep, name)
             assert np.array_equal(lg, outs[name][0]), (rep, name)
     assert not np.array_equal(outs["a"][0], outs["b"][0])
+
+
+def test_decode_r1_equals_full_attention_decode(tiny):
+    """sparse_prefill_and_decode endpoint: with r=1 the greedy
+    answer equals Full Attention greedy decoding, bit for bit (same kernels)."""
+    F, eng = tiny["F"], tiny["eng"]
+    T = 8 + 8 * 256 + 32
+    n = 6
+    ra = F.Result(eng, T + n)
+    eng.reprocess(tiny["store"], tiny["question"], tiny["ids"], 1.0, ra, system=tiny["system"])
+    ta = eng.decode(ra, n)
+    fa = F.Result(eng, T + n)
+    tokens = [t for c in tiny["chunks"] for t in c] + tiny["question"]
+    eng.full_prefill(tokens, fa, system=tiny["system"])
+    tb = eng.decode(fa, n)
+    assert np.array_equal(ta, tb)
+    assert np.array_equal(ra.logits(), fa.logits())
+    ka, va = ra.fused_kv()
+    kb, vb = fa.fused_kv()
+    assert ka.shape[1] == T + n - 1
+    assert np.array_equal(ka, kb) and np.array_equal(va, vb)
+
+
+def test_decode_contract_and_records_untouched(tiny):
+    F, eng, store, ids = tiny["F"], tiny["eng"], tiny["store"], tiny["ids"]
+    T = 8 + 8 * 256 + 32
+    r = F.Result(eng, T + 2)
+    eng.reprocess(store, tiny["question"], ids, 0.15, r, system=tiny["system"])
+    first = int(np.argmax(r.logits()[-1]))
+    before = store.read_kv(ids[0])
+    with pytest.raises(F.ContractError):  # capacity: T + 4 - 1 > T + 2
+        eng.decode(r, 4)
+    toks = eng.decode(r, 3)
+    assert int(toks[0]) == first
+    after = store.read_kv(ids[0])
+    assert np.array_equal(before[0], after[0]) and np.array_equal(before[1], after[1])  # SPEC.md:173
+    fresh = F.Result(eng, 64)
+    with pytest.raises(F.ContractError):  # nothing to continue from
+        eng.decode(fresh, 1)
