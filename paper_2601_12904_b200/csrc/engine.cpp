@@ -339,6 +339,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     n_splits = (int)((2L * sms + ctas - 1) / ctas);
     const int max_splits = (T + 255) / 256;
     if (n_splits > max_splits) n_splits = max_splits;
+    if (n_splits > 64) n_splits = 64;  // the combine kernel's limit
     split_keys = (int)align_up((size_t)((T + n_splits - 1) / n_splits), 128);
     n_splits = (T + split_keys - 1) / split_keys;
     if (n_splits <= 1) n_splits = 1, split_keys = 0;

@@ -1,2 +1,4 @@
-timeout 300 python -m pytest tests/test_kernels_gpu.py -q -x -k "stream_k or small_m" 2>&1 | tail -5
-timeout 300 python tools/gemm_small.py 32 tiny,small,qkv,o,gu,down > gpurun_out/gs.log 2>&1; cut -c1-400 gpurun_out/gs.log
+timeout 300 python -m pytest tests/test_kernels_gpu.py -q -x -k attention 2>&1 | tail -2
+for i in 1 2; do timeout 60 python tools/attn_bench.py; done
+FRAG_ATTN_POLY=4 timeout 60 python tools/attn_bench.py
+timeout 60 python tools/attn_bench.py 32 16416

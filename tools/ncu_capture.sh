@@ -10,10 +10,17 @@ ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control no
     --log-file $OUT/launches_$TAG.csv python tools/profile_step.py > /dev/null 2>&1
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_full_$TAG.csv python tools/profile_step.py --full > /dev/null 2>&1
+# sparse pass, layer 0: the four CTA-pair GEMMs (QKV, O, gate/up, down)
 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:gemm_tc -s 125 -c 4 -o $OUT/gemm_$TAG python tools/profile_step.py > /dev/null 2>&1
+    -k regex:gemm_tc2 -s 0 -c 4 -o $OUT/gemm_$TAG python tools/profile_step.py > /dev/null 2>&1
+# question pass, layer 0: the four weight-streaming GEMMs
 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:attn_tc -s 31 -c 1 -o $OUT/attn_$TAG python tools/profile_step.py > /dev/null 2>&1
+    -k regex:gemm_tc_kernel -s 0 -c 4 -o $OUT/gemmq_$TAG python tools/profile_step.py > /dev/null 2>&1
+# sparse pass, layer 0 attention (after the 32 question-pass launches) + one question-pass attention
+ncu --profile-from-start off --set full --clock-control none --import-source on \
+    -k regex:attn_tc -s 32 -c 1 -o $OUT/attn_$TAG python tools/profile_step.py > /dev/null 2>&1
+ncu --profile-from-start off --set full --clock-control none --import-source on \
+    -k regex:"attn_tc|attn_combine" -s 0 -c 2 -o $OUT/attnq_$TAG python tools/profile_step.py > /dev/null 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:"rope_shift|score_kernel|topk|rmsnorm" -c 6 -o $OUT/mem_$TAG python tools/profile_step.py > /dev/null 2>&1
 ls -la $OUT
