@@ -42,8 +42,28 @@ METRIC = "TTFT ms at 16k-token RAG prompt, 15% recompute vs full prefill; prefil
 CONFIGS = {
     "llama3-8b": dict(preset="llama3-8b", chunks=8, chunk_len=2048, qlen=32, ratio=0.15),
     "mistral-7b": dict(preset="mistral-7b", chunks=32, chunk_len=1024, qlen=32, ratio=0.15),
+    # 64 independent queries, each picking 32 of a
+    # 256-chunk corpus, split round-robin over the ranks (steps = queries/rank)
+    "mistral-7b-batch": dict(preset="mistral-7b", chunks=32, chunk_len=1024, qlen=32, ratio=0.15, corpus=256,
+                             queries=64),
+    # the full 80-layer model fits one B200 (141 GB bf16 weights)
+    "llama3-70b": dict(preset="llama3-70b", chunks=8, chunk_len=2048, qlen=32, ratio=0.15),
     "tiny": dict(preset="tiny", chunks=8, chunk_len=256, qlen=32, ratio=0.15),
 }
+
+
+def l2_note(w):
+    from paper_2601_12904_b200 import fusion as F
+    c = F.preset(w["preset"])
+    per_layer = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim * c.d_model + c.n_heads * c.head_dim * c.d_model \
+        + 3 * c.d_model * c.ffn_dim
+    wbytes = 2 * (c.layers * per_layer + 2 * c.vocab * c.d_model)
+    T = w["chunks"] * w["chunk_len"] + w["qlen"]
+    kv = 2 * c.layers * T * c.n_kv_heads * c.head_dim * 2
+    if wbytes + kv < 126e6:
+        return "fits in L2 (tiny test config, not a headline run)"
+    return (f"inputs larger than L2 ({wbytes / 1e9:.1f} GB weights, {kv / 1e9:.1f} GB fused KV per request "
+            f"streamed every step)")
 
 
 def parse():
@@ -183,8 +203,22 @@ def run_ours(args, rank, world, local_rank):
     c = eng.cfg
     store = F.ChunkKVStore(c, device=local_rank)
     rng = np.random.default_rng(1000 + rank)
-    chunks = [rng.integers(0, c.vocab, w["chunk_len"]).astype(np.int32) for _ in range(w["chunks"])]
-    ids = [eng.preprocess_isolated(store, ch) for ch in chunks]
+    if w.get("corpus"):
+        # the same seeded corpus on every rank (store replica); this rank serves
+        # queries rank, rank + world, ... each over 32 Rng-picked chunks
+        crng = np.random.default_rng(args.seed)
+        pool = [crng.integers(0, c.vocab, w["chunk_len"]).astype(np.int32) for _ in range(w["corpus"])]
+        pool_ids = [eng.preprocess_isolated(store, ch) for ch in pool]
+        mine = [q for q in range(w["queries"]) if q % world == rank]
+        picks = [np.random.default_rng(args.seed * 1000 + q).choice(w["corpus"], w["chunks"], replace=False)
+                 for q in mine]
+        id_sets = [[pool_ids[j] for j in pk] for pk in picks]
+        chunks = [pool[j] for j in picks[0]]
+        args.steps = len(mine)
+    else:
+        chunks = [rng.integers(0, c.vocab, w["chunk_len"]).astype(np.int32) for _ in range(w["chunks"])]
+        id_sets = [[eng.preprocess_isolated(store, ch) for ch in chunks]]
+    ids = id_sets[0]
     N = w["chunks"] * w["chunk_len"]
     T = N + w["qlen"]
     n_q = args.warmup + args.steps
@@ -195,8 +229,9 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
 
     def step_dev(i, r=ratio, **kw):
-        eng.reprocess(store, None, ids, r, res, stream=stream, question_dev_ptr=q_dev[i].data_ptr(),
-                      n_question=w["qlen"], logits_on_device=True, **kw)
+        # request i serves query (i - warmup): the timed loop covers every query of this rank once
+        eng.reprocess(store, None, id_sets[(i - args.warmup) % len(id_sets)], r, res, stream=stream,
+                      question_dev_ptr=q_dev[i].data_ptr(), n_question=w["qlen"], logits_on_device=True, **kw)
 
     for i in range(args.warmup):
         step_dev(i)
@@ -250,7 +285,8 @@ def run_ours(args, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.steps):
-        eng.reprocess(store, questions[n_q + i], ids, ratio, res, stream=stream)
+        eng.reprocess(store, questions[n_q + i], id_sets[i % len(id_sets)], ratio, res,
+                      stream=stream)
         _ = res.logits()
     e1.record(stream)
     torch.cuda.synchronize()
@@ -299,7 +335,10 @@ def main():
                             f"question, r={ratio}", "model": w["preset"], "chunks": w["chunks"],
                 "chunk_len": w["chunk_len"], "question_len": w["qlen"], "recompute_ratio": ratio,
                 "seq_len": w["chunks"] * w["chunk_len"] + w["qlen"], "parallelism": f"dp{args.gpus} (independent queries)",
-                "l2": "inputs larger than L2 (16 GB weights, 2.1 GB fused KV per request)"}
+                "l2": l2_note(w)}
+    if w.get("corpus"):
+        cfg_json.update({"corpus_chunks": w["corpus"], "queries": w["queries"],
+                         "steps_note": "steps = this rank's share of the queries (round-robin)"})
 
     if args.impl == "reference":
         if rank != 0:
@@ -359,6 +398,7 @@ def main():
         "ttft_ms": ttft, "full_prefill_ms": full_ms, "speedup_vs_full_prefill": full_ms / ttft,
         "recomputed_rows": r["k"] + r["w"]["qlen"], "stage_ms": r["stages"],
         "ratio_sweep_ttft_ms": r["sweep"] or None,
+        "queries_per_s": world * args.steps / (ms / 1e3),
         "decode": {"ms_per_token": r["decode_ms"], "tokens": r["n_dec"],
                    "note": "greedy single-row steps over the fused cache after the timed requests (not in value)"},
         "e2e": {"value": e2e_value, "unit": "tok/s", "ttft_ms": e2e_ms / args.steps,

@@ -1,4 +1,2 @@
-timeout 300 python -m pytest tests/test_kernels_gpu.py -q -x -k attention 2>&1 | tail -2
-for i in 1 2; do timeout 60 python tools/attn_bench.py; done
-FRAG_ATTN_POLY=4 timeout 60 python tools/attn_bench.py
-timeout 60 python tools/attn_bench.py 32 16416
+timeout 600 python bench.py --config mistral-7b-batch --warmup 3 --no-cpu-baseline > gpurun_out/m7.log 2>&1; tail -c 1500 gpurun_out/m7.log; echo
+timeout 900 python bench.py --config llama3-70b --steps 5 --warmup 3 --full-steps 1 --no-cpu-baseline > gpurun_out/b70.log 2>&1; tail -c 1500 gpurun_out/b70.log
