@@ -928,26 +928,38 @@ void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) 
   if (T0 + n_new - 1 > r->max_tokens)
     fail(FRAG_E_CONTRACT, "decoded tokens exceed the result capacity (" + std::to_string(r->max_tokens) + ")");
   DeviceGuard dg(e->device);
-  e->ensure_rope(T0 + n_new);
-  r->dec_tok.ensure((size_t)n_new * sizeof(int));
+  // every step attends over the result's whole capacity (keys past the row's
+  // position are masked by position, split-KV ranges past it are empty), so a
+  // step's launches do not depend on its position and replay from one graph
+  const int T_cap = r->max_tokens;
+  e->ensure_rope(T_cap);
+  r->dec_tok.ensure((size_t)(n_new + 1) * sizeof(int));
   r->staging.ensure((size_t)n_new * sizeof(int) + 64);
   int* stage = r->staging.as<int>();
   stage[0] = 0;  // the single decode row is logits row 0
+  stage[1] = 0;  // token slot counter
+  int* cnt = r->dec_tok.as<int>();  // [0] slot counter, [1..] tokens (fixed addresses for the graph)
+  int* toks = cnt + 1;
   check_cuda(cudaMemcpyAsync(r->row_map.p, stage, sizeof(int), cudaMemcpyHostToDevice, s), "row map");
-  const float* last = r->logits.as<float>() + (size_t)(r->logit_rows - 1) * c.vocab;
-  for (int i = 0; i < n_new; ++i) {
-    // token i = argmax(logits of the previous position); it becomes the next row's input
-    {
-      Scoped sc(e->prof, s, KC_SELECT, 0, 4.0 * c.vocab);
-      sc.launched(fragk::greedy_argmax(last, c.vocab, r->dec_tok.as<int>() + i, r->plan_tok.as<int>(),
-                                       r->plan_rows.as<int>(), T0 + i, s));
-    }
-    if (i == n_new - 1) break;
-    run_rows(e, r, s, 1, T0 + i + 1, PASS_FULL, r->row_map.as<int>(), 1);
-    last = r->logits.as<float>();
-  }
+  check_cuda(cudaMemcpyAsync(cnt, stage + 1, sizeof(int), cudaMemcpyHostToDevice, s), "slot counter");
+  auto argmax = [&](const float* logits, int next_row, cudaStream_t bs) {
+    Scoped sc(e->prof, bs, KC_SELECT, 0, 4.0 * c.vocab);
+    sc.launched(fragk::greedy_argmax(logits, c.vocab, toks, cnt, r->plan_tok.as<int>(),
+                                     r->plan_rows.as<int>(), next_row, bs));
+  };
+  // token 0 = argmax of the prefill's last logits row; its row is T0 (0-based)
+  argmax(r->logits.as<float>() + (size_t)(r->logit_rows - 1) * c.vocab, T0, s);
+  // step: one row through every layer at plan_rows[0], logits row 0, argmax ->
+  // next token and plan_rows[0] + 1 (graph-replayed after the first step)
+  auto step = [&](cudaStream_t bs) {
+    run_rows(e, r, bs, 1, T_cap, PASS_FULL, r->row_map.as<int>(), 1);
+    argmax(r->logits.as<float>(), -1, bs);
+  };
+  const bool graphable = !e->prof.on;
+  GraphKey key{T_cap, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, (uint64_t)(uintptr_t)e->rope.p};
+  for (int i = 1; i < n_new; ++i) run_graphed(r, s, graphable, key, step);
   peek("decode");
-  check_cuda(cudaMemcpyAsync(stage, r->dec_tok.p, (size_t)n_new * sizeof(int), cudaMemcpyDeviceToHost, s), "tokens");
+  check_cuda(cudaMemcpyAsync(stage, toks, (size_t)n_new * sizeof(int), cudaMemcpyDeviceToHost, s), "tokens");
   if (n_new > 1) {
     r->logit_rows = 1;
     if (!r->logits_on_device) {

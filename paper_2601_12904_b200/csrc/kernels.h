@@ -122,9 +122,11 @@ int qg_score(const ScoreArgs& a, cudaStream_t stream);
 // then the question rows appended. Writes plan_rows[k + nq] and plan_tok.
 int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* chunk_tok, const int* q_tok,
               int nq, int q_row0, int* plan_rows, int* plan_tok, cudaStream_t stream);
-// Greedy decoding step: out[0] = argmax(logits[0..V)) (lowest index on ties),
-// also stored as the next step's plan token / row when the pointers are set.
-int greedy_argmax(const float* logits, int V, int* out, int* plan_tok, int* plan_rows, int next_row,
+// Greedy decoding step: argmax(logits[0..V)) (lowest index on ties) -> out[0],
+// or out[*out_idx] with *out_idx incremented when out_idx is set; also stored
+// as the next step's plan token, and plan_rows[0] = next_row (next_row < 0:
+// incremented on the device).
+int greedy_argmax(const float* logits, int V, int* out, int* out_idx, int* plan_tok, int* plan_rows, int next_row,
                   cudaStream_t stream);
 
 // ------------------------------------------------------------------ weights

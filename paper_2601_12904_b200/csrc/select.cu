@@ -7,9 +7,8 @@
 // and question keys are excluded, heads are summed, and the
 // budget is a global top-k with lower-index tie-break.
 //
-// v1 uses fp32 CUDA-core FMAs (the whole stage is ~0.3% of TTFT) so scores
-// follow the fp32 oracle to summation-order rounding; no atomics, so the
-// result is bit-deterministic run to run.
+// fp32 CUDA-core FMAs so scores follow the fp32 oracle to summation-order
+// rounding; no atomics, so the result is bit-deterministic run to run.
 #include <cfloat>
 
 #include "kernels.h"
@@ -19,80 +18,119 @@ namespace fragk {
 
 namespace {
 
-constexpr int SC_KEYS = 32;     // keys per CTA
-constexpr int SC_ROWS = 32;     // query rows per smem tile
+constexpr int SC_KEYS = 64;     // keys per CTA
+constexpr int SC_ROWS = 128;    // query rows per shared-memory tile
 constexpr int SC_THREADS = 256;
+constexpr int SC_PAD = 4;       // row padding (floats): conflict-free 128-bit shared loads
 
+template <int DH>
+constexpr size_t score_smem() { return (size_t)(SC_KEYS + SC_ROWS) * (DH + SC_PAD) * sizeof(float); }
+
+// Register-tiled fp32 CUDA-core scoring: a CTA owns 64 keys and walks the kv
+// heads and their query rows; each thread computes an 8-row x 4-key block
+// with 128-bit shared-memory operand loads (12 loads per 128 FMAs). Every dot
+// product is a sequential fp32 FMA chain over dh, exactly as in the fp32
+// oracle restatement, and all reductions run in a fixed order (no atomics), so
+// scores are bit-deterministic.
 // MODE 1: per-(block,row) (max, sumexp) of scaled logits.
 // MODE 2: column sums of softmax probabilities (row_ms = (max, 1/Z)).
 // MODE 3: column sums of raw scaled logits.
 template <int MODE, int DH>
 __global__ void __launch_bounds__(SC_THREADS) score_kernel(const ScoreArgs a) {
-  __shared__ float sk[SC_KEYS][DH + 1];
-  __shared__ float sq[SC_ROWS][DH + 1];
-  __shared__ float colsum[SC_THREADS / 8][SC_KEYS];  // 32 row-groups x 32 keys
+  constexpr int LD = DH + SC_PAD;
+  extern __shared__ float4 sc_smem4[];
+  float* sk = reinterpret_cast<float*>(sc_smem4);  // [SC_KEYS][LD]
+  float* sq = sk + SC_KEYS * LD;                   // [SC_ROWS][LD]
+  __shared__ float colsum[SC_THREADS / 32][SC_KEYS];
   const int blk = blockIdx.x;
   const int key0 = blk * SC_KEYS;
   const int nrows_tot = a.nq * a.Hq;
   const int G = a.Hq / a.Hkv;
-  const int tid = threadIdx.x;
-  // thread -> (row, key quad): 32 rows x 8 key-groups; each thread owns
-  // row rg and keys {kg, kg+8, kg+16, kg+24} of the tile.
-  const int rg = tid >> 3, kg = tid & 7;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // thread -> rows rg*8 .. rg*8+7 of the row tile, keys kg + 16*j (j < 4)
+  const int rg = tid >> 4, kg = tid & 15;
   float csum[4] = {0.f, 0.f, 0.f, 0.f};
 
   for (int hk = 0; hk < a.Hkv; ++hk) {
     __syncthreads();
-    for (int idx = tid; idx < SC_KEYS * DH; idx += SC_THREADS) {
-      const int r = idx / DH, c = idx % DH;
+    for (int idx = tid; idx < SC_KEYS * (DH / 8); idx += SC_THREADS) {
+      const int r = idx / (DH / 8), c8 = (idx % (DH / 8)) * 8;
       const int j = key0 + r;
-      sk[r][c] = j < a.n_keys ? __bfloat162float(a.k[((size_t)(a.key_row0 + j) * a.Hkv + hk) * DH + c]) : 0.f;
+      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (j < a.n_keys) {
+        const uint4 u = *reinterpret_cast<const uint4*>(a.k + ((size_t)(a.key_row0 + j) * a.Hkv + hk) * DH + c8);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[2 * e] = __uint_as_float(w[e] << 16);
+          v[2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
+        }
+      }
+      float4* dst = reinterpret_cast<float4*>(sk + r * LD + c8);
+      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
     }
     const int nrows = a.nq * G;  // rows of this kv group: (t, g) -> row t*Hq + hk*G + g
     for (int r0 = 0; r0 < nrows; r0 += SC_ROWS) {
       __syncthreads();
-      for (int idx = tid; idx < SC_ROWS * DH; idx += SC_THREADS) {
-        const int r = idx / DH, c = idx % DH;
+      for (int idx = tid; idx < SC_ROWS * (DH / 4); idx += SC_THREADS) {
+        const int r = idx / (DH / 4), c4 = (idx % (DH / 4)) * 4;
         const int rr = r0 + r;
-        float v = 0.f;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (rr < nrows) {
           const int t = rr / G, g = rr % G;
-          v = a.q[((size_t)t * a.Hq + hk * G + g) * DH + c];
+          v = *reinterpret_cast<const float4*>(a.q + ((size_t)t * a.Hq + hk * G + g) * DH + c4);
         }
-        sq[r][c] = v;
+        *reinterpret_cast<float4*>(sq + r * LD + c4) = v;
       }
       __syncthreads();
-      float acc[1][4];
+      // both 8-row groups of this warp past the end (warp-uniform: the shuffles
+      // below need the full warp; no barrier follows inside this iteration)
+      if (r0 + (rg & ~1) * 8 >= nrows) continue;
+      float acc[8][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[0][j] = 0.f;
-#pragma unroll 8
-      for (int c = 0; c < DH; ++c) {
-        const float q0 = sq[rg][c];
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[0][j] = fmaf(q0, sk[kg + 8 * j][c], acc[0][j]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+      for (int c = 0; c < DH; c += 4) {
+        float4 kv[4], qv[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) kv[j] = *reinterpret_cast<const float4*>(sk + (kg + 16 * j) * LD + c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) qv[i] = *reinterpret_cast<const float4*>(sq + (rg * 8 + i) * LD + c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float t = fmaf(qv[i].x, kv[j].x, acc[i][j]);
+            t = fmaf(qv[i].y, kv[j].y, t);
+            t = fmaf(qv[i].z, kv[j].z, t);
+            acc[i][j] = fmaf(qv[i].w, kv[j].w, t);
+          }
       }
-      {
-        const int i = 0;
-        const int rr = r0 + rg;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = r0 + rg * 8 + i;
         const bool rvalid = rr < nrows;
         const int grow = rvalid ? (rr / G) * a.Hq + hk * G + rr % G : 0;
         if constexpr (MODE == 1) {
-          // local (max, sumexp) over this CTA's keys for row grow: reduce over the 8 kg lanes
-          float s[4];
+          // local (max, sumexp) over this CTA's 64 keys for row grow: the 16 kg lanes
+          float sv[4];
           float mx = -INFINITY;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const bool kvalid = key0 + kg + 8 * j < a.n_keys;
-            s[j] = kvalid ? acc[i][j] * a.scale : -INFINITY;
-            mx = fmaxf(mx, s[j]);
+            const bool kvalid = key0 + kg + 16 * j < a.n_keys;
+            sv[j] = kvalid ? acc[i][j] * a.scale : -INFINITY;
+            mx = fmaxf(mx, sv[j]);
           }
 #pragma unroll
-          for (int o = 1; o < 8; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          for (int o = 1; o < 16; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
           float z = 0.f;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) z += (s[j] == -INFINITY) ? 0.f : __expf(s[j] - mx);
+          for (int j = 0; j < 4; ++j) z += (sv[j] == -INFINITY) ? 0.f : __expf(sv[j] - mx);
 #pragma unroll
-          for (int o = 1; o < 8; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+          for (int o = 1; o < 16; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
           if (kg == 0 && rvalid) a.part_ms[(size_t)blk * nrows_tot + grow] = make_float2(mx, z);
         } else if constexpr (MODE == 2) {
           if (rvalid) {
@@ -110,13 +148,16 @@ __global__ void __launch_bounds__(SC_THREADS) score_kernel(const ScoreArgs a) {
     }
   }
   if constexpr (MODE != 1) {
-    // deterministic column reduction over the 32 row-groups
+    // deterministic column reduction: the two row groups of a warp, then the 8 warps in order
 #pragma unroll
-    for (int j = 0; j < 4; ++j) colsum[rg][kg + 8 * j] = csum[j];
+    for (int j = 0; j < 4; ++j) csum[j] += __shfl_xor_sync(0xffffffffu, csum[j], 16);
+    if (lane < 16)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) colsum[warp][kg + 16 * j] = csum[j];
     __syncthreads();
     if (tid < SC_KEYS) {
       float s = 0.f;
-      for (int r = 0; r < SC_THREADS / 8; ++r) s += colsum[r][tid];
+      for (int w = 0; w < SC_THREADS / 32; ++w) s += colsum[w][tid];
       const int j = key0 + tid;
       if (j < a.n_keys) a.scores[j] = s;
     }
@@ -266,35 +307,29 @@ __global__ void __launch_bounds__(TK_THREADS) topk_plan_kernel(const float* __re
 
 }  // namespace
 
+template <int DH>
+int qg_score_dh(const ScoreArgs& a, int nblk, cudaStream_t stream) {
+  constexpr int SM = (int)score_smem<DH>();
+  smem_attr_once(score_kernel<1, DH>, SM);
+  smem_attr_once(score_kernel<2, DH>, SM);
+  smem_attr_once(score_kernel<3, DH>, SM);
+  if (!a.raw) {
+    score_kernel<1, DH><<<nblk, SC_THREADS, SM, stream>>>(a);
+    score_combine_kernel<<<(a.nq * a.Hq + 255) / 256, 256, 0, stream>>>(a, nblk);
+    score_kernel<2, DH><<<nblk, SC_THREADS, SM, stream>>>(a);
+    return 3;
+  }
+  score_kernel<3, DH><<<nblk, SC_THREADS, SM, stream>>>(a);
+  return 1;
+}
+
 int qg_score(const ScoreArgs& a, cudaStream_t stream) {
   const int nblk = (a.n_keys + SC_KEYS - 1) / SC_KEYS;
   if (nblk <= 0) return 0;
   if (a.Hq % a.Hkv != 0) return -1;
-  int launches = 0;
-  if (a.dh == 128) {
-    if (!a.raw) {
-      score_kernel<1, 128><<<nblk, SC_THREADS, 0, stream>>>(a);
-      score_combine_kernel<<<(a.nq * a.Hq + 255) / 256, 256, 0, stream>>>(a, nblk);
-      score_kernel<2, 128><<<nblk, SC_THREADS, 0, stream>>>(a);
-      launches = 3;
-    } else {
-      score_kernel<3, 128><<<nblk, SC_THREADS, 0, stream>>>(a);
-      launches = 1;
-    }
-  } else if (a.dh == 64) {
-    if (!a.raw) {
-      score_kernel<1, 64><<<nblk, SC_THREADS, 0, stream>>>(a);
-      score_combine_kernel<<<(a.nq * a.Hq + 255) / 256, 256, 0, stream>>>(a, nblk);
-      score_kernel<2, 64><<<nblk, SC_THREADS, 0, stream>>>(a);
-      launches = 3;
-    } else {
-      score_kernel<3, 64><<<nblk, SC_THREADS, 0, stream>>>(a);
-      launches = 1;
-    }
-  } else {
-    return -1;
-  }
-  return launches;
+  if (a.dh == 128) return qg_score_dh<128>(a, nblk, stream);
+  if (a.dh == 64) return qg_score_dh<64>(a, nblk, stream);
+  return -1;
 }
 
 int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* chunk_tok, const int* q_tok, int nq,
@@ -306,12 +341,14 @@ int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* c
 
 // ------------------------------------------------------------------ greedy step
 // argmax over one logits row (lowest index on ties: the greedy decoding rule of
-// SPEC.md:137 / 438); the winner is written to out[0] and, for the next decode
-// step, to plan_tok[0] with plan_rows[0] = next_row.
+// SPEC.md:137 / 438); the winner is written to out[0] (or out[(*out_idx)++]) and,
+// for the next decode step, to plan_tok[0] with plan_rows[0] = next_row
+// (next_row < 0: plan_rows[0] + 1, so a captured step needs no host value).
 namespace {
 constexpr int AM_THREADS = 1024;
 __global__ void __launch_bounds__(AM_THREADS) argmax_kernel(const float* __restrict__ logits, int V, int* out,
-                                                            int* plan_tok, int* plan_rows, int next_row) {
+                                                            int* out_idx, int* plan_tok, int* plan_rows,
+                                                            int next_row) {
   float best = -INFINITY;
   int bi = 0x7fffffff;
   for (int i = threadIdx.x; i < V; i += AM_THREADS) {
@@ -339,17 +376,22 @@ __global__ void __launch_bounds__(AM_THREADS) argmax_kernel(const float* __restr
     }
     if (l == 0) {
       if (bi == 0x7fffffff) bi = 0;  // all-NaN row: token 0
-      out[0] = bi;
+      if (out_idx) {  // device-side slot counter: graph-replayable decode steps
+        out[out_idx[0]] = bi;
+        out_idx[0] += 1;
+      } else {
+        out[0] = bi;
+      }
       if (plan_tok) plan_tok[0] = bi;
-      if (plan_rows) plan_rows[0] = next_row;
+      if (plan_rows) plan_rows[0] = next_row >= 0 ? next_row : plan_rows[0] + 1;
     }
   }
 }
 }  // namespace
 
-int greedy_argmax(const float* logits, int V, int* out, int* plan_tok, int* plan_rows, int next_row,
+int greedy_argmax(const float* logits, int V, int* out, int* out_idx, int* plan_tok, int* plan_rows, int next_row,
                   cudaStream_t stream) {
-  argmax_kernel<<<1, AM_THREADS, 0, stream>>>(logits, V, out, plan_tok, plan_rows, next_row);
+  argmax_kernel<<<1, AM_THREADS, 0, stream>>>(logits, V, out, out_idx, plan_tok, plan_rows, next_row);
   return 1;
 }
 

@@ -1,2 +1,3 @@
-timeout 600 python bench.py --config mistral-7b-batch --warmup 3 --no-cpu-baseline > gpurun_out/m7.log 2>&1; tail -c 1500 gpurun_out/m7.log; echo
-timeout 900 python bench.py --config llama3-70b --steps 5 --warmup 3 --full-steps 1 --no-cpu-baseline > gpurun_out/b70.log 2>&1; tail -c 1500 gpurun_out/b70.log
+timeout 600 python -m pytest tests -q -x -m gpu 2>&1 | tail -3
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b.log 2>&1; python -c "
+import json;d=json.loads(open('gpurun_out/b.log').read().strip().splitlines()[-1]);print(d['ttft_ms'],d['stage_ms'],d['kernels']['select'])"
