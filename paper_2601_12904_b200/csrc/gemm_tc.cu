@@ -483,10 +483,19 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
   }
   // Large M: CTA-pair tiles (256 x 256, cta_group::2) beat every 1-CTA shape in
   // the B200 sweep (profiles/gemm_tune_r01.txt) for the projection shapes.
-  if (!force_bn && M >= 256 && N % 256 == 0 && ep.splits == 1)
-    // tail split-K only pays for long K (the FFN down projection): at K=4096 the
-    // partial write + fixup cost what the shorter last wave saves (gemm_tune)
-    return gemm_bf16_tc_pair(A, B, M, N, K, epi, ep, stream, 256, (force_bn_flags & 0x20000) == 0 && K >= 8192);
+  if (!force_bn && M >= 256 && N % 256 == 0 && ep.splits == 1) {
+    // Wave quantisation on 74 CTA pairs: 192-wide tiles (partial last N tile)
+    // when they cut the wave-weighted tile width by >= 15 % (O and down
+    // projections at M~2.5k: 160 -> 220 tiles, 3 waves of 0.75 the work);
+    // otherwise 256. Tail split-K only pays for long K (the FFN down
+    // projection): at K=4096 the partial write + fixup cost what the shorter
+    // last wave saves (tools/gemm_tune.py, profiles/gemm_tune_r01.txt).
+    const long m_t = (M + 255) / 256, pairs = num_sms() / 2;
+    const long w256 = (m_t * (N / 256) + pairs - 1) / pairs, w192 = (m_t * ((N + 191) / 192) + pairs - 1) / pairs;
+    const int bn2 = (w192 * 192 * 100 <= w256 * 256 * 85) ? 192 : 256;
+    return gemm_bf16_tc_pair(A, B, M, N, K, epi, ep, stream, bn2,
+                             (force_bn_flags & 0x20000) == 0 && K >= 8192);
+  }
   if (ep.splits == 1 && tail_ok && M > BM && (M + BM - 1) / BM < 64 && K >= 8192 && ep.ws && ep.counters) {
     // split-K only the last partial wave (deterministic last-CTA reduction)
     const long tiles = (long)((M + BM - 1) / BM) * (N / bn), sms = num_sms();

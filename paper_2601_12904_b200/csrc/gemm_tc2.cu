@@ -108,7 +108,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   const int m_tiles = (M + BM2 - 1) / BM2;
-  const int n_tiles = N / BN;
+  const int n_tiles = (N + BN - 1) / BN;  // last N tile may be partial (BN = 192)
   const int num_tiles = m_tiles * n_tiles;
   const int nk = K / BK2;
   // work items: the first n_full tiles whole, then each tail tile cut into
@@ -252,7 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
             tmem_ld32(t_row + c * 32, r);
             tmem_ld32(t_row + (c + 1) * 32, r2);
             tmem_ld_wait();
-            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+            if (row < M && n_blk * BN + c * 32 < N) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
           }
         } else {
 #pragma unroll 1
@@ -260,7 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
             uint32_t r[32];
             tmem_ld32(t_row + c * 32, r);
             tmem_ld_wait();
-            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
+            if (row < M && n_blk * BN + c * 32 < N) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
           }
         }
         tc_fence_before();
@@ -305,7 +305,7 @@ int launch2(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& 
   CUtensorMap ta, tb;
   if (!make_tmap_2d(&ta, A, M, K, K, 128)) return -1;
   if (!make_tmap_2d(&tb, B, N, K, K, BN / 2)) return -1;
-  const int tiles = ((M + BM2 - 1) / BM2) * (N / BN);
+  const int tiles = ((M + BM2 - 1) / BM2) * ((N + BN - 1) / BN);
   const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int pairs = num_sms() / 2;
   const int grid = 2 * (work < pairs ? work : pairs);
@@ -323,13 +323,13 @@ int pair_dispatch(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi
 
 int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
                       cudaStream_t s, int bn, bool tail_split) {
-  if (K % BK2 != 0 || N % bn != 0) return -1;
+  if (K % BK2 != 0 || N % 64 != 0 || (bn != 192 && N % bn != 0)) return -1;
   EpiParams ep2 = ep;
   ep2.splits = 1;
-  if (tail_split && ep.ws && ep.counters) {
+  if (tail_split && N % bn == 0 && ep.ws && ep.counters) {
     // split-K only the last partial wave of CTA pairs (deterministic reduction
     // per 128-row half by the last-arriving CTA)
-    const long tiles = (long)((M + BM2 - 1) / BM2) * (N / bn), pairs = num_sms() / 2, nk = K / BK2;
+    const long tiles = (long)((M + BM2 - 1) / BM2) * ((N + bn - 1) / bn), pairs = num_sms() / 2, nk = K / BK2;
     const long rem = tiles % pairs;
     long sp = rem ? pairs / rem : 1;
     if (sp > 8) sp = 8;
@@ -352,6 +352,14 @@ int pair_dispatch(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi
       case EPI_RESID: return launch2<256, EPI_RESID>(A, B, M, N, K, ep, s);
       case EPI_SWIGLU: return launch2<256, EPI_SWIGLU>(A, B, M, N, K, ep, s);
       case EPI_QKV: return launch2<256, EPI_QKV>(A, B, M, N, K, ep, s);
+    }
+  } else if (bn == 192) {
+    switch (epi) {
+      case EPI_STORE_BF16: return launch2<192, EPI_STORE_BF16>(A, B, M, N, K, ep, s);
+      case EPI_STORE_F32: return launch2<192, EPI_STORE_F32>(A, B, M, N, K, ep, s);
+      case EPI_RESID: return launch2<192, EPI_RESID>(A, B, M, N, K, ep, s);
+      case EPI_SWIGLU: return launch2<192, EPI_SWIGLU>(A, B, M, N, K, ep, s);
+      case EPI_QKV: return launch2<192, EPI_QKV>(A, B, M, N, K, ep, s);
     }
   } else if (bn == 128) {
     switch (epi) {

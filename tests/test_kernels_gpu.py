@@ -138,13 +138,14 @@ def test_rope_shift_bit_exact(cuda, delta):
 
 @pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 512, 256), (2490, 1024, 4096), (1000, 768, 512),
                                    (2490, 4096, 4096), (1000, 6144, 512)])
-@pytest.mark.parametrize("bn", [128, 256])
+@pytest.mark.parametrize("bn", [128, 192, 256])
 @pytest.mark.parametrize("tail", [0, 1])
 def test_gemm_cta_pair_vs_torch(cuda, M, N, K, bn, tail):
     """cta_group::2 GEMM (256-row tiles shared by a CTA pair); tail=1 splits the
-    last partial wave of pairs along K (deterministic last-CTA reduction)."""
+    last partial wave of pairs along K (deterministic cooperative reduction);
+    BN=192 leaves a partial last N tile when N % 192 != 0."""
     import torch
-    if N % bn:
+    if bn != 192 and N % bn:
         pytest.skip("N not a multiple of BN")
     g = torch.Generator(device="cuda").manual_seed(M + N + K + bn)
     a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
@@ -202,3 +203,22 @@ def test_gemm_stream_k_vs_torch(cuda, M, N, K, bn):
     uu = c[:, (idx // 32) * 64 + 32 + idx % 32]
     want = torch.nn.functional.silu(gg) * uu
     assert (out.float() - want).abs().max().item() <= 1e-2 * want.abs().max().item() + 1e-3
+
+
+@pytest.mark.parametrize("bn", [192, 256])
+def test_gemm_pair_swiglu_partial_tile(cuda, bn):
+    import torch
+    M, F, K = 600, 1280, 512   # 2F = 2560 = 13.3 tiles of 192
+    g = torch.Generator(device="cuda").manual_seed(bn)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16) * 0.5
+    wg = torch.randn(F, K, device=cuda, generator=g).to(torch.bfloat16) * 0.1
+    wu = torch.randn(F, K, device=cuda, generator=g).to(torch.bfloat16) * 0.1
+    packed = torch.empty(2 * F, K, device=cuda, dtype=torch.bfloat16)
+    idx = torch.arange(F, device=cuda)
+    packed[(idx // 32) * 64 + idx % 32] = wg
+    packed[(idx // 32) * 64 + 32 + idx % 32] = wu
+    out = torch.empty(M, F, device=cuda, dtype=torch.bfloat16)
+    _gemm(a, packed, out, 3, bn | 0x40000)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T)
+    assert (out.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()

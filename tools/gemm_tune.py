@@ -17,7 +17,7 @@ for M in Ms:
         b = torch.randn(N, K, device=dev).to(torch.bfloat16)
         c = torch.zeros(M, N, device=dev, dtype=torch.float32)
         res = []
-        for bn in (0, 64, 128, 256, 1128, 1256):
+        for bn in (0, 128, 256, 1128, 1192, 1256):
             for tail in ((0,) if bn == 0 else (0, 1)):
                 flags = (bn | (tail << 16) if bn < 1000 else (bn - 1000) | 0x40000 | (tail << 16)) if bn else 0
                 try:
