@@ -17,6 +17,8 @@ namespace {
 template <int DH>
 __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a) {
   constexpr int V = DH / 32;  // columns per lane
+  pdl_wait();
+  pdl_launch_dependents();
   const size_t MH = (size_t)a.M * a.Hq;
   const size_t qi = (size_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (qi >= MH) return;
@@ -93,9 +95,9 @@ int sparse_q_attention(const AttnArgs& a0, cudaStream_t stream) {
   if (a.n_splits > 64) return -1;  // combine holds two split weights per lane
   const unsigned blocks = (unsigned)(((size_t)a.M * a.Hq + 3) / 4);
   if (a.dh == 128)
-    attn_combine_kernel<128><<<blocks, 128, 0, stream>>>(a);
+    launch_pdl(attn_combine_kernel<128>, dim3(blocks), dim3(128), 0, stream, a);
   else
-    attn_combine_kernel<64><<<blocks, 128, 0, stream>>>(a);
+    launch_pdl(attn_combine_kernel<64>, dim3(blocks), dim3(128), 0, stream, a);
   return 2;
 }
 

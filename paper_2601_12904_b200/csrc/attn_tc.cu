@@ -89,11 +89,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   const int t0 = qb * AT_QT * tok_per_tile;
   const int t_end = min(t0 + AT_QT * tok_per_tile, a.M);
   const int n_qt = (t_end - t0 + tok_per_tile - 1) / tok_per_tile;  // live query tiles (1 or 2)
-  const int p_max = a.rows[t_end - 1];
   const int k_lo = a.n_splits > 1 ? split * a.split_keys : 0;
-  int k_hi = p_max + 1;
-  if (a.n_splits > 1) k_hi = min(k_hi, (split + 1) * a.split_keys);
-  const int n_tiles = k_hi > k_lo ? (k_hi - k_lo + AT_KEYS - 1) / AT_KEYS : 0;
 
   // warps 0-3 softmax A, 4-7 softmax B, 8 TMA, 9 MMA (the highest warp id wins
   // issue arbitration on its sub-partition, which keeps MMA issue off the
@@ -121,6 +117,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the prologue above overlapped the producing kernel's tail; the plan
+  // rows, Q and the fused K/V rows are read only after this point
+  pdl_wait();
+  pdl_launch_dependents();
+  const int p_max = a.rows[t_end - 1];
+  int k_hi = p_max + 1;
+  if (a.n_splits > 1) k_hi = min(k_hi, (split + 1) * a.split_keys);
+  const int n_tiles = k_hi > k_lo ? (k_hi - k_lo + AT_KEYS - 1) / AT_KEYS : 0;
 
   if (warp == W_TMA) {
     // ------------------------------------------------------------ TMA producer
@@ -359,7 +363,7 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   }();
   auto go = [&](auto kern, int smem) {
     smem_attr_once(kern, smem);
-    kern<<<grid, AT_THREADS, smem, stream>>>(tq, tk, tv, a, G, n_qblocks);
+    launch_pdl(kern, grid, dim3(AT_THREADS), smem, stream, tq, tk, tv, a, G, n_qblocks);
   };
   if (a.dh == 128) {
     constexpr int SM = (int)AttCfg<128>::SMEM;

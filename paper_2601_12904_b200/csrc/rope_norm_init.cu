@@ -96,37 +96,45 @@ __global__ void __launch_bounds__(256) rope_shift_kernel(const StitchChunk* __re
 }
 
 // ------------------------------------------------------------------ norms
-// One CTA per row. Sum of squares in fp32 (block reduction), scale in fp32,
-// bf16 output for the next GEMM's A operand.
-template <bool EMBED>
+// One CTA per row, the row held in registers (d/8 bf16x8 vectors over the CTA:
+// 8 fp32 values per vector, NV vectors per thread), so the fp32 residual is
+// read from HBM exactly once. Sum of squares in fp32 (block reduction), scale
+// in fp32, bf16 output for the next GEMM's A operand. Launched with PDL: the
+// next GEMM's CTAs start (and prefetch their weights) while rows finish.
+template <bool EMBED, int NV>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const bf16* __restrict__ E, const int* __restrict__ tok,
                                                       const float* __restrict__ h_in, const int* __restrict__ row_map,
                                                       int d, const bf16* __restrict__ gain, float eps,
                                                       float* __restrict__ h_out, bf16* __restrict__ x) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int row = blockIdx.x;
   __shared__ float red[8];
-  float ss = 0.f;
-  // d is a multiple of 256*... handled with a strided loop of 8-element vectors.
   const int nvec = d >> 3;
-  if constexpr (EMBED) {
-    const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok[row] * d);
-    float4* hdst = reinterpret_cast<float4*>(h_out + (size_t)row * d);
-    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-      uint4 e = src[v];
-      float f[8] = {bf16_lo(e.x), bf16_hi(e.x), bf16_lo(e.y), bf16_hi(e.y),
-                    bf16_lo(e.z), bf16_hi(e.z), bf16_lo(e.w), bf16_hi(e.w)};
-      hdst[2 * v] = make_float4(f[0], f[1], f[2], f[3]);
-      hdst[2 * v + 1] = make_float4(f[4], f[5], f[6], f[7]);
+  float f[NV][8];
+  float ss = 0.f;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) ss = fmaf(f[t], f[t], ss);
-    }
-  } else {
-    const int src_row = row_map ? row_map[row] : row;
-    const float4* src = reinterpret_cast<const float4*>(h_in + (size_t)src_row * d);
-    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-      float4 a = src[2 * v], b = src[2 * v + 1];
-      ss = fmaf(a.x, a.x, ss); ss = fmaf(a.y, a.y, ss); ss = fmaf(a.z, a.z, ss); ss = fmaf(a.w, a.w, ss);
-      ss = fmaf(b.x, b.x, ss); ss = fmaf(b.y, b.y, ss); ss = fmaf(b.z, b.z, ss); ss = fmaf(b.w, b.w, ss);
+  for (int i = 0; i < NV; ++i) {
+    const int v = threadIdx.x + i * 256;
+    if (v < nvec) {
+      if constexpr (EMBED) {
+        const uint4 e = reinterpret_cast<const uint4*>(E + (size_t)tok[row] * d)[v];
+        const float t[8] = {bf16_lo(e.x), bf16_hi(e.x), bf16_lo(e.y), bf16_hi(e.y),
+                            bf16_lo(e.z), bf16_hi(e.z), bf16_lo(e.w), bf16_hi(e.w)};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[i][k] = t[k];
+        float4* hdst = reinterpret_cast<float4*>(h_out + (size_t)row * d);
+        hdst[2 * v] = make_float4(t[0], t[1], t[2], t[3]);
+        hdst[2 * v + 1] = make_float4(t[4], t[5], t[6], t[7]);
+      } else {
+        const int src_row = row_map ? row_map[row] : row;
+        const float4* src = reinterpret_cast<const float4*>(h_in + (size_t)src_row * d);
+        const float4 a = src[2 * v], b = src[2 * v + 1];
+        f[i][0] = a.x, f[i][1] = a.y, f[i][2] = a.z, f[i][3] = a.w;
+        f[i][4] = b.x, f[i][5] = b.y, f[i][6] = b.z, f[i][7] = b.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ss = fmaf(f[i][k], f[i][k], ss);
     }
   }
   ss = warp_sum(ss);
@@ -139,22 +147,35 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const bf16* __restrict__ E
   }
   __syncthreads();
   const float rs = rsqrtf(red[0] / (float)d + eps);
-  const float* hrow;
-  if constexpr (EMBED) hrow = h_out + (size_t)row * d;
-  else hrow = h_in + (size_t)(row_map ? row_map[row] : row) * d;
-  const float4* hv = reinterpret_cast<const float4*>(hrow);
   const uint4* gv = reinterpret_cast<const uint4*>(gain);
   uint4* xo = reinterpret_cast<uint4*>(x + (size_t)row * d);
-  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    float4 a = hv[2 * v], b = hv[2 * v + 1];
-    uint4 g = gv[v];
-    uint4 o;
-    o.x = pack_bf16(a.x * rs * bf16_lo(g.x), a.y * rs * bf16_hi(g.x));
-    o.y = pack_bf16(a.z * rs * bf16_lo(g.y), a.w * rs * bf16_hi(g.y));
-    o.z = pack_bf16(b.x * rs * bf16_lo(g.z), b.y * rs * bf16_hi(g.z));
-    o.w = pack_bf16(b.z * rs * bf16_lo(g.w), b.w * rs * bf16_hi(g.w));
-    xo[v] = o;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = threadIdx.x + i * 256;
+    if (v < nvec) {
+      const uint4 g = gv[v];
+      uint4 o;
+      o.x = pack_bf16(f[i][0] * rs * bf16_lo(g.x), f[i][1] * rs * bf16_hi(g.x));
+      o.y = pack_bf16(f[i][2] * rs * bf16_lo(g.y), f[i][3] * rs * bf16_hi(g.y));
+      o.z = pack_bf16(f[i][4] * rs * bf16_lo(g.z), f[i][5] * rs * bf16_hi(g.z));
+      o.w = pack_bf16(f[i][6] * rs * bf16_lo(g.w), f[i][7] * rs * bf16_hi(g.w));
+      xo[v] = o;
+    }
   }
+}
+
+template <bool EMBED>
+void launch_rmsnorm(const bf16* E, const int* tok, const float* h_in, const int* row_map, int M, int d,
+                    const bf16* gain, float eps, float* h_out, bf16* x, cudaStream_t stream) {
+  const int nv = (d / 8 + 255) / 256;  // vectors per thread
+  if (nv <= 1)
+    launch_pdl(rmsnorm_kernel<EMBED, 1>, dim3(M), dim3(256), 0, stream, E, tok, h_in, row_map, d, gain, eps, h_out, x);
+  else if (nv <= 2)
+    launch_pdl(rmsnorm_kernel<EMBED, 2>, dim3(M), dim3(256), 0, stream, E, tok, h_in, row_map, d, gain, eps, h_out, x);
+  else if (nv <= 4)
+    launch_pdl(rmsnorm_kernel<EMBED, 4>, dim3(M), dim3(256), 0, stream, E, tok, h_in, row_map, d, gain, eps, h_out, x);
+  else
+    launch_pdl(rmsnorm_kernel<EMBED, 8>, dim3(M), dim3(256), 0, stream, E, tok, h_in, row_map, d, gain, eps, h_out, x);
 }
 
 // ------------------------------------------------------------------ init
@@ -212,13 +233,15 @@ void rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_ro
 void embed_rmsnorm(const bf16* E, const int* tok, int M, int d, const bf16* gain, float eps, float* h, bf16* x,
                    cudaStream_t stream) {
   if (M <= 0) return;
-  rmsnorm_kernel<true><<<M, 256, 0, stream>>>(E, tok, nullptr, nullptr, d, gain, eps, h, x);
+  if (d > 8 * 256 * 8 || d % 8) return;  // d <= 16384 (all presets)
+  launch_rmsnorm<true>(E, tok, nullptr, nullptr, M, d, gain, eps, h, x, stream);
 }
 
 void rmsnorm(const float* h, int M, int d, const bf16* gain, float eps, bf16* x, cudaStream_t stream,
              const int* row_map) {
   if (M <= 0) return;
-  rmsnorm_kernel<false><<<M, 256, 0, stream>>>(nullptr, nullptr, h, row_map, d, gain, eps, nullptr, x);
+  if (d > 8 * 256 * 8 || d % 8) return;
+  launch_rmsnorm<false>(nullptr, nullptr, h, row_map, M, d, gain, eps, nullptr, x, stream);
 }
 
 void init_normal_bf16(bf16* dst, uint64_t seed, size_t rows, size_t cols, float sigma, int blk, int blk_stride,
