@@ -34,29 +34,37 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int GEMM_THREADS = 192;
 
-template <int BN>
+// AR = A rows loaded per stage (128, or 64 / 32 for the one-M-tile
+// weight-streaming GEMMs). A stage is [A: AR rows][B: BN rows]; the UMMA still
+// reads 128 A rows from the stage base, so rows AR..127 alias the stage's B
+// bytes: they only feed accumulator rows >= M, which are never stored. Small
+// stages leave room for a second CTA per SM (the next kernel's, under PDL).
+template <int BN, int AR = BM>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = AR < BM ? (AR == 32 ? 8 : 7) : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int MIN_BLOCKS = 1;
-  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t A_BYTES = AR * BK * 2;  // TMA bytes of A per stage
   static constexpr uint32_t B_BYTES = BN * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1024-byte aligned (SW128 atoms)");
+  static_assert(AR == BM || STAGE_BYTES >= BM * BK * 2, "aliased A rows must stay inside the stage");
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
   static_assert(SMEM <= 232448, "GEMM pipeline exceeds the 227 KB shared-memory limit");
 };
 
-template <int BN, int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
+template <int BN, int EPI, int AR = BM>
+__global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, const EpiParams ep) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, AR>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // stage s: A at smem + s*STAGE_BYTES, B right after it
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint8_t* sB = smem + C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -145,7 +153,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
           npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
           for (int i = 0; i < npre; ++i) {
             mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
-            tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
+            tma_load_2d(sB + i * C::STAGE_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
           }
         }
       }
@@ -160,9 +168,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
           if (it >= npre) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+            tma_load_2d(sB + stage * C::STAGE_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
           }
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          tma_load_2d(sA + stage * C::STAGE_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -186,8 +194,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN>::MIN_BLOCKS)
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t a_base = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
+          const uint32_t a_base = smem_u32(sA + stage * C::STAGE_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * C::STAGE_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
@@ -351,30 +359,30 @@ bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, ui
 
 namespace {
 
-template <int BN, int EPI>
+template <int BN, int EPI, int AR = BM>
 int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& ep, cudaStream_t stream) {
-  using C = GemmCfg<BN>;
-  smem_attr_once(gemm_tc_kernel<BN, EPI>, (int)C::SMEM);
+  using C = GemmCfg<BN, AR>;
+  smem_attr_once(gemm_tc_kernel<BN, EPI, AR>, (int)C::SMEM);
   CUtensorMap ta, tb;
-  if (!make_tmap_2d(&ta, A, M, K, K, BM)) return -1;
+  if (!make_tmap_2d(&ta, A, M, K, K, AR)) return -1;
   if (!make_tmap_2d(&tb, B, N, K, K, BN)) return -1;
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int slots = num_sms() * C::MIN_BLOCKS;
   const int grid = ep.streamk ? ep.streamk : (work < slots ? work : slots);
-  launch_pdl(gemm_tc_kernel<BN, EPI>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
+  launch_pdl(gemm_tc_kernel<BN, EPI, AR>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-template <int BN>
+template <int BN, int AR = BM>
 int dispatch_epi(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
                  cudaStream_t s) {
   switch (epi) {
-    case EPI_STORE_BF16: return launch<BN, EPI_STORE_BF16>(A, B, M, N, K, ep, s);
-    case EPI_STORE_F32: return launch<BN, EPI_STORE_F32>(A, B, M, N, K, ep, s);
-    case EPI_RESID: return launch<BN, EPI_RESID>(A, B, M, N, K, ep, s);
-    case EPI_SWIGLU: return launch<BN, EPI_SWIGLU>(A, B, M, N, K, ep, s);
-    case EPI_QKV: return launch<BN, EPI_QKV>(A, B, M, N, K, ep, s);
+    case EPI_STORE_BF16: return launch<BN, EPI_STORE_BF16, AR>(A, B, M, N, K, ep, s);
+    case EPI_STORE_F32: return launch<BN, EPI_STORE_F32, AR>(A, B, M, N, K, ep, s);
+    case EPI_RESID: return launch<BN, EPI_RESID, AR>(A, B, M, N, K, ep, s);
+    case EPI_SWIGLU: return launch<BN, EPI_SWIGLU, AR>(A, B, M, N, K, ep, s);
+    case EPI_QKV: return launch<BN, EPI_QKV, AR>(A, B, M, N, K, ep, s);
   }
   return -1;
 }
@@ -506,6 +514,13 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
       ep.splits = s;
       ep.full_tiles = (int)(tiles - tail);
     }
+  }
+  // one-M-tile weight streaming at BN=128: load only the live A rows (32 / 64)
+  // per stage -> 20-24 KB stages, 7-8 of them (bit 27 of the flags: force the
+  // full 128-row A box, tuning only)
+  if (bn == 128 && M <= 64 && !(force_bn_flags & 0x8000000)) {
+    if (M <= 32) return dispatch_epi<128, 32>(A, B, M, N, K, epi, ep, stream);
+    return dispatch_epi<128, 64>(A, B, M, N, K, epi, ep, stream);
   }
   switch (bn) {
     case 256: return dispatch_epi<256>(A, B, M, N, K, epi, ep, stream);

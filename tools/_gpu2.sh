@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests -q -x -m gpu 2>&1 | tail -2
-for i in 1 2; do timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b.log 2>&1; python -c "
-import json;d=json.loads(open('gpurun_out/b.log').read().strip().splitlines()[-1]);print(round(d['ttft_ms'],2),d['stage_ms'],d['kernels']['norm'],d['clocks']['sm_mhz'])"; done
+timeout 600 python -m pytest tests/test_kernels_gpu.py -q -x -k "gemm" 2>&1 | tail -2
+timeout 300 python tools/gemm_small.py 32 qkv,o,gu,down,lm > gpurun_out/gs.log 2>&1; cut -c1-300 gpurun_out/gs.log
+timeout 300 python tools/gemm_small.py 1 qkv,o,gu,down > gpurun_out/gs1.log 2>&1; cut -c1-300 gpurun_out/gs1.log

@@ -23,11 +23,11 @@ for name, (N, K) in shapes.items():
     a = torch.randn(M, K, device=dev).to(torch.bfloat16)
     c = torch.zeros(M, N, device=dev, dtype=torch.float32)
     res = []
-    for bn in (0, 64, 128, 256, 2064, 2128):
-        for sp in ((0,) if bn == 0 or bn > 2000 else (1, 2, 3, 4, 6, 8)):
+    for bn in (0, 128, 4128):
+        for sp in ((0,) if bn == 0 else (1, 2, 3, 4, 6, 8)):
             if bn and N % (bn % 1000):
                 continue
-            fl = (bn - 2000) | 0x2000000 if bn > 2000 else bn
+            fl = 128 | 0x8000000 if bn == 4128 else bn
             flags = (fl | (sp << 20) | 0x20000 | 0x80000) if bn else 0x80000
             try:
                 st = torch.cuda.Stream()
@@ -49,7 +49,7 @@ for name, (N, K) in shapes.items():
                 e1.record()
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) / 30 * 1e3
-                nm = {2064: "sk64_", 2128: "sk128_"}.get(bn, f"bn{bn or 'auto'}")
+                nm = {4128: "bn128full_"}.get(bn, f"bn{bn or 'auto'}")
                 res.append((f"{nm}s{sp}", round(us, 1), round(N * K * 2 / us / 1e3)))
             except Exception as ex:
                 res.append((f"bn{bn}s{sp}", "err", str(ex)[:50]))
