@@ -141,6 +141,34 @@ FRAG_API frag_status frag_store_put(frag_store* st, const frag_chunk_id* id, con
 FRAG_API frag_status frag_store_fetch(frag_store* st, const frag_chunk_id* id, frag_record_view* out);
 FRAG_API frag_status frag_store_release(frag_store* st, const frag_chunk_id* id);
 FRAG_API frag_status frag_store_peek(const frag_store* st, const frag_chunk_id* id, frag_record_view* out);
+/* FKVC record files (serialize_record / deserialize_record): magic
+ * "FKVC", version u32 = 1, chunk_id[16], variant u8, native_start u32, layers
+ * u16, heads u16 (KV heads), head_dim u16, tokens u32, then for every layer K
+ * then V, [tokens][heads][head_dim] little-endian fp32. Token ids are not in
+ * the file; the loader takes them from the caller. Errors: FRAG_E_FORMAT with
+ * frag_last_format_kind() = FRAG_FORMAT_BAD_MAGIC / BAD_VERSION / TRUNCATED /
+ * MALFORMED / IO (FormatError::Kind, common.hpp:33). */
+typedef struct {
+  frag_chunk_id id;
+  int32_t variant, native_start, layers, heads, head_dim, tokens;
+} frag_fkvc_header;
+enum { FRAG_FORMAT_BAD_MAGIC = 0, FRAG_FORMAT_BAD_VERSION = 1, FRAG_FORMAT_TRUNCATED = 2, FRAG_FORMAT_MALFORMED = 3,
+       FRAG_FORMAT_IO = 4 };
+FRAG_API int32_t frag_last_format_kind(void);
+/* Host-only codec: k, v host fp32 [layers][tokens][heads][head_dim]. */
+FRAG_API frag_status frag_fkvc_write(const char* path, const frag_fkvc_header* h, const float* k, const float* v);
+/* Reads the header (and, if k/v are non-null, the tensors: cap_floats = capacity
+ * of each of k and v in floats). */
+FRAG_API frag_status frag_fkvc_read(const char* path, frag_fkvc_header* h, float* k, float* v, size_t cap_floats);
+/* Write a store record to an FKVC file (bf16 -> fp32, exact). */
+FRAG_API frag_status frag_store_save(frag_store* st, const frag_chunk_id* id, const char* path);
+/* KVCache loader (DISK -> GPU tier): reads an FKVC file layer
+ * by layer into pinned ping-pong buffers while the previous layer is copied
+ * H2D and converted to bf16 on `stream`; inserts the record (id from the file)
+ * when the copy completes. Safe to call from a loader thread while other
+ * threads run frag_reprocess on other streams. */
+FRAG_API frag_status frag_store_load(frag_store* st, const char* path, const int32_t* tokens, int32_t n_tok,
+                                     int32_t overwrite, void* stream, frag_chunk_id* id_out);
 FRAG_API int64_t frag_store_count(const frag_store* st);
 FRAG_API uint64_t frag_store_bytes_used(const frag_store* st);
 

@@ -36,6 +36,11 @@ class ChunkId(C.Structure):
         return hash(bytes(self.bytes))
 
 
+class FkvcHeader(C.Structure):
+    _fields_ = [("id", ChunkId), ("variant", C.c_int32), ("native_start", C.c_int32), ("layers", C.c_int32),
+                ("heads", C.c_int32), ("head_dim", C.c_int32), ("tokens", C.c_int32)]
+
+
 class RecordView(C.Structure):
     _fields_ = [("id", ChunkId), ("n_tok", C.c_int32), ("native_start", C.c_int32), ("variant", C.c_int32),
                 ("tier", C.c_int32), ("heat", C.c_uint64), ("last_access", C.c_uint64),
@@ -83,6 +88,11 @@ _SIGS = {
     "frag_store_release": (C.c_int, [_P, C.POINTER(ChunkId)]),
     "frag_store_peek": (C.c_int, [_P, C.POINTER(ChunkId), C.POINTER(RecordView)]),
     "frag_store_count": (C.c_int64, [_P]),
+    "frag_last_format_kind": (C.c_int32, []),
+    "frag_fkvc_write": (C.c_int, [C.c_char_p, C.POINTER(FkvcHeader), _P, _P]),
+    "frag_fkvc_read": (C.c_int, [C.c_char_p, C.POINTER(FkvcHeader), _P, _P, C.c_size_t]),
+    "frag_store_save": (C.c_int, [_P, C.POINTER(ChunkId), C.c_char_p]),
+    "frag_store_load": (C.c_int, [_P, C.c_char_p, _I32P, C.c_int32, C.c_int32, _P, C.POINTER(ChunkId)]),
     "frag_store_bytes_used": (C.c_uint64, [_P]),
     "frag_preprocess_isolated": (C.c_int, [_P, _P, _I32P, C.c_int32, _I32P, C.c_int32, C.c_int32,
                                            C.POINTER(ChunkId)]),
@@ -133,7 +143,13 @@ class StoreError(FragError):
 
 
 class FormatError(FragError):
+    """FormatError::Kind (common.hpp:33) in .kind: BadMagic, BadVersion, Truncated, Malformed, Io."""
     code = FRAG_E_FORMAT
+    KINDS = ("BadMagic", "BadVersion", "Truncated", "Malformed", "Io")
+
+    def __init__(self, msg, kind=None):
+        super().__init__(msg)
+        self.kind = kind
 
 
 class CudaError(FragError):
@@ -151,6 +167,9 @@ _ERRS = {FRAG_E_CONTRACT: ContractError, FRAG_E_STORE: StoreError, FRAG_E_FORMAT
 def check(status: int) -> None:
     if status != FRAG_OK:
         msg = lib.frag_last_error().decode(errors="replace")
+        if status == FRAG_E_FORMAT:
+            k = int(lib.frag_last_format_kind())
+            raise FormatError(msg, FormatError.KINDS[k] if 0 <= k < len(FormatError.KINDS) else None)
         raise _ERRS.get(status, FragError)(msg)
 
 

@@ -22,10 +22,12 @@ struct frag_result {
 namespace fragimpl {
 
 thread_local std::string t_last_error;
+thread_local int t_format_kind = -1;
 
 void set_last_error(const std::string& m) { t_last_error = m; }
 
 [[noreturn]] void fail(frag_status code, const std::string& msg) { throw Error{code, msg}; }
+[[noreturn]] void fail_format(int kind, const std::string& msg) { throw Error{FRAG_E_FORMAT, msg, kind}; }
 
 namespace {
 template <class F>
@@ -35,6 +37,7 @@ frag_status guard(F&& f) {
     return FRAG_OK;
   } catch (const Error& e) {
     set_last_error(e.msg);
+    t_format_kind = e.format_kind;
     return e.code;
   } catch (const std::bad_alloc&) {
     set_last_error("host allocation failed");
@@ -59,6 +62,21 @@ using namespace fragimpl;
 extern "C" {
 
 FRAG_API const char* frag_last_error(void) { return t_last_error.c_str(); }
+FRAG_API int32_t frag_last_format_kind(void) { return t_format_kind; }
+
+FRAG_API frag_status frag_fkvc_write(const char* path, const frag_fkvc_header* h, const float* k, const float* v) {
+  return guard([&] {
+    need(path && h && k && v, "null argument");
+    fkvc_write(path, *h, k, v);
+  });
+}
+
+FRAG_API frag_status frag_fkvc_read(const char* path, frag_fkvc_header* h, float* k, float* v, size_t cap_floats) {
+  return guard([&] {
+    need(path && h, "null argument");
+    fkvc_read(path, h, k, v, cap_floats);
+  });
+}
 FRAG_API const char* frag_version(void) { return "fusionrag-b200 0.1 (sm_100a)"; }
 
 FRAG_API frag_status frag_model_preset(const char* name, frag_model_cfg* out) {
@@ -260,6 +278,21 @@ FRAG_API frag_status frag_store_peek(const frag_store* st, const frag_chunk_id* 
     auto it = st->s->recs.find(key_of(*id));
     if (it == st->s->recs.end()) fail(FRAG_E_STORE, "missing chunk record");
     fill_view(it->second.get(), out);
+  });
+}
+
+FRAG_API frag_status frag_store_save(frag_store* st, const frag_chunk_id* id, const char* path) {
+  return guard([&] {
+    need(st && id && path, "null argument");
+    store_save(st->s, *id, path);
+  });
+}
+
+FRAG_API frag_status frag_store_load(frag_store* st, const char* path, const int32_t* tokens, int32_t n_tok,
+                                     int32_t overwrite, void* stream, frag_chunk_id* id_out) {
+  return guard([&] {
+    need(st && path && tokens, "null argument");
+    store_load(st->s, path, tokens, n_tok, overwrite != 0, static_cast<cudaStream_t>(stream), id_out);
   });
 }
 

@@ -28,8 +28,10 @@ using fragk::bf16;
 struct Error {
   frag_status code;
   std::string msg;
+  int format_kind = -1;  // FRAG_FORMAT_* for FRAG_E_FORMAT
 };
 [[noreturn]] void fail(frag_status code, const std::string& msg);
+[[noreturn]] void fail_format(int kind, const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
 void set_last_error(const std::string& m);
 
@@ -242,6 +244,13 @@ void store_put(Store* st, const frag_chunk_id& id, const int32_t* tokens, int n_
                const void* k, const void* v, bool overwrite, size_t src_layer_pitch_elems = 0,
                cudaStream_t s = nullptr);
 Record* store_fetch(Store* st, const frag_chunk_id& id);  // heat++, pin
+// FKVC record files (serialize_record / deserialize_record): fp32
+// K then V per layer; tokens are supplied by the caller (the format omits them).
+void store_save(Store* st, const frag_chunk_id& id, const char* path);
+void store_load(Store* st, const char* path, const int32_t* tokens, int n_tok, bool overwrite, cudaStream_t s,
+                frag_chunk_id* id_out);
+void fkvc_write(const char* path, const frag_fkvc_header& h, const float* k, const float* v);
+void fkvc_read(const char* path, frag_fkvc_header* h, float* k, float* v, size_t cap_floats);
 void store_release(Store* st, const frag_chunk_id& id);
 
 void hash_tokens(const int32_t* t, int n, uint64_t salt, frag_chunk_id* out);

@@ -137,6 +137,8 @@ int greedy_argmax(const float* logits, int V, int* out, int* out_idx, int* plan_
 void init_normal_bf16(bf16* dst, uint64_t seed, size_t rows, size_t cols, float sigma, int blk, int blk_stride,
                       int blk_off, cudaStream_t stream);
 void fill_bf16(bf16* dst, size_t n, float v, cudaStream_t stream);
+// fp32 -> bf16 round-to-nearest-even, n % 4 == 0 (FKVC loads)
+void f32_to_bf16(const float* src, bf16* dst, size_t n, cudaStream_t stream);
 
 }  // namespace fragk
 

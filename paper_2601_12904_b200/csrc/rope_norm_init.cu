@@ -244,6 +244,25 @@ void rmsnorm(const float* h, int M, int d, const bf16* gain, float eps, bf16* x,
   launch_rmsnorm<false>(nullptr, nullptr, h, row_map, M, d, gain, eps, nullptr, x, stream);
 }
 
+namespace {
+__global__ void f32_to_bf16_kernel(const float4* __restrict__ src, uint2* __restrict__ dst, size_t n4) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 f = src[i];
+    dst[i] = make_uint2(pack_bf16(f.x, f.y), pack_bf16(f.z, f.w));
+  }
+}
+}  // namespace
+
+// fp32 -> bf16 (round to nearest even), n a multiple of 4 (FKVC record loads)
+void f32_to_bf16(const float* src, bf16* dst, size_t n, cudaStream_t stream) {
+  const size_t n4 = n / 4;
+  size_t blocks = (n4 + 255) / 256;
+  if (blocks > (size_t)num_sms() * 8) blocks = (size_t)num_sms() * 8;
+  if (blocks == 0) return;
+  f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(src),
+                                                          reinterpret_cast<uint2*>(dst), n4);
+}
+
 void init_normal_bf16(bf16* dst, uint64_t seed, size_t rows, size_t cols, float sigma, int blk, int blk_stride,
                       int blk_off, cudaStream_t stream) {
   const size_t pairs = (rows * cols + 1) / 2;

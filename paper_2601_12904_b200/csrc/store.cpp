@@ -2,9 +2,11 @@
 // (SPEC.md:265-273), fetch, reader/writer locking with pin
 // counts. Records live in device memory of the store's GPU; the
 // host keeps the index, heat metadata and a copy of each record's token ids.
-// Tiering (CPU/DISK), eviction and the FKVC file format are out of scope
-// (SURVEY.md §2 kv_store row, §8(f) rank 2).
+// FKVC record files + the DISK -> GPU loader are
+// at the end; tier eviction policy is out of scope (SURVEY.md §2 kv_store row).
+#include <cstdio>
 #include <cstring>
+#include <memory>
 
 #include "engine.h"
 
@@ -56,6 +58,31 @@ Store* store_create(const frag_model_cfg& cfg, int device, size_t cap) {
   return s;
 }
 
+// Insert an uploaded record under the writer lock: single copy per chunk id
+// (SPEC.md:269), pinned records are never replaced, GPU-tier
+// capacity accounting.
+void store_insert(Store* st, std::unique_ptr<Record> rec, bool overwrite) {
+  std::unique_lock<std::shared_mutex> g(st->mu);
+  const ChunkKey key = key_of(rec->id);
+  auto it = st->recs.find(key);
+  size_t freed = 0;
+  if (it != st->recs.end()) {
+    if (!overwrite) fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
+    if (it->second->pins > 0) fail(FRAG_E_STORE, "cannot overwrite a pinned record (SPEC.md:320)");
+    freed = it->second->bytes;
+  }
+  if (st->capacity && st->used - freed + rec->bytes > st->capacity)
+    fail(FRAG_E_STORE, "GPU tier capacity exhausted (tiering/eviction out of scope in this build)");
+  const size_t bytes = rec->bytes;
+  if (it != st->recs.end()) {
+    st->used -= freed;
+    it->second = std::move(rec);
+  } else {
+    st->recs.emplace(key, std::move(rec));
+  }
+  st->used += bytes;
+}
+
 void store_put(Store* st, const frag_chunk_id& id, const int32_t* tokens, int n_tok, int native_start, int variant,
                const void* k, const void* v, bool overwrite, size_t src_layer_pitch_elems, cudaStream_t s) {
   const auto& c = st->cfg;
@@ -67,17 +94,12 @@ void store_put(Store* st, const frag_chunk_id& id, const int32_t* tokens, int n_
     if (tokens[i] < 0 || tokens[i] >= c.vocab) fail(FRAG_E_CONTRACT, "record token out of vocabulary");
   const size_t bytes = st->record_bytes(n_tok);
   DeviceGuard dg(st->device);
-  std::unique_lock<std::shared_mutex> g(st->mu);
   const ChunkKey key = key_of(id);
-  auto it = st->recs.find(key);
-  size_t freed = 0;
-  if (it != st->recs.end()) {
-    if (!overwrite) fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
-    if (it->second->pins > 0) fail(FRAG_E_STORE, "cannot overwrite a pinned record (SPEC.md:320)");
-    freed = it->second->bytes;
+  {
+    std::shared_lock<std::shared_mutex> g(st->mu);  // early duplicate check (re-checked at insert)
+    if (!overwrite && st->recs.count(key)) fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
   }
-  if (st->capacity && st->used - freed + bytes > st->capacity)
-    fail(FRAG_E_STORE, "GPU tier capacity exhausted (tiering/eviction out of scope in this build)");
+  // upload outside the store lock: readers (reprocess) keep going meanwhile
   auto rec = std::make_unique<Record>();
   rec->id = id;
   rec->n_tok = n_tok;
@@ -96,13 +118,7 @@ void store_put(Store* st, const frag_chunk_id& id, const int32_t* tokens, int n_
              "record V");
   check_cuda(cudaMemcpyAsync(rec->tok.p, tokens, n_tok * sizeof(int32_t), cudaMemcpyDefault, s), "record tokens");
   check_cuda(cudaStreamSynchronize(s), "record upload");
-  if (it != st->recs.end()) {
-    st->used -= freed;
-    it->second = std::move(rec);
-  } else {
-    st->recs.emplace(key, std::move(rec));
-  }
-  st->used += bytes;
+  store_insert(st, std::move(rec), overwrite);
 }
 
 Record* store_fetch(Store* st, const frag_chunk_id& id) {
@@ -121,6 +137,209 @@ void store_release(Store* st, const frag_chunk_id& id) {
   auto it = st->recs.find(key_of(id));
   if (it == st->recs.end()) fail(FRAG_E_STORE, "missing chunk record");
   if (it->second->pins > 0) it->second->pins -= 1;
+}
+
+// ---------------------------------------------------------------- FKVC files
+namespace {
+constexpr uint32_t kFkvcVersion = 1;
+constexpr size_t kFkvcHeader = 4 + 4 + 16 + 1 + 4 + 2 + 2 + 2 + 4;  // 39 bytes, packed little-endian
+
+struct FileCloser {
+  void operator()(FILE* f) const {
+    if (f) std::fclose(f);
+  }
+};
+using FilePtr = std::unique_ptr<FILE, FileCloser>;
+
+template <class T>
+void put_le(uint8_t*& p, T v) {
+  for (size_t i = 0; i < sizeof(T); ++i) *p++ = (uint8_t)((uint64_t)v >> (8 * i));
+}
+template <class T>
+T get_le(const uint8_t*& p) {
+  uint64_t v = 0;
+  for (size_t i = 0; i < sizeof(T); ++i) v |= (uint64_t)(*p++) << (8 * i);
+  return (T)v;
+}
+
+void encode_header(const frag_fkvc_header& h, uint8_t* buf) {
+  uint8_t* p = buf;
+  std::memcpy(p, "FKVC", 4);
+  p += 4;
+  put_le<uint32_t>(p, kFkvcVersion);
+  std::memcpy(p, h.id.bytes, 16);
+  p += 16;
+  put_le<uint8_t>(p, (uint8_t)h.variant);
+  put_le<uint32_t>(p, (uint32_t)h.native_start);
+  put_le<uint16_t>(p, (uint16_t)h.layers);
+  put_le<uint16_t>(p, (uint16_t)h.heads);
+  put_le<uint16_t>(p, (uint16_t)h.head_dim);
+  put_le<uint32_t>(p, (uint32_t)h.tokens);
+}
+
+frag_fkvc_header read_header(FILE* f, const char* path) {
+  uint8_t buf[kFkvcHeader];
+  const size_t got = std::fread(buf, 1, kFkvcHeader, f);
+  if (got >= 4 && std::memcmp(buf, "FKVC", 4) != 0) fail_format(FRAG_FORMAT_BAD_MAGIC, std::string("not an FKVC file: ") + path);
+  if (got < kFkvcHeader) fail_format(FRAG_FORMAT_TRUNCATED, std::string("truncated FKVC header: ") + path);
+  const uint8_t* p = buf + 4;
+  const uint32_t ver = get_le<uint32_t>(p);
+  if (ver != kFkvcVersion)
+    fail_format(FRAG_FORMAT_BAD_VERSION, "FKVC version " + std::to_string(ver) + " (expected 1): " + path);
+  frag_fkvc_header h{};
+  std::memcpy(h.id.bytes, p, 16);
+  p += 16;
+  h.variant = get_le<uint8_t>(p);
+  h.native_start = (int32_t)get_le<uint32_t>(p);
+  h.layers = get_le<uint16_t>(p);
+  h.heads = get_le<uint16_t>(p);
+  h.head_dim = get_le<uint16_t>(p);
+  h.tokens = (int32_t)get_le<uint32_t>(p);
+  if (h.layers < 1 || h.heads < 1 || h.head_dim < 1 || h.tokens < 1 || h.native_start < 1 ||
+      (h.variant != FRAG_VARIANT_ISOLATED && h.variant != FRAG_VARIANT_FUSED))
+    fail_format(FRAG_FORMAT_MALFORMED, std::string("malformed FKVC header: ") + path);
+  return h;
+}
+
+void read_exact(FILE* f, void* dst, size_t bytes, const char* path) {
+  if (std::fread(dst, 1, bytes, f) != bytes)
+    fail_format(FRAG_FORMAT_TRUNCATED, std::string("truncated FKVC payload: ") + path);
+}
+
+FilePtr open_or_fail(const char* path, const char* mode) {
+  FilePtr f(std::fopen(path, mode));
+  if (!f) fail_format(FRAG_FORMAT_IO, std::string("cannot open ") + path);
+  return f;
+}
+}  // namespace
+
+void fkvc_write(const char* path, const frag_fkvc_header& h, const float* k, const float* v) {
+  if (h.layers < 1 || h.heads < 1 || h.head_dim < 1 || h.tokens < 1 || h.native_start < 1)
+    fail(FRAG_E_CONTRACT, "invalid FKVC header fields");
+  FilePtr f = open_or_fail(path, "wb");
+  uint8_t buf[kFkvcHeader];
+  encode_header(h, buf);
+  bool ok = std::fwrite(buf, 1, kFkvcHeader, f.get()) == kFkvcHeader;
+  const size_t per = (size_t)h.tokens * h.heads * h.head_dim;
+  for (int l = 0; l < h.layers && ok; ++l) {
+    ok = std::fwrite(k + (size_t)l * per, sizeof(float), per, f.get()) == per &&
+         std::fwrite(v + (size_t)l * per, sizeof(float), per, f.get()) == per;
+  }
+  if (!ok || std::fflush(f.get()) != 0) fail_format(FRAG_FORMAT_IO, std::string("write failed: ") + path);
+}
+
+void fkvc_read(const char* path, frag_fkvc_header* h, float* k, float* v, size_t cap_floats) {
+  FilePtr f = open_or_fail(path, "rb");
+  *h = read_header(f.get(), path);
+  if (!k && !v) return;
+  const size_t per = (size_t)h->tokens * h->heads * h->head_dim;
+  if (!k || !v || cap_floats < per * h->layers) fail(FRAG_E_CONTRACT, "output buffers too small for the FKVC record");
+  for (int l = 0; l < h->layers; ++l) {
+    read_exact(f.get(), k + (size_t)l * per, per * sizeof(float), path);
+    read_exact(f.get(), v + (size_t)l * per, per * sizeof(float), path);
+  }
+}
+
+void store_save(Store* st, const frag_chunk_id& id, const char* path) {
+  const auto& c = st->cfg;
+  DeviceGuard dg(st->device);
+  Record* r = nullptr;
+  {  // pin while it is read (saving is not an access: heat unchanged)
+    std::unique_lock<std::shared_mutex> g(st->mu);
+    auto it = st->recs.find(key_of(id));
+    if (it == st->recs.end()) fail(FRAG_E_STORE, "missing chunk record (SPEC.md:287)");
+    r = it->second.get();
+    r->pins += 1;
+  }
+  struct Unpin {
+    Store* st;
+    frag_chunk_id id;
+    ~Unpin() {
+      try {
+        store_release(st, id);
+      } catch (...) {
+      }
+    }
+  } unpin{st, id};
+  const size_t per = (size_t)r->n_tok * c.n_kv_heads * c.head_dim;
+  std::vector<uint16_t> kb(per * c.layers), vb(per * c.layers);
+  check_cuda(cudaMemcpy(kb.data(), r->k(), kb.size() * 2, cudaMemcpyDeviceToHost), "record K D2H");
+  check_cuda(cudaMemcpy(vb.data(), r->v(), vb.size() * 2, cudaMemcpyDeviceToHost), "record V D2H");
+  std::vector<float> kf(kb.size()), vf(vb.size());
+  for (size_t i = 0; i < kb.size(); ++i) {  // bf16 -> fp32 is exact
+    uint32_t a = (uint32_t)kb[i] << 16, b = (uint32_t)vb[i] << 16;
+    std::memcpy(&kf[i], &a, 4);
+    std::memcpy(&vf[i], &b, 4);
+  }
+  frag_fkvc_header h{};
+  h.id = r->id;
+  h.variant = r->variant;
+  h.native_start = r->native_start;
+  h.layers = c.layers;
+  h.heads = c.n_kv_heads;
+  h.head_dim = c.head_dim;
+  h.tokens = r->n_tok;
+  fkvc_write(path, h, kf.data(), vf.data());
+}
+
+void store_load(Store* st, const char* path, const int32_t* tokens, int n_tok, bool overwrite, cudaStream_t s,
+                frag_chunk_id* id_out) {
+  const auto& c = st->cfg;
+  FilePtr f = open_or_fail(path, "rb");
+  const frag_fkvc_header h = read_header(f.get(), path);
+  if (h.layers != c.layers || h.heads != c.n_kv_heads || h.head_dim != c.head_dim)
+    fail_format(FRAG_FORMAT_MALFORMED, std::string("FKVC record shape does not match the store's model: ") + path);
+  if (n_tok != h.tokens) fail(FRAG_E_CONTRACT, "token count differs from the FKVC record's");
+  for (int i = 0; i < n_tok; ++i)
+    if (tokens[i] < 0 || tokens[i] >= c.vocab) fail(FRAG_E_CONTRACT, "record token out of vocabulary");
+  const ChunkKey key = key_of(h.id);
+  {
+    std::shared_lock<std::shared_mutex> g(st->mu);
+    if (!overwrite && st->recs.count(key)) fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
+  }
+  DeviceGuard dg(st->device);
+  const size_t per = (size_t)n_tok * c.n_kv_heads * c.head_dim;  // floats of K (or V) per layer
+  auto rec = std::make_unique<Record>();
+  rec->id = h.id;
+  rec->n_tok = n_tok;
+  rec->native_start = h.native_start;
+  rec->variant = h.variant;
+  rec->bytes = st->record_bytes(n_tok);
+  rec->kv.alloc(rec->bytes);
+  rec->tok.alloc(n_tok * sizeof(int32_t));
+  rec->tok_host.assign(tokens, tokens + n_tok);
+  // ping-pong: read layer l+1 from the file while layer l is copied + converted
+  PinnedBuf host[2];
+  DevBuf dev[2];
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  for (int b = 0; b < 2; ++b) {
+    host[b].ensure(2 * per * sizeof(float));
+    dev[b].alloc(2 * per * sizeof(float));
+    check_cuda(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "event");
+  }
+  struct Events {
+    cudaEvent_t* e;
+    ~Events() {
+      for (int b = 0; b < 2; ++b)
+        if (e[b]) cudaEventDestroy(e[b]);
+    }
+  } ev_guard{done};
+  bool in_flight[2] = {false, false};
+  for (int l = 0; l < c.layers; ++l) {
+    const int b = l & 1;
+    if (in_flight[b]) check_cuda(cudaEventSynchronize(done[b]), "loader buffer");
+    read_exact(f.get(), host[b].p, 2 * per * sizeof(float), path);  // K then V of layer l
+    check_cuda(cudaMemcpyAsync(dev[b].p, host[b].p, 2 * per * sizeof(float), cudaMemcpyHostToDevice, s), "H2D");
+    fragk::f32_to_bf16(dev[b].as<float>(), rec->k() + (size_t)l * per, per, s);
+    fragk::f32_to_bf16(dev[b].as<float>() + per, rec->v() + (size_t)l * per, per, s);
+    check_cuda(cudaEventRecord(done[b], s), "event record");
+    in_flight[b] = true;
+  }
+  g_launches += 2 * (uint64_t)c.layers;
+  check_cuda(cudaMemcpyAsync(rec->tok.p, tokens, n_tok * sizeof(int32_t), cudaMemcpyHostToDevice, s), "tokens");
+  check_cuda(cudaStreamSynchronize(s), "record load");
+  if (id_out) *id_out = h.id;
+  store_insert(st, std::move(rec), overwrite);
 }
 
 }  // namespace fragimpl

@@ -16,12 +16,12 @@ from typing import Iterable, Sequence
 
 import numpy as np
 
-from ._lib import (ChunkId, ContractError, CudaError, FormatError, FragError, ModelCfg, OutOfMemory,
+from ._lib import (ChunkId, FkvcHeader, ContractError, CudaError, FormatError, FragError, ModelCfg, OutOfMemory,
                    RecordView, ReprocessOpts, StoreError, Timing, check, lib)
 
 __all__ = ["ModelCfg", "ChunkId", "Engine", "ChunkKVStore", "Result", "preset", "hash_tokens",
            "ContractError", "StoreError", "FormatError", "CudaError", "OutOfMemory", "FragError",
-           "ISOLATED", "FUSED", "launch_count", "memcpy"]
+           "ISOLATED", "FUSED", "launch_count", "memcpy", "fkvc_write", "fkvc_read"]
 
 ISOLATED, FUSED = 0, 1
 WEIGHT_IDS = {"emb": 0, "lm_head": 1, "wq": 2, "wk": 3, "wv": 4, "wo": 5, "w_gate": 6, "w_up": 7,
@@ -234,6 +234,20 @@ class ChunkKVStore:
         memcpy(v.ctypes.data, r.v_dev, v.nbytes)
         return k, v
 
+    # ------------------------------------------------ FKVC files
+    def save_record(self, chunk_id: ChunkId, path: str):
+        """serialize_record: the record as an FKVC file (fp32, exact)."""
+        check(lib.frag_store_save(self._h, C.byref(chunk_id), str(path).encode()))
+
+    def load_record(self, path: str, tokens: Sequence[int], *, overwrite: bool = False, stream=None) -> ChunkId:
+        """deserialize_record + DISK -> GPU load: the file's
+        record (id from the file) with the caller's token ids."""
+        t = _i32(tokens)
+        cid = ChunkId()
+        check(lib.frag_store_load(self._h, str(path).encode(), _i32p(t), len(t), int(overwrite),
+                                  _stream_ptr(stream), C.byref(cid)))
+        return cid
+
     @staticmethod
     def _rec(v: RecordView) -> Record:
         cid = ChunkId()
@@ -323,3 +337,34 @@ class Result:
         if n.value:
             memcpy(s.ctypes.data, sc.value, n.value * 4)
         return {"q_final": q, "scores": s[:n.value]}
+
+
+def fkvc_write(path: str, chunk_id: ChunkId, k: np.ndarray, v: np.ndarray, native_start: int,
+               variant: int = ISOLATED):
+    """Host FKVC writer (no GPU): k, v fp32 [layers][tokens][heads][head_dim]."""
+    k = np.ascontiguousarray(k, np.float32)
+    v = np.ascontiguousarray(v, np.float32)
+    assert k.shape == v.shape and k.ndim == 4
+    h = FkvcHeader()
+    C.memmove(C.byref(h.id), C.byref(chunk_id), 16)
+    h.variant, h.native_start = variant, native_start
+    h.layers, h.tokens, h.heads, h.head_dim = k.shape
+    check(lib.frag_fkvc_write(str(path).encode(), C.byref(h), C.c_void_p(k.ctypes.data), C.c_void_p(v.ctypes.data)))
+
+
+def fkvc_read(path: str, header_only: bool = False):
+    """Host FKVC reader (no GPU) -> (header dict, k, v) with fp32 [layers][tokens][heads][head_dim]."""
+    h = FkvcHeader()
+    check(lib.frag_fkvc_read(str(path).encode(), C.byref(h), None, None, 0))
+    cid = ChunkId()
+    C.memmove(C.byref(cid), C.byref(h.id), 16)
+    hd = {"id": cid, "variant": h.variant, "native_start": h.native_start, "layers": h.layers, "heads": h.heads,
+          "head_dim": h.head_dim, "tokens": h.tokens}
+    if header_only:
+        return hd, None, None
+    shp = (h.layers, h.tokens, h.heads, h.head_dim)
+    k = np.empty(shp, np.float32)
+    v = np.empty(shp, np.float32)
+    check(lib.frag_fkvc_read(str(path).encode(), C.byref(h), C.c_void_p(k.ctypes.data), C.c_void_p(v.ctypes.data),
+                             k.size))
+    return hd, k, v

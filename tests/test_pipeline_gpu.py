@@ -147,3 +147,78 @@ def test_decode_contract_and_records_untouched(tiny):
     fresh = F.Result(eng, 64)
     with pytest.raises(F.ContractError):  # nothing to continue from
         eng.decode(fresh, 1)
+
+
+def test_fkvc_store_round_trip_and_reprocess(tiny, tmp_path):
+    """serialize_record -> deserialize_record through the GPU loader: bit-exact
+    record, and a reprocess over loaded records equals the original request."""
+    F, eng, store, ids, chunks = tiny["F"], tiny["eng"], tiny["store"], tiny["ids"], tiny["chunks"]
+    res = tiny["res"]
+    eng.reprocess(store, tiny["question"], ids, 0.15, res, system=tiny["system"])
+    want = res.logits().copy()
+    paths = []
+    for i, cid in enumerate(ids):
+        p = tmp_path / f"c{i}.fkvc"
+        store.save_record(cid, p)
+        paths.append(p)
+        h, k, v = F.fkvc_read(p)
+        kb, vb = store.read_kv(cid)
+        assert h["id"] == cid and h["native_start"] == 9 and h["tokens"] == 256
+        assert np.array_equal((k.view(np.uint32) >> 16).astype(np.uint16), kb)  # bf16 -> fp32 exact
+    st2 = F.ChunkKVStore(eng.cfg)
+    got = [st2.load_record(p, ch) for p, ch in zip(paths, chunks)]
+    assert got == list(ids)
+    for cid in ids:
+        a, b = store.read_kv(cid), st2.read_kv(cid)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    eng.reprocess(st2, tiny["question"], ids, 0.15, res, system=tiny["system"])
+    assert np.array_equal(res.logits(), want)
+    with pytest.raises(F.StoreError):  # single copy per chunk id (SPEC.md:269)
+        st2.load_record(paths[0], chunks[0])
+    st2.load_record(paths[0], chunks[0], overwrite=True)
+    with pytest.raises(F.ContractError):  # the file holds 256 tokens
+        st2.load_record(paths[0], chunks[0][:10], overwrite=True)
+
+
+def test_fkvc_loader_rejects_other_model(tiny, tmp_path):
+    F = tiny["F"]
+    p = tmp_path / "odd.fkvc"
+    k = np.zeros((3, 4, 4, 64), np.float32)  # 3 layers: tiny has 2
+    F.fkvc_write(p, F.hash_tokens([1]), k, k, native_start=1)
+    with pytest.raises(F.FormatError) as ei:
+        tiny["store"].load_record(p, [1, 2, 3, 4])
+    assert ei.value.kind == "Malformed"
+
+
+def test_fkvc_loader_thread_overlaps_requests(tiny, tmp_path):
+    """A loader thread fills a second store on its own stream while requests
+    keep running on the first: both sides' results are unaffected."""
+    import threading
+    import torch
+    F, eng, store, ids, chunks = tiny["F"], tiny["eng"], tiny["store"], tiny["ids"], tiny["chunks"]
+    paths = []
+    for i, cid in enumerate(ids):
+        p = tmp_path / f"t{i}.fkvc"
+        store.save_record(cid, p)
+        paths.append(p)
+    st2 = F.ChunkKVStore(eng.cfg)
+    side = torch.cuda.Stream()
+    err = []
+
+    def loader():
+        try:
+            for p, ch in zip(paths, chunks):
+                st2.load_record(p, ch, stream=side)
+        except Exception as e:  # pragma: no cover
+            err.append(e)
+
+    res = F.Result(eng, 8 + 8 * 256 + 32)
+    eng.reprocess(store, tiny["question"], ids, 0.15, res, system=tiny["system"])
+    want = res.logits().copy()
+    th = threading.Thread(target=loader)
+    th.start()
+    for _ in range(3):
+        eng.reprocess(store, tiny["question"], ids, 0.15, res, system=tiny["system"])
+        assert np.array_equal(res.logits(), want)
+    th.join()
+    assert not err and len(st2) == 8
