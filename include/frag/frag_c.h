@@ -183,6 +183,17 @@ FRAG_API frag_status frag_preprocess_isolated(frag_engine* eng, frag_store* st, 
  * A result owns the fused KV cache of one request (the per-request
  * exclusive pages of SPEC.md:148 are the rows recomputed in it) and its
  * logits; it can be reused across requests of at most max_tokens tokens. */
+/* preprocess_fused (Eq. 10): prefill C at
+ * positions |X|+1.. against cat(KV_S, the listed neighbours' ISOLATED records
+ * from `src` stitched consecutively after S), neighbours in the given order
+ * (descending similarity), truncated from the tail once their total exceeds
+ * `budget` tokens (0 = 2048). Puts a FUSED record (native_start |X|+1) into
+ * `dst` (may be `src`; overwrite replaces the ISOLATED record). Missing
+ * neighbour -> FRAG_E_STORE naming it. No neighbours -> the ISOLATED K/V. */
+FRAG_API frag_status frag_preprocess_fused(frag_engine* eng, frag_store* src, frag_store* dst, const int32_t* sys,
+                                          int32_t n_sys, const int32_t* tokens, int32_t n_tok,
+                                          const frag_chunk_id* neighbors, int32_t n_neighbors, int32_t budget,
+                                          int32_t overwrite, frag_chunk_id* id_out);
 FRAG_API frag_status frag_result_create(frag_engine* eng, int32_t max_tokens, frag_result** out);
 FRAG_API frag_status frag_result_free(frag_result* res);
 

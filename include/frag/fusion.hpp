@@ -3,6 +3,7 @@
 // Mirrors the reference's operation surface for the online stage:
 //   ChunkStore::put_record / fetch
 //   Engine::preprocess_isolated             SPEC.md:344-352 (Eq. 5)
+//   Engine::preprocess_fused                SPEC.md:353-361 (Eq. 10)
 //   Engine::reprocess                        stitch_full_reuse + select_query_guided +
 //                                            sparse_prefill_and_decode to the first token
 //
@@ -157,6 +158,21 @@ class Engine {
     frag_chunk_id id{};
     check(frag_preprocess_isolated(h_, st.handle(), system.data(), static_cast<int32_t>(system.size()), chunk.data(),
                                    static_cast<int32_t>(chunk.size()), overwrite ? 1 : 0, &id));
+    return from_c(id);
+  }
+
+  // preprocess_fused (Eq. 10): FUSED record of `chunk` prefilled
+  // against KV_S + the neighbours' ISOLATED records (descending similarity).
+  ChunkId preprocess_fused(ChunkStore& src, std::span<const Token> chunk, std::span<const ChunkId> neighbors,
+                           std::span<const Token> system = {}, ChunkStore* dst = nullptr, int budget = 2048,
+                           bool overwrite = false) {
+    std::vector<frag_chunk_id> nb;
+    nb.reserve(neighbors.size());
+    for (const auto& n : neighbors) nb.push_back(to_c(n));
+    frag_chunk_id id{};
+    check(frag_preprocess_fused(h_, src.handle(), (dst ? dst : &src)->handle(), system.data(),
+                                static_cast<int32_t>(system.size()), chunk.data(), static_cast<int32_t>(chunk.size()),
+                                nb.data(), static_cast<int32_t>(nb.size()), budget, overwrite ? 1 : 0, &id));
     return from_c(id);
   }
 

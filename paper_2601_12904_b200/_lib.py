@@ -88,6 +88,8 @@ _SIGS = {
     "frag_store_release": (C.c_int, [_P, C.POINTER(ChunkId)]),
     "frag_store_peek": (C.c_int, [_P, C.POINTER(ChunkId), C.POINTER(RecordView)]),
     "frag_store_count": (C.c_int64, [_P]),
+    "frag_preprocess_fused": (C.c_int, [_P, _P, _P, _I32P, C.c_int32, _I32P, C.c_int32, C.POINTER(ChunkId),
+                                        C.c_int32, C.c_int32, C.c_int32, C.POINTER(ChunkId)]),
     "frag_last_format_kind": (C.c_int32, []),
     "frag_fkvc_write": (C.c_int, [C.c_char_p, C.POINTER(FkvcHeader), _P, _P]),
     "frag_fkvc_read": (C.c_int, [C.c_char_p, C.POINTER(FkvcHeader), _P, _P, C.c_size_t]),

@@ -319,6 +319,18 @@ FRAG_API frag_status frag_preprocess_isolated(frag_engine* eng, frag_store* st, 
 }
 
 // ---------------------------------------------------------------- results
+FRAG_API frag_status frag_preprocess_fused(frag_engine* eng, frag_store* src, frag_store* dst, const int32_t* sys,
+                                          int32_t n_sys, const int32_t* tokens, int32_t n_tok,
+                                          const frag_chunk_id* neighbors, int32_t n_neighbors, int32_t budget,
+                                          int32_t overwrite, frag_chunk_id* id_out) {
+  return guard([&] {
+    need(eng && src && dst && tokens, "null argument");
+    need(n_sys == 0 || sys, "null system prompt");
+    preprocess_fused(eng->e, src->s, dst->s, sys, n_sys, tokens, n_tok, neighbors, n_neighbors, budget,
+                     overwrite != 0, id_out);
+  });
+}
+
 FRAG_API frag_status frag_result_create(frag_engine* eng, int32_t max_tokens, frag_result** out) {
   return guard([&] {
     need(eng && out, "null argument");

@@ -1016,4 +1016,77 @@ void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, co
   if (id_out) *id_out = id;
 }
 
+// preprocess_fused (Eq. 10): C_i prefilled
+// against cat(KV_S, its top-n neighbours' ISOLATED records stitched exactly as
+// the online Full Reuse path) at positions [|X|+1 : |X|+|C_i|], X = S + the
+// neighbours. Neighbours in the given order (descending similarity), truncated
+// from the tail to the fused-context budget; the record (variant FUSED,
+// native_start |X|+1) goes to dst. With no neighbours the K/V are exactly
+// preprocess_isolated's (same launches, bit-identical record data).
+void preprocess_fused(Engine* e, Store* src, Store* dst, const int32_t* sys, int n_sys, const int32_t* tokens,
+                      int n_tok, const frag_chunk_id* nb, int n_nb, int budget, bool overwrite, frag_chunk_id* id_out) {
+  const auto& c = e->cfg;
+  if (n_tok < 1) fail(FRAG_E_CONTRACT, "chunk must have at least one token (SPEC.md:197)");
+  if (n_nb < 0 || (n_nb > 0 && !nb)) fail(FRAG_E_CONTRACT, "bad neighbour list");
+  for (int i = 0; i < n_tok; ++i)
+    if (tokens[i] < 0 || tokens[i] >= c.vocab) fail(FRAG_E_CONTRACT, "token out of vocabulary");
+  if (src->device != e->device || dst->device != e->device)
+    fail(FRAG_E_CONTRACT, "stores and engine are on different devices");
+  if (budget <= 0) budget = 2048;  // SPEC.md design decision: default fused-context budget
+  frag_chunk_id id;
+  hash_tokens(tokens, n_tok, 0, &id);
+  {
+    std::shared_lock<std::shared_mutex> g(dst->mu);
+    if (!overwrite && dst->recs.count(key_of(id)))
+      fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
+  }
+  PinGuard pins{src, {}};
+  std::vector<Record*> recs;
+  int X = n_sys;
+  for (int i = 0; i < n_nb; ++i) {
+    Record* rec = nullptr;
+    try {
+      rec = store_fetch(src, nb[i]);
+    } catch (const Error&) {
+      static const char* hx = "0123456789abcdef";
+      std::string h;
+      for (int b = 0; b < 16; ++b) h += hx[nb[i].bytes[b] >> 4], h += hx[nb[i].bytes[b] & 15];
+      fail(FRAG_E_STORE, "missing neighbour record " + h + " (SPEC.md:357)");
+    }
+    pins.ids.push_back(nb[i]);
+    if (rec->variant != FRAG_VARIANT_ISOLATED)
+      fail(FRAG_E_CONTRACT, "Eq. 10 neighbours must be ISOLATED records (two-round fusion is out of scope)");
+    if (X - n_sys + rec->n_tok > budget) break;  // truncate from the tail of the list
+    recs.push_back(rec);
+    X += rec->n_tok;
+  }
+  DeviceGuard dg(e->device);
+  cudaStream_t s;
+  check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  struct SG {
+    cudaStream_t s;
+    ~SG() { cudaStreamDestroy(s); }
+  } sg{s};
+  const int T = X + n_tok;
+  e->ensure_rope(T);
+  SysKV* skv = get_sys_kv(e, sys, n_sys, s);
+  std::lock_guard<std::mutex> g(e->mu);  // scratch result is shared
+  Result* r = scratch_for(e, T);
+  r->staging.ensure(64 * 1024 + (size_t)(recs.size() + 2) * (64 + c.head_dim * 4) + (size_t)8 * T + 1024);
+  Stage stg(r->staging);
+  stitch(e, r, s, stg, skv, recs, n_sys);  // KV_S + neighbours at consecutive positions (Full Reuse)
+  int* rows_h = stg.take<int>(n_tok);
+  int* tok_h = stg.take<int>(n_tok);
+  for (int i = 0; i < n_tok; ++i) rows_h[i] = X + i, tok_h[i] = tokens[i];
+  check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "rows");
+  check_cuda(cudaMemcpyAsync(r->plan_tok.p, tok_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "tok");
+  run_rows(e, r, s, n_tok, T, PASS_KV_ONLY, nullptr, 0);
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  store_put(dst, id, tokens, n_tok, X + 1, FRAG_VARIANT_FUSED,
+            r->k_fused.as<bf16>() + (size_t)X * kvc, r->v_fused.as<bf16>() + (size_t)X * kvc, overwrite,
+            (size_t)r->max_tokens * kvc, s);
+  check_cuda(cudaStreamSynchronize(s), "preprocess_fused");
+  if (id_out) *id_out = id;
+}
+
 }  // namespace fragimpl

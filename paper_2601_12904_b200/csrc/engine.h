@@ -237,6 +237,8 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
 void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host);
 void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                          bool overwrite, frag_chunk_id* id_out);
+void preprocess_fused(Engine* e, Store* src, Store* dst, const int32_t* sys, int n_sys, const int32_t* tokens,
+                      int n_tok, const frag_chunk_id* nb, int n_nb, int budget, bool overwrite, frag_chunk_id* id_out);
 
 // Store operations (store.cpp)
 Store* store_create(const frag_model_cfg& cfg, int device, size_t cap);

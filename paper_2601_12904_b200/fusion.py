@@ -116,6 +116,18 @@ class Engine:
                                            C.byref(out)))
         return out
 
+    def preprocess_fused(self, store: "ChunkKVStore", chunk: Sequence[int], neighbors: Sequence[ChunkId],
+                         system: Sequence[int] = (), *, dst: "ChunkKVStore | None" = None, budget: int = 2048,
+                         overwrite: bool = False) -> ChunkId:
+        """Eq. 10: prefill `chunk` against KV_S + its neighbours'
+        ISOLATED records (descending similarity order) -> FUSED record in dst."""
+        t, s = _i32(chunk), _i32(system)
+        nb = (ChunkId * max(len(neighbors), 1))(*neighbors)
+        cid = ChunkId()
+        check(lib.frag_preprocess_fused(self._h, store._h, (dst if dst is not None else store)._h, _i32p(s), len(s), _i32p(t), len(t),
+                                        nb, len(neighbors), int(budget), int(overwrite), C.byref(cid)))
+        return cid
+
     def reprocess(self, store: "ChunkKVStore", question: Sequence[int], chunk_ids: Sequence[ChunkId],
                   ratio: float, result: "Result", system: Sequence[int] = (), *, raw_scores: bool = False,
                   all_logits: bool = False, timing: bool = False, inject_crit: Sequence[int] | None = None,

@@ -209,3 +209,50 @@ def test_decode_parity_teacher_forced(tiny):
     gk = O.bf16_bits_to_f32(kd[:, T:T + n - 1])
     rk = O.bf16_bits_to_f32(O.f32_to_bf16_bits(out["k_cache"][:, T:T + n - 1]))
     assert _rel_l2(gk, rk) <= 2e-2 and _cos(gk, rk) >= 0.999
+
+
+def test_preprocess_fused(cuda):
+    """Eq. 10: FUSED records. top_n = 0 -> the ISOLATED
+    record exactly; C2 fused against its real predecessor C1 reproduces the
+    Full-Attention KV of C2 in cat(S, C1, C2) (strictly closer than the
+    ISOLATED record, the §3.1 deviation claim) and matches the oracle's
+    prefill over the stitched context; budget truncation; missing neighbour."""
+    t = _setup("tiny", 3, 256, 8, 32)
+    F, O, eng, store, S = t["F"], t["O"], t["eng"], t["store"], t["S"]
+    c1, c2, c3 = t["chunks"]
+    i1, i2, i3 = t["ids"]
+    out = F.ChunkKVStore(eng.cfg)
+    f0 = eng.preprocess_fused(store, c2, [], system=t["system"], dst=out)
+    r0 = out.peek(f0)
+    assert f0 == i2 and r0.variant == F.FUSED and r0.native_start == S + 1
+    a, b = out.read_kv(f0), store.read_kv(i2)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # C2 fused against C1 (then C3, truncated by the 256-token budget)
+    f2 = eng.preprocess_fused(store, c2, [i1, i3], system=t["system"], dst=out, budget=256, overwrite=True)
+    r2 = out.peek(f2)
+    assert r2.variant == F.FUSED and r2.native_start == S + 256 + 1
+    kf, vf = out.read_kv(f2)
+    # Full Attention of cat(S, C1, C2): rows of C2
+    fa = F.Result(eng, S + 512)
+    eng.full_prefill(c1 + c2, fa, system=t["system"])
+    kfa, vfa = fa.fused_kv()
+    k_fa = O.bf16_bits_to_f32(kfa[:, S + 256:S + 512])
+    k_fu = O.bf16_bits_to_f32(kf)
+    rec2 = t["recs"][1]  # the ISOLATED record of C2 re-positioned to S+257.. (Full Reuse)
+    k_iso = O.stitch(eng.cfg, [(rec2["k"], rec2["v"], rec2["native_start"], S + 256)], S + 512)[0][:, S + 256:]
+    dev_fu = float(np.sum((k_fu[1] - k_fa[1]) ** 2))
+    dev_iso = float(np.sum((k_iso[1] - k_fa[1]) ** 2))
+    assert _rel_l2(k_fu, k_fa) <= 1e-2 and dev_fu < 0.1 * dev_iso, (dev_fu, dev_iso)
+    # oracle: prefill C2 at positions S+257.. over the stitched (S + C1) cache
+    sys_kv = (O.bf16_bits_to_f32(kfa[:, :S]), O.bf16_bits_to_f32(vfa[:, :S]))
+    rec1 = t["recs"][0]
+    ck, cv = O.stitch(eng.cfg, [(sys_kv[0], sys_kv[1], 1, 0), (rec1["k"], rec1["v"], rec1["native_start"], S)],
+                      S + 512)
+    pos = np.zeros(S + 512, np.int32)
+    pos[:S + 256] = np.arange(1, S + 257)
+    t["om"].forward(c2, list(range(S + 257, S + 513)), list(range(S + 256, S + 512)), ck, cv, pos,
+                    emulate_bf16=True)
+    ko = O.bf16_bits_to_f32(O.f32_to_bf16_bits(ck[:, S + 256:S + 512]))
+    assert _rel_l2(k_fu, ko) <= 2e-2 and _cos(k_fu, ko) >= 0.999
+    with pytest.raises(F.StoreError, match="missing neighbour"):
+        eng.preprocess_fused(store, c3, [F.hash_tokens([1, 2, 3])], dst=out)
