@@ -46,8 +46,9 @@ CONFIGS = {
     # 256-chunk corpus, split round-robin over the ranks (steps = queries/rank)
     "mistral-7b-batch": dict(preset="mistral-7b", chunks=32, chunk_len=1024, qlen=32, ratio=0.15, corpus=256,
                              queries=64),
-    # the full 80-layer model fits one B200 (141 GB bf16 weights)
-    "llama3-70b": dict(preset="llama3-70b", chunks=8, chunk_len=2048, qlen=32, ratio=0.15),
+    # the full 80-layer model fits one B200 (141 GB bf16
+    # weights); the chunk-KV store is partitioned over the ranks (NVLink peer reads)
+    "llama3-70b": dict(preset="llama3-70b", chunks=8, chunk_len=2048, qlen=32, ratio=0.15, partition=True),
     "tiny": dict(preset="tiny", chunks=8, chunk_len=256, qlen=32, ratio=0.15),
 }
 
@@ -79,6 +80,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-layers", type=int, default=1)
     p.add_argument("--sweep", default="", help="comma list of extra ratios to time (e.g. 0,0.05,0.3)")
+    p.add_argument("--partition", action="store_true",
+                   help="chunk-partitioned store: each chunk's record lives on rank hash(id) mod N only and "
+                        "the other ranks read it over NVLink inside K1 (SURVEY.md §8(e))")
     p.add_argument("--with-load", action="store_true",
                    help="also time TTFT including the FKVC record load (DISK -> GPU, SPEC.md:301-308)")
     return p.parse_args()
@@ -210,13 +214,39 @@ def run_ours(args, rank, world, local_rank):
         # queries rank, rank + world, ... each over 32 Rng-picked chunks
         crng = np.random.default_rng(args.seed)
         pool = [crng.integers(0, c.vocab, w["chunk_len"]).astype(np.int32) for _ in range(w["corpus"])]
-        pool_ids = [eng.preprocess_isolated(store, ch) for ch in pool]
+        if args.partition or w.get("partition"):
+            from paper_2601_12904_b200 import partition as P
+            pool_ids = [F.hash_tokens(ch) for ch in pool]
+            owned = {}
+            for cid, ch, o in zip(pool_ids, pool, P.owners(pool_ids, world)):
+                if o == rank:
+                    eng.preprocess_isolated(store, ch)
+                    owned[cid] = ch
+            if world > 1:
+                P.share_records(store, owned)
+        else:
+            pool_ids = [eng.preprocess_isolated(store, ch) for ch in pool]
         mine = [q for q in range(w["queries"]) if q % world == rank]
         picks = [np.random.default_rng(args.seed * 1000 + q).choice(w["corpus"], w["chunks"], replace=False)
                  for q in mine]
         id_sets = [[pool_ids[j] for j in pk] for pk in picks]
         chunks = [pool[j] for j in picks[0]]
         args.steps = len(mine)
+    elif args.partition or w.get("partition"):
+        # one shared set of chunks; rank hash(id) mod N owns each record, the
+        # others import a CUDA-IPC view of it (K1 reads it over NVLink)
+        from paper_2601_12904_b200 import partition as P
+        crng = np.random.default_rng(args.seed)
+        chunks = [crng.integers(0, c.vocab, w["chunk_len"]).astype(np.int32) for _ in range(w["chunks"])]
+        cids = [F.hash_tokens(ch) for ch in chunks]
+        owned = {}
+        for cid, ch, o in zip(cids, chunks, P.owners(cids, world)):
+            if o == rank:
+                eng.preprocess_isolated(store, ch)
+                owned[cid] = ch
+        if world > 1:
+            P.share_records(store, owned)
+        id_sets = [cids]
     else:
         chunks = [rng.integers(0, c.vocab, w["chunk_len"]).astype(np.int32) for _ in range(w["chunks"])]
         id_sets = [[eng.preprocess_isolated(store, ch) for ch in chunks]]
@@ -353,6 +383,8 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         sweep[str(r)] = round(s0.elapsed_time(s1) / 2, 3)
 
+    if world > 1:
+        torch.distributed.barrier()  # peers may still read this rank's records until every rank is done
     return dict(ms=ms, e2e_ms=e2e_ms, full_ms=full_ms, launches=launches, prof=prof, stages=stages, T=T,
                 crit=crit, clocks=clk.summary(), cfg=c, w=w, ratio=ratio, h2d=h2d, d2h=d2h, sweep=sweep,
                 k=len(crit), decode_ms=decode_ms, n_dec=len(answer), load_leg=load_leg)
@@ -370,6 +402,9 @@ def main():
                 "chunk_len": w["chunk_len"], "question_len": w["qlen"], "recompute_ratio": ratio,
                 "seq_len": w["chunks"] * w["chunk_len"] + w["qlen"], "parallelism": f"dp{args.gpus} (independent queries)",
                 "l2": l2_note(w)}
+    part = args.partition or w.get("partition", False)
+    cfg_json["store"] = ("partitioned: record on rank hash(chunk_id) mod N only, read by the other ranks over "
+                         "NVLink inside K1 (CUDA IPC views)") if part else "replicated per rank"
     if w.get("corpus"):
         cfg_json.update({"corpus_chunks": w["corpus"], "queries": w["queries"],
                          "steps_note": "steps = this rank's share of the queries (round-robin)"})

@@ -65,7 +65,9 @@ typedef struct frag_store frag_store;
 typedef struct frag_result frag_result;
 
 enum { FRAG_VARIANT_ISOLATED = 0, FRAG_VARIANT_FUSED = 1 }; /* ChunkKVRecord.variant */
-enum { FRAG_TIER_GPU = 0, FRAG_TIER_CPU = 1, FRAG_TIER_DISK = 2 };
+/* FRAG_TIER_PEER: the record's pages live in another GPU's store (chunk-
+ * partitioned store) and are read over NVLink 5 / NVSwitch. */
+enum { FRAG_TIER_GPU = 0, FRAG_TIER_CPU = 1, FRAG_TIER_DISK = 2, FRAG_TIER_PEER = 3 };
 
 /* Read-only view of a ChunkKVRecord. */
 typedef struct {
@@ -73,7 +75,7 @@ typedef struct {
   int32_t n_tok;
   int32_t native_start; /* 1-based position of the record's first token */
   int32_t variant;
-  int32_t tier;         /* always FRAG_TIER_GPU in this build (HBM-resident store) */
+  int32_t tier;         /* FRAG_TIER_GPU (this store's HBM) or FRAG_TIER_PEER (another GPU's HBM) */
   uint64_t heat;        /* access count */
   uint64_t last_access; /* store tick of the last fetch */
   uint64_t size_bytes;
@@ -169,6 +171,41 @@ FRAG_API frag_status frag_store_save(frag_store* st, const frag_chunk_id* id, co
  * threads run frag_reprocess on other streams. */
 FRAG_API frag_status frag_store_load(frag_store* st, const char* path, const int32_t* tokens, int32_t n_tok,
                                      int32_t overwrite, void* stream, frag_chunk_id* id_out);
+/* Chunk-partitioned store across the GPUs of one box (the
+ * spec's single-copy invariant, held across GPUs): each chunk's
+ * record lives in exactly one GPU's store (owner = frag_chunk_owner) and the
+ * other GPUs read its pages in place over NVLink — K1 (rope_shift_assemble)
+ * streams them straight into the local fused cache, so fetch and
+ * re-positioning are one pass and no collective runs on the data path.
+ *
+ * Same process, several devices: after frag_store_attach_peer(local, remote),
+ * a fetch that misses `local` is served from `remote` (heat/pins are kept by
+ * the owning store; peer access is enabled between the two devices). Records
+ * of `remote` are not re-exported through `local` (no transitive lookup).
+ * `remote` must outlive `local`.
+ *
+ * One process per GPU: the owner exports a record (its CUDA IPC memory handle
+ * plus metadata in a plain 128-byte struct that any transport can carry, e.g.
+ * torch.distributed all_gather_object); every other process imports it as a
+ * FRAG_TIER_PEER view. An exported record cannot be overwritten (FRAG_E_STORE);
+ * the owning store must outlive its importers (barrier before destroy).
+ * Importing a record exported by the same process is a contract error (use
+ * attach_peer); importing an id the store already holds needs overwrite. */
+typedef struct {
+  frag_chunk_id id;
+  int32_t n_tok, native_start, variant, owner_device;
+  int32_t layers, n_kv_heads, head_dim, reserved;
+  uint64_t kv_bytes;         /* K|V allocation size, 2*L*n_tok*Hkv*dh*2 */
+  uint64_t owner_pid;        /* exporting process */
+  uint8_t ipc_handle[64];    /* cudaIpcMemHandle_t of the K|V allocation */
+} frag_peer_record;
+/* owner rank of a chunk in a world of n_owners GPUs: little-endian u64 of the
+ * first 8 id bytes mod n_owners (ids are content hashes, so this is uniform). */
+FRAG_API int32_t frag_chunk_owner(const frag_chunk_id* id, int32_t n_owners);
+FRAG_API frag_status frag_store_attach_peer(frag_store* local, frag_store* remote);
+FRAG_API frag_status frag_store_export(frag_store* st, const frag_chunk_id* id, frag_peer_record* out);
+FRAG_API frag_status frag_store_import(frag_store* st, const frag_peer_record* rec, const int32_t* tokens,
+                                       int32_t n_tok, int32_t overwrite);
 FRAG_API int64_t frag_store_count(const frag_store* st);
 FRAG_API uint64_t frag_store_bytes_used(const frag_store* st);
 

@@ -48,6 +48,17 @@ class RecordView(C.Structure):
                 ("tokens_dev", C.c_void_p)]
 
 
+class PeerRecord(C.Structure):
+    """frag_peer_record: one exported record (CUDA IPC handle + metadata), 128 bytes."""
+    _fields_ = [("id", ChunkId), ("n_tok", C.c_int32), ("native_start", C.c_int32), ("variant", C.c_int32),
+                ("owner_device", C.c_int32), ("layers", C.c_int32), ("n_kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("reserved", C.c_int32), ("kv_bytes", C.c_uint64),
+                ("owner_pid", C.c_uint64), ("ipc_handle", C.c_uint8 * 64)]
+
+
+assert C.sizeof(PeerRecord) == 128
+
+
 class ReprocessOpts(C.Structure):
     _fields_ = [("raw_scores", C.c_int32), ("all_logits", C.c_int32), ("timing", C.c_int32),
                 ("inject_crit", C.POINTER(C.c_int32)), ("n_inject", C.c_int32),
@@ -88,6 +99,10 @@ _SIGS = {
     "frag_store_release": (C.c_int, [_P, C.POINTER(ChunkId)]),
     "frag_store_peek": (C.c_int, [_P, C.POINTER(ChunkId), C.POINTER(RecordView)]),
     "frag_store_count": (C.c_int64, [_P]),
+    "frag_chunk_owner": (C.c_int32, [C.POINTER(ChunkId), C.c_int32]),
+    "frag_store_attach_peer": (C.c_int, [_P, _P]),
+    "frag_store_export": (C.c_int, [_P, C.POINTER(ChunkId), C.POINTER(PeerRecord)]),
+    "frag_store_import": (C.c_int, [_P, C.POINTER(PeerRecord), _I32P, C.c_int32, C.c_int32]),
     "frag_preprocess_fused": (C.c_int, [_P, _P, _P, _I32P, C.c_int32, _I32P, C.c_int32, C.POINTER(ChunkId),
                                         C.c_int32, C.c_int32, C.c_int32, C.POINTER(ChunkId)]),
     "frag_last_format_kind": (C.c_int32, []),

@@ -246,7 +246,7 @@ static void fill_view(const Record* r, frag_record_view* out) {
   out->n_tok = r->n_tok;
   out->native_start = r->native_start;
   out->variant = r->variant;
-  out->tier = FRAG_TIER_GPU;
+  out->tier = r->tier;
   out->heat = r->heat;
   out->last_access = r->last_access;
   out->size_bytes = r->bytes;
@@ -274,10 +274,20 @@ FRAG_API frag_status frag_store_release(frag_store* st, const frag_chunk_id* id)
 FRAG_API frag_status frag_store_peek(const frag_store* st, const frag_chunk_id* id, frag_record_view* out) {
   return guard([&] {
     need(st && id && out, "null argument");
-    std::shared_lock<std::shared_mutex> g(st->s->mu);
-    auto it = st->s->recs.find(key_of(*id));
-    if (it == st->s->recs.end()) fail(FRAG_E_STORE, "missing chunk record");
-    fill_view(it->second.get(), out);
+    std::vector<Store*> stores{st->s};
+    {
+      std::shared_lock<std::shared_mutex> g(st->s->mu);
+      stores.insert(stores.end(), st->s->peers.begin(), st->s->peers.end());
+    }
+    for (Store* s : stores) {  // local index first, then attached peers (as fetch)
+      std::shared_lock<std::shared_mutex> g(s->mu);
+      auto it = s->recs.find(key_of(*id));
+      if (it != s->recs.end()) {
+        fill_view(it->second.get(), out);
+        return;
+      }
+    }
+    fail(FRAG_E_STORE, "missing chunk record");
   });
 }
 
@@ -293,6 +303,33 @@ FRAG_API frag_status frag_store_load(frag_store* st, const char* path, const int
   return guard([&] {
     need(st && path && tokens, "null argument");
     store_load(st->s, path, tokens, n_tok, overwrite != 0, static_cast<cudaStream_t>(stream), id_out);
+  });
+}
+
+FRAG_API int32_t frag_chunk_owner(const frag_chunk_id* id, int32_t n_owners) {
+  if (!id || n_owners < 1) return -1;
+  return chunk_owner(*id, n_owners);
+}
+
+FRAG_API frag_status frag_store_attach_peer(frag_store* local, frag_store* remote) {
+  return guard([&] {
+    need(local && remote, "null argument");
+    store_attach_peer(local->s, remote->s);
+  });
+}
+
+FRAG_API frag_status frag_store_export(frag_store* st, const frag_chunk_id* id, frag_peer_record* out) {
+  return guard([&] {
+    need(st && id && out, "null argument");
+    store_export(st->s, *id, out);
+  });
+}
+
+FRAG_API frag_status frag_store_import(frag_store* st, const frag_peer_record* rec, const int32_t* tokens,
+                                       int32_t n_tok, int32_t overwrite) {
+  return guard([&] {
+    need(st && rec, "null argument");
+    store_import(st->s, *rec, tokens, n_tok, overwrite != 0);
   });
 }
 

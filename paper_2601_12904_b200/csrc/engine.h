@@ -121,8 +121,19 @@ struct Record {
   DevBuf kv;            // K then V, each [L][n][Hkv][dh] bf16
   DevBuf tok;           // int32 [n]
   std::vector<int32_t> tok_host;
+  // chunk-partitioned store: an imported record is a view of
+  // another process's record pages mapped through CUDA IPC (read over NVLink
+  // by K1); the mapping is closed, never freed, when the view is dropped
+  int tier = FRAG_TIER_GPU;
+  int owner_device = -1;
+  bool ipc_mapped = false;
+  bool exported = false;  // IPC handle handed out: never replaced while peers may map it
   bf16* k() const { return kv.as<bf16>(); }
   bf16* v() const { return kv.as<bf16>() + kv.bytes / 4; }
+  Record() = default;
+  Record(const Record&) = delete;
+  Record& operator=(const Record&) = delete;
+  ~Record();
 };
 
 struct Store {
@@ -132,6 +143,9 @@ struct Store {
   uint64_t tick = 0;
   mutable std::shared_mutex mu;
   std::unordered_map<ChunkKey, std::unique_ptr<Record>, ChunkKeyHash> recs;
+  // same-process stores on other GPUs whose records this store serves on a
+  // local miss (frag_store_attach_peer); their pages are read over NVLink
+  std::vector<Store*> peers;
   size_t record_bytes(int n_tok) const {
     return (size_t)2 * cfg.layers * n_tok * cfg.n_kv_heads * cfg.head_dim * sizeof(bf16);
   }
@@ -254,6 +268,12 @@ void store_load(Store* st, const char* path, const int32_t* tokens, int n_tok, b
 void fkvc_write(const char* path, const frag_fkvc_header& h, const float* k, const float* v);
 void fkvc_read(const char* path, frag_fkvc_header* h, float* k, float* v, size_t cap_floats);
 void store_release(Store* st, const frag_chunk_id& id);
+// chunk-partitioned store across GPUs: same-process peers and
+// cross-process CUDA-IPC export/import of record pages
+int32_t chunk_owner(const frag_chunk_id& id, int32_t n);
+void store_attach_peer(Store* local, Store* remote);
+void store_export(Store* st, const frag_chunk_id& id, frag_peer_record* out);
+void store_import(Store* st, const frag_peer_record& pr, const int32_t* tokens, int n_tok, bool overwrite);
 
 void hash_tokens(const int32_t* t, int n, uint64_t salt, frag_chunk_id* out);
 uint64_t weight_seed(uint64_t seed, int tensor_id);

@@ -4,6 +4,8 @@
 // host keeps the index, heat metadata and a copy of each record's token ids.
 // FKVC record files + the DISK -> GPU loader are
 // at the end; tier eviction policy is out of scope (SURVEY.md §2 kv_store row).
+#include <unistd.h>
+
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -69,11 +71,13 @@ void store_insert(Store* st, std::unique_ptr<Record> rec, bool overwrite) {
   if (it != st->recs.end()) {
     if (!overwrite) fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
     if (it->second->pins > 0) fail(FRAG_E_STORE, "cannot overwrite a pinned record (SPEC.md:320)");
-    freed = it->second->bytes;
+    if (it->second->exported) fail(FRAG_E_STORE, "cannot overwrite a record exported to peer GPUs");
+    freed = it->second->tier == FRAG_TIER_PEER ? 0 : it->second->bytes;
   }
-  if (st->capacity && st->used - freed + rec->bytes > st->capacity)
+  // peer views occupy no local HBM
+  const size_t bytes = rec->tier == FRAG_TIER_PEER ? 0 : rec->bytes;
+  if (st->capacity && st->used - freed + bytes > st->capacity)
     fail(FRAG_E_STORE, "GPU tier capacity exhausted (tiering/eviction out of scope in this build)");
-  const size_t bytes = rec->bytes;
   if (it != st->recs.end()) {
     st->used -= freed;
     it->second = std::move(rec);
@@ -121,22 +125,160 @@ void store_put(Store* st, const frag_chunk_id& id, const int32_t* tokens, int n_
   store_insert(st, std::move(rec), overwrite);
 }
 
-Record* store_fetch(Store* st, const frag_chunk_id& id) {
+namespace {
+// fetch from this store's own index only (heat++, pin); null on a miss
+Record* fetch_local(Store* st, const ChunkKey& key) {
   std::unique_lock<std::shared_mutex> g(st->mu);  // heat/pin are mutated
-  auto it = st->recs.find(key_of(id));
-  if (it == st->recs.end()) fail(FRAG_E_STORE, "missing chunk record (SPEC.md:287)");
+  auto it = st->recs.find(key);
+  if (it == st->recs.end()) return nullptr;
   Record* r = it->second.get();
   r->heat += 1;
   r->last_access = ++st->tick;
   r->pins += 1;
   return r;
 }
+bool release_local(Store* st, const ChunkKey& key) {
+  std::unique_lock<std::shared_mutex> g(st->mu);
+  auto it = st->recs.find(key);
+  if (it == st->recs.end()) return false;
+  if (it->second->pins > 0) it->second->pins -= 1;
+  return true;
+}
+}  // namespace
+
+// A miss in this store falls through to the attached same-process peers (the
+// owning store keeps heat and pins); cross-process records were imported into
+// the local index as FRAG_TIER_PEER views and hit locally.
+Record* store_fetch(Store* st, const frag_chunk_id& id) {
+  const ChunkKey key = key_of(id);
+  if (Record* r = fetch_local(st, key)) return r;
+  std::vector<Store*> peers;
+  {
+    std::shared_lock<std::shared_mutex> g(st->mu);
+    peers = st->peers;
+  }
+  for (Store* p : peers)
+    if (Record* r = fetch_local(p, key)) return r;
+  fail(FRAG_E_STORE, "missing chunk record (SPEC.md:287)");
+}
 
 void store_release(Store* st, const frag_chunk_id& id) {
+  const ChunkKey key = key_of(id);
+  if (release_local(st, key)) return;
+  std::vector<Store*> peers;
+  {
+    std::shared_lock<std::shared_mutex> g(st->mu);
+    peers = st->peers;
+  }
+  for (Store* p : peers)
+    if (release_local(p, key)) return;
+  fail(FRAG_E_STORE, "missing chunk record");
+}
+
+Record::~Record() {
+  if (ipc_mapped && kv.p) {
+    cudaIpcCloseMemHandle(kv.p);  // a mapping of the owner's pages: never cudaFree'd here
+    kv.p = nullptr;
+    kv.bytes = 0;
+  }
+}
+
+// ---------------------------------------------------------------- partitioned store
+int32_t chunk_owner(const frag_chunk_id& id, int32_t n) {
+  if (n < 1) fail(FRAG_E_CONTRACT, "n_owners must be >= 1");
+  uint64_t a = 0;
+  for (int i = 7; i >= 0; --i) a = (a << 8) | id.bytes[i];
+  return (int32_t)(a % (uint64_t)n);
+}
+
+void store_attach_peer(Store* local, Store* remote) {
+  if (!local || !remote) fail(FRAG_E_CONTRACT, "null store");
+  if (local == remote) fail(FRAG_E_CONTRACT, "a store cannot be its own peer");
+  const auto &a = local->cfg, &b = remote->cfg;
+  if (a.layers != b.layers || a.n_kv_heads != b.n_kv_heads || a.head_dim != b.head_dim || a.vocab != b.vocab)
+    fail(FRAG_E_CONTRACT, "peer store has a different record layout");
+  if (local->device != remote->device) {
+    DeviceGuard dg(local->device);
+    int ok = 0;
+    check_cuda(cudaDeviceCanAccessPeer(&ok, local->device, remote->device), "cudaDeviceCanAccessPeer");
+    if (!ok) fail(FRAG_E_CUDA, "no peer access between device " + std::to_string(local->device) + " and " +
+                                   std::to_string(remote->device));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(remote->device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled)
+      cudaGetLastError();
+    else
+      check_cuda(e, "cudaDeviceEnablePeerAccess");
+  }
+  std::unique_lock<std::shared_mutex> g(local->mu);
+  for (Store* p : local->peers)
+    if (p == remote) return;
+  local->peers.push_back(remote);
+}
+
+void store_export(Store* st, const frag_chunk_id& id, frag_peer_record* out) {
+  if (!out) fail(FRAG_E_CONTRACT, "null output");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   std::unique_lock<std::shared_mutex> g(st->mu);
   auto it = st->recs.find(key_of(id));
-  if (it == st->recs.end()) fail(FRAG_E_STORE, "missing chunk record");
-  if (it->second->pins > 0) it->second->pins -= 1;
+  if (it == st->recs.end()) fail(FRAG_E_STORE, "missing chunk record (SPEC.md:287)");
+  Record* r = it->second.get();
+  if (r->tier == FRAG_TIER_PEER) fail(FRAG_E_CONTRACT, "only the owning store can export a record");
+  DeviceGuard dg(st->device);
+  cudaIpcMemHandle_t h;
+  check_cuda(cudaIpcGetMemHandle(&h, r->kv.p), "cudaIpcGetMemHandle");
+  std::memset(out, 0, sizeof(*out));
+  out->id = r->id;
+  out->n_tok = r->n_tok;
+  out->native_start = r->native_start;
+  out->variant = r->variant;
+  out->owner_device = st->device;
+  out->layers = st->cfg.layers;
+  out->n_kv_heads = st->cfg.n_kv_heads;
+  out->head_dim = st->cfg.head_dim;
+  out->kv_bytes = r->kv.bytes;
+  out->owner_pid = (uint64_t)getpid();
+  std::memcpy(out->ipc_handle, &h, sizeof(h));
+  r->exported = true;
+}
+
+void store_import(Store* st, const frag_peer_record& pr, const int32_t* tokens, int n_tok, bool overwrite) {
+  const auto& c = st->cfg;
+  if (pr.layers != c.layers || pr.n_kv_heads != c.n_kv_heads || pr.head_dim != c.head_dim)
+    fail(FRAG_E_CONTRACT, "peer record has a different record layout");
+  if (pr.n_tok < 1 || pr.n_tok != n_tok) fail(FRAG_E_CONTRACT, "token count does not match the peer record");
+  if (pr.kv_bytes != st->record_bytes(n_tok)) fail(FRAG_E_CONTRACT, "peer record size does not match its shape");
+  if (pr.native_start < 1) fail(FRAG_E_CONTRACT, "native_start must be >= 1 (SPEC.md:257)");
+  if (pr.variant != FRAG_VARIANT_ISOLATED && pr.variant != FRAG_VARIANT_FUSED) fail(FRAG_E_CONTRACT, "unknown variant");
+  if (pr.owner_pid == (uint64_t)getpid())
+    fail(FRAG_E_CONTRACT, "record was exported by this process: use frag_store_attach_peer");
+  if (!tokens) fail(FRAG_E_CONTRACT, "null tokens");
+  for (int i = 0; i < n_tok; ++i)
+    if (tokens[i] < 0 || tokens[i] >= c.vocab) fail(FRAG_E_CONTRACT, "record token out of vocabulary");
+  {
+    std::shared_lock<std::shared_mutex> g(st->mu);
+    if (!overwrite && st->recs.count(key_of(pr.id)))
+      fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
+  }
+  DeviceGuard dg(st->device);
+  auto rec = std::make_unique<Record>();
+  rec->id = pr.id;
+  rec->n_tok = n_tok;
+  rec->native_start = pr.native_start;
+  rec->variant = pr.variant;
+  rec->bytes = pr.kv_bytes;
+  rec->tier = FRAG_TIER_PEER;
+  rec->owner_device = pr.owner_device;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, pr.ipc_handle, sizeof(h));
+  void* p = nullptr;
+  check_cuda(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  rec->kv.p = p;
+  rec->kv.bytes = pr.kv_bytes;
+  rec->ipc_mapped = true;
+  rec->tok.alloc(n_tok * sizeof(int32_t));  // token ids are local (K2 gathers their embeddings)
+  rec->tok_host.assign(tokens, tokens + n_tok);
+  check_cuda(cudaMemcpy(rec->tok.p, tokens, n_tok * sizeof(int32_t), cudaMemcpyHostToDevice), "peer record tokens");
+  store_insert(st, std::move(rec), overwrite);
 }
 
 // ---------------------------------------------------------------- FKVC files

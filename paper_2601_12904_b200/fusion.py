@@ -17,13 +17,15 @@ from typing import Iterable, Sequence
 import numpy as np
 
 from ._lib import (ChunkId, FkvcHeader, ContractError, CudaError, FormatError, FragError, ModelCfg, OutOfMemory,
-                   RecordView, ReprocessOpts, StoreError, Timing, check, lib)
+                   PeerRecord, RecordView, ReprocessOpts, StoreError, Timing, check, lib)
 
 __all__ = ["ModelCfg", "ChunkId", "Engine", "ChunkKVStore", "Result", "preset", "hash_tokens",
            "ContractError", "StoreError", "FormatError", "CudaError", "OutOfMemory", "FragError",
-           "ISOLATED", "FUSED", "launch_count", "memcpy", "fkvc_write", "fkvc_read"]
+           "ISOLATED", "FUSED", "launch_count", "memcpy", "fkvc_write", "fkvc_read", "chunk_owner",
+           "PeerRecord", "TIER_GPU", "TIER_PEER"]
 
 ISOLATED, FUSED = 0, 1
+TIER_GPU, TIER_CPU, TIER_DISK, TIER_PEER = 0, 1, 2, 3
 WEIGHT_IDS = {"emb": 0, "lm_head": 1, "wq": 2, "wk": 3, "wv": 4, "wo": 5, "w_gate": 6, "w_up": 7,
               "w_down": 8, "attn_norm": 9, "ffn_norm": 10, "final_norm": 11}
 
@@ -47,6 +49,14 @@ def hash_tokens(tokens: Sequence[int], salt: int = 0) -> ChunkId:
     out = ChunkId()
     lib.frag_hash_tokens(_i32p(t), len(t), salt, C.byref(out))
     return out
+
+
+def chunk_owner(chunk_id: ChunkId, n_owners: int) -> int:
+    """Owning rank of a chunk in the chunk-partitioned store (frag_chunk_owner)."""
+    r = int(lib.frag_chunk_owner(C.byref(chunk_id), int(n_owners)))
+    if r < 0:
+        raise ContractError("n_owners must be >= 1")
+    return r
 
 
 def launch_count() -> int:
@@ -258,6 +268,30 @@ class ChunkKVStore:
         cid = ChunkId()
         check(lib.frag_store_load(self._h, str(path).encode(), _i32p(t), len(t), int(overwrite),
                                   _stream_ptr(stream), C.byref(cid)))
+        return cid
+
+    # ------------------------------------------------ chunk-partitioned store
+    def attach_peer(self, other: "ChunkKVStore"):
+        """Serve misses from `other` (a store on another GPU of this process);
+        its pages are read in place over NVLink. `other` must outlive self."""
+        check(lib.frag_store_attach_peer(self._h, other._h))
+        self._peers = getattr(self, "_peers", []) + [other]  # keep the owner alive
+
+    def export_record(self, chunk_id: ChunkId) -> bytes:
+        """CUDA-IPC export of an owned record: 128 bytes for any transport."""
+        pr = PeerRecord()
+        check(lib.frag_store_export(self._h, C.byref(chunk_id), C.byref(pr)))
+        return bytes(pr)
+
+    def import_record(self, blob: bytes, tokens: Sequence[int], *, overwrite: bool = False) -> ChunkId:
+        """Register another process's exported record as a FRAG_TIER_PEER view."""
+        if len(blob) != C.sizeof(PeerRecord):
+            raise ContractError("peer record blob must be 128 bytes")
+        pr = PeerRecord.from_buffer_copy(blob)
+        t = _i32(tokens)
+        check(lib.frag_store_import(self._h, C.byref(pr), _i32p(t), len(t), int(overwrite)))
+        cid = ChunkId()
+        C.memmove(C.byref(cid), C.byref(pr.id), 16)
         return cid
 
     @staticmethod
