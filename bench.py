@@ -383,11 +383,26 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         sweep[str(r)] = round(s0.elapsed_time(s1) / 2, 3)
 
+    # ---- CacheBlend selector on the same requests: 2-layer
+    # Full-Attention pass + layer-2 K deviation instead of the question pass + K9
+    step_dev(1, selector="cacheblend")
+    step_dev(2, selector="cacheblend")
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for i in range(2):
+        step_dev(3 + i, selector="cacheblend")
+    c1.record(stream)
+    torch.cuda.synchronize()
+    cacheblend_ms = c0.elapsed_time(c1) / 2
+    step_dev(1, selector="cacheblend", timing=True)
+    cacheblend_stages = res.timing()
+
     if world > 1:
         torch.distributed.barrier()  # peers may still read this rank's records until every rank is done
     return dict(ms=ms, e2e_ms=e2e_ms, full_ms=full_ms, launches=launches, prof=prof, stages=stages, T=T,
                 crit=crit, clocks=clk.summary(), cfg=c, w=w, ratio=ratio, h2d=h2d, d2h=d2h, sweep=sweep,
-                k=len(crit), decode_ms=decode_ms, n_dec=len(answer), load_leg=load_leg)
+                k=len(crit), decode_ms=decode_ms, n_dec=len(answer), load_leg=load_leg,
+                cacheblend_ms=cacheblend_ms, cacheblend_stages=cacheblend_stages)
 
 
 def main():
@@ -467,6 +482,9 @@ def main():
         "ttft_ms": ttft, "full_prefill_ms": full_ms, "speedup_vs_full_prefill": full_ms / ttft,
         "recomputed_rows": r["k"] + r["w"]["qlen"], "stage_ms": r["stages"],
         "ratio_sweep_ttft_ms": r["sweep"] or None,
+        "cacheblend": {"ttft_ms": r["cacheblend_ms"], "stage_ms": r["cacheblend_stages"],
+                       "note": "same requests with the CacheBlend selector (2-layer Full-Attention pass + layer-2 "
+                               "K deviation, SPEC.md:417) instead of the query-guided one; not in value"},
         "queries_per_s": world * args.steps / (ms / 1e3),
         "ttft_with_load": r["load_leg"],
         "decode": {"ms_per_token": r["decode_ms"], "tokens": r["n_dec"],

@@ -92,7 +92,16 @@ typedef struct {
                                   query-guided selector ("selection-injection" parity mode) */
   int32_t n_inject;
   int32_t logits_on_device;    /* do not copy logits to host (device-resident benchmark leg) */
+  int32_t selector;            /* FRAG_SELECT_QUERY_GUIDED (default) or FRAG_SELECT_CACHEBLEND */
+  int32_t deviation_layer;     /* CacheBlend: 1-based layer of the deviation (0 -> 2: Delta_KV[:, 2], Eq. 8) */
+  int32_t deviation_component; /* CacheBlend: FRAG_DEV_K (default, Delta_KV[:, 2, 1]), FRAG_DEV_V, FRAG_DEV_KV */
 } frag_reprocess_opts;
+/* Critical-token selectors of the reprocessing module: select_query_guided
+ * (FusionRAG §3.2) and select_cacheblend (SPEC.md:417-425,
+ * Eq. 8: argTopk of the layer-2 K deviation between Full Attention and Full
+ * Reuse over cat(S, chunks), lower index on ties). */
+enum { FRAG_SELECT_QUERY_GUIDED = 0, FRAG_SELECT_CACHEBLEND = 1 };
+enum { FRAG_DEV_K = 0, FRAG_DEV_V = 1, FRAG_DEV_KV = 2 };
 
 typedef struct {
   float stitch_ms;   /* K1 */
@@ -251,6 +260,15 @@ FRAG_API frag_status frag_reprocess_dev(frag_engine* eng, frag_store* st, const 
 FRAG_API frag_status frag_full_prefill(frag_engine* eng, const int32_t* sys, int32_t n_sys, const int32_t* tokens,
                                        int32_t n_tok, const frag_reprocess_opts* opts, void* stream,
                                        frag_result* res);
+
+/* kv_deviation (Eq. 7): Full Reuse (the
+ * stitched records) against Full Attention over cat(S, chunks) through the
+ * first n_layers layers; dev_host receives [N][n_layers][2] fp32 (K, V sums of
+ * squared per-dim differences, N = total chunk tokens). Afterwards `res` holds
+ * the Full-Reuse stitched cache of the context (question rows unset). */
+FRAG_API frag_status frag_kv_deviation(frag_engine* eng, frag_store* st, const int32_t* sys, int32_t n_sys,
+                                       const frag_chunk_id* chunk_ids, int32_t n_chunks, int32_t n_layers,
+                                       void* stream, frag_result* res, float* dev_host);
 
 /* sparse_prefill_and_decode, decode half: greedy decoding
  * continuing the last frag_reprocess / frag_full_prefill of `res`. Token 0 is

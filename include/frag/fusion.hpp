@@ -88,6 +88,24 @@ class ChunkStore {
   uint64_t bytes_used() const { return frag_store_bytes_used(h_); }
   frag_store* handle() const { return h_; }
 
+  // Chunk-partitioned store: owner rank of a chunk, a
+  // same-process peer store on another GPU (misses served in place over
+  // NVLink), and the cross-process CUDA-IPC export / import of one record.
+  static int owner_of(const ChunkId& id, int n_owners) {
+    const frag_chunk_id c = to_c(id);
+    return frag_chunk_owner(&c, n_owners);
+  }
+  void attach_peer(ChunkStore& remote) { check(frag_store_attach_peer(h_, remote.h_)); }
+  frag_peer_record export_record(const ChunkId& id) {
+    const frag_chunk_id c = to_c(id);
+    frag_peer_record pr{};
+    check(frag_store_export(h_, &c, &pr));
+    return pr;
+  }
+  void import_record(const frag_peer_record& pr, std::span<const Token> tokens, bool overwrite = false) {
+    check(frag_store_import(h_, &pr, tokens.data(), static_cast<int32_t>(tokens.size()), overwrite ? 1 : 0));
+  }
+
  private:
   frag_store* h_ = nullptr;
 };
@@ -186,6 +204,25 @@ class Engine {
     check(frag_reprocess(h_, st.handle(), system.data(), static_cast<int32_t>(system.size()), question.data(),
                          static_cast<int32_t>(question.size()), ids.data(), static_cast<int32_t>(ids.size()), ratio,
                          opts, cuda_stream, out.handle()));
+  }
+
+  // kv_deviation (Eq. 7): [N][n_layers][2] K/V deviation between
+  // Full Attention and Full Reuse; select_cacheblend is reprocess() with
+  // opts->selector = FRAG_SELECT_CACHEBLEND.
+  std::vector<float> kv_deviation(ChunkStore& st, std::span<const ChunkId> chunk_ids, Result& scratch,
+                                  std::span<const Token> system = {}, int n_layers = 2, void* cuda_stream = nullptr) {
+    std::vector<frag_chunk_id> ids;
+    size_t n = 0;
+    for (const auto& c : chunk_ids) {
+      ids.push_back(to_c(c));
+      frag_record_view v{};
+      check(frag_store_peek(st.handle(), &ids.back(), &v));
+      n += static_cast<size_t>(v.n_tok);
+    }
+    std::vector<float> dev(n * static_cast<size_t>(n_layers) * 2);
+    check(frag_kv_deviation(h_, st.handle(), system.data(), static_cast<int32_t>(system.size()), ids.data(),
+                            static_cast<int32_t>(ids.size()), n_layers, cuda_stream, scratch.handle(), dev.data()));
+    return dev;
   }
 
   void full_prefill(std::span<const Token> tokens, Result& out, std::span<const Token> system = {},

@@ -23,6 +23,8 @@
 //   q_sparse_attn        SPEC.md:153-161; build_equivalent_mask SPEC.md:162-170
 //   stitch_full_reuse    SPEC.md:399-407 (Eq. 6)
 //   select_query_guided
+//   kv_deviation         SPEC.md:408-416 (Eq. 7)
+//   select_cacheblend    SPEC.md:417-425 (Eq. 8)
 //   sparse_prefill       SPEC.md:435-444 (Eq. 9)
 //   preprocess_isolated  SPEC.md:344-352 (Eq. 5)
 // ============================================================================
@@ -212,10 +214,13 @@ struct Cache {
 // else cache row j valid and pos[j] <= positions[i].
 // stop_layer_q: if >= 0, return after the QKV projection of the final layer with
 // post-RoPE queries in q_out (last_layer_query_states).
+// n_layers > 0 runs only the first n_layers layers (with stop_after_last_q the
+// pass ends after layer n_layers-1's QKV: kv_deviation's FA pass).
 void forward(const Model& m, int n, const int32_t* tokens, const int32_t* positions, const int32_t* slots,
              Cache& cache, const uint8_t* mask, float* logits, int n_logit_rows, const int32_t* logit_rows,
-             float* q_out, bool stop_after_last_q, bool emu) {
+             float* q_out, bool stop_after_last_q, bool emu, int n_layers = 0) {
   const auto& c = m.c;
+  const int L = (n_layers > 0 && n_layers < c.layers) ? n_layers : c.layers;
   const int d = c.d_model, Hq = c.n_heads, Hkv = c.n_kv_heads, dh = c.head_dim, F = c.ffn_dim;
   const int qc = Hq * dh, kc = Hkv * dh, G = Hq / Hkv;
   const float scale = 1.0f / std::sqrt((float)dh);
@@ -224,13 +229,13 @@ void forward(const Model& m, int n, const int32_t* tokens, const int32_t* positi
   for (int i = 0; i < n; ++i)
     std::memcpy(&h[(size_t)i * d], &m.emb[(size_t)tokens[i] * d], d * sizeof(float));
   for (int i = 0; i < n; ++i) cache.pos[slots[i]] = positions[i];
-  for (int l = 0; l < c.layers; ++l) {
+  for (int l = 0; l < L; ++l) {
     const Layer& W = m.layers[l];
     rmsnorm_rows(h.data(), W.attn_norm.data(), x.data(), n, d, c.norm_eps, emu);
     gemm_nt(x.data(), W.wq.data(), q.data(), n, qc, d, false);
     gemm_nt(x.data(), W.wk.data(), kk.data(), n, kc, d, false);
     gemm_nt(x.data(), W.wv.data(), vv.data(), n, kc, d, false);
-    const bool last_q = stop_after_last_q && l == c.layers - 1;
+    const bool last_q = stop_after_last_q && l == L - 1;
 #pragma omp parallel for schedule(static)
     for (int i = 0; i < n; ++i) {
       for (int hh = 0; hh < Hq; ++hh) rope_apply(&q[(size_t)i * qc + hh * dh], dh, positions[i], m.theta);
@@ -304,7 +309,7 @@ void forward(const Model& m, int n, const int32_t* tokens, const int32_t* positi
     }
     gemm_nt(gg.data(), W.wd.data(), h.data(), n, d, F, true);
   }
-  if (logits && n_logit_rows > 0) {
+  if (logits && n_logit_rows > 0 && L == c.layers) {
     std::vector<float> hr((size_t)n_logit_rows * d), xr((size_t)n_logit_rows * d);
     for (int r = 0; r < n_logit_rows; ++r)
       std::memcpy(&hr[(size_t)r * d], &h[(size_t)logit_rows[r] * d], d * sizeof(float));
@@ -633,6 +638,88 @@ void orc_build_equivalent_mask(const int32_t* q_idx, const uint8_t* is_new, int 
     if (is_new[j]) kpos[w++] = q_idx[j];
   for (int i = 0; i < nq; ++i)
     for (int j = 0; j < W; ++j) mask[(size_t)i * W + j] = kpos[j] <= q_idx[i] ? 1 : 0;
+}
+
+// ---- kv_deviation (Eq. 7) over
+// X = cat(S, chunks): Full Reuse = the stitched records (K1); Full Attention =
+// KV_S (identical in both modes: prefix reuse, Eq. 4) followed by a prefill of
+// every chunk token at its global position through the first n_layers layers.
+// dev [N][n_layers][2] (fp64): sum over Hkv*dh of the squared K / V differences.
+int orc_kv_deviation(const orc_model* mm, int S, const float* sys_k, const float* sys_v, int n_chunks,
+                     const float* const* rec_k, const float* const* rec_v, const int32_t* const* rec_tok,
+                     const int32_t* rec_n, const int32_t* rec_native, int n_layers, int emulate_bf16, double* dev) {
+  const Model* m = reinterpret_cast<const Model*>(mm);
+  const auto& c = m->c;
+  if (n_layers < 1 || n_layers > c.layers) return 1;
+  const int kc = c.n_kv_heads * c.head_dim;
+  int N = 0;
+  for (int i = 0; i < n_chunks; ++i) N += rec_n[i];
+  const int cap = S + N;
+  std::vector<float> fr_k((size_t)c.layers * cap * kc, 0.f), fr_v(fr_k.size(), 0.f);
+  std::vector<const float*> ks, vs;
+  std::vector<int32_t> ns, nat, dst;
+  if (S > 0) {
+    ks.push_back(sys_k), vs.push_back(sys_v), ns.push_back(S), nat.push_back(1), dst.push_back(0);
+  }
+  int row = S;
+  for (int i = 0; i < n_chunks; ++i) {
+    ks.push_back(rec_k[i]), vs.push_back(rec_v[i]), ns.push_back(rec_n[i]), nat.push_back(rec_native[i]);
+    dst.push_back(row);
+    row += rec_n[i];
+  }
+  orc_stitch(&c, (int)ks.size(), ks.data(), vs.data(), ns.data(), nat.data(), dst.data(), fr_k.data(), fr_v.data(),
+             cap, emulate_bf16);
+  // FA: system rows from KV_S, chunk rows prefilled at positions S+1..S+N
+  std::vector<float> fa_k(fr_k.size(), 0.f), fa_v(fr_v.size(), 0.f);
+  for (int l = 0; l < c.layers; ++l)
+    for (int r = 0; r < S; ++r) {
+      std::memcpy(&fa_k[((size_t)l * cap + r) * kc], &fr_k[((size_t)l * cap + r) * kc], kc * sizeof(float));
+      std::memcpy(&fa_v[((size_t)l * cap + r) * kc], &fr_v[((size_t)l * cap + r) * kc], kc * sizeof(float));
+    }
+  std::vector<int32_t> pos(cap, 0), tok(N), p(N), sl(N);
+  for (int r = 0; r < S; ++r) pos[r] = r + 1;
+  {
+    int off = 0;
+    for (int i = 0; i < n_chunks; ++i) {
+      std::memcpy(&tok[off], rec_tok[i], rec_n[i] * sizeof(int32_t));
+      off += rec_n[i];
+    }
+  }
+  for (int j = 0; j < N; ++j) p[j] = S + j + 1, sl[j] = S + j;
+  Cache cc{cap, fa_k.data(), fa_v.data(), pos.data()};
+  forward(*m, N, tok.data(), p.data(), sl.data(), cc, nullptr, nullptr, 0, nullptr, nullptr, true, emulate_bf16 != 0,
+          n_layers);
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < N; ++j)
+    for (int l = 0; l < n_layers; ++l) {
+      const size_t o = ((size_t)l * cap + S + j) * kc;
+      double dk = 0.0, dv = 0.0;
+      for (int e = 0; e < kc; ++e) {
+        const double a = (double)fa_k[o + e] - fr_k[o + e], b = (double)fa_v[o + e] - fr_v[o + e];
+        dk += a * a;
+        dv += b * b;
+      }
+      dev[((size_t)j * n_layers + l) * 2 + 0] = dk;
+      dev[((size_t)j * n_layers + l) * 2 + 1] = dv;
+    }
+  return 0;
+}
+
+// ---- select_cacheblend (Eq. 8): argTopk of one deviation
+// column (restricted to chunk tokens by construction), lower index on ties,
+// returned ascending (0-based chunk-token indices).
+void orc_select_cacheblend(const double* dev, int N, int n_layers, int layer, int comp, int k, int32_t* sel) {
+  std::vector<double> v(N);
+  for (int j = 0; j < N; ++j) {
+    const double* d = dev + ((size_t)j * n_layers + (layer - 1)) * 2;
+    v[j] = comp == 0 ? d[0] : (comp == 1 ? d[1] : d[0] + d[1]);
+  }
+  std::vector<int32_t> idx(N);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return v[a] > v[b]; });
+  std::vector<int32_t> top(idx.begin(), idx.begin() + k);
+  std::sort(top.begin(), top.end());
+  std::copy(top.begin(), top.end(), sel);
 }
 
 // ---- full reprocess on one engine-shaped model.

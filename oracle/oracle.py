@@ -50,6 +50,8 @@ def _load():
         "orc_select": (None, [P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P]),
         "orc_q_sparse_attn": (C.c_int, [P, P, P, C.c_int, P, P, P, P, C.c_int, C.c_int, C.c_int, P]),
         "orc_build_equivalent_mask": (None, [P, P, C.c_int, C.c_int, P]),
+        "orc_kv_deviation": (C.c_int, [P, C.c_int, P, P, C.c_int, P, P, P, P, P, C.c_int, C.c_int, P]),
+        "orc_select_cacheblend": (None, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P]),
         "orc_reprocess": (C.c_int, [P, C.c_int, P, P, P, C.c_int, P, P, P, P, P, C.c_int, P, C.c_float, C.c_int,
                                     P, C.c_int, C.c_int, P, P, C.c_int, P, P, P, P, P, P]),
     }
@@ -227,6 +229,29 @@ class Model:
         return {"k": kc[:, :T], "v": vc[:, :T], "logits": logits, "crit": crit[:k].copy(), "q_final": qf,
                 "scores": scores[:N], "stage_seconds": stages, "T": T, "k_cache": kc, "v_cache": vc}
 
+    # ------------------------------------------------------------ CacheBlend
+    def kv_deviation(self, sys_kv, records, n_layers=2, emulate_bf16=True):
+        """Eq. 7 over cat(S, chunks): [N][n_layers][2] fp64 (K, V)."""
+        S = 0 if sys_kv is None else sys_kv[0].shape[1]
+        N = sum(len(r["tokens"]) for r in records)
+        ks = [_c(r["k"], _F) for r in records]
+        vs = [_c(r["v"], _F) for r in records]
+        toks = [_c(r["tokens"], np.int32) for r in records]
+        kp = (C.c_void_p * len(ks))(*[a.ctypes.data for a in ks])
+        vp = (C.c_void_p * len(vs))(*[a.ctypes.data for a in vs])
+        tp = (C.c_void_p * len(toks))(*[a.ctypes.data for a in toks])
+        ns = _c([len(t) for t in toks], np.int32)
+        nat = _c([r["native_start"] for r in records], np.int32)
+        sk = sv = None
+        if S:
+            sk, sv = _c(sys_kv[0], _F), _c(sys_kv[1], _F)
+        dev = np.zeros((N, n_layers, 2), np.float64)
+        rc = lib.orc_kv_deviation(self._h, S, _p(sk), _p(sv), len(records), kp, vp, tp, _p(ns), _p(nat),
+                                  int(n_layers), int(emulate_bf16), _p(dev))
+        if rc != 0:
+            raise ValueError(f"orc_kv_deviation failed ({rc})")
+        return dev
+
     # ------------------------------------------------------------ decode (SPEC.md:435-438)
     def decode_forced(self, cache_k, cache_v, T, tokens, emulate_bf16=True):
         """Decode steps of sparse_prefill_and_decode with given inputs: token i
@@ -284,6 +309,16 @@ def select(q, keys, k, raw=False):
     sel = np.empty(max(k, 1), np.int32)
     lib.orc_select(_p(q), _p(keys), nq, Hq, Hkv, dh, N, k, int(raw), _p(scores), _p(sel))
     return scores, sel[:k].copy()
+
+
+def select_cacheblend(dev, k, layer=2, comp=0):
+    """argTopk of dev[:, layer-1, comp] (comp 2 = K+V), lower index on ties,
+    ascending 0-based chunk-token indices."""
+    dev = _c(dev, np.float64)
+    N, L, _ = dev.shape
+    sel = np.empty(max(k, 1), np.int32)
+    lib.orc_select_cacheblend(_p(dev), N, L, int(layer), int(comp), int(k), _p(sel))
+    return sel[:k].copy()
 
 
 def q_sparse_attn(q, shared_k, shared_v, fresh_k, fresh_v, q_idx, is_new):

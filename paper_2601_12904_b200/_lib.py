@@ -62,7 +62,8 @@ assert C.sizeof(PeerRecord) == 128
 class ReprocessOpts(C.Structure):
     _fields_ = [("raw_scores", C.c_int32), ("all_logits", C.c_int32), ("timing", C.c_int32),
                 ("inject_crit", C.POINTER(C.c_int32)), ("n_inject", C.c_int32),
-                ("logits_on_device", C.c_int32)]
+                ("logits_on_device", C.c_int32), ("selector", C.c_int32), ("deviation_layer", C.c_int32),
+                ("deviation_component", C.c_int32)]
 
 
 class Timing(C.Structure):
@@ -121,6 +122,8 @@ _SIGS = {
                                      C.c_float, C.POINTER(ReprocessOpts), _P, _P]),
     "frag_full_prefill": (C.c_int, [_P, _I32P, C.c_int32, _I32P, C.c_int32, C.POINTER(ReprocessOpts), _P, _P]),
     "frag_decode": (C.c_int, [_P, _P, C.c_int32, _P, _I32P]),
+    "frag_kv_deviation": (C.c_int, [_P, _P, _I32P, C.c_int32, C.POINTER(ChunkId), C.c_int32, C.c_int32, _P, _P,
+                                    _P]),
     "frag_result_sync": (C.c_int, [_P]),
     "frag_result_fused_kv": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), _I32P]),
     "frag_result_logits": (C.c_int, [_P, C.POINTER(C.POINTER(C.c_float)), _I32P, _I32P, C.c_int32]),

@@ -428,6 +428,17 @@ FRAG_API frag_status frag_full_prefill(frag_engine* eng, const int32_t* sys, int
   });
 }
 
+FRAG_API frag_status frag_kv_deviation(frag_engine* eng, frag_store* st, const int32_t* sys, int32_t n_sys,
+                                       const frag_chunk_id* chunk_ids, int32_t n_chunks, int32_t n_layers,
+                                       void* stream, frag_result* res, float* dev_host) {
+  return guard([&] {
+    need(eng && st && res && dev_host, "null argument");
+    need(n_sys == 0 || sys, "null system prompt");
+    kv_deviation(eng->e, st->s, sys, n_sys, chunk_ids, n_chunks, n_layers, static_cast<cudaStream_t>(stream), res->r,
+                 dev_host);
+  });
+}
+
 FRAG_API frag_status frag_decode(frag_engine* eng, frag_result* res, int32_t max_new_tokens, void* stream,
                                  int32_t* tokens_out) {
   return guard([&] {

@@ -308,9 +308,10 @@ void result_init(Result* r, Engine* e, int max_tokens) {
 
 // ---------------------------------------------------------------- run_rows
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
-              int n_logit_rows) {
+              int n_logit_rows, int n_layers) {
   if (M <= 0) return;
   const auto& c = e->cfg;
+  const int L = (n_layers > 0 && n_layers < c.layers) ? n_layers : c.layers;
   const int d = c.d_model, Hq = c.n_heads, Hkv = c.n_kv_heads, dh = c.head_dim, F = c.ffn_dim;
   const size_t qc = (size_t)Hq * dh, kvc = (size_t)Hkv * dh, qkv = e->qkv_cols();
   const size_t lstride = (size_t)r->max_tokens * kvc;
@@ -355,7 +356,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     fragk::embed_rmsnorm(e->emb, ptok, M, d, e->layers[0].attn_norm, c.norm_eps, h, x, s);
     sc.launched(1);
   }
-  for (int l = 0; l < c.layers; ++l) {
+  for (int l = 0; l < L; ++l) {
     const auto& W = e->layers[l];
     if (l > 0) {
       Scoped sc(P, s, KC_NORM, 0, (double)M * d * (4 + 2));
@@ -368,7 +369,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       ep.rows = prow;
       ep.rope = e->rope.as<float2>();
       ep.q_out = r->q.as<bf16>();
-      ep.q_out_f32 = (mode == PASS_QUESTION && l == c.layers - 1) ? r->q_final.as<float>() : nullptr;
+      ep.q_out_f32 = (mode == PASS_QUESTION && l == L - 1) ? r->q_final.as<float>() : nullptr;
       ep.k_cache = kf + l * lstride;
       ep.v_cache = vf + l * lstride;
       ep.Hq = Hq;
@@ -377,7 +378,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       Scoped sc(P, s, gemm_class(M), 2.0 * M * qkv * d, 2.0 * (qkv * d + (double)M * (d + qkv)));
       sc.launched(fragk::gemm_bf16_tc(x, W.wqkv, M, (int)qkv, d, fragk::EPI_QKV, ep, s));
     }
-    if (mode != PASS_FULL && l == c.layers - 1) break;
+    if (mode != PASS_FULL && l == L - 1) break;
     {
       fragk::AttnArgs a{};
       a.q = r->q.as<bf16>();
@@ -429,7 +430,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     }
     peek("layer");
   }
-  if (mode == PASS_FULL && n_logit_rows > 0) {
+  if (mode == PASS_FULL && n_logit_rows > 0 && L == c.layers) {
     r->lm_x.ensure((size_t)n_logit_rows * d * sizeof(bf16));
     r->logits.ensure((size_t)n_logit_rows * c.vocab * sizeof(float));
     {
@@ -639,6 +640,60 @@ SysKV* get_sys_kv(Engine* e, const int32_t* sys, int n_sys, cudaStream_t s) {
   return out;
 }
 
+// ---- kv_deviation / select_cacheblend (Eq. 7-8)
+// The Full-Attention rows of the first Ld layers are computed in place over the
+// chunk rows [S, S+N) of the result's fused cache (system rows are KV_S in
+// both modes, Eq. 4), after the stitched Full-Reuse rows of those layers were
+// saved to r->fr_save; the deviation kernel compares the two, then the saved
+// rows are copied back so the cache is Full Reuse again for the sparse pass.
+void fr_copy(Engine* e, Result* r, cudaStream_t s, int S, int N, int Ld, bool restore) {
+  const auto& c = e->cfg;
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  const size_t w = (size_t)N * kvc * sizeof(bf16), pitch = (size_t)r->max_tokens * kvc * sizeof(bf16);
+  char* kf = r->k_fused.as<char>() + (size_t)S * kvc * sizeof(bf16);
+  char* vf = r->v_fused.as<char>() + (size_t)S * kvc * sizeof(bf16);
+  char* ks = r->fr_save.as<char>();
+  char* vs = ks + (size_t)Ld * w;
+  const cudaMemcpyKind kd = cudaMemcpyDeviceToDevice;
+  if (!restore) {
+    check_cuda(cudaMemcpy2DAsync(ks, w, kf, pitch, w, Ld, kd, s), "save FR K");
+    check_cuda(cudaMemcpy2DAsync(vs, w, vf, pitch, w, Ld, kd, s), "save FR V");
+  } else {
+    check_cuda(cudaMemcpy2DAsync(kf, pitch, ks, w, w, Ld, kd, s), "restore FR K");
+    check_cuda(cudaMemcpy2DAsync(vf, pitch, vs, w, w, Ld, kd, s), "restore FR V");
+  }
+}
+
+// FA pass over the chunk rows (plan rows S.. / chunk tokens must be on the
+// device) + the deviation kernel. dev: [N][Ld][2] or null; sel: [N] or null.
+void deviation_body(Engine* e, Result* r, cudaStream_t s, int S, int N, int Ld, float* dev, float* sel,
+                    int sel_comp) {
+  const auto& c = e->cfg;
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  fr_copy(e, r, s, S, N, Ld, false);
+  run_rows(e, r, s, N, S + N, PASS_KV_ONLY, nullptr, 0, Ld);
+  fragk::DeviationArgs a{};
+  a.k_fa = r->k_fused.as<bf16>() + (size_t)S * kvc;
+  a.v_fa = r->v_fused.as<bf16>() + (size_t)S * kvc;
+  a.fa_layer_stride = (size_t)r->max_tokens * kvc;
+  a.k_fr = r->fr_save.as<bf16>();
+  a.v_fr = r->fr_save.as<bf16>() + (size_t)Ld * N * kvc;
+  a.fr_layer_stride = (size_t)N * kvc;
+  a.n_rows = N;
+  a.n_layers = Ld;
+  a.width = (int)kvc;
+  a.dev = dev;
+  a.sel_scores = sel;
+  a.sel_layer = Ld - 1;
+  a.sel_comp = sel_comp;
+  {
+    Scoped sc(e->prof, s, KC_SELECT, 0, 4.0 * N * Ld * kvc * sizeof(bf16));
+    sc.launched(fragk::kv_deviation(a, s));
+  }
+  fr_copy(e, r, s, S, N, Ld, true);
+  peek("kv_deviation");
+}
+
 void ev_record(Result* r, bool on, int i, cudaStream_t s) {
   if (on) cudaEventRecord(r->ev[i], s);
 }
@@ -720,8 +775,21 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     if (q_on_device) fail(FRAG_E_CONTRACT, "selection injection requires host question tokens");
   }
   const int M = k + n_q;
+  const int selector = o ? o->selector : FRAG_SELECT_QUERY_GUIDED;
+  if (selector != FRAG_SELECT_QUERY_GUIDED && selector != FRAG_SELECT_CACHEBLEND)
+    fail(FRAG_E_CONTRACT, "unknown selector");
+  const int dev_layer = (o && o->deviation_layer > 0) ? o->deviation_layer : 2;
+  const int dev_comp = o ? o->deviation_component : FRAG_DEV_K;
+  if (selector == FRAG_SELECT_CACHEBLEND) {
+    if (dev_layer > c.layers) fail(FRAG_E_CONTRACT, "deviation_layer exceeds the model depth");
+    if (dev_comp < FRAG_DEV_K || dev_comp > FRAG_DEV_KV) fail(FRAG_E_CONTRACT, "unknown deviation component");
+  }
+  // select_cacheblend replaces the question pass + K9
+  const bool cacheblend = selector == FRAG_SELECT_CACHEBLEND && !inject && N > 0;
   e->ensure_rope(T);
   SysKV* skv = get_sys_kv(e, sys, n_sys, s);
+  if (cacheblend)
+    r->fr_save.ensure((size_t)2 * dev_layer * N * c.n_kv_heads * c.head_dim * sizeof(bf16));
 
   r->T = T;
   r->S = S;
@@ -741,6 +809,9 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   // so their offsets must depend only on the graph key
   int* inj_rows = inject ? stg.take<int>(M) : nullptr;
   int* inj_tok = inject ? stg.take<int>(M) : nullptr;
+  int* cb_rows = cacheblend ? stg.take<int>(N) : nullptr;  // FA-pass plan rows S..S+N-1 (copied in the body)
+  if (cacheblend)
+    for (int i = 0; i < N; ++i) cb_rows[i] = S + i;
   StitchPlan sp = stitch_prepare(e, r, s, stg, skv, recs, S);
   {
     int off = 0;  // chunk token ids in prompt order (the recompute gather, K2)
@@ -805,10 +876,20 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     stitch_launch(e, r, bs, sp);  // K1: stitch_full_reuse
     ev_record(r, timing, 1, bs);
     // question pass: last_layer_query_states against the stitched cache
-    run_rows(e, r, bs, n_q, T, PASS_QUESTION, nullptr, 0);
+    if (!cacheblend) run_rows(e, r, bs, n_q, T, PASS_QUESTION, nullptr, 0);
     ev_record(r, timing, 2, bs);
     // select_query_guided (K9 + K10) -> QIndexPlan on device
-    if (inject) {
+    if (cacheblend) {
+      // select_cacheblend: Delta_KV[:, dev_layer, comp] between Full Attention and
+      // Full Reuse over cat(S, chunks) (Eq. 7-8), then the same top-k plan (K10)
+      check_cuda(cudaMemcpyAsync(r->plan_rows.p, cb_rows, N * sizeof(int), cudaMemcpyHostToDevice, bs), "fa rows");
+      check_cuda(cudaMemcpyAsync(r->plan_tok.p, r->chunk_tok.p, N * sizeof(int), cudaMemcpyDeviceToDevice, bs),
+                 "fa tok");
+      deviation_body(e, r, bs, S, N, dev_layer, nullptr, r->scores.as<float>(), dev_comp);
+      Scoped sc(e->prof, bs, KC_SELECT, 0, 4.0 * N * 6);
+      sc.launched(fragk::topk_plan(r->scores.as<float>(), N, k, S, r->chunk_tok.as<int>(), r->q_tok.as<int>(), n_q,
+                                   T - n_q, r->plan_rows.as<int>(), r->plan_tok.as<int>(), bs));
+    } else if (inject) {
       check_cuda(cudaMemcpyAsync(r->plan_rows.p, inj_rows, M * sizeof(int), cudaMemcpyHostToDevice, bs), "plan rows");
       check_cuda(cudaMemcpyAsync(r->plan_tok.p, inj_tok, M * sizeof(int), cudaMemcpyHostToDevice, bs), "plan tok");
     } else {
@@ -867,7 +948,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
 
   const bool graphable = !timing && !e->prof.on;
   GraphKey key{T, S, N, n_q, k, (int)inject, (int)all_logits, (int)raw, (int)r->logits_on_device, sp.n_desc,
-               sp.max_rows, (uint64_t)(uintptr_t)e->rope.p};
+               sp.max_rows, cacheblend ? 1 + dev_layer * 4 + dev_comp : 0, (uint64_t)(uintptr_t)e->rope.p};
   r->timing.host_prep_ms =
       std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
   run_graphed(r, s, graphable, key, body);
@@ -918,6 +999,57 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
   finish(r, timing, s);
 }
 
+void kv_deviation(Engine* e, Store* st, const int32_t* sys, int n_sys, const frag_chunk_id* ids, int n_chunks,
+                  int n_layers, cudaStream_t s, Result* r, float* dev_host) {
+  const auto& c = e->cfg;
+  if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
+  if (!st) fail(FRAG_E_CONTRACT, "store is null");
+  if (st->device != e->device) fail(FRAG_E_CONTRACT, "store and engine are on different devices");
+  if (n_layers < 1 || n_layers > c.layers) fail(FRAG_E_CONTRACT, "n_layers must lie in [1, layers]");
+  if (n_sys < 0 || n_chunks < 1 || !ids) fail(FRAG_E_CONTRACT, "kv_deviation needs at least one chunk");
+  DeviceGuard dg(e->device);
+  PinGuard pins{st, {}};
+  std::vector<Record*> recs;
+  for (int i = 0; i < n_chunks; ++i) {
+    recs.push_back(store_fetch(st, ids[i]));
+    pins.ids.push_back(ids[i]);
+  }
+  const int S = n_sys;
+  int N = 0;
+  for (Record* rec : recs) N += rec->n_tok;
+  const int T = S + N;
+  if (T > r->max_tokens) fail(FRAG_E_CONTRACT, "context exceeds the result capacity");
+  e->ensure_rope(T);
+  SysKV* skv = get_sys_kv(e, sys, n_sys, s);
+  r->T = T;
+  r->S = S;
+  r->N = N;
+  r->nq = 0;
+  r->k_sel = 0;
+  r->M = 0;
+  r->logit_rows = 0;
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  r->fr_save.ensure((size_t)2 * n_layers * N * kvc * sizeof(bf16));
+  r->dev.ensure((size_t)N * n_layers * 2 * sizeof(float));
+  r->staging.ensure(64 * 1024 + (size_t)(n_chunks + 2) * (64 + c.head_dim * 4) + (size_t)8 * N);
+  Stage stg(r->staging);
+  stitch(e, r, s, stg, skv, recs, S);
+  int* rows_h = stg.take<int>(N);
+  for (int i = 0; i < N; ++i) rows_h[i] = S + i;
+  check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, N * sizeof(int), cudaMemcpyHostToDevice, s), "fa rows");
+  int off = 0;
+  for (Record* rec : recs) {
+    check_cuda(cudaMemcpyAsync(r->plan_tok.as<int>() + off, rec->tok.p, rec->n_tok * sizeof(int),
+                               cudaMemcpyDeviceToDevice, s),
+               "fa tokens");
+    off += rec->n_tok;
+  }
+  deviation_body(e, r, s, S, N, n_layers, r->dev.as<float>(), nullptr, 0);
+  check_cuda(cudaMemcpyAsync(dev_host, r->dev.p, (size_t)N * n_layers * 2 * sizeof(float), cudaMemcpyDefault, s),
+             "deviation D2H");
+  check_cuda(cudaStreamSynchronize(s), "kv_deviation");
+}
+
 void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) {
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
@@ -956,7 +1088,7 @@ void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) 
     argmax(r->logits.as<float>(), -1, bs);
   };
   const bool graphable = !e->prof.on;
-  GraphKey key{T_cap, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, (uint64_t)(uintptr_t)e->rope.p};
+  GraphKey key{T_cap, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, (uint64_t)(uintptr_t)e->rope.p};
   for (int i = 1; i < n_new; ++i) run_graphed(r, s, graphable, key, step);
   peek("decode");
   check_cuda(cudaMemcpyAsync(stage, toks, (size_t)n_new * sizeof(int), cudaMemcpyDeviceToHost, s), "tokens");

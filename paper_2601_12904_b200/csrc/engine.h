@@ -187,12 +187,12 @@ struct Engine {
 
 // Shape of a request body; a captured CUDA graph is valid for one key.
 struct GraphKey {
-  int T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows;
+  int T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows, selector;
   uint64_t rope;
   bool operator<(const GraphKey& o) const {
-    return std::tie(T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows, rope) <
+    return std::tie(T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows, selector, rope) <
            std::tie(o.T, o.S, o.N, o.nq, o.k, o.inject, o.all_logits, o.raw, o.logits_on_device, o.n_desc,
-                    o.max_rows, o.rope);
+                    o.max_rows, o.selector, o.rope);
   }
 };
 struct GraphEntry {
@@ -216,7 +216,7 @@ struct Result {
   int T = 0, S = 0, N = 0, nq = 0, k_sel = 0, M = 0, logit_rows = 0;
   // workspace
   DevBuf h, x, q, attn, act, plan_rows, plan_tok, chunk_tok, q_tok, q_final, scores, part_ms, row_ms, part_o,
-      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok;
+      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok, fr_save, dev;
   PinnedBuf staging, logits_host;
   // timing
   cudaEvent_t ev[7] = {};
@@ -236,14 +236,21 @@ enum PassMode { PASS_FULL = 0, PASS_QUESTION = 1, PASS_KV_ONLY = 2 };
 // result's fused cache with T valid rows; PASS_QUESTION stops after the final
 // layer's QKV projection with fp32 queries in r->q_final; PASS_FULL ends with
 // logits for the rows listed in row_map (n_logit_rows of them, device).
+// n_layers > 0 runs only the first n_layers layers (a non-FULL pass then stops
+// after layer n_layers-1's QKV projection: kv_deviation's 2-layer FA pass).
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
-              int n_logit_rows);
+              int n_logit_rows, int n_layers = 0);
 
 void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
                bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio, const frag_reprocess_opts* o,
                cudaStream_t s, Result* r);
 void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                   const frag_reprocess_opts* o, cudaStream_t s, Result* r);
+// kv_deviation (Eq. 7): Full Reuse (stitched) vs Full Attention
+// over cat(S, chunks) through the first n_layers layers; dev_host [N][n_layers][2]
+// (K, V). The result holds the Full-Reuse stitched cache afterwards.
+void kv_deviation(Engine* e, Store* st, const int32_t* sys, int n_sys, const frag_chunk_id* ids, int n_chunks,
+                  int n_layers, cudaStream_t s, Result* r, float* dev_host);
 // Greedy decoding after a reprocess / full prefill: token 0 =
 // argmax of the last logits row, then n_new-1 single-row steps at positions
 // T+1.. whose K/V are appended to the result's own fused cache (its exclusive

@@ -122,6 +122,20 @@ int qg_score(const ScoreArgs& a, cudaStream_t stream);
 // then the question rows appended. Writes plan_rows[k + nq] and plan_tok.
 int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* chunk_tok, const int* q_tok,
               int nq, int q_row0, int* plan_rows, int* plan_tok, cudaStream_t stream);
+// kv_deviation (Eq. 7): per chunk token j and layer l < n_layers,
+// dev[j][l][0|1] = sum over Hkv*dh of the squared K|V difference between the
+// Full-Attention rows (k_fa/v_fa + l*fa_layer_stride + j*width) and the Full-Reuse
+// rows (k_fr/v_fr + l*fr_layer_stride + j*width); sel_scores[j] = the sel_comp
+// (0 K, 1 V, 2 K+V) deviation at layer sel_layer (select_cacheblend, Eq. 8).
+struct DeviationArgs {
+  const bf16 *k_fa, *v_fa, *k_fr, *v_fr;
+  size_t fa_layer_stride, fr_layer_stride;  // elements
+  int n_rows, n_layers, width;
+  float* dev;         // [n_rows][n_layers][2] or null
+  float* sel_scores;  // [n_rows] or null
+  int sel_layer, sel_comp;
+};
+int kv_deviation(const DeviationArgs& a, cudaStream_t stream);
 // Greedy decoding step: argmax(logits[0..V)) (lowest index on ties) -> out[0],
 // or out[*out_idx] with *out_idx incremented when out_idx is set; also stored
 // as the next step's plan token, and plan_rows[0] = next_row (next_row < 0:

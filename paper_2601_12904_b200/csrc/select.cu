@@ -395,4 +395,67 @@ int greedy_argmax(const float* logits, int V, int* out, int* out_idx, int* plan_
   return 1;
 }
 
+// ------------------------------------------------------------------ kv_deviation (Eq. 7)
+// Delta_KV[j, l, c] = sum_{e < Hkv*dh} (KV_FA[l][j][e] - KV_FR[l][j][e])^2 for
+// c = K, V. One warp per (token, layer):
+// 128-bit loads of both caches (each row read once: HBM-bound), fp32 squared
+// differences summed per lane in a fixed order, then a fixed butterfly -> bit-
+// deterministic. The selection vector of select_cacheblend (SPEC.md:417-425,
+// Eq. 8: Delta_KV[:, 2, 1]) is written for layer sel_layer from the same sums.
+namespace {
+constexpr int DV_WARPS = 8;
+__device__ __forceinline__ float sq_diff8(const uint4 a, const uint4 b) {
+  const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 fa = __bfloat1622float2(pa[i]);
+    const float2 fb = __bfloat1622float2(pb[i]);
+    const float d0 = fa.x - fb.x, d1 = fa.y - fb.y;
+    acc = fmaf(d0, d0, acc);
+    acc = fmaf(d1, d1, acc);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(DV_WARPS * 32) kv_deviation_kernel(const DeviationArgs a) {
+  const int warp = blockIdx.x * DV_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (warp >= a.n_rows * a.n_layers) return;
+  const int j = warp / a.n_layers, l = warp % a.n_layers;
+  const int nvec = a.width / 8;
+  const uint4* ka = reinterpret_cast<const uint4*>(a.k_fa + (size_t)l * a.fa_layer_stride + (size_t)j * a.width);
+  const uint4* va = reinterpret_cast<const uint4*>(a.v_fa + (size_t)l * a.fa_layer_stride + (size_t)j * a.width);
+  const uint4* kb = reinterpret_cast<const uint4*>(a.k_fr + (size_t)l * a.fr_layer_stride + (size_t)j * a.width);
+  const uint4* vb = reinterpret_cast<const uint4*>(a.v_fr + (size_t)l * a.fr_layer_stride + (size_t)j * a.width);
+  float dk = 0.f, dv = 0.f;
+  for (int i = lane; i < nvec; i += 32) {
+    dk += sq_diff8(__ldcs(ka + i), __ldcs(kb + i));
+    dv += sq_diff8(__ldcs(va + i), __ldcs(vb + i));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dk += __shfl_xor_sync(0xffffffffu, dk, o);
+    dv += __shfl_xor_sync(0xffffffffu, dv, o);
+  }
+  if (lane == 0) {
+    if (a.dev) {
+      a.dev[((size_t)j * a.n_layers + l) * 2 + 0] = dk;
+      a.dev[((size_t)j * a.n_layers + l) * 2 + 1] = dv;
+    }
+    if (a.sel_scores && l == a.sel_layer)
+      a.sel_scores[j] = a.sel_comp == 0 ? dk : (a.sel_comp == 1 ? dv : dk + dv);
+  }
+}
+}  // namespace
+
+int kv_deviation(const DeviationArgs& a, cudaStream_t stream) {
+  if (a.n_rows <= 0 || a.n_layers <= 0) return 0;
+  if (a.width % 8 != 0) return -1;
+  const long warps = (long)a.n_rows * a.n_layers;
+  kv_deviation_kernel<<<(unsigned)((warps + DV_WARPS - 1) / DV_WARPS), DV_WARPS * 32, 0, stream>>>(a);
+  return 1;
+}
+
 }  // namespace fragk

@@ -26,6 +26,8 @@ __all__ = ["ModelCfg", "ChunkId", "Engine", "ChunkKVStore", "Result", "preset", 
 
 ISOLATED, FUSED = 0, 1
 TIER_GPU, TIER_CPU, TIER_DISK, TIER_PEER = 0, 1, 2, 3
+SELECTORS = {"query_guided": 0, "cacheblend": 1}
+DEV_COMPONENTS = {"k": 0, "v": 1, "kv": 2}
 WEIGHT_IDS = {"emb": 0, "lm_head": 1, "wq": 2, "wk": 3, "wv": 4, "wo": 5, "w_gate": 6, "w_up": 7,
               "w_down": 8, "attn_norm": 9, "ffn_norm": 10, "final_norm": 11}
 
@@ -142,7 +144,12 @@ class Engine:
                   ratio: float, result: "Result", system: Sequence[int] = (), *, raw_scores: bool = False,
                   all_logits: bool = False, timing: bool = False, inject_crit: Sequence[int] | None = None,
                   logits_on_device: bool = False, stream=None, question_dev_ptr: int | None = None,
-                  n_question: int | None = None) -> "Result":
+                  n_question: int | None = None, selector: str = "query_guided", deviation_layer: int = 2,
+                  deviation_component: str = "k") -> "Result":
+        """One request of the online reprocessing stage.
+        selector: "query_guided" (FusionRAG, SPEC.md:426) or "cacheblend"
+        (layer-`deviation_layer` KV deviation; component "k", "v"
+        or "kv")."""
         s = _i32(system)
         ids = (ChunkId * max(len(chunk_ids), 1))(*chunk_ids)
         opts = ReprocessOpts()
@@ -150,6 +157,9 @@ class Engine:
         opts.all_logits = int(all_logits)
         opts.timing = int(timing)
         opts.logits_on_device = int(logits_on_device)
+        opts.selector = SELECTORS[selector]
+        opts.deviation_layer = int(deviation_layer)
+        opts.deviation_component = DEV_COMPONENTS[deviation_component]
         inj = None
         if inject_crit is not None:
             inj = _i32(inject_crit)
@@ -173,6 +183,19 @@ class Engine:
         check(lib.frag_full_prefill(self._h, _i32p(s), len(s), _i32p(t), len(t), C.byref(opts), _stream_ptr(stream),
                                     result._h))
         return result
+
+    def kv_deviation(self, store: "ChunkKVStore", chunk_ids: Sequence[ChunkId], result: "Result",
+                     system: Sequence[int] = (), n_layers: int = 2, *, stream=None) -> np.ndarray:
+        """kv_deviation (Eq. 7): [N][n_layers][2] fp32 sums of
+        squared K / V differences between Full Attention and Full Reuse over
+        cat(system, chunks); `result` holds the Full-Reuse cache afterwards."""
+        s = _i32(system)
+        ids = (ChunkId * max(len(chunk_ids), 1))(*chunk_ids)
+        n = sum(store.peek(i).n_tok for i in chunk_ids)
+        out = np.empty((max(n, 1), n_layers, 2), np.float32)
+        check(lib.frag_kv_deviation(self._h, store._h, _i32p(s), len(s), ids, len(chunk_ids), int(n_layers),
+                                    _stream_ptr(stream), result._h, C.c_void_p(out.ctypes.data)))
+        return out[:n]
 
     def decode(self, result: "Result", max_new_tokens: int, *, stream=None) -> np.ndarray:
         """Greedy decoding continuing the last reprocess / full prefill of
@@ -378,7 +401,7 @@ class Result:
         c = self.engine.cfg
         q = np.empty((nq.value, c.n_heads, c.head_dim), dtype=np.float32)
         s = np.empty(max(n.value, 1), dtype=np.float32)
-        if nq.value:
+        if nq.value and qf.value:  # the cacheblend selector runs no question pass
             memcpy(q.ctypes.data, qf.value, q.nbytes)
         if n.value:
             memcpy(s.ctypes.data, sc.value, n.value * 4)

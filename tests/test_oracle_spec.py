@@ -348,3 +348,50 @@ def test_oracle_decode_equals_prefill_of_extended_prompt():
     lg, _ = m.forward(prompt, list(range(1, T + 1)), list(range(T)), k3, v3, pos3, logit_rows=[T - 1])
     toks = m.greedy_decode(k3, v3, T, lg[0], 4, emulate_bf16=False)
     assert toks[0] == int(np.argmax(lg[0])) and len(toks) == 4
+
+
+# ---------------------------------------------------------------- CacheBlend
+def test_kv_deviation_single_chunk_is_zero(small):
+    # a single retrieved chunk -> Delta ~ 0 everywhere (FR == FA, Eq. 4)
+    rng = np.random.default_rng(20)
+    for S in (0, 3):
+        sys_toks = rng.integers(0, 64, S)
+        recs, skv = _isolated_records(small, sys_toks, [rng.integers(0, 64, 17)])
+        dev = small.kv_deviation(skv, recs, n_layers=2, emulate_bf16=False)
+        assert dev.shape == (17, 2, 2)
+        assert np.max(dev) <= 1e-10
+
+
+def test_kv_deviation_first_layer_zero_second_layer_positive(small):
+    # layer-1 Delta = 0 (embeddings + positions only); SPEC.md:416:
+    # chunk 2 after chunk 1 -> layer-2 Delta strictly positive on chunk-2 tokens,
+    # while chunk 1 (at its native offset) has Delta = 0
+    rng = np.random.default_rng(21)
+    for S in (0, 2):
+        sys_toks = rng.integers(0, 64, S)
+        c1, c2 = rng.integers(0, 64, 9), rng.integers(0, 64, 11)
+        recs, skv = _isolated_records(small, sys_toks, [c1, c2])
+        dev = small.kv_deviation(skv, recs, n_layers=2, emulate_bf16=False)
+        assert np.all(dev[:, 0, 1] == 0.0)  # V of layer 1: same row, same GEMM
+        assert np.max(dev[:, 0, 0]) <= 1e-9  # K of layer 1: shift-rotation rounding only
+        assert np.max(dev[:9, 1, :]) <= 1e-10
+        assert np.all(dev[9:, 1, 0] > 1e-8) and np.all(dev[9:, 1, 1] > 1e-8)
+
+
+def test_select_cacheblend_equals_brute_force_sort():
+    # SPEC.md:421-425, acceptance #6: exact argTopk of the deviation column, lower index on ties
+    rng = np.random.default_rng(22)
+    for t in range(100):
+        N, L = int(rng.integers(1, 300)), int(rng.integers(2, 4))
+        dev = rng.random((N, L, 2))
+        if t % 4 == 0:
+            dev = np.round(dev, 1)  # many ties
+        k = int(rng.integers(0, N + 1))
+        layer, comp = int(rng.integers(1, L + 1)), int(rng.integers(0, 3))
+        sel = O.select_cacheblend(dev, k, layer, comp)
+        col = dev[:, layer - 1, 0] + dev[:, layer - 1, 1] if comp == 2 else dev[:, layer - 1, comp]
+        assert np.array_equal(sel, np.sort(np.argsort(-col, kind="stable")[:k]))
+    dev = np.ones((10, 2, 2))
+    assert O.select_cacheblend(dev, 0).tolist() == []  # r = 0 -> empty
+    assert O.select_cacheblend(dev, 10).tolist() == list(range(10))  # r = 1 -> all chunk tokens
+    assert O.select_cacheblend(dev, 3).tolist() == [0, 1, 2]
