@@ -607,8 +607,11 @@ FRAG_API frag_status frag_kernel_qg_select(const float* q, const void* k, int32_
     need(k_sel >= 0 && k_sel <= n_keys, "k out of range");
     auto s = static_cast<cudaStream_t>(stream);
     const int nblk = (n_keys + 31) / 32;
-    DevBuf pms, rms, tok, ptok;
+    DevBuf pms, rms, tok, ptok, col;
     pms.alloc((size_t)nblk * nq * Hq * sizeof(float2));
+    col.alloc(fragk::score_col_part_elems(nq, Hq, Hkv, n_keys) * sizeof(float));
+    DevBuf qsp;
+    qsp.alloc(fragk::score_q_split_elems(nq, Hq, Hkv, dh) * sizeof(bf16));
     rms.alloc((size_t)nq * Hq * sizeof(float2));
     tok.alloc((size_t)n_keys * sizeof(int));
     ptok.alloc((size_t)(k_sel + 1) * sizeof(int));
@@ -627,6 +630,8 @@ FRAG_API frag_status frag_kernel_qg_select(const float* q, const void* k, int32_
     a.row_ms = rms.as<float2>();
     a.scores = scores_dev;
     a.raw = raw;
+    a.col_part = col.as<float>();
+    a.q_split = qsp.as<bf16>();
     const int n1 = fragk::qg_score(a, s);
     if (n1 < 0) fail(FRAG_E_CONTRACT, "unsupported head_dim");
     fragk::topk_plan(scores_dev, n_keys, k_sel, 0, tok.as<int>(), tok.as<int>(), 0, 0, sel_dev, ptok.as<int>(), s);

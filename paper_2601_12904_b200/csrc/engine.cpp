@@ -865,6 +865,8 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   if (N > 0 && !inject) {
     r->part_ms.ensure((size_t)((N + 31) / 32) * n_q * c.n_heads * sizeof(float2));
     r->row_ms.ensure((size_t)n_q * c.n_heads * sizeof(float2));
+    r->score_col.ensure(fragk::score_col_part_elems(n_q, c.n_heads, c.n_kv_heads, N) * sizeof(float));
+    r->score_q.ensure(fragk::score_q_split_elems(n_q, c.n_heads, c.n_kv_heads, c.head_dim) * sizeof(bf16));
   }
   r->lm_x.ensure((size_t)r->logit_rows * c.d_model * sizeof(bf16));
   r->logits.ensure((size_t)r->logit_rows * c.vocab * sizeof(float));
@@ -908,6 +910,8 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
         a.row_ms = r->row_ms.as<float2>();
         a.scores = r->scores.as<float>();
         a.raw = raw;
+        a.col_part = r->score_col.as<float>();
+        a.q_split = r->score_q.as<bf16>();
         Scoped sc(e->prof, bs, KC_SELECT, 4.0 * n_q * c.n_heads * (double)N * c.head_dim,
                   2.0 * N * (double)c.n_kv_heads * c.head_dim * 2);
         sc.launched(fragk::qg_score(a, bs));

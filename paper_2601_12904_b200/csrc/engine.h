@@ -216,7 +216,7 @@ struct Result {
   int T = 0, S = 0, N = 0, nq = 0, k_sel = 0, M = 0, logit_rows = 0;
   // workspace
   DevBuf h, x, q, attn, act, plan_rows, plan_tok, chunk_tok, q_tok, q_final, scores, part_ms, row_ms, part_o,
-      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok, fr_save, dev;
+      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok, fr_save, dev, score_col, score_q;
   PinnedBuf staging, logits_host;
   // timing
   cudaEvent_t ev[7] = {};

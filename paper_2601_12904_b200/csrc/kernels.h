@@ -116,8 +116,15 @@ struct ScoreArgs {
   float2* row_ms;      // [nq*Hq] (max, 1/Z)
   float* scores;       // [n_keys]
   int raw;             // 1 = raw (unnormalised) attention logits summed (SPEC.md:464 flag)
+  float* col_part;     // [score_col_part_elems] per (kv head, row tile) column partials (tensor path)
+  bf16* q_split;       // [score_q_split_elems] three-term bf16 split of q (tensor path)
 };
 int qg_score(const ScoreArgs& a, cudaStream_t stream);
+// tcgen05 scoring (score_tc.cu): 3-term bf16 split of the fp32 queries
+int qg_score_tc(const ScoreArgs& a, cudaStream_t stream);
+size_t score_col_part_elems(int nq, int Hq, int Hkv, int n_keys);
+size_t score_q_split_elems(int nq, int Hq, int Hkv, int dh);
+int score_combine(const ScoreArgs& a, int nblk, cudaStream_t stream);
 // crit rows (ascending, = key_row0 + j) of the k largest scores, ties to lower j,
 // then the question rows appended. Writes plan_rows[k + nq] and plan_tok.
 int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* chunk_tok, const int* q_tok,

@@ -7,8 +7,10 @@
 // and question keys are excluded, heads are summed, and the
 // budget is a global top-k with lower-index tie-break.
 //
-// fp32 CUDA-core FMAs so scores follow the fp32 oracle to summation-order
-// rounding; no atomics, so the result is bit-deterministic run to run.
+// The scoring passes run on the tensor cores (score_tc.cu: exact three-term
+// bf16 split of the fp32 queries); this file holds the row-statistics merge,
+// the top-k plan (K10), the kv_deviation kernel of the CacheBlend selector and
+// the greedy-decode argmax. No atomics on values: bit-deterministic.
 #include <cfloat>
 
 #include "kernels.h"
@@ -18,152 +20,7 @@ namespace fragk {
 
 namespace {
 
-constexpr int SC_KEYS = 64;     // keys per CTA
-constexpr int SC_ROWS = 128;    // query rows per shared-memory tile
-constexpr int SC_THREADS = 256;
-constexpr int SC_PAD = 4;       // row padding (floats): conflict-free 128-bit shared loads
-
-template <int DH>
-constexpr size_t score_smem() { return (size_t)(SC_KEYS + SC_ROWS) * (DH + SC_PAD) * sizeof(float); }
-
-// Register-tiled fp32 CUDA-core scoring: a CTA owns 64 keys and walks the kv
-// heads and their query rows; each thread computes an 8-row x 4-key block
-// with 128-bit shared-memory operand loads (12 loads per 128 FMAs). Every dot
-// product is a sequential fp32 FMA chain over dh, exactly as in the fp32
-// oracle restatement, and all reductions run in a fixed order (no atomics), so
-// scores are bit-deterministic.
-// MODE 1: per-(block,row) (max, sumexp) of scaled logits.
-// MODE 2: column sums of softmax probabilities (row_ms = (max, 1/Z)).
-// MODE 3: column sums of raw scaled logits.
-template <int MODE, int DH>
-__global__ void __launch_bounds__(SC_THREADS) score_kernel(const ScoreArgs a) {
-  constexpr int LD = DH + SC_PAD;
-  extern __shared__ float4 sc_smem4[];
-  float* sk = reinterpret_cast<float*>(sc_smem4);  // [SC_KEYS][LD]
-  float* sq = sk + SC_KEYS * LD;                   // [SC_ROWS][LD]
-  __shared__ float colsum[SC_THREADS / 32][SC_KEYS];
-  const int blk = blockIdx.x;
-  const int key0 = blk * SC_KEYS;
-  const int nrows_tot = a.nq * a.Hq;
-  const int G = a.Hq / a.Hkv;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // thread -> rows rg*8 .. rg*8+7 of the row tile, keys kg + 16*j (j < 4)
-  const int rg = tid >> 4, kg = tid & 15;
-  float csum[4] = {0.f, 0.f, 0.f, 0.f};
-
-  for (int hk = 0; hk < a.Hkv; ++hk) {
-    __syncthreads();
-    for (int idx = tid; idx < SC_KEYS * (DH / 8); idx += SC_THREADS) {
-      const int r = idx / (DH / 8), c8 = (idx % (DH / 8)) * 8;
-      const int j = key0 + r;
-      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (j < a.n_keys) {
-        const uint4 u = *reinterpret_cast<const uint4*>(a.k + ((size_t)(a.key_row0 + j) * a.Hkv + hk) * DH + c8);
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          v[2 * e] = __uint_as_float(w[e] << 16);
-          v[2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
-        }
-      }
-      float4* dst = reinterpret_cast<float4*>(sk + r * LD + c8);
-      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
-      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
-    }
-    const int nrows = a.nq * G;  // rows of this kv group: (t, g) -> row t*Hq + hk*G + g
-    for (int r0 = 0; r0 < nrows; r0 += SC_ROWS) {
-      __syncthreads();
-      for (int idx = tid; idx < SC_ROWS * (DH / 4); idx += SC_THREADS) {
-        const int r = idx / (DH / 4), c4 = (idx % (DH / 4)) * 4;
-        const int rr = r0 + r;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (rr < nrows) {
-          const int t = rr / G, g = rr % G;
-          v = *reinterpret_cast<const float4*>(a.q + ((size_t)t * a.Hq + hk * G + g) * DH + c4);
-        }
-        *reinterpret_cast<float4*>(sq + r * LD + c4) = v;
-      }
-      __syncthreads();
-      // both 8-row groups of this warp past the end (warp-uniform: the shuffles
-      // below need the full warp; no barrier follows inside this iteration)
-      if (r0 + (rg & ~1) * 8 >= nrows) continue;
-      float acc[8][4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-#pragma unroll 2
-      for (int c = 0; c < DH; c += 4) {
-        float4 kv[4], qv[8];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) kv[j] = *reinterpret_cast<const float4*>(sk + (kg + 16 * j) * LD + c);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) qv[i] = *reinterpret_cast<const float4*>(sq + (rg * 8 + i) * LD + c);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float t = fmaf(qv[i].x, kv[j].x, acc[i][j]);
-            t = fmaf(qv[i].y, kv[j].y, t);
-            t = fmaf(qv[i].z, kv[j].z, t);
-            acc[i][j] = fmaf(qv[i].w, kv[j].w, t);
-          }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int rr = r0 + rg * 8 + i;
-        const bool rvalid = rr < nrows;
-        const int grow = rvalid ? (rr / G) * a.Hq + hk * G + rr % G : 0;
-        if constexpr (MODE == 1) {
-          // local (max, sumexp) over this CTA's 64 keys for row grow: the 16 kg lanes
-          float sv[4];
-          float mx = -INFINITY;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const bool kvalid = key0 + kg + 16 * j < a.n_keys;
-            sv[j] = kvalid ? acc[i][j] * a.scale : -INFINITY;
-            mx = fmaxf(mx, sv[j]);
-          }
-#pragma unroll
-          for (int o = 1; o < 16; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          float z = 0.f;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) z += (sv[j] == -INFINITY) ? 0.f : __expf(sv[j] - mx);
-#pragma unroll
-          for (int o = 1; o < 16; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-          if (kg == 0 && rvalid) a.part_ms[(size_t)blk * nrows_tot + grow] = make_float2(mx, z);
-        } else if constexpr (MODE == 2) {
-          if (rvalid) {
-            const float2 ms = a.row_ms[grow];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) csum[j] += __expf(acc[i][j] * a.scale - ms.x) * ms.y;
-          }
-        } else {
-          if (rvalid) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) csum[j] += acc[i][j] * a.scale;
-          }
-        }
-      }
-    }
-  }
-  if constexpr (MODE != 1) {
-    // deterministic column reduction: the two row groups of a warp, then the 8 warps in order
-#pragma unroll
-    for (int j = 0; j < 4; ++j) csum[j] += __shfl_xor_sync(0xffffffffu, csum[j], 16);
-    if (lane < 16)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) colsum[warp][kg + 16 * j] = csum[j];
-    __syncthreads();
-    if (tid < SC_KEYS) {
-      float s = 0.f;
-      for (int w = 0; w < SC_THREADS / 32; ++w) s += colsum[w][tid];
-      const int j = key0 + tid;
-      if (j < a.n_keys) a.scores[j] = s;
-    }
-  }
-}
-
+// (max, sumexp) partials of the key groups -> (max, 1/Z) per (token, head) row
 __global__ void score_combine_kernel(const ScoreArgs a, int nblk) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   const int nrows = a.nq * a.Hq;
@@ -186,116 +43,164 @@ __device__ __forceinline__ uint32_t fkey(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// Block-wide exclusive scan of one int per thread (1024 threads).
-__device__ int block_excl_scan(int v, int* sh, int* total) {
-  const int lane = lane_id(), w = warp_id();
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) sh[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int s = sh[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    sh[lane] = s;  // inclusive warp totals
-  }
-  __syncthreads();
-  const int base = w > 0 ? sh[w - 1] : 0;
-  if (total) *total = sh[31];
-  __syncthreads();
-  return base + x - v;
-}
-
+// Single-CTA top-k select + QIndexPlan. Each of the 32 warps owns a contiguous
+// segment of the chunk keys and walks it 32 keys at a time (coalesced), so
+// index order is kept with ballots instead of per-thread serial ranges:
+//   1. 4 x 8-bit radix passes over order-preserving keys find the k-th largest
+//      key tau and how many keys equal to tau are still needed (histogram with
+//      leader-aggregated shared atomics: one request's scores share their
+//      leading key bytes; match.any measured far slower);
+//   2. per-warp counts of keys > tau and == tau, one warp-scan over the 32
+//      warps -> each warp's output offset and its share of the tau ties (the
+//      lowest indices win, SPEC.md:391 / SPEC.md:454);
+//   3. ballot compaction in index order: plan_rows / plan_tok of the critical
+//      rows, then the question rows.
+template <bool STAGED>
 __global__ void __launch_bounds__(TK_THREADS) topk_plan_kernel(const float* __restrict__ scores, int n, int k,
                                                                 int key_row0, const int* __restrict__ chunk_tok,
                                                                 const int* __restrict__ q_tok, int nq, int q_row0,
                                                                 int* __restrict__ plan_rows,
                                                                 int* __restrict__ plan_tok) {
+  constexpr int NW = TK_THREADS / 32;
   __shared__ int hist[256];
-  __shared__ int sh[32];
+  __shared__ int w_gt[NW], w_eq[NW];
   __shared__ uint32_t s_prefix;
   __shared__ int s_remaining;
-  const int tid = threadIdx.x;
-  const int per = (n + TK_THREADS - 1) / TK_THREADS;
-  const int lo = tid * per, hi = min(lo + per, n);
+  extern __shared__ uint32_t s_keys[];  // order-preserving keys of all scores (when they fit)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int seg = ((n + NW * 32 - 1) / (NW * 32)) * 32;  // per-warp segment, whole rounds
+  const int w_lo = warp * seg, w_hi = min(n, w_lo + seg);
+  if (STAGED) {
+#pragma unroll 4
+    for (int i = tid; i < n; i += TK_THREADS) s_keys[i] = fkey(scores[i]);
+    __syncthreads();
+  }
+  auto key_at = [&](int i) { return STAGED ? s_keys[i] : fkey(scores[i]); };
+  const bool all = k >= n;
 
   uint32_t tau = 0xFFFFFFFFu;
   int need_eq = 0;
-  if (k > 0 && k < n) {
+  if (k > 0 && !all) {
     if (tid == 0) {
       s_prefix = 0;
       s_remaining = k;
     }
     uint32_t mask = 0;
     for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int b = tid; b < 256; b += TK_THREADS) hist[b] = 0;
+      if (tid < 256) hist[tid] = 0;
       __syncthreads();
       const uint32_t prefix = s_prefix;
-      for (int i = lo; i < hi; ++i) {
-        const uint32_t key = fkey(scores[i]);
-        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+      for (int base = w_lo; base < w_hi; base += 32) {
+        const int i = base + lane;
+        const uint32_t key = i < w_hi ? key_at(i) : 0u;
+        const bool hit = i < w_hi && (key & mask) == prefix;
+        const int bin = hit ? (int)((key >> shift) & 255) : -1;
+        // the first hit lane's bin takes one aggregated atomic (most keys of a
+        // request share their leading bytes); the other lanes add their own
+        const unsigned hits = __ballot_sync(0xffffffffu, hit);
+        const int b0 = __shfl_sync(0xffffffffu, bin, hits ? __ffs(hits) - 1 : 0);
+        const unsigned same = __ballot_sync(0xffffffffu, hit && bin == b0);
+        if (hit) {
+          if (bin != b0)
+            atomicAdd(&hist[bin], 1);
+          else if (lane == __ffs(same) - 1)
+            atomicAdd(&hist[bin], __popc(same));
+        }
       }
       __syncthreads();
-      if (tid == 0) {
-        int rem = s_remaining, cum = 0, b = 255;
-        for (; b > 0; --b) {
-          if (cum + hist[b] >= rem) break;
-          cum += hist[b];
+      if (warp == 0) {
+        // the bin holding the rem-th largest key: lane l scans bins 255-8l ..
+        // 248-8l (descending); a warp scan gives each lane the count above them
+        const int rem = s_remaining;
+        int cnt[8], tot = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) tot += (cnt[e] = hist[255 - (lane * 8 + e)]);
+        int incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
         }
-        s_remaining = rem - cum;
-        s_prefix = prefix | ((uint32_t)b << shift);
+        const int excl = incl - tot;
+        const unsigned hit = __ballot_sync(0xffffffffu, excl < rem && rem <= incl);
+        const int src = hit ? __ffs(hit) - 1 : 31;
+        if (lane == src) {
+          int cum = excl, b = 255 - lane * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            b = 255 - (lane * 8 + e);
+            if (cum + cnt[e] >= rem || b == 0) break;
+            cum += cnt[e];
+          }
+          s_remaining = rem - cum;
+          s_prefix = prefix | ((uint32_t)b << shift);
+        }
       }
       mask |= 255u << shift;
       __syncthreads();
     }
     tau = s_prefix;
     need_eq = s_remaining;
-  } else if (k >= n) {
-    tau = 0;
-    need_eq = n;  // everything selected (all keys >= 0 in key space)
   }
-  // pass: count > tau and == tau in my range
+  // per-warp counts of keys > tau and == tau
   int n_gt = 0, n_eq = 0;
-  if (k > 0) {
-    for (int i = lo; i < hi; ++i) {
-      const uint32_t key = fkey(scores[i]);
-      if (k >= n) {
-        ++n_gt;
-      } else {
-        n_gt += key > tau;
-        n_eq += key == tau;
-      }
+  if (k > 0 && !all) {
+    for (int base = w_lo; base < w_hi; base += 32) {
+      const int i = base + lane;
+      const uint32_t key = i < w_hi ? key_at(i) : 0u;
+      n_gt += __popc(__ballot_sync(0xffffffffu, i < w_hi && key > tau));
+      n_eq += __popc(__ballot_sync(0xffffffffu, i < w_hi && key == tau));
     }
+  } else if (all) {
+    n_gt = max(w_hi - w_lo, 0);
   }
-  const int eq_before = block_excl_scan(n_eq, sh, nullptr);
-  int take_eq = (k >= n) ? 0 : min(max(need_eq - eq_before, 0), n_eq);
-  const int my_sel = n_gt + take_eq;
-  int total = 0;
-  int out = block_excl_scan(my_sel, sh, &total);
+  if (lane == 0) w_gt[warp] = n_gt, w_eq[warp] = n_eq;
+  __syncthreads();
+  // every warp scans the 32 warp totals: ties go to the lowest indices
+  int take_eq = 0, out = 0;
+  {
+    const int g = w_gt[lane], e = w_eq[lane];
+    int eq_in = e;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, eq_in, o);
+      if (lane >= o) eq_in += y;
+    }
+    const int take_l = min(max(need_eq - (eq_in - e), 0), e);
+    const int sel_l = g + take_l;
+    int sel_in = sel_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, sel_in, o);
+      if (lane >= o) sel_in += y;
+    }
+    take_eq = __shfl_sync(0xffffffffu, take_l, warp);
+    out = __shfl_sync(0xffffffffu, sel_in - sel_l, warp);
+  }
+  // ballot compaction in index order
   if (k > 0) {
     int eq_seen = 0;
-    for (int i = lo; i < hi; ++i) {
+    for (int base = w_lo; base < w_hi; base += 32) {
+      const int i = base + lane;
+      const bool valid = i < w_hi;
       bool sel;
-      if (k >= n) {
-        sel = true;
+      if (all) {
+        sel = valid;
       } else {
-        const uint32_t key = fkey(scores[i]);
-        if (key > tau) sel = true;
-        else if (key == tau) sel = (eq_seen++ < take_eq);
-        else sel = false;
+        const uint32_t key = valid ? key_at(i) : 0u;
+        const bool eq = valid && key == tau;
+        const unsigned eqm = __ballot_sync(0xffffffffu, eq);
+        sel = (valid && key > tau) || (eq && eq_seen + __popc(eqm & lt) < take_eq);
+        eq_seen += __popc(eqm);
       }
+      const unsigned sm = __ballot_sync(0xffffffffu, sel);
       if (sel) {
-        plan_rows[out] = key_row0 + i;
-        plan_tok[out] = chunk_tok[i];
-        ++out;
+        const int o = out + __popc(sm & lt);
+        plan_rows[o] = key_row0 + i;
+        plan_tok[o] = chunk_tok[i];
       }
+      out += __popc(sm);
     }
   }
   // question rows follow the critical rows (they are the last positions)
@@ -307,35 +212,24 @@ __global__ void __launch_bounds__(TK_THREADS) topk_plan_kernel(const float* __re
 
 }  // namespace
 
-template <int DH>
-int qg_score_dh(const ScoreArgs& a, int nblk, cudaStream_t stream) {
-  constexpr int SM = (int)score_smem<DH>();
-  smem_attr_once(score_kernel<1, DH>, SM);
-  smem_attr_once(score_kernel<2, DH>, SM);
-  smem_attr_once(score_kernel<3, DH>, SM);
-  if (!a.raw) {
-    score_kernel<1, DH><<<nblk, SC_THREADS, SM, stream>>>(a);
-    score_combine_kernel<<<(a.nq * a.Hq + 255) / 256, 256, 0, stream>>>(a, nblk);
-    score_kernel<2, DH><<<nblk, SC_THREADS, SM, stream>>>(a);
-    return 3;
-  }
-  score_kernel<3, DH><<<nblk, SC_THREADS, SM, stream>>>(a);
+int score_combine(const ScoreArgs& a, int nblk, cudaStream_t stream) {
+  score_combine_kernel<<<(a.nq * a.Hq + 255) / 256, 256, 0, stream>>>(a, nblk);
   return 1;
 }
 
-int qg_score(const ScoreArgs& a, cudaStream_t stream) {
-  const int nblk = (a.n_keys + SC_KEYS - 1) / SC_KEYS;
-  if (nblk <= 0) return 0;
-  if (a.Hq % a.Hkv != 0) return -1;
-  if (a.dh == 128) return qg_score_dh<128>(a, nblk, stream);
-  if (a.dh == 64) return qg_score_dh<64>(a, nblk, stream);
-  return -1;
-}
+int qg_score(const ScoreArgs& a, cudaStream_t stream) { return qg_score_tc(a, stream); }
 
 int topk_plan(const float* scores, int n_keys, int k, int key_row0, const int* chunk_tok, const int* q_tok, int nq,
               int q_row0, int* plan_rows, int* plan_tok, cudaStream_t stream) {
-  topk_plan_kernel<<<1, TK_THREADS, 0, stream>>>(scores, n_keys, k, key_row0, chunk_tok, q_tok, nq, q_row0,
-                                                 plan_rows, plan_tok);
+  const int smem = n_keys * (int)sizeof(uint32_t);
+  if (smem <= 200 * 1024) {
+    smem_attr_once(topk_plan_kernel<true>, 200 * 1024);
+    topk_plan_kernel<true><<<1, TK_THREADS, smem, stream>>>(scores, n_keys, k, key_row0, chunk_tok, q_tok, nq,
+                                                            q_row0, plan_rows, plan_tok);
+  } else {  // > 51200 chunk tokens: every pass reads the scores from L2
+    topk_plan_kernel<false><<<1, TK_THREADS, 0, stream>>>(scores, n_keys, k, key_row0, chunk_tok, q_tok, nq,
+                                                          q_row0, plan_rows, plan_tok);
+  }
   return 1;
 }
 

@@ -222,3 +222,53 @@ def test_gemm_pair_swiglu_partial_tile(cuda, bn):
     torch.cuda.synchronize()
     ref = torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T)
     assert (out.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("nq,Hq,Hkv,dh,N,raw", [(32, 32, 8, 128, 16384, 0), (64, 32, 8, 128, 3000, 0),
+                                               (5, 4, 2, 64, 1000, 0), (32, 32, 8, 128, 2050, 1),
+                                               (1, 8, 8, 128, 129, 0), (2, 8, 2, 64, 60000, 0)])
+def test_qg_score_tcgen05_vs_fp64(cuda, nq, Hq, Hkv, dh, N, raw):
+    """K9 on the tensor cores (3-term bf16 split of the fp32 queries) against
+    the fp64 materialise + column-sum oracle; K10 against the
+    stable sort up to an epsilon window at the k-th score."""
+    import torch
+    from oracle import oracle as O
+    g = torch.Generator(device="cuda").manual_seed(N + nq)
+    q = (torch.randn(nq, Hq, dh, device=cuda, generator=g) * 2.0).float()
+    k = torch.randn(N, Hkv, dh, device=cuda, generator=g).to(torch.bfloat16)
+    k_sel = int(0.15 * N + 0.5)
+    scores = torch.empty(N, device=cuda, dtype=torch.float32)
+    sel = torch.empty(max(k_sel, 1), device=cuda, dtype=torch.int32)
+    L = _lib()
+    L.check(L.lib.frag_kernel_qg_select(q.data_ptr(), k.data_ptr(), nq, Hq, Hkv, dh, N, k_sel, raw,
+                                        scores.data_ptr(), sel.data_ptr(), None))
+    ref, ref_sel = O.select(q.cpu().numpy(), k.float().cpu().numpy(), k_sel, raw=bool(raw))
+    got = scores.cpu().numpy().astype(np.float64)
+    tol = 1e-4 * np.abs(ref).max() if raw else 0.0
+    assert np.allclose(got, ref, rtol=1e-4, atol=max(tol, 1e-7)), np.abs(got - ref).max()
+    gs = sel[:k_sel].cpu().numpy()
+    tau = np.sort(ref)[::-1][k_sel - 1]
+    eps = 1e-4 * np.abs(ref).mean()
+    diff = set(gs.tolist()) ^ set(ref_sel.tolist())
+    assert all(abs(ref[j] - tau) <= eps for j in diff)
+    # bit-deterministic (no atomics)
+    s2 = torch.empty_like(scores)
+    L.check(L.lib.frag_kernel_qg_select(q.data_ptr(), k.data_ptr(), nq, Hq, Hkv, dh, N, k_sel, raw,
+                                        s2.data_ptr(), sel.data_ptr(), None))
+    assert torch.equal(scores, s2)
+
+
+@pytest.mark.parametrize("N,k", [(16384, 2458), (3000, 3000), (1000, 0), (777, 1), (60000, 9000)])
+def test_topk_ties_go_to_lower_index(cuda, N, k):
+    """All scores tie (zero queries -> uniform softmax): the k lowest chunk
+    indices are selected."""
+    import torch
+    q = torch.zeros(4, 8, 64, device=cuda, dtype=torch.float32)
+    kk = torch.randn(N, 2, 64, device=cuda).to(torch.bfloat16)
+    scores = torch.empty(N, device=cuda, dtype=torch.float32)
+    sel = torch.full((max(k, 1),), -1, device=cuda, dtype=torch.int32)
+    L = _lib()
+    L.check(L.lib.frag_kernel_qg_select(q.data_ptr(), kk.data_ptr(), 4, 8, 2, 64, N, k, 0, scores.data_ptr(),
+                                        sel.data_ptr(), None))
+    assert torch.all(scores == scores[0])
+    assert sel[:k].cpu().tolist() == list(range(k))
