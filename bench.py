@@ -79,7 +79,8 @@ def parse():
     p.add_argument("--full-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-layers", type=int, default=1)
-    p.add_argument("--sweep", default="", help="comma list of extra ratios to time (e.g. 0,0.05,0.3)")
+    p.add_argument("--sweep", default="0,0.05,0.3,1.0",
+                   help="comma list of extra ratios to time (BASELINE.json configs[2]; '' to skip)")
     p.add_argument("--partition", action="store_true",
                    help="chunk-partitioned store: each chunk's record lives on rank hash(id) mod N only and "
                         "the other ranks read it over NVLink inside K1 (SURVEY.md §8(e))")
@@ -374,7 +375,8 @@ def run_ours(args, rank, world, local_rank):
 
     sweep = {}
     for r in [float(x) for x in args.sweep.split(",") if x.strip()]:
-        step_dev(1, r=r)
+        step_dev(1, r=r)  # first sighting of this request shape: eager
+        step_dev(1, r=r)  # second: graph capture; the timed requests replay it
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for i in range(2):

@@ -215,6 +215,31 @@ FRAG_API frag_status frag_store_attach_peer(frag_store* local, frag_store* remot
 FRAG_API frag_status frag_store_export(frag_store* st, const frag_chunk_id* id, frag_peer_record* out);
 FRAG_API frag_status frag_store_import(frag_store* st, const frag_peer_record* rec, const int32_t* tokens,
                                        int32_t n_tok, int32_t overwrite);
+/* alternative_path_match (§4.1 "progressive
+ * backtracking"): a per-store prefix index maps PrefixKey = rolling 128-bit
+ * hash over (system-prompt id, ordered chunk ids) to the
+ * last chunk of that path. frag_store_register_prefix records that `path`
+ * (n >= 1 chunk ids, the record of path[n-1] computed under the preceding
+ * ones) is cached; frag_preprocess_isolated registers (sys, [chunk]) itself.
+ * frag_store_match walks the context: chunk i matches via PREFIX when the key
+ * of (sys, context[0..i]) is registered, else the earliest remaining preceding
+ * chunk is dropped until a key hits (ALT_PATH); a chunk whose record exists
+ * but no path hits still matches ALT_PATH on its own (alternative-path
+ * completeness). Unmatched chunks are simply absent from the
+ * output (no error). sys_id: frag_hash_tokens of the system prompt (or null
+ * for none). out must hold n entries; *n_out = matches written, in context
+ * order. */
+enum { FRAG_MATCH_PREFIX = 0, FRAG_MATCH_ALT_PATH = 1 };
+typedef struct {
+  frag_chunk_id id;
+  int32_t matched_via; /* FRAG_MATCH_PREFIX or FRAG_MATCH_ALT_PATH */
+  int32_t position;    /* index of the chunk in the context */
+  int32_t path_start;  /* first context index of the path that hit (== position for the chunk alone) */
+} frag_match;
+FRAG_API frag_status frag_store_register_prefix(frag_store* st, const frag_chunk_id* sys_id, const frag_chunk_id* path,
+                                                int32_t n);
+FRAG_API frag_status frag_store_match(frag_store* st, const frag_chunk_id* sys_id, const frag_chunk_id* context,
+                                      int32_t n, frag_match* out, int32_t* n_out);
 FRAG_API int64_t frag_store_count(const frag_store* st);
 FRAG_API uint64_t frag_store_bytes_used(const frag_store* st);
 

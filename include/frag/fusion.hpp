@@ -96,6 +96,23 @@ class ChunkStore {
     return frag_chunk_owner(&c, n_owners);
   }
   void attach_peer(ChunkStore& remote) { check(frag_store_attach_peer(h_, remote.h_)); }
+  // alternative_path_match: matches in context order; unmatched chunks absent
+  void register_prefix(std::span<const ChunkId> path, const ChunkId* sys_id = nullptr) {
+    std::vector<frag_chunk_id> p;
+    for (const auto& c : path) p.push_back(to_c(c));
+    const frag_chunk_id s = sys_id ? to_c(*sys_id) : frag_chunk_id{};
+    check(frag_store_register_prefix(h_, sys_id ? &s : nullptr, p.data(), static_cast<int32_t>(p.size())));
+  }
+  std::vector<frag_match> match(std::span<const ChunkId> context, const ChunkId* sys_id = nullptr) {
+    std::vector<frag_chunk_id> c;
+    for (const auto& x : context) c.push_back(to_c(x));
+    std::vector<frag_match> out(c.size());
+    int32_t n = 0;
+    const frag_chunk_id s = sys_id ? to_c(*sys_id) : frag_chunk_id{};
+    check(frag_store_match(h_, sys_id ? &s : nullptr, c.data(), static_cast<int32_t>(c.size()), out.data(), &n));
+    out.resize(n);
+    return out;
+  }
   frag_peer_record export_record(const ChunkId& id) {
     const frag_chunk_id c = to_c(id);
     frag_peer_record pr{};

@@ -338,3 +338,27 @@ def build_equivalent_mask(q_idx, is_new, T):
     m = np.empty((len(qi), W), np.uint8)
     lib.orc_build_equivalent_mask(_p(qi), _p(nw), len(qi), T, _p(m))
     return m
+
+
+# ------------------------------------------------------------ alternative_path_match
+def alt_path_match(cached_paths, records, context, sys_id=None):
+    """Restatement of alternative_path_match (design decision
+    SPEC.md:317; §4.1 "progressive backtracking"): cached_paths is a
+    set of (sys_id, tuple of chunk ids) whose last chunk's record was computed
+    under the preceding ones; records the set of chunk ids holding a record.
+    For each context chunk with a record: PREFIX if (sys, context[:i+1]) is
+    cached, else drop the earliest remaining preceding chunk until a cached
+    path ending at the chunk is found (ALT_PATH); a chunk with a record but no
+    cached path still matches ALT_PATH on its own (completeness).
+    Returns [(chunk, via, position, path_start)]."""
+    out = []
+    for i, c in enumerate(context):
+        if c not in records:
+            continue
+        hit = None
+        for start in range(0, i + 1):
+            if (sys_id, tuple(context[start:i + 1])) in cached_paths:
+                hit = start
+                break
+        out.append((c, "PREFIX" if hit == 0 else "ALT_PATH", i, i if hit is None else hit))
+    return out

@@ -59,6 +59,10 @@ class PeerRecord(C.Structure):
 assert C.sizeof(PeerRecord) == 128
 
 
+class Match(C.Structure):
+    _fields_ = [("id", ChunkId), ("matched_via", C.c_int32), ("position", C.c_int32), ("path_start", C.c_int32)]
+
+
 class ReprocessOpts(C.Structure):
     _fields_ = [("raw_scores", C.c_int32), ("all_logits", C.c_int32), ("timing", C.c_int32),
                 ("inject_crit", C.POINTER(C.c_int32)), ("n_inject", C.c_int32),
@@ -100,6 +104,8 @@ _SIGS = {
     "frag_store_release": (C.c_int, [_P, C.POINTER(ChunkId)]),
     "frag_store_peek": (C.c_int, [_P, C.POINTER(ChunkId), C.POINTER(RecordView)]),
     "frag_store_count": (C.c_int64, [_P]),
+    "frag_store_register_prefix": (C.c_int, [_P, C.POINTER(ChunkId), C.POINTER(ChunkId), C.c_int32]),
+    "frag_store_match": (C.c_int, [_P, C.POINTER(ChunkId), C.POINTER(ChunkId), C.c_int32, C.POINTER(Match), _I32P]),
     "frag_chunk_owner": (C.c_int32, [C.POINTER(ChunkId), C.c_int32]),
     "frag_store_attach_peer": (C.c_int, [_P, _P]),
     "frag_store_export": (C.c_int, [_P, C.POINTER(ChunkId), C.POINTER(PeerRecord)]),

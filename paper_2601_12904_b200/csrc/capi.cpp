@@ -333,6 +333,22 @@ FRAG_API frag_status frag_store_import(frag_store* st, const frag_peer_record* r
   });
 }
 
+FRAG_API frag_status frag_store_register_prefix(frag_store* st, const frag_chunk_id* sys_id, const frag_chunk_id* path,
+                                                int32_t n) {
+  return guard([&] {
+    need(st, "null store");
+    store_register_prefix(st->s, sys_id, path, n);
+  });
+}
+
+FRAG_API frag_status frag_store_match(frag_store* st, const frag_chunk_id* sys_id, const frag_chunk_id* context,
+                                      int32_t n, frag_match* out, int32_t* n_out) {
+  return guard([&] {
+    need(st && out && n_out, "null argument");
+    *n_out = store_match(st->s, sys_id, context, n, out);
+  });
+}
+
 FRAG_API int64_t frag_store_count(const frag_store* st) {
   if (!st) return -1;
   std::shared_lock<std::shared_mutex> g(st->s->mu);

@@ -329,7 +329,9 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
   };
 
-  // split-KV policy: enough CTAs for >= 2 waves, splits of >= 256 keys
+  // split-KV policy, splits of >= 256 keys: very few query blocks (question
+  // pass, decode) fill exactly one wave (the attention CTA takes a whole SM);
+  // otherwise >= 2 waves
   const int G = Hq / Hkv;
   const int tpc = fragk::attn_rows_per_cta() / G;  // tokens per attention CTA
   const int nqb = (M + tpc - 1) / tpc;
@@ -337,7 +339,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
   int n_splits = 1, split_keys = 0;
   const int sms = fragk::num_sms();
   if (ctas < 2L * sms && T > 512) {
-    n_splits = (int)((2L * sms + ctas - 1) / ctas);
+    n_splits = ctas <= sms / 2 ? (int)(sms / ctas) : (int)((2L * sms + ctas - 1) / ctas);
     const int max_splits = (T + 255) / 256;
     if (n_splits > max_splits) n_splits = max_splits;
     if (n_splits > 64) n_splits = 64;  // the combine kernel's limit
@@ -1149,6 +1151,10 @@ void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, co
   store_put(st, id, tokens, n_tok, S + 1, FRAG_VARIANT_ISOLATED, r->k_fused.as<bf16>() + (size_t)S * kvc,
             r->v_fused.as<bf16>() + (size_t)S * kvc, overwrite, (size_t)r->max_tokens * kvc, s);
   check_cuda(cudaStreamSynchronize(s), "preprocess");
+  // cached under context (S, [chunk]) (alternative_path_match index)
+  frag_chunk_id sid;
+  if (n_sys > 0) hash_tokens(sys, n_sys, 0, &sid);
+  store_register_prefix(st, n_sys > 0 ? &sid : nullptr, &id, 1);
   if (id_out) *id_out = id;
 }
 
@@ -1222,6 +1228,14 @@ void preprocess_fused(Engine* e, Store* src, Store* dst, const int32_t* sys, int
             r->k_fused.as<bf16>() + (size_t)X * kvc, r->v_fused.as<bf16>() + (size_t)X * kvc, overwrite,
             (size_t)r->max_tokens * kvc, s);
   check_cuda(cudaStreamSynchronize(s), "preprocess_fused");
+  {  // cached under context (S, [neighbours used..., chunk])
+    std::vector<frag_chunk_id> path;
+    for (Record* rec : recs) path.push_back(rec->id);
+    path.push_back(id);
+    frag_chunk_id sid;
+    if (n_sys > 0) hash_tokens(sys, n_sys, 0, &sid);
+    store_register_prefix(dst, n_sys > 0 ? &sid : nullptr, path.data(), (int)path.size());
+  }
   if (id_out) *id_out = id;
 }
 

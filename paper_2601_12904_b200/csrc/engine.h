@@ -146,6 +146,8 @@ struct Store {
   // same-process stores on other GPUs whose records this store serves on a
   // local miss (frag_store_attach_peer); their pages are read over NVLink
   std::vector<Store*> peers;
+  // alternative_path_match prefix index: PrefixKey(sys, path) -> last chunk of the path
+  std::unordered_map<ChunkKey, ChunkKey, ChunkKeyHash> prefix_index;
   size_t record_bytes(int n_tok) const {
     return (size_t)2 * cfg.layers * n_tok * cfg.n_kv_heads * cfg.head_dim * sizeof(bf16);
   }
@@ -279,6 +281,9 @@ void store_release(Store* st, const frag_chunk_id& id);
 // cross-process CUDA-IPC export/import of record pages
 int32_t chunk_owner(const frag_chunk_id& id, int32_t n);
 void store_attach_peer(Store* local, Store* remote);
+ChunkKey prefix_key(const frag_chunk_id* sys_id, const frag_chunk_id* path, int n);
+void store_register_prefix(Store* st, const frag_chunk_id* sys_id, const frag_chunk_id* path, int n);
+int store_match(Store* st, const frag_chunk_id* sys_id, const frag_chunk_id* ctx, int n, frag_match* out);
 void store_export(Store* st, const frag_chunk_id& id, frag_peer_record* out);
 void store_import(Store* st, const frag_peer_record& pr, const int32_t* tokens, int n_tok, bool overwrite);
 

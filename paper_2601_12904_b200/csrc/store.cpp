@@ -183,6 +183,71 @@ Record::~Record() {
   }
 }
 
+// ---------------------------------------------------------------- alternative_path_match
+// PrefixKey: two splitmix64-mixed lanes seeded by the
+// system-prompt id, folded over the ordered chunk ids, finalised with the
+// path length.
+ChunkKey prefix_key(const frag_chunk_id* sys_id, const frag_chunk_id* path, int n) {
+  ChunkKey s{0x6a09e667f3bcc908ULL, 0xbb67ae8584caa73bULL};
+  if (sys_id) {
+    const ChunkKey k = key_of(*sys_id);
+    s.a ^= k.a;
+    s.b ^= k.b;
+  }
+  uint64_t a = mix64(s.a), b = mix64(s.b + 0x9e3779b97f4a7c15ULL);
+  for (int i = 0; i < n; ++i) {
+    const ChunkKey c = key_of(path[i]);
+    a = mix64(a ^ mix64(c.a + 0x3c6ef372fe94f82bULL * (uint64_t)(i + 1)));
+    b = mix64(b + mix64(c.b ^ 0xa54ff53a5f1d36f1ULL) + (uint64_t)i);
+  }
+  return ChunkKey{mix64(a ^ (uint64_t)n), mix64(b + (uint64_t)n * 0x9e3779b97f4a7c15ULL)};
+}
+
+void store_register_prefix(Store* st, const frag_chunk_id* sys_id, const frag_chunk_id* path, int n) {
+  if (n < 1 || !path) fail(FRAG_E_CONTRACT, "a cached path needs at least one chunk");
+  const ChunkKey pk = prefix_key(sys_id, path, n);
+  std::unique_lock<std::shared_mutex> g(st->mu);
+  st->prefix_index[pk] = key_of(path[n - 1]);
+}
+
+// Progressive backtracking (design decision SPEC.md:317): for
+// context chunk i try the full preceding path, then drop the EARLIEST
+// remaining preceding chunk, down to the chunk alone; a hit must name chunk i
+// and its record must still exist (here or in an attached peer).
+int store_match(Store* st, const frag_chunk_id* sys_id, const frag_chunk_id* ctx, int n, frag_match* out) {
+  if (n < 1 || !ctx) fail(FRAG_E_CONTRACT, "context must be non-empty (SPEC.md:276)");
+  std::vector<Store*> stores{st};
+  {
+    std::shared_lock<std::shared_mutex> g(st->mu);
+    stores.insert(stores.end(), st->peers.begin(), st->peers.end());
+  }
+  auto has_record = [&](const ChunkKey& k) {
+    for (Store* s : stores) {
+      std::shared_lock<std::shared_mutex> g(s->mu);
+      if (s->recs.count(k)) return true;
+    }
+    return false;
+  };
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    const ChunkKey ck = key_of(ctx[i]);
+    if (!has_record(ck)) continue;  // uncached: absent from the result
+    int hit = -1;
+    for (int start = 0; start <= i && hit < 0; ++start) {
+      const ChunkKey pk = prefix_key(sys_id, ctx + start, i - start + 1);
+      std::shared_lock<std::shared_mutex> g(st->mu);
+      auto it = st->prefix_index.find(pk);
+      if (it != st->prefix_index.end() && it->second == ck) hit = start;
+    }
+    out[m].id = ctx[i];
+    out[m].position = i;
+    out[m].path_start = hit >= 0 ? hit : i;
+    out[m].matched_via = hit == 0 ? FRAG_MATCH_PREFIX : FRAG_MATCH_ALT_PATH;
+    ++m;
+  }
+  return m;
+}
+
 // ---------------------------------------------------------------- partitioned store
 int32_t chunk_owner(const frag_chunk_id& id, int32_t n) {
   if (n < 1) fail(FRAG_E_CONTRACT, "n_owners must be >= 1");

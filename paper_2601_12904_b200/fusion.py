@@ -16,8 +16,8 @@ from typing import Iterable, Sequence
 
 import numpy as np
 
-from ._lib import (ChunkId, FkvcHeader, ContractError, CudaError, FormatError, FragError, ModelCfg, OutOfMemory,
-                   PeerRecord, RecordView, ReprocessOpts, StoreError, Timing, check, lib)
+from ._lib import (ChunkId, FkvcHeader, ContractError, CudaError, FormatError, FragError, Match, ModelCfg,
+                   OutOfMemory, PeerRecord, RecordView, ReprocessOpts, StoreError, Timing, check, lib)
 
 __all__ = ["ModelCfg", "ChunkId", "Engine", "ChunkKVStore", "Result", "preset", "hash_tokens",
            "ContractError", "StoreError", "FormatError", "CudaError", "OutOfMemory", "FragError",
@@ -292,6 +292,29 @@ class ChunkKVStore:
         check(lib.frag_store_load(self._h, str(path).encode(), _i32p(t), len(t), int(overwrite),
                                   _stream_ptr(stream), C.byref(cid)))
         return cid
+
+    # ------------------------------------------------ alternative_path_match
+    def register_prefix(self, path: Sequence[ChunkId], system: Sequence[int] | None = None):
+        """Record that path[-1]'s record was computed under (system, path[:-1])."""
+        ids = (ChunkId * max(len(path), 1))(*path)
+        sid = hash_tokens(system) if system else None
+        check(lib.frag_store_register_prefix(self._h, None if sid is None else C.byref(sid), ids, len(path)))
+
+    def match(self, context: Sequence[ChunkId], system: Sequence[int] | None = None) -> list[tuple]:
+        """[(chunk_id, "PREFIX" | "ALT_PATH", position, path_start)] for every
+        context chunk with a record (in context order); others are absent."""
+        n = len(context)
+        ids = (ChunkId * max(n, 1))(*context)
+        out = (Match * max(n, 1))()
+        got = C.c_int32()
+        sid = hash_tokens(system) if system else None
+        check(lib.frag_store_match(self._h, None if sid is None else C.byref(sid), ids, n, out, C.byref(got)))
+        res = []
+        for m in out[:got.value]:
+            cid = ChunkId()
+            C.memmove(C.byref(cid), C.byref(m.id), 16)
+            res.append((cid, "PREFIX" if m.matched_via == 0 else "ALT_PATH", m.position, m.path_start))
+        return res
 
     # ------------------------------------------------ chunk-partitioned store (SURVEY.md §8(e))
     def attach_peer(self, other: "ChunkKVStore"):

@@ -395,3 +395,47 @@ def test_select_cacheblend_equals_brute_force_sort():
     assert O.select_cacheblend(dev, 0).tolist() == []  # r = 0 -> empty
     assert O.select_cacheblend(dev, 10).tolist() == list(range(10))  # r = 1 -> all chunk tokens
     assert O.select_cacheblend(dev, 3).tolist() == [0, 1, 2]
+
+
+# ---------------------------------------------------------------- alternative_path_match
+def test_alt_path_paper_query3():
+    # Query1 caches b under S, Query2 caches a under S; Query3 context [b, a]:
+    # b via PREFIX, a via ALT_PATH (path "system prompt + Chunk a")
+    cached = {("S", ("b",)), ("S", ("a",))}
+    got = O.alt_path_match(cached, {"a", "b"}, ["b", "a"], "S")
+    assert got == [("b", "PREFIX", 0, 0), ("a", "ALT_PATH", 1, 1)]
+    assert O.alt_path_match(cached, {"a", "b"}, ["x", "y"], "S") == []  # uncached context -> empty
+
+
+def test_alt_path_permutations_and_completeness():
+    import itertools
+    # every chunk cached under "S + chunk": every permutation of any subset matches all
+    for N in range(1, 6):
+        chunks = [f"c{i}" for i in range(N)]
+        cached = {("S", (c,)) for c in chunks}
+        for r in range(1, N + 1):
+            for sub in itertools.permutations(chunks, r):
+                got = O.alt_path_match(cached, set(chunks), list(sub), "S")
+                assert [g[0] for g in got] == list(sub)
+    # completeness: a record cached under a longer path still matches anywhere
+    cached = {("S", ("a", "c"))}
+    got = O.alt_path_match(cached, {"a", "c"}, ["b", "c"], "S")
+    assert got == [("c", "ALT_PATH", 1, 1)]
+    assert O.alt_path_match(cached, {"a", "c"}, ["a", "c"], "S")[1] == ("c", "PREFIX", 1, 0)
+
+
+def test_alt_path_hit_rate_dominates_plain_prefix():
+    # alt-path hits >= plain prefix-cache hits on any workload
+    rng = np.random.default_rng(7)
+    chunks = [f"k{i}" for i in range(12)]
+    cached, records = set(), set()
+    alt = plain = 0
+    for _ in range(300):
+        ctx = list(rng.choice(chunks, int(rng.integers(1, 6)), replace=False))
+        got = O.alt_path_match(cached, records, ctx, "S")
+        alt += len(got)
+        plain += sum(1 for g in got if g[1] == "PREFIX")
+        for i, c in enumerate(ctx):  # the query caches its chunks under its own context
+            records.add(c)
+            cached.add(("S", tuple(ctx[:i + 1])))
+    assert alt >= plain and alt > 0
