@@ -29,6 +29,7 @@
 
 #include <cfloat>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const int st = j & 1;
         mbar_wait(&k_full[st], (j >> 1) & 1);
         tc_fence_after();
+        if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256) a.trace[(t * 256 + j) * 4 + 2] = clock64();
         if (elect_one()) {
           const uint64_t q0 = dq + ((t * C::Q_TILE) >> 4);
           const uint64_t k0 = dk + ((st * C::KV_BYTES) >> 4);
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const int st = j & 1;
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
+        if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256) a.trace[(t * 256 + j) * 4 + 3] = clock64();
         if (elect_one()) {
           const uint64_t v0 = dv + ((st * C::KV_BYTES) >> 4);
           const uint32_t d_tmem = tmem + t * C::T_TILE + C::T_O;
@@ -223,6 +226,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const int key0 = k_lo + j * AT_KEYS;
         mbar_wait(&s_full[t], j & 1);
         tc_fence_after();
+        if (a.trace && blockIdx.x == 0 && lane == 0 && (warp & 3) == 0 && j < 256)
+          a.trace[(t * 256 + j) * 4 + 0] = clock64();
         uint32_t s[AT_KEYS];
 #pragma unroll
         for (int cc = 0; cc < AT_KEYS / 32; ++cc)
@@ -291,6 +296,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
+        if (a.trace && blockIdx.x == 0 && lane == 0 && (warp & 3) == 0 && j < 256)
+          a.trace[(t * 256 + j) * 4 + 1] = clock64();
       }
       // ---- epilogue
       if (n_tiles > 0) {
@@ -361,9 +368,29 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
     const char* v = std::getenv("FRAG_ATTN_POLY");
     return v ? std::atoi(v) : kDefaultPoly;
   }();
+  // FRAG_ATTN_TRACE=<file>: tooling only (tools/attn_trace.py) -- clock64
+  // timeline of CTA 0 (S ready / P done per softmax tile, S / PV issue in the
+  // MMA warp) appended to <file> after the launch
+  static const char* trace_path = std::getenv("FRAG_ATTN_TRACE");
+  static unsigned long long* trace_dev = nullptr;
+  AttnArgs at = a;
+  if (trace_path) {
+    if (!trace_dev) cudaMalloc(&trace_dev, 2 * 256 * 4 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_dev, 0, 2 * 256 * 4 * sizeof(unsigned long long), stream);
+    at.trace = trace_dev;
+  }
   auto go = [&](auto kern, int smem) {
     smem_attr_once(kern, smem);
-    launch_pdl(kern, grid, dim3(AT_THREADS), smem, stream, tq, tk, tv, a, G, n_qblocks);
+    launch_pdl(kern, grid, dim3(AT_THREADS), smem, stream, tq, tk, tv, at, G, n_qblocks);
+    if (trace_path) {
+      unsigned long long h[2 * 256 * 4];
+      cudaMemcpyAsync(h, trace_dev, sizeof(h), cudaMemcpyDeviceToHost, stream);
+      cudaStreamSynchronize(stream);
+      if (FILE* f = std::fopen(trace_path, "ab")) {
+        std::fwrite(h, sizeof(h), 1, f);
+        std::fclose(f);
+      }
+    }
   };
   if (a.dh == 128) {
     constexpr int SM = (int)AttCfg<128>::SMEM;

@@ -99,6 +99,7 @@ struct AttnArgs {
   int split_keys;        // keys per split (multiple of 64); <=0: no split
   int n_splits;
   float scale;           // 1/sqrt(dh)
+  unsigned long long* trace = nullptr;  // tooling: clock64 timeline of CTA 0 (FRAG_ATTN_TRACE)
 };
 int sparse_q_attention(const AttnArgs& a, cudaStream_t stream);  // returns launches
 int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream);
