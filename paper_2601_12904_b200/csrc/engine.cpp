@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "engine.h"
 
 namespace fragimpl {
@@ -273,6 +275,10 @@ Result::~Result() {
   for (auto& g : graphs)
     if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
   if (cap_stream) cudaStreamDestroy(cap_stream);
+  if (side) cudaStreamDestroy(side);
+  if (fork_ev) cudaEventDestroy(fork_ev);
+  for (auto& e : layer_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
 }
@@ -308,7 +314,7 @@ void result_init(Result* r, Engine* e, int max_tokens) {
 
 // ---------------------------------------------------------------- run_rows
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
-              int n_logit_rows, int n_layers) {
+              int n_logit_rows, int n_layers, const cudaEvent_t* layer_ready) {
   if (M <= 0) return;
   const auto& c = e->cfg;
   const int L = (n_layers > 0 && n_layers < c.layers) ? n_layers : c.layers;
@@ -381,6 +387,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       sc.launched(fragk::gemm_bf16_tc(x, W.wqkv, M, (int)qkv, d, fragk::EPI_QKV, ep, s));
     }
     if (mode != PASS_FULL && l == L - 1) break;
+    if (layer_ready) check_cuda(cudaStreamWaitEvent(s, layer_ready[l], 0), "wait stitched layer");
     {
       fragk::AttnArgs a{};
       a.q = r->q.as<bf16>();
@@ -530,15 +537,44 @@ StitchPlan stitch_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, cons
   return p;
 }
 
-void stitch_launch(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p) {
+void stitch_launch(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p, int l0 = 0, int l1 = -1) {
   if (p.n_desc == 0) return;
   const auto& c = e->cfg;
-  Scoped sc(e->prof, s, KC_STITCH, 0, p.bytes);
+  if (l1 < 0) l1 = c.layers;
+  Scoped sc(e->prof, s, KC_STITCH, 0, p.bytes * (l1 - l0) / c.layers);
   fragk::rope_shift_assemble(r->stitch_desc.as<fragk::StitchChunk>(), p.n_desc, p.max_rows,
-                             r->stitch_tab.as<float2>(), r->k_fused.as<bf16>(), r->v_fused.as<bf16>(), c.layers,
-                             r->max_tokens, c.n_kv_heads, c.head_dim, s);
+                             r->stitch_tab.as<float2>(), r->k_fused.as<bf16>(), r->v_fused.as<bf16>(), l1 - l0,
+                             r->max_tokens, c.n_kv_heads, c.head_dim, s, l0);
   sc.launched(1);
   peek("stitch");
+}
+
+// K1 layer by layer on the result's side stream, forked from `s`; layer l's
+// completion is r->layer_ev[l]. The question pass (on `s`) waits for layer l
+// only before its layer-l attention, so the HBM-bound stitch streams under the
+// latency-bound M = |Q| weight stream instead of in front of it.
+bool stitch_overlap_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("FRAG_STITCH_OVERLAP");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+void stitch_fork(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p) {
+  const int L = e->cfg.layers;
+  if (!r->side) check_cuda(cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking), "side stream");
+  if (!r->fork_ev) check_cuda(cudaEventCreateWithFlags(&r->fork_ev, cudaEventDisableTiming), "fork event");
+  while ((int)r->layer_ev.size() < L) {
+    cudaEvent_t ev;
+    check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "layer event");
+    r->layer_ev.push_back(ev);
+  }
+  check_cuda(cudaEventRecord(r->fork_ev, s), "fork");
+  check_cuda(cudaStreamWaitEvent(r->side, r->fork_ev, 0), "fork wait");
+  for (int l = 0; l < L; ++l) {
+    stitch_launch(e, r, r->side, p, l, l + 1);
+    check_cuda(cudaEventRecord(r->layer_ev[l], r->side), "layer stitched");
+  }
 }
 
 void stitch(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys, const std::vector<Record*>& recs,
@@ -875,12 +911,20 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   if (!r->logits_on_device) r->logits_host.ensure((size_t)r->logit_rows * c.vocab * sizeof(float));
 
   // ---- device body
+  // K1 overlapped with the question pass (the stitch_ms stage is then ~0 and
+  // question_ms covers both); CacheBlend's 2-layer FA pass needs it up front
+  const bool overlap = !cacheblend && sp.n_desc > 0 && c.layers > 1 && stitch_overlap_enabled();
   auto body = [&](cudaStream_t bs) {
     ev_record(r, timing, 0, bs);
-    stitch_launch(e, r, bs, sp);  // K1: stitch_full_reuse
+    if (overlap)
+      stitch_fork(e, r, bs, sp);  // K1 per layer on the side stream
+    else
+      stitch_launch(e, r, bs, sp);  // K1: stitch_full_reuse
     ev_record(r, timing, 1, bs);
     // question pass: last_layer_query_states against the stitched cache
-    if (!cacheblend) run_rows(e, r, bs, n_q, T, PASS_QUESTION, nullptr, 0);
+    if (!cacheblend) run_rows(e, r, bs, n_q, T, PASS_QUESTION, nullptr, 0, 0, overlap ? r->layer_ev.data() : nullptr);
+    if (overlap)  // join: every stitched layer (the last one feeds the selection keys)
+      check_cuda(cudaStreamWaitEvent(bs, r->layer_ev[c.layers - 1], 0), "join stitch");
     ev_record(r, timing, 2, bs);
     // select_query_guided (K9 + K10) -> QIndexPlan on device
     if (cacheblend) {
@@ -954,7 +998,8 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
 
   const bool graphable = !timing && !e->prof.on;
   GraphKey key{T, S, N, n_q, k, (int)inject, (int)all_logits, (int)raw, (int)r->logits_on_device, sp.n_desc,
-               sp.max_rows, cacheblend ? 1 + dev_layer * 4 + dev_comp : 0, (uint64_t)(uintptr_t)e->rope.p};
+               sp.max_rows, (cacheblend ? 1 + dev_layer * 4 + dev_comp : 0) + (overlap ? 1000 : 0),
+               (uint64_t)(uintptr_t)e->rope.p};
   r->timing.host_prep_ms =
       std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
   run_graphed(r, s, graphable, key, body);

@@ -212,6 +212,10 @@ struct Result {
   std::map<GraphKey, GraphEntry> graphs;
   std::set<GraphKey> seen;
   cudaStream_t cap_stream = nullptr;
+  // K1 per layer on a side stream overlapping the question pass
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr;
+  std::vector<cudaEvent_t> layer_ev;
   int max_tokens = 0;
   // fused cache [L][max_tokens][Hkv][dh]
   DevBuf k_fused, v_fused;
@@ -240,8 +244,10 @@ enum PassMode { PASS_FULL = 0, PASS_QUESTION = 1, PASS_KV_ONLY = 2 };
 // logits for the rows listed in row_map (n_logit_rows of them, device).
 // n_layers > 0 runs only the first n_layers layers (a non-FULL pass then stops
 // after layer n_layers-1's QKV projection: kv_deviation's 2-layer FA pass).
+// layer_ready: optional per-layer events the stream waits on before layer l's
+// attention (the stitch of that layer running on another stream).
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
-              int n_logit_rows, int n_layers = 0);
+              int n_logit_rows, int n_layers = 0, const cudaEvent_t* layer_ready = nullptr);
 
 void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
                bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio, const frag_reprocess_opts* o,

@@ -77,7 +77,8 @@ struct StitchChunk {
 };
 // fused K/V [L][T][Hkv][dh]; tables: [n_tables][dh/2] float2 for delta*theta_i.
 void rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_rows, const float2* tables,
-                         bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream);
+                         bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream,
+                         int layer0 = 0);
 
 // ------------------------------------------------------------------ K2/K3
 // h[i] = E[tok[i]] (fp32), x[i] = bf16(rmsnorm(h[i]) * g)

@@ -40,17 +40,18 @@ __device__ __forceinline__ uint32_t rot_pair(uint32_t kv, float2 cs) {
 // fully coalesced 128-bit streams.
 __global__ void __launch_bounds__(256) rope_shift_kernel(const StitchChunk* __restrict__ chunks,
                                                          const float2* __restrict__ tables, bf16* __restrict__ kf,
-                                                         bf16* __restrict__ vf, int L, int T, int Hkv, int dh) {
+                                                         bf16* __restrict__ vf, int L, int T, int Hkv, int dh,
+                                                         int layer0) {
   const StitchChunk c = chunks[blockIdx.y];
   const int vec_per_row = (Hkv * dh) >> 3;  // 16-byte vectors per token row
   const long per_layer = (long)c.n_tok * vec_per_row;
-  const long total = per_layer * L;
+  const long total = per_layer * L;  // layers [layer0, layer0 + L)
   const int dvec = dh >> 3;
   const float2* tab = c.table >= 0 ? tables + (size_t)c.table * (dh >> 1) : nullptr;
-  const uint4* ks = reinterpret_cast<const uint4*>(c.k_src);
-  const uint4* vs = reinterpret_cast<const uint4*>(c.v_src);
+  const uint4* ks = reinterpret_cast<const uint4*>(c.k_src) + layer0 * per_layer;
+  const uint4* vs = reinterpret_cast<const uint4*>(c.v_src) + layer0 * per_layer;
   const long layer_stride_dst = (long)T * vec_per_row;
-  const long dst0 = (long)c.dst_row * vec_per_row;
+  const long dst0 = (long)c.dst_row * vec_per_row + layer0 * layer_stride_dst;
   uint4* kd = reinterpret_cast<uint4*>(kf);
   uint4* vd = reinterpret_cast<uint4*>(vf);
   const long stride = (long)gridDim.x * blockDim.x;
@@ -219,15 +220,16 @@ __global__ void fill_kernel(bf16* dst, size_t n, float v) {
 }  // namespace
 
 void rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_rows, const float2* tables,
-                         bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream) {
-  if (n_chunks <= 0 || max_rows <= 0) return;
+                         bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream,
+                         int layer0) {
+  if (n_chunks <= 0 || max_rows <= 0 || L <= 0) return;
   const long vecs = (long)max_rows * L * (Hkv * dh / 8);
   long bx = (vecs + 2 * 256 - 1) / (2 * 256);
   const long cap = (long)num_sms() * 8 / (n_chunks < 8 ? n_chunks : 8) + 1;
   if (bx > cap) bx = cap;
   if (bx < 1) bx = 1;
   dim3 grid((unsigned)bx, (unsigned)n_chunks);
-  rope_shift_kernel<<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, L, T, Hkv, dh);
+  rope_shift_kernel<<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, L, T, Hkv, dh, layer0);
 }
 
 void embed_rmsnorm(const bf16* E, const int* tok, int M, int d, const bf16* gain, float eps, float* h, bf16* x,
