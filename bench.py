@@ -84,6 +84,8 @@ def parse():
     p.add_argument("--partition", action="store_true",
                    help="chunk-partitioned store: each chunk's record lives on rank hash(id) mod N only and "
                         "the other ranks read it over NVLink inside K1 (SURVEY.md §8(e))")
+    p.add_argument("--batch", type=int, default=4,
+                   help="also time multi-request batching (frag_reprocess_batch) with this many requests; 0 = skip")
     p.add_argument("--with-load", action="store_true",
                    help="also time TTFT including the FKVC record load (DISK -> GPU, SPEC.md:301-308)")
     return p.parse_args()
@@ -150,8 +152,10 @@ class ClockSampler:
             for n, v in zip(names, s[5:9]):
                 if v.lower() == "active":
                     reasons.add(n)
+        pw = [float(s[3]) for s in self.samples if s[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(self.samples),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 def peaks():
@@ -399,12 +403,36 @@ def run_ours(args, rank, world, local_rank):
     step_dev(1, selector="cacheblend", timing=True)
     cacheblend_stages = res.timing()
 
+    # ---- multi-request batching: B requests (this rank's next queries) in one
+    # fused cache, one question pass + one sparse pass streaming the weights once
+    batch_leg = None
+    if args.batch and args.batch > 1:
+        B = args.batch
+        rb = F.Result(eng, B * T)
+        reqs = [(questions[(3 + i) % len(questions)], id_sets[i % len(id_sets)], ratio) for i in range(B)]
+        eng.reprocess_batch(store, reqs, rb, T, stream=stream)  # warm
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nb = 3
+        b0.record(stream)
+        for _ in range(nb):
+            eng.reprocess_batch(store, reqs, rb, T, stream=stream, logits_on_device=True)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1) / nb
+        eng.reprocess_batch(store, reqs, rb, T, stream=stream, timing=True)
+        batch_leg = {"requests": B, "batch_ms": bms, "ms_per_request": bms / B, "tok_s": B * T / (bms / 1e3),
+                     "stage_ms": rb.timing(),
+                     "note": "frag_reprocess_batch: every request's TTFT is the batch latency; throughput leg, "
+                             "not in value"}
+        del rb
+
     if world > 1:
         torch.distributed.barrier()  # peers may still read this rank's records until every rank is done
     return dict(ms=ms, e2e_ms=e2e_ms, full_ms=full_ms, launches=launches, prof=prof, stages=stages, T=T,
                 crit=crit, clocks=clk.summary(), cfg=c, w=w, ratio=ratio, h2d=h2d, d2h=d2h, sweep=sweep,
                 k=len(crit), decode_ms=decode_ms, n_dec=len(answer), load_leg=load_leg,
-                cacheblend_ms=cacheblend_ms, cacheblend_stages=cacheblend_stages)
+                cacheblend_ms=cacheblend_ms, cacheblend_stages=cacheblend_stages, batch_leg=batch_leg)
 
 
 def main():
@@ -484,6 +512,7 @@ def main():
         "ttft_ms": ttft, "full_prefill_ms": full_ms, "speedup_vs_full_prefill": full_ms / ttft,
         "recomputed_rows": r["k"] + r["w"]["qlen"], "stage_ms": r["stages"],
         "ratio_sweep_ttft_ms": r["sweep"] or None,
+        "batched": r["batch_leg"],
         "cacheblend": {"ttft_ms": r["cacheblend_ms"], "stage_ms": r["cacheblend_stages"],
                        "note": "same requests with the CacheBlend selector (2-layer Full-Attention pass + layer-2 "
                                "K deviation, SPEC.md:417) instead of the query-guided one; not in value"},

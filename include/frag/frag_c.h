@@ -286,6 +286,33 @@ FRAG_API frag_status frag_full_prefill(frag_engine* eng, const int32_t* sys, int
                                        int32_t n_tok, const frag_reprocess_opts* opts, void* stream,
                                        frag_result* res);
 
+/* Multi-request batching (the scheduler's continuous
+ * batching): n_req independent requests reprocessed together.
+ * Request b owns rows [b*slot_tokens, b*slot_tokens + T_b) of the result's
+ * fused cache (result capacity >= n_req * slot_tokens, T_b <= slot_tokens);
+ * the question pass and the sparse pass run once over all requests' rows, so
+ * every weight matrix streams once per batch, while attention, scoring and
+ * top-k stay per request. Each request's fused KV rows, critical set and
+ * first-token logits equal those of frag_reprocess on the same inputs.
+ * Logits: n_req rows (row b = request b's last question token). Options:
+ * timing / raw_scores / logits_on_device; no injection, no CacheBlend, no
+ * all_logits; frag_decode is not available after a batch. */
+typedef struct {
+  const int32_t* sys;
+  int32_t n_sys;
+  const int32_t* question;
+  int32_t n_q;
+  const frag_chunk_id* chunk_ids;
+  int32_t n_chunks;
+  float recompute_ratio;
+} frag_request;
+FRAG_API frag_status frag_reprocess_batch(frag_engine* eng, frag_store* st, const frag_request* reqs, int32_t n_req,
+                                          int32_t slot_tokens, const frag_reprocess_opts* opts, void* stream,
+                                          frag_result* res);
+/* Critical positions (1-based, ascending) of request b of the last batch;
+ * returns their count (or -1), writing up to cap of them when host_out != NULL. */
+FRAG_API int32_t frag_result_batch_crit(const frag_result* res, int32_t b, int32_t* host_out, int32_t cap);
+
 /* kv_deviation (Eq. 7): Full Reuse (the
  * stitched records) against Full Attention over cat(S, chunks) through the
  * first n_layers layers; dev_host receives [N][n_layers][2] fp32 (K, V sums of

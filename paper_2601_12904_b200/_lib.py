@@ -63,6 +63,12 @@ class Match(C.Structure):
     _fields_ = [("id", ChunkId), ("matched_via", C.c_int32), ("position", C.c_int32), ("path_start", C.c_int32)]
 
 
+class Request(C.Structure):
+    _fields_ = [("sys", C.POINTER(C.c_int32)), ("n_sys", C.c_int32), ("question", C.POINTER(C.c_int32)),
+                ("n_q", C.c_int32), ("chunk_ids", C.POINTER(ChunkId)), ("n_chunks", C.c_int32),
+                ("recompute_ratio", C.c_float)]
+
+
 class ReprocessOpts(C.Structure):
     _fields_ = [("raw_scores", C.c_int32), ("all_logits", C.c_int32), ("timing", C.c_int32),
                 ("inject_crit", C.POINTER(C.c_int32)), ("n_inject", C.c_int32),
@@ -128,6 +134,9 @@ _SIGS = {
                                      C.c_float, C.POINTER(ReprocessOpts), _P, _P]),
     "frag_full_prefill": (C.c_int, [_P, _I32P, C.c_int32, _I32P, C.c_int32, C.POINTER(ReprocessOpts), _P, _P]),
     "frag_decode": (C.c_int, [_P, _P, C.c_int32, _P, _I32P]),
+    "frag_reprocess_batch": (C.c_int, [_P, _P, C.POINTER(Request), C.c_int32, C.c_int32, C.POINTER(ReprocessOpts),
+                                       _P, _P]),
+    "frag_result_batch_crit": (C.c_int32, [_P, C.c_int32, _I32P, C.c_int32]),
     "frag_kv_deviation": (C.c_int, [_P, _P, _I32P, C.c_int32, C.POINTER(ChunkId), C.c_int32, C.c_int32, _P, _P,
                                     _P]),
     "frag_result_sync": (C.c_int, [_P]),

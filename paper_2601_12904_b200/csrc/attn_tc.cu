@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   // rows, Q and the fused K/V rows are read only after this point
   pdl_wait();
   pdl_launch_dependents();
-  const int p_max = a.rows[t_end - 1];
+  const int p_max = a.rows[t_end - 1] - a.row_base;
   int k_hi = p_max + 1;
   if (a.n_splits > 1) k_hi = min(k_hi, (split + 1) * a.split_keys);
   const int n_tiles = k_hi > k_lo ? (k_hi - k_lo + AT_KEYS - 1) / AT_KEYS : 0;
@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       const int tok = t0 + tl;
       const int head = hk * G + r % G;
       const bool live = tok < a.M;
-      const int prow = live ? a.rows[tok] : -1;
-      const int p_min = a.rows[t0 + t * tok_per_tile];
+      const int prow = live ? a.rows[tok] - a.row_base : -1;
+      const int p_min = a.rows[t0 + t * tok_per_tile] - a.row_base;
       const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16) + t * C::T_TILE;
       const float c = a.scale * 1.4426950408889634f;
       float m_used = -INFINITY, l = 0.f;

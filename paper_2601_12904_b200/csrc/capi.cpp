@@ -444,6 +444,23 @@ FRAG_API frag_status frag_full_prefill(frag_engine* eng, const int32_t* sys, int
   });
 }
 
+FRAG_API frag_status frag_reprocess_batch(frag_engine* eng, frag_store* st, const frag_request* reqs, int32_t n_req,
+                                          int32_t slot_tokens, const frag_reprocess_opts* opts, void* stream,
+                                          frag_result* res) {
+  return guard([&] {
+    need(eng && st && res && reqs, "null argument");
+    reprocess_batch(eng->e, st->s, reqs, n_req, slot_tokens, opts, static_cast<cudaStream_t>(stream), res->r);
+  });
+}
+
+FRAG_API int32_t frag_result_batch_crit(const frag_result* res, int32_t b, int32_t* host_out, int32_t cap) {
+  if (!res || b < 0 || b >= (int32_t)res->r->batch.size()) return -1;
+  const auto& c = res->r->batch[b].crit;
+  if (host_out)
+    for (int32_t i = 0; i < (int32_t)c.size() && i < cap; ++i) host_out[i] = c[i];
+  return (int32_t)c.size();
+}
+
 FRAG_API frag_status frag_kv_deviation(frag_engine* eng, frag_store* st, const int32_t* sys, int32_t n_sys,
                                        const frag_chunk_id* chunk_ids, int32_t n_chunks, int32_t n_layers,
                                        void* stream, frag_result* res, float* dev_host) {
@@ -501,6 +518,7 @@ FRAG_API int32_t frag_result_crit(const frag_result* res, int32_t* host_out, int
   if (!res) return -1;
   const Result* r = res->r;
   if (r->nq == 0) return 0;  // full prefill: no selection
+  if (r->rows_per_seq > 0) return -1;  // batched: frag_result_batch_crit per request
   const int k = r->k_sel;
   if (host_out && cap > 0) {
     const int n = k < cap ? k : cap;

@@ -314,7 +314,7 @@ void result_init(Result* r, Engine* e, int max_tokens) {
 
 // ---------------------------------------------------------------- run_rows
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
-              int n_logit_rows, int n_layers, const cudaEvent_t* layer_ready) {
+              int n_logit_rows, int n_layers, const cudaEvent_t* layer_ready, const std::vector<Seg>* segs_in) {
   if (M <= 0) return;
   const auto& c = e->cfg;
   const int L = (n_layers > 0 && n_layers < c.layers) ? n_layers : c.layers;
@@ -335,27 +335,37 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
   };
 
-  // split-KV policy, splits of >= 256 keys: very few query blocks (question
-  // pass, decode) fill exactly one wave (the attention CTA takes a whole SM);
-  // otherwise >= 2 waves
+  // one sequence unless batched (segments of plan rows, each over its own
+  // slice of the fused cache starting at cache row `base`)
+  const std::vector<Seg> one{Seg{0, M, 0, T}};
+  const std::vector<Seg>& segs = segs_in ? *segs_in : one;
+  // split-KV policy per segment, splits of >= 256 keys: very few query blocks
+  // (question pass, decode) fill exactly one wave (the attention CTA takes a
+  // whole SM); otherwise >= 2 waves
   const int G = Hq / Hkv;
   const int tpc = fragk::attn_rows_per_cta() / G;  // tokens per attention CTA
-  const int nqb = (M + tpc - 1) / tpc;
-  const long ctas = (long)nqb * Hkv;
-  int n_splits = 1, split_keys = 0;
   const int sms = fragk::num_sms();
-  if (ctas < 2L * sms && T > 512) {
-    n_splits = ctas <= sms / 2 ? (int)(sms / ctas) : (int)((2L * sms + ctas - 1) / ctas);
-    const int max_splits = (T + 255) / 256;
-    if (n_splits > max_splits) n_splits = max_splits;
-    if (n_splits > 64) n_splits = 64;  // the combine kernel's limit
-    split_keys = (int)align_up((size_t)((T + n_splits - 1) / n_splits), 128);
-    n_splits = (T + split_keys - 1) / split_keys;
-    if (n_splits <= 1) n_splits = 1, split_keys = 0;
-  }
-  if (n_splits > 1) {
-    r->part_o.ensure((size_t)n_splits * M * qc * sizeof(float));
-    r->part_lse.ensure((size_t)n_splits * M * Hq * sizeof(float));
+  auto split_policy = [&](int Ms, int Ts, int& n_splits, int& split_keys) {
+    const int nqb = (Ms + tpc - 1) / tpc;
+    const long ctas = (long)nqb * Hkv;
+    n_splits = 1, split_keys = 0;
+    if (ctas < 2L * sms && Ts > 512) {
+      n_splits = ctas <= sms / 2 ? (int)(sms / ctas) : (int)((2L * sms + ctas - 1) / ctas);
+      const int max_splits = (Ts + 255) / 256;
+      if (n_splits > max_splits) n_splits = max_splits;
+      if (n_splits > 64) n_splits = 64;  // the combine kernel's limit
+      split_keys = (int)align_up((size_t)((Ts + n_splits - 1) / n_splits), 128);
+      n_splits = (Ts + split_keys - 1) / split_keys;
+      if (n_splits <= 1) n_splits = 1, split_keys = 0;
+    }
+  };
+  std::vector<std::pair<int, int>> seg_split(segs.size());
+  for (size_t i = 0; i < segs.size(); ++i) {
+    split_policy(segs[i].M, segs[i].T, seg_split[i].first, seg_split[i].second);
+    if (seg_split[i].first > 1) {
+      r->part_o.ensure((size_t)seg_split[i].first * segs[i].M * qc * sizeof(float));
+      r->part_lse.ensure((size_t)seg_split[i].first * segs[i].M * Hq * sizeof(float));
+    }
   }
   if (mode == PASS_QUESTION) r->q_final.ensure((size_t)M * qc * sizeof(float));
 
@@ -380,6 +390,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       ep.q_out_f32 = (mode == PASS_QUESTION && l == L - 1) ? r->q_final.as<float>() : nullptr;
       ep.k_cache = kf + l * lstride;
       ep.v_cache = vf + l * lstride;
+      ep.rows_per_seq = r->rows_per_seq;
       ep.Hq = Hq;
       ep.Hkv = Hkv;
       ep.dh = dh;
@@ -388,22 +399,25 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     }
     if (mode != PASS_FULL && l == L - 1) break;
     if (layer_ready) check_cuda(cudaStreamWaitEvent(s, layer_ready[l], 0), "wait stitched layer");
-    {
+    for (size_t si = 0; si < segs.size(); ++si) {
+      const Seg& g = segs[si];
+      if (g.M <= 0) continue;
       fragk::AttnArgs a{};
-      a.q = r->q.as<bf16>();
-      a.k = kf + l * lstride;
-      a.v = vf + l * lstride;
-      a.rows = prow;
-      a.out = r->attn.as<bf16>();
+      a.q = r->q.as<bf16>() + (size_t)g.off * qc;
+      a.k = kf + l * lstride + (size_t)g.base * kvc;
+      a.v = vf + l * lstride + (size_t)g.base * kvc;
+      a.rows = prow + g.off;
+      a.row_base = g.base;
+      a.out = r->attn.as<bf16>() + (size_t)g.off * qc;
       a.part_o = r->part_o.as<float>();
       a.part_lse = r->part_lse.as<float>();
-      a.M = M;
-      a.T = T;
+      a.M = g.M;
+      a.T = g.T;
       a.Hq = Hq;
       a.Hkv = Hkv;
       a.dh = dh;
-      a.split_keys = split_keys;
-      a.n_splits = n_splits;
+      a.split_keys = seg_split[si].second;
+      a.n_splits = seg_split[si].first;
       a.scale = 1.0f / std::sqrt((float)dh);
       Scoped sc(P, s, KC_ATTN, 0, 0);
       sc.launched(fragk::sparse_q_attention(a, s));
@@ -491,37 +505,46 @@ struct Stage {
 
 // K1 host side: per-chunk descriptors and cos/sin(delta*theta) tables staged and
 // copied to the device (per request); the kernel launch is part of the body.
-StitchPlan stitch_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys,
-                          const std::vector<Record*>& recs, int S) {
+// One part per sequence: its KV_S and records placed from cache row `base`
+// (base > 0 only for batched requests sharing one fused cache).
+struct StitchPart {
+  const SysKV* sys;
+  const std::vector<Record*>* recs;
+  int S, base;
+};
+StitchPlan stitch_prepare_parts(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std::vector<StitchPart>& parts) {
   const auto& c = e->cfg;
   const int half = c.head_dim / 2;
   StitchPlan p;
-  p.n_desc = (sys && sys->n > 0 ? 1 : 0) + (int)recs.size();
+  for (const auto& pt : parts) p.n_desc += (pt.sys && pt.sys->n > 0 ? 1 : 0) + (int)pt.recs->size();
   if (p.n_desc == 0) return p;
   auto* desc = stg.take<fragk::StitchChunk>(p.n_desc);
   std::vector<float2> tabs;
   int nd = 0, n_tab = 0;
   const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
-  if (sys && sys->n > 0) {
-    desc[nd++] = {sys->kv.as<bf16>(), sys->kv.as<bf16>() + (size_t)c.layers * sys->n * kvc, sys->n, 0, -1};
-    p.max_rows = sys->n;
-  }
-  int row = S;
-  for (Record* rec : recs) {
-    const int target_start = row + 1;  // 1-based
-    const int delta = target_start - rec->native_start;
-    int table = -1;
-    if (delta != 0) {
-      // shift_rope = apply_rope(v, new - old): cos/sin(delta * theta_i), fp64 angles
-      table = n_tab++;
-      for (int i = 0; i < half; ++i) {
-        const double a = (double)delta * e->theta[i];
-        tabs.push_back(make_float2((float)std::cos(a), (float)std::sin(a)));
-      }
+  for (const auto& pt : parts) {
+    if (pt.sys && pt.sys->n > 0) {
+      desc[nd++] = {pt.sys->kv.as<bf16>(), pt.sys->kv.as<bf16>() + (size_t)c.layers * pt.sys->n * kvc, pt.sys->n,
+                    pt.base, -1};
+      if (pt.sys->n > p.max_rows) p.max_rows = pt.sys->n;
     }
-    desc[nd++] = {rec->k(), rec->v(), rec->n_tok, row, table};
-    if (rec->n_tok > p.max_rows) p.max_rows = rec->n_tok;
-    row += rec->n_tok;
+    int row = pt.S;  // local row = position - 1
+    for (Record* rec : *pt.recs) {
+      const int target_start = row + 1;  // 1-based
+      const int delta = target_start - rec->native_start;
+      int table = -1;
+      if (delta != 0) {
+        // shift_rope = apply_rope(v, new - old): cos/sin(delta * theta_i), fp64 angles
+        table = n_tab++;
+        for (int i = 0; i < half; ++i) {
+          const double ang = (double)delta * e->theta[i];
+          tabs.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
+        }
+      }
+      desc[nd++] = {rec->k(), rec->v(), rec->n_tok, pt.base + row, table};
+      if (rec->n_tok > p.max_rows) p.max_rows = rec->n_tok;
+      row += rec->n_tok;
+    }
   }
   float2* tab_h = stg.take<float2>(tabs.size() > 0 ? tabs.size() : 1);
   if (!tabs.empty()) std::memcpy(tab_h, tabs.data(), tabs.size() * sizeof(float2));
@@ -535,6 +558,11 @@ StitchPlan stitch_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, cons
                "stitch tab");
   for (int i = 0; i < p.n_desc; ++i) p.bytes += 4.0 * c.layers * desc[i].n_tok * kvc * sizeof(bf16);
   return p;
+}
+
+StitchPlan stitch_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys,
+                          const std::vector<Record*>& recs, int S) {
+  return stitch_prepare_parts(e, r, s, stg, {StitchPart{sys, &recs, S, 0}});
 }
 
 void stitch_launch(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p, int l0 = 0, int l1 = -1) {
@@ -830,6 +858,8 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     r->fr_save.ensure((size_t)2 * dev_layer * N * c.n_kv_heads * c.head_dim * sizeof(bf16));
 
   r->T = T;
+  r->rows_per_seq = 0;
+  r->batch.clear();
   r->S = S;
   r->N = N;
   r->nq = n_q;
@@ -1006,6 +1036,191 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   finish(r, timing, s);
 }
 
+// Multi-request batching (SPEC.md:482 continuous
+// batching): B independent requests share one fused cache (request b owns rows
+// [b*slot, b*slot + T_b)), so one question pass over all B*|Q| rows and one
+// sparse pass over all selected rows stream every weight matrix once for the
+// whole batch; attention, scoring and top-k run per request on its own cache
+// slice (Seg). Each request's result equals its single-request reprocess
+// (same kernels, same per-request plans; GEMM rows are independent).
+void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int slot, const frag_reprocess_opts* o,
+                     cudaStream_t s, Result* r) {
+  const auto& c = e->cfg;
+  if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
+  if (!st) fail(FRAG_E_CONTRACT, "store is null");
+  if (st->device != e->device) fail(FRAG_E_CONTRACT, "store and engine are on different devices");
+  if (B < 1 || !reqs) fail(FRAG_E_CONTRACT, "batch needs at least one request");
+  if (slot < 1 || (long)B * slot > r->max_tokens)
+    fail(FRAG_E_CONTRACT, "batch of " + std::to_string(B) + " x " + std::to_string(slot) +
+                              " rows exceeds the result capacity " + std::to_string(r->max_tokens));
+  if (o && (o->inject_crit || o->all_logits || o->selector != FRAG_SELECT_QUERY_GUIDED))
+    fail(FRAG_E_CONTRACT, "batched reprocess supports the query-guided selector with last-row logits only");
+  DeviceGuard dg(e->device);
+  const bool timing = o && o->timing;
+  const bool raw = o && o->raw_scores;
+  PinGuard pins{st, {}};
+  std::vector<std::vector<Record*>> recs(B);
+  std::vector<SysKV*> skv(B);
+  std::vector<Result::BatchReq> br(B);
+  int Qtot = 0, Ntot = 0, Mtot = 0, maxN = 0, maxQ = 0;
+  e->ensure_rope(slot);
+  for (int b = 0; b < B; ++b) {
+    const frag_request& q = reqs[b];
+    if (q.n_q < 1 || !q.question) fail(FRAG_E_CONTRACT, "every request needs a question");
+    if (q.n_sys < 0 || q.n_chunks < 0 || (q.n_sys > 0 && !q.sys) || (q.n_chunks > 0 && !q.chunk_ids))
+      fail(FRAG_E_CONTRACT, "bad request");
+    if (!(q.recompute_ratio >= 0.f && q.recompute_ratio <= 1.f))
+      fail(FRAG_E_CONTRACT, "recompute_ratio must lie in [0, 1]");
+    for (int i = 0; i < q.n_q; ++i)
+      if (q.question[i] < 0 || q.question[i] >= c.vocab) fail(FRAG_E_CONTRACT, "question token out of vocabulary");
+    int N = 0;
+    for (int i = 0; i < q.n_chunks; ++i) {
+      recs[b].push_back(store_fetch(st, q.chunk_ids[i]));
+      pins.ids.push_back(q.chunk_ids[i]);
+      N += recs[b].back()->n_tok;
+    }
+    const int T = q.n_sys + N + q.n_q;
+    if (T > slot) fail(FRAG_E_CONTRACT, "request " + std::to_string(b) + " has " + std::to_string(T) +
+                                            " tokens, more than the batch slot of " + std::to_string(slot));
+    const int k = (int)std::floor((double)q.recompute_ratio * (double)N + 0.5);
+    br[b] = {T, q.n_sys, N, q.n_q, k, Mtot, {}};
+    skv[b] = get_sys_kv(e, q.sys, q.n_sys, s);
+    Qtot += q.n_q;
+    Ntot += N;
+    Mtot += k + q.n_q;
+    maxN = std::max(maxN, N);
+    maxQ = std::max(maxQ, q.n_q);
+  }
+  r->T = B * slot;
+  r->S = 0;
+  r->N = Ntot;
+  r->nq = Qtot;
+  r->k_sel = Mtot - Qtot;
+  r->M = Mtot;
+  r->logit_rows = B;
+  r->rows_per_seq = slot;
+  r->logits_on_device = o && o->logits_on_device;
+  r->batch = br;
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+
+  // ---- host prep
+  r->staging.ensure(64 * 1024 + (size_t)(pins.ids.size() + 2 * B) * (64 + c.head_dim * 4) +
+                    (size_t)(4 * Qtot + 4 * B) * 4);
+  Stage stg(r->staging);
+  std::vector<StitchPart> parts;
+  for (int b = 0; b < B; ++b) parts.push_back(StitchPart{skv[b], &recs[b], br[b].S, b * slot});
+  StitchPlan sp = stitch_prepare_parts(e, r, s, stg, parts);
+  std::vector<int> cofs(B), qofs(B);
+  {
+    int co = 0, qo = 0;
+    int* qh = stg.take<int>(Qtot);
+    int* rows_h = stg.take<int>(Qtot);
+    for (int b = 0; b < B; ++b) {
+      cofs[b] = co;
+      qofs[b] = qo;
+      for (Record* rec : recs[b]) {
+        check_cuda(cudaMemcpyAsync(r->chunk_tok.as<int>() + co, rec->tok.p, rec->n_tok * sizeof(int),
+                                   cudaMemcpyDeviceToDevice, s),
+                   "chunk tokens");
+        co += rec->n_tok;
+      }
+      for (int i = 0; i < br[b].nq; ++i) {
+        qh[qo + i] = reqs[b].question[i];
+        rows_h[qo + i] = b * slot + br[b].T - br[b].nq + i;
+      }
+      qo += br[b].nq;
+    }
+    check_cuda(cudaMemcpyAsync(r->q_tok.p, qh, Qtot * sizeof(int), cudaMemcpyHostToDevice, s), "q tok");
+    check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, Qtot * sizeof(int), cudaMemcpyHostToDevice, s), "q rows");
+    check_cuda(cudaMemcpyAsync(r->plan_tok.p, r->q_tok.p, Qtot * sizeof(int), cudaMemcpyDeviceToDevice, s), "q plan");
+    int* map_h = stg.take<int>(B);
+    for (int b = 0; b < B; ++b) map_h[b] = br[b].plan_off + br[b].k + br[b].nq - 1;
+    check_cuda(cudaMemcpyAsync(r->row_map.p, map_h, B * sizeof(int), cudaMemcpyHostToDevice, s), "map");
+  }
+  if (maxN > 0) {
+    r->part_ms.ensure((size_t)((maxN + 31) / 32) * maxQ * c.n_heads * sizeof(float2));
+    r->row_ms.ensure((size_t)maxQ * c.n_heads * sizeof(float2));
+    r->score_col.ensure(fragk::score_col_part_elems(maxQ, c.n_heads, c.n_kv_heads, maxN) * sizeof(float));
+    r->score_q.ensure(fragk::score_q_split_elems(maxQ, c.n_heads, c.n_kv_heads, c.head_dim) * sizeof(bf16));
+  }
+  r->lm_x.ensure((size_t)B * c.d_model * sizeof(bf16));
+  r->logits.ensure((size_t)B * c.vocab * sizeof(float));
+  if (!r->logits_on_device) r->logits_host.ensure((size_t)B * c.vocab * sizeof(float));
+  std::vector<Seg> qsegs, psegs;
+  for (int b = 0; b < B; ++b) {
+    qsegs.push_back(Seg{qofs[b], br[b].nq, b * slot, br[b].T});
+    psegs.push_back(Seg{br[b].plan_off, br[b].k + br[b].nq, b * slot, br[b].T});
+  }
+
+  // ---- device body (eager: one batch shape is rarely repeated)
+  ev_record(r, timing, 0, s);
+  stitch_launch(e, r, s, sp);
+  ev_record(r, timing, 1, s);
+  run_rows(e, r, s, Qtot, slot, PASS_QUESTION, nullptr, 0, 0, nullptr, &qsegs);
+  ev_record(r, timing, 2, s);
+  for (int b = 0; b < B; ++b) {
+    const auto& q = br[b];
+    if (q.N > 0) {
+      fragk::ScoreArgs a{};
+      a.q = r->q_final.as<float>() + (size_t)qofs[b] * c.n_heads * c.head_dim;
+      a.k = r->k_fused.as<bf16>() + (size_t)(c.layers - 1) * r->max_tokens * kvc + (size_t)b * slot * kvc;
+      a.nq = q.nq;
+      a.Hq = c.n_heads;
+      a.Hkv = c.n_kv_heads;
+      a.dh = c.head_dim;
+      a.key_row0 = q.S;
+      a.n_keys = q.N;
+      a.scale = 1.0f / std::sqrt((float)c.head_dim);
+      a.part_ms = r->part_ms.as<float2>();
+      a.row_ms = r->row_ms.as<float2>();
+      a.scores = r->scores.as<float>() + cofs[b];
+      a.raw = raw;
+      a.col_part = r->score_col.as<float>();
+      a.q_split = r->score_q.as<bf16>();
+      Scoped sc(e->prof, s, KC_SELECT, 4.0 * q.nq * c.n_heads * (double)q.N * c.head_dim,
+                2.0 * q.N * (double)kvc * 2);
+      sc.launched(fragk::qg_score(a, s));
+    }
+    Scoped sc(e->prof, s, KC_SELECT, 0, 4.0 * q.N * 6);
+    sc.launched(fragk::topk_plan(r->scores.as<float>() + cofs[b], q.N, q.k, b * slot + q.S,
+                                 r->chunk_tok.as<int>() + cofs[b], r->q_tok.as<int>() + qofs[b], q.nq,
+                                 b * slot + q.T - q.nq, r->plan_rows.as<int>() + q.plan_off,
+                                 r->plan_tok.as<int>() + q.plan_off, s));
+  }
+  peek("batch select");
+  ev_record(r, timing, 3, s);
+  run_rows(e, r, s, Mtot, slot, PASS_FULL, nullptr, 0, 0, nullptr, &psegs);
+  ev_record(r, timing, 4, s);
+  {
+    const int d = c.d_model;
+    {
+      Scoped sc(e->prof, s, KC_NORM, 0, (double)B * d * 6);
+      fragk::rmsnorm(r->h.as<float>(), B, d, e->final_norm, c.norm_eps, r->lm_x.as<bf16>(), s, r->row_map.as<int>());
+      sc.launched(1);
+    }
+    fragk::EpiParams ep;
+    ep.ws = r->gemm_ws.as<float>();
+    ep.ws_bytes = r->gemm_ws.bytes;
+    ep.counters = r->gemm_cnt.as<int>();
+    ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
+    ep.out_f32 = r->logits.as<float>();
+    ep.ldo = c.vocab;
+    Scoped sc(e->prof, s, gemm_class(B), 2.0 * B * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
+    sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, B, c.vocab, d, fragk::EPI_STORE_F32, ep, s));
+  }
+  peek("batch lm_head");
+  ev_record(r, timing, 5, s);
+  logits_d2h(r, s);
+  // per-request critical positions (host copies for frag_result_batch_crit)
+  std::vector<int32_t> plan_h((size_t)Mtot);
+  check_cuda(cudaMemcpyAsync(plan_h.data(), r->plan_rows.p, Mtot * sizeof(int), cudaMemcpyDeviceToHost, s), "plan");
+  finish(r, timing, s);
+  for (int b = 0; b < B; ++b) {
+    r->batch[b].crit.resize(br[b].k);
+    for (int i = 0; i < br[b].k; ++i) r->batch[b].crit[i] = plan_h[br[b].plan_off + i] - b * slot + 1;
+  }
+}
+
 void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                   const frag_reprocess_opts* o, cudaStream_t s, Result* r) {
   const auto& c = e->cfg;
@@ -1020,6 +1235,8 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
   e->ensure_rope(T);
   SysKV* skv = get_sys_kv(e, sys, n_sys, s);
   r->T = T;
+  r->rows_per_seq = 0;
+  r->batch.clear();
   r->S = S;
   r->N = n_tok;
   r->nq = 0;
@@ -1073,6 +1290,8 @@ void kv_deviation(Engine* e, Store* st, const int32_t* sys, int n_sys, const fra
   e->ensure_rope(T);
   SysKV* skv = get_sys_kv(e, sys, n_sys, s);
   r->T = T;
+  r->rows_per_seq = 0;
+  r->batch.clear();
   r->S = S;
   r->N = N;
   r->nq = 0;
@@ -1107,6 +1326,7 @@ void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) 
   if (n_new < 1) fail(FRAG_E_CONTRACT, "max_new_tokens must be >= 1");
   if (!out_host) fail(FRAG_E_CONTRACT, "tokens_out is null");
   if (r->T <= 0 || r->logit_rows < 1) fail(FRAG_E_CONTRACT, "decode needs a preceding reprocess or full prefill");
+  if (r->rows_per_seq > 0) fail(FRAG_E_CONTRACT, "decode after a batched reprocess is not supported");
   const int T0 = r->T;
   if (T0 + n_new - 1 > r->max_tokens)
     fail(FRAG_E_CONTRACT, "decoded tokens exceed the result capacity (" + std::to_string(r->max_tokens) + ")");

@@ -220,6 +220,14 @@ struct Result {
   // fused cache [L][max_tokens][Hkv][dh]
   DevBuf k_fused, v_fused;
   int T = 0, S = 0, N = 0, nq = 0, k_sel = 0, M = 0, logit_rows = 0;
+  // batched requests (reprocess_batch): request b owns cache rows
+  // [b * rows_per_seq, ...); 0 = one sequence
+  int rows_per_seq = 0;
+  struct BatchReq {
+    int T, S, N, nq, k, plan_off;
+    std::vector<int32_t> crit;  // host copy after the request (1-based positions)
+  };
+  std::vector<BatchReq> batch;
   // workspace
   DevBuf h, x, q, attn, act, plan_rows, plan_tok, chunk_tok, q_tok, q_final, scores, part_ms, row_ms, part_o,
       part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok, fr_save, dev, score_col, score_q;
@@ -246,14 +254,24 @@ enum PassMode { PASS_FULL = 0, PASS_QUESTION = 1, PASS_KV_ONLY = 2 };
 // after layer n_layers-1's QKV projection: kv_deviation's 2-layer FA pass).
 // layer_ready: optional per-layer events the stream waits on before layer l's
 // attention (the stitch of that layer running on another stream).
+// segs: optional batched sequences (plan-row ranges over their own cache slices)
+struct Seg {
+  int off;   // first plan row of the sequence
+  int M;     // plan rows of the sequence
+  int base;  // first fused-cache row of the sequence
+  int T;     // cache rows visible to the sequence
+};
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
-              int n_logit_rows, int n_layers = 0, const cudaEvent_t* layer_ready = nullptr);
+              int n_logit_rows, int n_layers = 0, const cudaEvent_t* layer_ready = nullptr,
+              const std::vector<Seg>* segs = nullptr);
 
 void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
                bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio, const frag_reprocess_opts* o,
                cudaStream_t s, Result* r);
 void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                   const frag_reprocess_opts* o, cudaStream_t s, Result* r);
+void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int slot, const frag_reprocess_opts* o,
+                     cudaStream_t s, Result* r);
 // kv_deviation (Eq. 7): Full Reuse (stitched) vs Full Attention
 // over cat(S, chunks) through the first n_layers layers; dev_host [N][n_layers][2]
 // (K, V). The result holds the Full-Reuse stitched cache afterwards.

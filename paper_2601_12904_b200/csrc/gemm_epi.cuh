@@ -70,7 +70,8 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
     if (col < q_cols + k_cols) {
       // RoPE, interleaved pairs: o0 = k0 c - k1 s, o1 = k1 c + k0 s
       const int d0 = col % dh;
-      const float2* cs = ep.rope + (size_t)prow * (dh >> 1) + (d0 >> 1);
+      const int ppos = ep.rows_per_seq > 0 ? prow % ep.rows_per_seq : prow;
+      const float2* cs = ep.rope + (size_t)ppos * (dh >> 1) + (d0 >> 1);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         float2 t = cs[j];

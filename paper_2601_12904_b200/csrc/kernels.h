@@ -31,6 +31,7 @@ struct EpiParams {
   // EPI_QKV
   const int* rows = nullptr;       // fused-cache row (position-1) of each GEMM row
   const float2* rope = nullptr;    // [pos_row][dh/2] (cos, sin) of (row+1)*theta_i
+  int rows_per_seq = 0;            // > 0: position row = row % rows_per_seq (batched sequences)
   bf16* q_out = nullptr;           // [M][Hq][dh]
   float* q_out_f32 = nullptr;      // optional fp32 copy (question pass, final layer)
   bf16* k_cache = nullptr;         // layer base, [T][Hkv][dh]
@@ -92,7 +93,8 @@ struct AttnArgs {
   const bf16* q;         // [M][Hq][dh]
   const bf16* k;         // fused layer base [T][Hkv][dh]
   const bf16* v;
-  const int* rows;       // [M] query fused-cache row (ascending)
+  const int* rows;       // [M] query fused-cache row (ascending); row - row_base indexes k/v
+  int row_base = 0;      // first cache row of this sequence (batched requests share one cache)
   bf16* out;             // [M][Hq][dh]
   float* part_o;         // split partials [splits][M][Hq][dh]
   float* part_lse;       // [splits][M][Hq]

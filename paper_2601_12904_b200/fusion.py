@@ -17,7 +17,7 @@ from typing import Iterable, Sequence
 import numpy as np
 
 from ._lib import (ChunkId, FkvcHeader, ContractError, CudaError, FormatError, FragError, Match, ModelCfg,
-                   OutOfMemory, PeerRecord, RecordView, ReprocessOpts, StoreError, Timing, check, lib)
+                   OutOfMemory, PeerRecord, Request, RecordView, ReprocessOpts, StoreError, Timing, check, lib)
 
 __all__ = ["ModelCfg", "ChunkId", "Engine", "ChunkKVStore", "Result", "preset", "hash_tokens",
            "ContractError", "StoreError", "FormatError", "CudaError", "OutOfMemory", "FragError",
@@ -173,6 +173,35 @@ class Engine:
             q = _i32(question)
             check(lib.frag_reprocess(self._h, store._h, _i32p(s), len(s), _i32p(q), len(q), ids, len(chunk_ids),
                                      float(ratio), C.byref(opts), _stream_ptr(stream), result._h))
+        return result
+
+    def reprocess_batch(self, store: "ChunkKVStore", requests: Sequence, result: "Result", slot_tokens: int, *,
+                        raw_scores: bool = False, timing: bool = False, logits_on_device: bool = False,
+                        stream=None) -> "Result":
+        """Multi-request batching: requests = [(question, chunk_ids, ratio[, system])]; request b
+        occupies fused-cache rows [b*slot_tokens, ...) of `result` (capacity >= len * slot_tokens).
+        Logits: one row per request; critical positions via result.batch_crit(b)."""
+        keep = []
+        arr = (Request * len(requests))()
+        for i, rq in enumerate(requests):
+            q, ids, ratio = rq[0], rq[1], rq[2]
+            sysm = rq[3] if len(rq) > 3 else ()
+            qa, sa = _i32(q), _i32(sysm)
+            ia = (ChunkId * max(len(ids), 1))(*ids)
+            keep += [qa, sa, ia]
+            arr[i].sys = _i32p(sa)
+            arr[i].n_sys = len(sa)
+            arr[i].question = _i32p(qa)
+            arr[i].n_q = len(qa)
+            arr[i].chunk_ids = ia
+            arr[i].n_chunks = len(ids)
+            arr[i].recompute_ratio = float(ratio)
+        opts = ReprocessOpts()
+        opts.raw_scores = int(raw_scores)
+        opts.timing = int(timing)
+        opts.logits_on_device = int(logits_on_device)
+        check(lib.frag_reprocess_batch(self._h, store._h, arr, len(requests), int(slot_tokens), C.byref(opts),
+                                       _stream_ptr(stream), result._h))
         return result
 
     def full_prefill(self, tokens: Sequence[int], result: "Result", system: Sequence[int] = (), *,
@@ -411,6 +440,15 @@ class Result:
         if k > 0:
             lib.frag_result_crit(self._h, _i32p(out), k)
         return out[:k]
+
+    def batch_crit(self, b: int) -> np.ndarray:
+        """Critical positions (1-based) of request b of the last reprocess_batch."""
+        n = int(lib.frag_result_batch_crit(self._h, int(b), None, 0))
+        if n < 0:
+            raise ContractError("no such request in the last batch")
+        out = np.empty(max(n, 1), dtype=np.int32)
+        lib.frag_result_batch_crit(self._h, int(b), _i32p(out), n)
+        return out[:n]
 
     def timing(self) -> dict:
         t = Timing()
