@@ -159,6 +159,13 @@ class Result {
     if (k > 0) frag_result_crit(h_, out.data(), k);
     return out;
   }
+  std::vector<Pos> batch_critical_positions(int b) const {
+    const int32_t k = frag_result_batch_crit(h_, b, nullptr, 0);
+    if (k < 0) throw ContractError("no such request in the last batch");
+    std::vector<Pos> out(k);
+    if (k > 0) frag_result_batch_crit(h_, b, out.data(), k);
+    return out;
+  }
   frag_timing timing() const {
     frag_timing t{};
     check(frag_result_timing(h_, &t));
@@ -240,6 +247,28 @@ class Engine {
     check(frag_kv_deviation(h_, st.handle(), system.data(), static_cast<int32_t>(system.size()), ids.data(),
                             static_cast<int32_t>(ids.size()), n_layers, cuda_stream, scratch.handle(), dev.data()));
     return dev;
+  }
+
+  // Multi-request batching (frag_reprocess_batch): request b uses fused-cache
+  // rows [b * slot_tokens, ...) of `out`; logits row b = request b's first token.
+  struct Request {
+    std::span<const Token> question;
+    std::span<const ChunkId> chunk_ids;
+    float recompute_ratio = 0.15f;
+    std::span<const Token> system = {};
+  };
+  void reprocess_batch(ChunkStore& st, std::span<const Request> reqs, Result& out, int slot_tokens,
+                       const frag_reprocess_opts* opts = nullptr, void* cuda_stream = nullptr) {
+    std::vector<std::vector<frag_chunk_id>> ids(reqs.size());
+    std::vector<frag_request> cr(reqs.size());
+    for (size_t b = 0; b < reqs.size(); ++b) {
+      for (const auto& c : reqs[b].chunk_ids) ids[b].push_back(to_c(c));
+      cr[b] = frag_request{reqs[b].system.data(), static_cast<int32_t>(reqs[b].system.size()),
+                           reqs[b].question.data(), static_cast<int32_t>(reqs[b].question.size()), ids[b].data(),
+                           static_cast<int32_t>(ids[b].size()), reqs[b].recompute_ratio};
+    }
+    check(frag_reprocess_batch(h_, st.handle(), cr.data(), static_cast<int32_t>(cr.size()), slot_tokens, opts,
+                               cuda_stream, out.handle()));
   }
 
   void full_prefill(std::span<const Token> tokens, Result& out, std::span<const Token> system = {},

@@ -581,10 +581,15 @@ void stitch_launch(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p, in
 // completion is r->layer_ev[l]. The question pass (on `s`) waits for layer l
 // only before its layer-l attention, so the HBM-bound stitch streams under the
 // latency-bound M = |Q| weight stream instead of in front of it.
+// Off by default (FRAG_STITCH_OVERLAP=1 enables it): measured on B200 the
+// request is power-capped end to end (sw_power_cap, ~1.45 GHz), so hiding the
+// 0.7 ms stitch under the question pass moved no TTFT (45.9 vs 45.8 ms), while
+// 32 per-layer launches run the HBM stream at half the bandwidth of the single
+// launch (3.0 vs 5.9 TB/s) -- kept as an option for uncapped parts.
 bool stitch_overlap_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("FRAG_STITCH_OVERLAP");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }

@@ -222,3 +222,42 @@ def test_fkvc_loader_thread_overlaps_requests(tiny, tmp_path):
         assert np.array_equal(res.logits(), want)
     th.join()
     assert not err and len(st2) == 8
+
+
+_OVERLAP_SNIPPET = r"""
+import hashlib, sys, numpy as np
+sys.path.insert(0, '.')
+from paper_2601_12904_b200 import fusion as F
+eng = F.Engine("tiny", seed=1234)
+store = F.ChunkKVStore(eng.cfg)
+rng = np.random.default_rng(5)
+system = rng.integers(0, eng.cfg.vocab, 8).tolist()
+chunks = [rng.integers(0, eng.cfg.vocab, 256).tolist() for _ in range(8)]
+ids = [eng.preprocess_isolated(store, c, system=system) for c in chunks]
+question = rng.integers(0, eng.cfg.vocab, 32).tolist()
+res = F.Result(eng, 8 + 8 * 256 + 32 + 64)
+h = hashlib.sha256()
+for i in range(3):  # eager, capture, replay
+    eng.reprocess(store, question, ids, 0.15, res, system=system)
+    k, v = res.fused_kv()
+    h.update(k.tobytes()); h.update(v.tobytes()); h.update(res.logits().tobytes()); h.update(res.crit().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_stitch_overlap_is_bit_identical(cuda):
+    """K1 per layer on a side stream under the question pass (FRAG_STITCH_OVERLAP=1)
+    gives the same bits as the single-launch stitch, eager and graph-replayed."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    out = {}
+    for ov in ("0", "1"):
+        env = dict(os.environ, FRAG_STITCH_OVERLAP=ov)
+        p = subprocess.run([sys.executable, "-c", _OVERLAP_SNIPPET], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[ov] = p.stdout.strip().splitlines()[-1]
+    assert out["0"] == out["1"]

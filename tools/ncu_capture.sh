@@ -22,5 +22,5 @@ ncu --profile-from-start off --set full --clock-control none --import-source on 
 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:"attn_tc|attn_combine" -s 0 -c 2 -o $OUT/attnq_$TAG python tools/profile_step.py > /dev/null 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:"rope_shift|score_kernel|topk|rmsnorm" -c 6 -o $OUT/mem_$TAG python tools/profile_step.py > /dev/null 2>&1
+    -k regex:"rope_shift|score_tc|score_split|topk|rmsnorm" -c 8 -o $OUT/mem_$TAG python tools/profile_step.py > /dev/null 2>&1
 ls -la $OUT
