@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -77,7 +78,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
   const int num_tiles = m_tiles * n_tiles;
   const int nk = K / BK;
 
+  auto stamp = [&](int k) {
+    if (ep.trace && blockIdx.x < 256) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ep.trace[blockIdx.x * 8 + k] = t;
+    }
+  };
   if (warp == 0 && lane == 0) {
+    stamp(0);
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
@@ -158,6 +167,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
         }
       }
       pdl_wait();
+      stamp(1);
       int stage = 0, it = 0;
       uint32_t phase = 0;
       long long st = first();
@@ -193,6 +203,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (kb == kb0 && lane == 0) stamp(2);
         if (elect_one()) {
           const uint32_t a_base = smem_u32(sA + stage * C::STAGE_BYTES);
           const uint32_t b_base = smem_u32(sB + stage * C::STAGE_BYTES);
@@ -206,6 +217,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
           if (kb == kb1 - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
+        if (kb == kb1 - 1 && lane == 0) stamp(3);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -228,6 +240,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
       const int ti = tile - n_full;  // tail index (workspace / counter slot)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (warp == 2 && lane == 0) stamp(4);
       const int row = m_blk * BM + row_in_tile;
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (S == 0 && !(kb0 == 0 && kb1 == nk)) {
@@ -296,12 +309,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (warp == 2 && lane == 0) stamp(5);
         split_fixup<BN, EPI>(ep, ti, S, sp, ws_rows, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
+  if (warp == 2 && lane == 0) stamp(6);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -370,7 +385,27 @@ int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& e
   const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int slots = num_sms() * C::MIN_BLOCKS;
   const int grid = ep.streamk ? ep.streamk : (work < slots ? work : slots);
-  launch_pdl(gemm_tc_kernel<BN, EPI, AR>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
+  // FRAG_GEMM_TRACE=<file>: tooling only (tools/gemm_trace.py) -- per-CTA
+  // globaltimer stamps [start, after PDL wait, first stage, last MMA,
+  // accumulator ready, partial written, end] appended after the launch
+  static const char* trace_path = std::getenv("FRAG_GEMM_TRACE");
+  static unsigned long long* trace_dev = nullptr;
+  EpiParams et = ep;
+  if (trace_path) {
+    if (!trace_dev) cudaMalloc(&trace_dev, 256 * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_dev, 0, 256 * 8 * sizeof(unsigned long long), stream);
+    et.trace = trace_dev;
+  }
+  launch_pdl(gemm_tc_kernel<BN, EPI, AR>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, ta, tb, M, N, K, et);
+  if (trace_path) {
+    unsigned long long h[256 * 8];
+    cudaMemcpyAsync(h, trace_dev, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    if (FILE* f = std::fopen(trace_path, "ab")) {
+      std::fwrite(h, sizeof(h), 1, f);
+      std::fclose(f);
+    }
+  }
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

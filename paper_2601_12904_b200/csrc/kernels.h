@@ -47,6 +47,7 @@ struct EpiParams {
   int full_tiles = 0;  // tiles before the split tail
   int streamk = 0;     // set by gemm_bf16_tc: stream-K decomposition (one M tile)
   int sk_maxc = 0;     // stream-K: max CTAs sharing one tile (workspace slots per tile)
+  unsigned long long* trace = nullptr;  // tooling: per-CTA globaltimer stamps (FRAG_GEMM_TRACE)
 };
 
 struct GemmTimer;  // optional per-launch event hook (bench roofline)
