@@ -406,7 +406,12 @@ def run_ours(args, rank, world, local_rank):
     # ---- multi-request batching: B requests (this rank's next queries) in one
     # fused cache, one question pass + one sparse pass streaming the weights once
     batch_leg = None
-    if args.batch and args.batch > 1:
+    kv_bytes = 2 * c.layers * T * c.n_kv_heads * c.head_dim * 2
+    free_b = torch.cuda.mem_get_info(dev)[0]
+    if args.batch and args.batch > 1 and args.batch * kv_bytes * 1.3 > free_b:
+        batch_leg = {"skipped": f"{args.batch} x {kv_bytes / 1e9:.1f} GB fused KV does not fit the "
+                                f"{free_b / 1e9:.0f} GB free"}
+    elif args.batch and args.batch > 1:
         B = args.batch
         rb = F.Result(eng, B * T)
         reqs = [(questions[(3 + i) % len(questions)], id_sets[i % len(id_sets)], ratio) for i in range(B)]
