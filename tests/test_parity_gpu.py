@@ -157,12 +157,15 @@ def test_end_to_end_selection_overlap(tiny):
 
 
 @pytest.mark.slow
-def test_llama8b_width_two_layer_parity(cuda):
-    """8B-shaped layers (d=4096, GQA 32/8, dh=128, F=14336, V=128256) at reduced depth."""
+@pytest.mark.parametrize("preset,layers,n_chunks", [("llama3-8b", 2, 4), ("mistral-7b", 2, 4), ("llama3-70b", 1, 2)])
+def test_large_width_reduced_depth_parity(cuda, preset, layers, n_chunks):
+    """Full-width layers of the bench presets at reduced depth: Llama-3-8B (d=4096,
+    GQA 32/8, F=14336, V=128256), Mistral-7B (V=32768, RoPE base 1e6) and
+    Llama-3-70B (d=8192, GQA 64/8 -> 8 heads per KV group, F=28672)."""
     from paper_2601_12904_b200 import fusion as F
-    cfg = F.preset("llama3-8b")
-    cfg.layers = 2
-    t = _setup(cfg, 4, 256, 0, 32)
+    cfg = F.preset(preset)
+    cfg.layers = layers
+    t = _setup(cfg, n_chunks, 256, 0, 32)
     O = t["O"]
     g = _gpu_run(t, 0.15)
     out = t["om"].reprocess(None, t["recs"], t["question"], 0.15, inject=g["crit"], emulate_bf16=True)
@@ -171,10 +174,10 @@ def test_llama8b_width_two_layer_parity(cuda):
     gk = O.bf16_bits_to_f32(g["k"])
     assert _rel_l2(gk, rk) <= 3e-2
     # selection on identical inputs (stitched keys, before the sparse pass)
-    N = 4 * 256
+    N = n_chunks * 256
     chunks = [(r["k"], r["v"], r["native_start"], i * 256) for i, r in enumerate(t["recs"])]
     ko, _ = O.stitch(cfg, chunks, N)
-    keys = ko[1]
+    keys = ko[cfg.layers - 1]
     scores, sel = O.select(g["debug"]["q_final"], keys, len(g["crit"]))
     tau = np.sort(scores)[::-1][len(sel) - 1]
     diff = set((g["crit"] - 1).tolist()) ^ set(sel.tolist())
