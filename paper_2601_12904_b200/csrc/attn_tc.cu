@@ -59,11 +59,17 @@ struct AttCfg {
 
 // POLY: every POLY-th pair of P elements takes the FMA-pipe 2^x (ex2_poly)
 // instead of MUFU.EX2, balancing the two pipes (0 = all MUFU).
-template <int DH, int POLY>
+// DUAL (one query tile per CTA: the question pass and decode): the two tile
+// slots share the single Q tile and split every 128-key tile in halves
+// (slot t takes keys t*64 .. t*64+63), so both softmax warp groups and the
+// MMA ping-pong stay busy; the two partial softmaxes (m, l, O) are merged in
+// the epilogue.
+template <int DH, int POLY, bool DUAL = false>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int G, int n_qblocks) {
   using C = AttCfg<DH>;
+  constexpr int KT = DUAL ? AT_KEYS / 2 : AT_KEYS;  // keys per tile slot per K/V tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                       // [QT][Q_TILE]
@@ -126,6 +132,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   int k_hi = p_max + 1;
   if (a.n_splits > 1) k_hi = min(k_hi, (split + 1) * a.split_keys);
   const int n_tiles = k_hi > k_lo ? (k_hi - k_lo + AT_KEYS - 1) / AT_KEYS : 0;
+  const int n_slots = DUAL ? AT_QT : n_qt;  // tile slots in use (DUAL: both on the one Q tile)
 
   if (warp == W_TMA) {
     // ------------------------------------------------------------ TMA producer
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   } else if (warp == W_MMA) {
     // ------------------------------------------------------------ MMA issuer
     if (n_tiles > 0) {
-      constexpr uint32_t idesc_s = umma_idesc_bf16(AT_ROWS, AT_KEYS, 0, 0);
+      constexpr uint32_t idesc_s = umma_idesc_bf16(AT_ROWS, KT, 0, 0);
       constexpr uint32_t idesc_o = umma_idesc_bf16(AT_ROWS, DH, 0, 1);
       mbar_wait(q_full, 0);
       // descriptor templates: only the 14-bit start-address field changes per MMA
@@ -166,8 +173,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256) a.trace[(t * 256 + j) * 4 + 2] = clock64();
         if (elect_one()) {
-          const uint64_t q0 = dq + ((t * C::Q_TILE) >> 4);
-          const uint64_t k0 = dk + ((st * C::KV_BYTES) >> 4);
+          const uint64_t q0 = dq + (((DUAL ? 0 : t) * C::Q_TILE) >> 4);
+          // DUAL: keys t*64.. of the tile = 8 KB into each 128-key K atom
+          const uint64_t k0 = dk + ((st * C::KV_BYTES + (DUAL ? t * KT * 128 : 0)) >> 4);
           const uint32_t d_tmem = tmem + t * C::T_TILE + C::T_S;
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk) {
@@ -188,20 +196,21 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           const uint32_t d_tmem = tmem + t * C::T_TILE + C::T_O;
           const uint32_t p_tmem = tmem + t * C::T_TILE + C::T_S;
 #pragma unroll
-          for (int kk = 0; kk < AT_KEYS / 16; ++kk) {
+          for (int kk = 0; kk < KT / 16; ++kk) {
             // P: 16 keys = 8 packed bf16x2 TMEM columns; V: 16 key rows = 2048 B,
             // MN-major, next 64-wide dh atom at LBO = 128 keys * 128 B
-            umma_bf16_ts(d_tmem, p_tmem + kk * 8, v0 + ((kk * 2048) >> 4), idesc_o, (j | kk) != 0);
+            const int vrow = (DUAL ? t * KT : 0) + kk * 16;
+            umma_bf16_ts(d_tmem, p_tmem + kk * 8, v0 + ((vrow * 128) >> 4), idesc_o, (j | kk) != 0);
           }
           umma_commit(&pv_done[t]);
-          if (t == n_qt - 1) umma_commit(&kv_empty[st]);
+          if (t == n_slots - 1) umma_commit(&kv_empty[st]);
         }
         __syncwarp();
       };
-      for (int t = 0; t < n_qt; ++t) issue_s(t, 0);
+      for (int t = 0; t < n_slots; ++t) issue_s(t, 0);
       for (int j = 0; j < n_tiles; ++j) {
         mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-        for (int t = 0; t < n_qt; ++t) {
+        for (int t = 0; t < n_slots; ++t) {
           issue_pv(t, j);
           if (j + 1 < n_tiles) issue_s(t, j + 1);
         }
@@ -209,46 +218,47 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
-    const int t = warp >> 2;  // query tile of this warp group
-    if (t < n_qt) {
+    const int t = warp >> 2;  // query tile (DUAL: key half) of this warp group
+    const int tq = DUAL ? 0 : t;  // query tile of this warp group's rows
+    if (t < n_slots) {
       const int q4 = warp & 3;
       const int r = q4 * 32 + lane;  // query row within the tile = TMEM lane
-      const int tl = (t * AT_ROWS + r) / G;
+      const int tl = (tq * AT_ROWS + r) / G;
       const int tok = t0 + tl;
       const int head = hk * G + r % G;
       const bool live = tok < a.M;
       const int prow = live ? a.rows[tok] - a.row_base : -1;
-      const int p_min = a.rows[t0 + t * tok_per_tile] - a.row_base;
+      const int p_min = a.rows[t0 + tq * tok_per_tile] - a.row_base;
       const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16) + t * C::T_TILE;
       const float c = a.scale * 1.4426950408889634f;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_tiles; ++j) {
-        const int key0 = k_lo + j * AT_KEYS;
+        const int key0 = k_lo + j * AT_KEYS + (DUAL ? t * KT : 0);
         mbar_wait(&s_full[t], j & 1);
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && (warp & 3) == 0 && j < 256)
           a.trace[(t * 256 + j) * 4 + 0] = clock64();
-        uint32_t s[AT_KEYS];
+        uint32_t s[KT];
 #pragma unroll
-        for (int cc = 0; cc < AT_KEYS / 32; ++cc)
+        for (int cc = 0; cc < KT / 32; ++cc)
           tmem_ld32(lane_base + C::T_S + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[cc * 32]));
         tmem_ld_wait();
         // causal mask by position (keys > p_row or beyond the split), raw scores
         const int lim = min(prow, k_hi - 1) - key0;
-        if ((key0 + AT_KEYS - 1 > p_min) || (key0 + AT_KEYS > k_hi)) {
+        if ((key0 + KT - 1 > p_min) || (key0 + KT > k_hi)) {
 #pragma unroll
-          for (int k = 0; k < AT_KEYS; ++k)
+          for (int k = 0; k < KT; ++k)
             if (k > lim) s[k] = 0xff800000u;  // -inf
         }
         float mx8[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(s[e]);
 #pragma unroll
-        for (int k = 8; k < AT_KEYS - 8; k += 16)
+        for (int k = 8; k < KT - 8; k += 16)
 #pragma unroll
           for (int e = 0; e < 8; ++e) mx8[e] = fmax3(mx8[e], __uint_as_float(s[k + e]), __uint_as_float(s[k + 8 + e]));
 #pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(mx8[e], __uint_as_float(s[AT_KEYS - 8 + e]));
+        for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(mx8[e], __uint_as_float(s[KT - 8 + e]));
         const float mt = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])) * c;
         // lazy rescale: only when the max grows by more than 2^8
         const bool grow = mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt != -INFINITY);
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const float mneg = m_used == -INFINITY ? 0.f : -m_used;
         float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < KT / 64; ++half) {
           uint32_t pk[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
@@ -304,14 +314,50 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
         tc_fence_after();
       }
+      float a0 = 1.f, a1 = 0.f;  // DUAL: weights of the two key halves' partial O
+      if constexpr (DUAL) {
+        // slot 1 publishes (m, l) of its key half in the unused second Q slot;
+        // slot 0 merges: m = max, O = (O0 2^(m0-m) + O1 2^(m1-m)) / (l0 2^(m0-m) + l1 2^(m1-m))
+        float* pub = reinterpret_cast<float*>(sQ + C::Q_TILE);
+        if (t == 1) {
+          pub[r] = m_used;
+          pub[AT_ROWS + r] = l;
+        }
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        if (t == 1) {
+          m_used = -INFINITY;  // nothing to store for slot 1
+          l = 0.f;
+        } else {
+          const float m1 = pub[r], l1 = pub[AT_ROWS + r];
+          if (n_tiles > 0) {
+            mbar_wait(&pv_done[1], (n_tiles - 1) & 1);
+            tc_fence_after();
+          }
+          const float m = fmaxf(m_used, m1);
+          a0 = m_used == -INFINITY ? 0.f : ex2_approx(m_used - m);
+          a1 = m1 == -INFINITY ? 0.f : ex2_approx(m1 - m);
+          l = l * a0 + l1 * a1;
+          m_used = m;
+        }
+      }
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const size_t qi = (size_t)tok * a.Hq + head;
+      const bool writer = !(DUAL && t == 1);  // warp-uniform: slot 1's half was merged by slot 0
 #pragma unroll 1
-      for (int cc = 0; cc < DH / 32; ++cc) {
+      for (int cc = 0; cc < (writer ? DH / 32 : 0); ++cc) {
         uint32_t o[32];
         if (n_tiles > 0) {
           tmem_ld32(lane_base + C::T_O + cc * 32, o);
-          tmem_ld_wait();
+          if constexpr (DUAL) {
+            uint32_t o1[32];
+            tmem_ld32(lane_base + C::T_TILE + C::T_O + cc * 32, o1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              o[e] = __float_as_uint(__uint_as_float(o[e]) * a0 + __uint_as_float(o1[e]) * a1);
+          } else {
+            tmem_ld_wait();
+          }
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = 0u;
@@ -336,7 +382,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           }
         }
       }
-      if (live && a.n_splits > 1) {
+      if (writer && live && a.n_splits > 1) {
         // natural-log LSE of the scaled scores: m (log2 units) * ln2 + ln(l)
         a.part_lse[(size_t)split * a.M * a.Hq + qi] =
             l > 0.f ? m_used * 0.6931471805599453f + __logf(l) : -INFINITY;
@@ -392,6 +438,18 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
       }
     }
   };
+  // one query tile per CTA (question pass, decode): split each key tile
+  // between the two slots instead of leaving one idle
+  const bool dual = a.M <= AT_ROWS / G;
+  if (dual) {
+    if (a.dh == 128)
+      go(attn_tc_kernel<128, 0, true>, (int)AttCfg<128>::SMEM);
+    else if (a.dh == 64)
+      go(attn_tc_kernel<64, 0, true>, (int)AttCfg<64>::SMEM);
+    else
+      return -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+  }
   if (a.dh == 128) {
     constexpr int SM = (int)AttCfg<128>::SMEM;
     switch (poly) {
