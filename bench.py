@@ -504,10 +504,13 @@ def main():
         except Exception:
             traffic = None
     c = r["cfg"]
-    # attention FLOPs: 4*Hq*dh*L*sum_rows(p_i) (each query row sees exactly p_i keys)
+    # attention FLOPs: 4*Hq*dh*sum_rows(p_i) per layer (each query row sees exactly
+    # p_i keys); the last layer attends only for the logit row (no other
+    # consumer of its output)
     crit = r["crit"]
     qpos = np.arange(T - r["w"]["qlen"] + 1, T + 1)
-    attn_flops = 4.0 * c.n_heads * c.head_dim * c.layers * (float(np.sum(crit)) + float(np.sum(qpos)))
+    attn_flops = 4.0 * c.n_heads * c.head_dim * ((c.layers - 1) * (float(np.sum(crit)) + float(np.sum(qpos)))
+                                                 + float(T))
     a = r["prof"][1]
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,

@@ -314,7 +314,8 @@ void result_init(Result* r, Engine* e, int max_tokens) {
 
 // ---------------------------------------------------------------- run_rows
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
-              int n_logit_rows, int n_layers, const cudaEvent_t* layer_ready, const std::vector<Seg>* segs_in) {
+              int n_logit_rows, int n_layers, const cudaEvent_t* layer_ready, const std::vector<Seg>* segs_in,
+              int keep_last) {
   if (M <= 0) return;
   const auto& c = e->cfg;
   const int L = (n_layers > 0 && n_layers < c.layers) ? n_layers : c.layers;
@@ -399,8 +400,28 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     }
     if (mode != PASS_FULL && l == L - 1) break;
     if (layer_ready) check_cuda(cudaStreamWaitEvent(s, layer_ready[l], 0), "wait stitched layer");
-    for (size_t si = 0; si < segs.size(); ++si) {
-      const Seg& g = segs[si];
+    // Last layer: every row's K/V are in the cache now (the QKV epilogue), and
+    // only the trailing keep_last rows' hidden states feed anything (the
+    // logits); the other rows' last-layer attention, O projection and MLP have
+    // no consumer, so the rest of the layer runs on those rows only.
+    const bool prune = mode == PASS_FULL && l == c.layers - 1 && keep_last > 0 && keep_last < M && !segs_in;
+    const int Ml = prune ? keep_last : M;
+    const size_t off = (size_t)(M - Ml);
+    std::vector<Seg> last_seg;
+    std::vector<std::pair<int, int>> last_split;
+    if (prune) {
+      last_seg.push_back(Seg{(int)off, Ml, 0, T});
+      last_split.resize(1);
+      split_policy(Ml, T, last_split[0].first, last_split[0].second);
+      if (last_split[0].first > 1) {
+        r->part_o.ensure((size_t)last_split[0].first * Ml * qc * sizeof(float));
+        r->part_lse.ensure((size_t)last_split[0].first * Ml * Hq * sizeof(float));
+      }
+    }
+    const std::vector<Seg>& asegs = prune ? last_seg : segs;
+    const std::vector<std::pair<int, int>>& asplit = prune ? last_split : seg_split;
+    for (size_t si = 0; si < asegs.size(); ++si) {
+      const Seg& g = asegs[si];
       if (g.M <= 0) continue;
       fragk::AttnArgs a{};
       a.q = r->q.as<bf16>() + (size_t)g.off * qc;
@@ -416,8 +437,8 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       a.Hq = Hq;
       a.Hkv = Hkv;
       a.dh = dh;
-      a.split_keys = seg_split[si].second;
-      a.n_splits = seg_split[si].first;
+      a.split_keys = asplit[si].second;
+      a.n_splits = asplit[si].first;
       a.scale = 1.0f / std::sqrt((float)dh);
       Scoped sc(P, s, KC_ATTN, 0, 0);
       sc.launched(fragk::sparse_q_attention(a, s));
@@ -425,31 +446,32 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     {
       fragk::EpiParams ep;
       with_ws(ep);
-      ep.resid = h;
+      ep.resid = h + off * d;
       ep.ldo = d;
-      Scoped sc(P, s, gemm_class(M), 2.0 * M * d * qc, 2.0 * (qc * d + (double)M * qc) + 8.0 * M * d);
-      sc.launched(fragk::gemm_bf16_tc(r->attn.as<bf16>(), W.wo, M, d, (int)qc, fragk::EPI_RESID, ep, s));
+      Scoped sc(P, s, gemm_class(Ml), 2.0 * Ml * d * qc, 2.0 * (qc * d + (double)Ml * qc) + 8.0 * Ml * d);
+      sc.launched(fragk::gemm_bf16_tc(r->attn.as<bf16>() + off * qc, W.wo, Ml, d, (int)qc, fragk::EPI_RESID, ep, s));
     }
     {
-      Scoped sc(P, s, KC_NORM, 0, (double)M * d * (4 + 2));
-      fragk::rmsnorm(h, M, d, W.ffn_norm, c.norm_eps, x, s);
+      Scoped sc(P, s, KC_NORM, 0, (double)Ml * d * (4 + 2));
+      fragk::rmsnorm(h + off * d, Ml, d, W.ffn_norm, c.norm_eps, x + off * d, s);
       sc.launched(1);
     }
     {
       fragk::EpiParams ep;
       with_ws(ep);
-      ep.out_bf16 = r->act.as<bf16>();
+      ep.out_bf16 = r->act.as<bf16>() + off * F;
       ep.ldo = F;
-      Scoped sc(P, s, gemm_class(M), 2.0 * M * 2.0 * F * d, 2.0 * (2.0 * F * d + (double)M * d + (double)M * F));
-      sc.launched(fragk::gemm_bf16_tc(x, W.wgu, M, 2 * F, d, fragk::EPI_SWIGLU, ep, s));
+      Scoped sc(P, s, gemm_class(Ml), 2.0 * Ml * 2.0 * F * d, 2.0 * (2.0 * F * d + (double)Ml * d + (double)Ml * F));
+      sc.launched(fragk::gemm_bf16_tc(x + off * d, W.wgu, Ml, 2 * F, d, fragk::EPI_SWIGLU, ep, s));
     }
     {
       fragk::EpiParams ep;
       with_ws(ep);
-      ep.resid = h;
+      ep.resid = h + off * d;
       ep.ldo = d;
-      Scoped sc(P, s, gemm_class(M), 2.0 * M * (double)d * F, 2.0 * ((double)F * d + (double)M * F) + 8.0 * M * d);
-      sc.launched(fragk::gemm_bf16_tc(r->act.as<bf16>(), W.wd, M, d, F, fragk::EPI_RESID, ep, s));
+      Scoped sc(P, s, gemm_class(Ml), 2.0 * Ml * (double)d * F,
+                2.0 * ((double)F * d + (double)Ml * F) + 8.0 * Ml * d);
+      sc.launched(fragk::gemm_bf16_tc(r->act.as<bf16>() + off * F, W.wd, Ml, d, F, fragk::EPI_RESID, ep, s));
     }
     peek("layer");
   }
@@ -1004,7 +1026,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     peek("select");
     ev_record(r, timing, 3, bs);
     // sparse_prefill (Eq. 9) to the first-token logits
-    run_rows(e, r, bs, M, T, PASS_FULL, nullptr, 0);
+    run_rows(e, r, bs, M, T, PASS_FULL, nullptr, 0, 0, nullptr, nullptr, r->logit_rows);
     ev_record(r, timing, 4, bs);
     {
       // final norm + lm_head on the logit rows (K3 + K11)
@@ -1263,7 +1285,7 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
   map_h[0] = n_tok - 1;
   check_cuda(cudaMemcpyAsync(r->row_map.p, map_h, sizeof(int), cudaMemcpyHostToDevice, s), "map");
   ev_record(r, timing, 3, s);
-  run_rows(e, r, s, n_tok, T, PASS_FULL, r->row_map.as<int>(), 1);
+  run_rows(e, r, s, n_tok, T, PASS_FULL, r->row_map.as<int>(), 1, 0, nullptr, nullptr, 1);
   ev_record(r, timing, 4, s);
   ev_record(r, timing, 5, s);
   r->logits_on_device = o && o->logits_on_device;

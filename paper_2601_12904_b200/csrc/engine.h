@@ -263,7 +263,10 @@ struct Seg {
 };
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
               int n_logit_rows, int n_layers = 0, const cudaEvent_t* layer_ready = nullptr,
-              const std::vector<Seg>* segs = nullptr);
+              const std::vector<Seg>* segs = nullptr, int keep_last = 0);
+// keep_last > 0 (PASS_FULL, one sequence): only the trailing keep_last rows'
+// final-layer hidden states are needed (the logit rows), so the last layer
+// runs attention / O / MLP on those rows only (all rows' K/V still written).
 
 void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
                bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio, const frag_reprocess_opts* o,
