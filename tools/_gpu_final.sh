@@ -3,4 +3,4 @@ timeout 900 python -m pytest tests -q -x -m gpu -p no:cacheprovider > gpurun_out
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_final.log 2>&1; tail -1 gpurun_out/bench_final.log | cut -c1-300
 timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-300
-timeout 1500 bash tools/ncu_capture.sh r01c > gpurun_out/cap.log 2>&1; ls gpurun_out
+timeout 1500 bash tools/ncu_capture.sh r01d > gpurun_out/cap.log 2>&1; ls gpurun_out
