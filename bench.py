@@ -415,7 +415,8 @@ def run_ours(args, rank, world, local_rank):
         B = args.batch
         rb = F.Result(eng, B * T)
         reqs = [(questions[(3 + i) % len(questions)], id_sets[i % len(id_sets)], ratio) for i in range(B)]
-        eng.reprocess_batch(store, reqs, rb, T, stream=stream)  # warm
+        for _ in range(2):  # eager first sighting, then the graph capture; the timed batches replay it
+            eng.reprocess_batch(store, reqs, rb, T, stream=stream, logits_on_device=True)
         torch.cuda.synchronize()
         b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         nb = 3

@@ -405,8 +405,45 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     // logits); the other rows' last-layer attention, O projection and MLP have
     // no consumer, so the rest of the layer runs on those rows only.
     const bool prune = mode == PASS_FULL && l == c.layers - 1 && keep_last > 0 && keep_last < M && !segs_in;
-    const int Ml = prune ? keep_last : M;
-    const size_t off = (size_t)(M - Ml);
+    // batched: keep the last row of every sequence, compacted into the rows
+    // [M, M + n_seq) of the workspaces (their order = the sequences')
+    const bool seg_prune = mode == PASS_FULL && l == c.layers - 1 && keep_last < 0 && segs_in &&
+                           M + (int)segs.size() <= r->max_tokens;
+    const int Ml = prune ? keep_last : (seg_prune ? (int)segs.size() : M);
+    const size_t off = prune ? (size_t)(M - Ml) : (seg_prune ? (size_t)M : 0);
+    if (seg_prune) {
+      for (size_t si = 0; si < segs.size(); ++si) {
+        const Seg& g = segs[si];
+        const size_t src = (size_t)g.off + g.M - 1;
+        check_cuda(cudaMemcpyAsync(h + (off + si) * d, h + src * d, d * sizeof(float), cudaMemcpyDeviceToDevice, s),
+                   "gather last rows");
+        int ns, sk;
+        split_policy(1, g.T, ns, sk);
+        if (ns > 1) {
+          r->part_o.ensure((size_t)ns * qc * sizeof(float));
+          r->part_lse.ensure((size_t)ns * Hq * sizeof(float));
+        }
+        fragk::AttnArgs a{};
+        a.q = r->q.as<bf16>() + src * qc;
+        a.k = kf + l * lstride + (size_t)g.base * kvc;
+        a.v = vf + l * lstride + (size_t)g.base * kvc;
+        a.rows = prow + src;
+        a.row_base = g.base;
+        a.out = r->attn.as<bf16>() + (off + si) * qc;
+        a.part_o = r->part_o.as<float>();
+        a.part_lse = r->part_lse.as<float>();
+        a.M = 1;
+        a.T = g.T;
+        a.Hq = Hq;
+        a.Hkv = Hkv;
+        a.dh = dh;
+        a.split_keys = sk;
+        a.n_splits = ns;
+        a.scale = 1.0f / std::sqrt((float)dh);
+        Scoped sc(P, s, KC_ATTN, 0, 0);
+        sc.launched(fragk::sparse_q_attention(a, s));
+      }
+    }
     std::vector<Seg> last_seg;
     std::vector<std::pair<int, int>> last_split;
     if (prune) {
@@ -418,7 +455,8 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
         r->part_lse.ensure((size_t)last_split[0].first * Ml * Hq * sizeof(float));
       }
     }
-    const std::vector<Seg>& asegs = prune ? last_seg : segs;
+    static const std::vector<Seg> no_segs;
+    const std::vector<Seg>& asegs = prune ? last_seg : (seg_prune ? no_segs : segs);
     const std::vector<std::pair<int, int>>& asplit = prune ? last_split : seg_split;
     for (size_t si = 0; si < asegs.size(); ++si) {
       const Seg& g = asegs[si];
@@ -1161,7 +1199,10 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
     check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, Qtot * sizeof(int), cudaMemcpyHostToDevice, s), "q rows");
     check_cuda(cudaMemcpyAsync(r->plan_tok.p, r->q_tok.p, Qtot * sizeof(int), cudaMemcpyDeviceToDevice, s), "q plan");
     int* map_h = stg.take<int>(B);
-    for (int b = 0; b < B; ++b) map_h[b] = br[b].plan_off + br[b].k + br[b].nq - 1;
+    // logits rows: the sparse pass keeps each request's last row, compacted
+    // after the plan rows (last-layer pruning of run_rows)
+    const bool compact = Mtot + B <= r->max_tokens;
+    for (int b = 0; b < B; ++b) map_h[b] = compact ? Mtot + b : br[b].plan_off + br[b].k + br[b].nq - 1;
     check_cuda(cudaMemcpyAsync(r->row_map.p, map_h, B * sizeof(int), cudaMemcpyHostToDevice, s), "map");
   }
   if (maxN > 0) {
@@ -1179,65 +1220,74 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
     psegs.push_back(Seg{br[b].plan_off, br[b].k + br[b].nq, b * slot, br[b].T});
   }
 
-  // ---- device body (eager: one batch shape is rarely repeated)
-  ev_record(r, timing, 0, s);
-  stitch_launch(e, r, s, sp);
-  ev_record(r, timing, 1, s);
-  run_rows(e, r, s, Qtot, slot, PASS_QUESTION, nullptr, 0, 0, nullptr, &qsegs);
-  ev_record(r, timing, 2, s);
-  for (int b = 0; b < B; ++b) {
-    const auto& q = br[b];
-    if (q.N > 0) {
-      fragk::ScoreArgs a{};
-      a.q = r->q_final.as<float>() + (size_t)qofs[b] * c.n_heads * c.head_dim;
-      a.k = r->k_fused.as<bf16>() + (size_t)(c.layers - 1) * r->max_tokens * kvc + (size_t)b * slot * kvc;
-      a.nq = q.nq;
-      a.Hq = c.n_heads;
-      a.Hkv = c.n_kv_heads;
-      a.dh = c.head_dim;
-      a.key_row0 = q.S;
-      a.n_keys = q.N;
-      a.scale = 1.0f / std::sqrt((float)c.head_dim);
-      a.part_ms = r->part_ms.as<float2>();
-      a.row_ms = r->row_ms.as<float2>();
-      a.scores = r->scores.as<float>() + cofs[b];
-      a.raw = raw;
-      a.col_part = r->score_col.as<float>();
-      a.q_split = r->score_q.as<bf16>();
-      Scoped sc(e->prof, s, KC_SELECT, 4.0 * q.nq * c.n_heads * (double)q.N * c.head_dim,
-                2.0 * q.N * (double)kvc * 2);
-      sc.launched(fragk::qg_score(a, s));
+  // ---- device body: captured into a CUDA graph per batch shape (like a
+  // single request's body) and replayed from the third batch of that shape on
+  auto body = [&](cudaStream_t s) {
+    ev_record(r, timing, 0, s);
+    stitch_launch(e, r, s, sp);
+    ev_record(r, timing, 1, s);
+    run_rows(e, r, s, Qtot, slot, PASS_QUESTION, nullptr, 0, 0, nullptr, &qsegs);
+    ev_record(r, timing, 2, s);
+    for (int b = 0; b < B; ++b) {
+      const auto& q = br[b];
+      if (q.N > 0) {
+        fragk::ScoreArgs a{};
+        a.q = r->q_final.as<float>() + (size_t)qofs[b] * c.n_heads * c.head_dim;
+        a.k = r->k_fused.as<bf16>() + (size_t)(c.layers - 1) * r->max_tokens * kvc + (size_t)b * slot * kvc;
+        a.nq = q.nq;
+        a.Hq = c.n_heads;
+        a.Hkv = c.n_kv_heads;
+        a.dh = c.head_dim;
+        a.key_row0 = q.S;
+        a.n_keys = q.N;
+        a.scale = 1.0f / std::sqrt((float)c.head_dim);
+        a.part_ms = r->part_ms.as<float2>();
+        a.row_ms = r->row_ms.as<float2>();
+        a.scores = r->scores.as<float>() + cofs[b];
+        a.raw = raw;
+        a.col_part = r->score_col.as<float>();
+        a.q_split = r->score_q.as<bf16>();
+        Scoped sc(e->prof, s, KC_SELECT, 4.0 * q.nq * c.n_heads * (double)q.N * c.head_dim,
+                  2.0 * q.N * (double)kvc * 2);
+        sc.launched(fragk::qg_score(a, s));
+      }
+      Scoped sc(e->prof, s, KC_SELECT, 0, 4.0 * q.N * 6);
+      sc.launched(fragk::topk_plan(r->scores.as<float>() + cofs[b], q.N, q.k, b * slot + q.S,
+                                   r->chunk_tok.as<int>() + cofs[b], r->q_tok.as<int>() + qofs[b], q.nq,
+                                   b * slot + q.T - q.nq, r->plan_rows.as<int>() + q.plan_off,
+                                   r->plan_tok.as<int>() + q.plan_off, s));
     }
-    Scoped sc(e->prof, s, KC_SELECT, 0, 4.0 * q.N * 6);
-    sc.launched(fragk::topk_plan(r->scores.as<float>() + cofs[b], q.N, q.k, b * slot + q.S,
-                                 r->chunk_tok.as<int>() + cofs[b], r->q_tok.as<int>() + qofs[b], q.nq,
-                                 b * slot + q.T - q.nq, r->plan_rows.as<int>() + q.plan_off,
-                                 r->plan_tok.as<int>() + q.plan_off, s));
-  }
-  peek("batch select");
-  ev_record(r, timing, 3, s);
-  run_rows(e, r, s, Mtot, slot, PASS_FULL, nullptr, 0, 0, nullptr, &psegs);
-  ev_record(r, timing, 4, s);
-  {
-    const int d = c.d_model;
+    peek("batch select");
+    ev_record(r, timing, 3, s);
+    run_rows(e, r, s, Mtot, slot, PASS_FULL, nullptr, 0, 0, nullptr, &psegs, -1);
+    ev_record(r, timing, 4, s);
     {
-      Scoped sc(e->prof, s, KC_NORM, 0, (double)B * d * 6);
-      fragk::rmsnorm(r->h.as<float>(), B, d, e->final_norm, c.norm_eps, r->lm_x.as<bf16>(), s, r->row_map.as<int>());
-      sc.launched(1);
+      const int d = c.d_model;
+      {
+        Scoped sc(e->prof, s, KC_NORM, 0, (double)B * d * 6);
+        fragk::rmsnorm(r->h.as<float>(), B, d, e->final_norm, c.norm_eps, r->lm_x.as<bf16>(), s, r->row_map.as<int>());
+        sc.launched(1);
+      }
+      fragk::EpiParams ep;
+      ep.ws = r->gemm_ws.as<float>();
+      ep.ws_bytes = r->gemm_ws.bytes;
+      ep.counters = r->gemm_cnt.as<int>();
+      ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
+      ep.out_f32 = r->logits.as<float>();
+      ep.ldo = c.vocab;
+      Scoped sc(e->prof, s, gemm_class(B), 2.0 * B * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
+      sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, B, c.vocab, d, fragk::EPI_STORE_F32, ep, s));
     }
-    fragk::EpiParams ep;
-    ep.ws = r->gemm_ws.as<float>();
-    ep.ws_bytes = r->gemm_ws.bytes;
-    ep.counters = r->gemm_cnt.as<int>();
-    ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
-    ep.out_f32 = r->logits.as<float>();
-    ep.ldo = c.vocab;
-    Scoped sc(e->prof, s, gemm_class(B), 2.0 * B * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
-    sc.launched(fragk::gemm_bf16_tc(r->lm_x.as<bf16>(), e->lm_head, B, c.vocab, d, fragk::EPI_STORE_F32, ep, s));
-  }
-  peek("batch lm_head");
-  ev_record(r, timing, 5, s);
-  logits_d2h(r, s);
+    peek("batch lm_head");
+    ev_record(r, timing, 5, s);
+    logits_d2h(r, s);
+  };
+  uint64_t sig = 0xcbf29ce484222325ULL;  // batch shape: every request's (T, S, N, |Q|, k)
+  for (const auto& q : br)
+    for (int v : {q.T, q.S, q.N, q.nq, q.k}) sig = (sig ^ (uint64_t)(uint32_t)v) * 0x100000001b3ULL;
+  GraphKey key{B * slot, -2 - B, Ntot, Qtot, Mtot - Qtot, 0, 0, (int)raw, (int)r->logits_on_device, sp.n_desc,
+               sp.max_rows, (int)(sig & 0x7fffffff), (uint64_t)(uintptr_t)e->rope.p ^ (sig << 1)};
+  run_graphed(r, s, !timing && !e->prof.on, key, body);
   // per-request critical positions (host copies for frag_result_batch_crit)
   std::vector<int32_t> plan_h((size_t)Mtot);
   check_cuda(cudaMemcpyAsync(plan_h.data(), r->plan_rows.p, Mtot * sizeof(int), cudaMemcpyDeviceToHost, s), "plan");
