@@ -259,3 +259,62 @@ def test_preprocess_fused(cuda):
     assert _rel_l2(k_fu, ko) <= 2e-2 and _cos(k_fu, ko) >= 0.999
     with pytest.raises(F.StoreError, match="missing neighbour"):
         eng.preprocess_fused(store, c3, [F.hash_tokens([1, 2, 3])], dst=out)
+
+
+@pytest.mark.parametrize("lens,S,nq,ratio", [((37, 256, 1, 129), 3, 1, 0.15), ((300, 5), 0, 7, 0.5),
+                                             ((1,), 1, 2, 1.0), ((64, 64, 64), 8, 32, 0.0)])
+def test_ragged_chunks_parity(cuda, lens, S, nq, ratio):
+    """Ragged inputs (chunks of 1..300 tokens, 0-8 system tokens, 1-32 question
+    tokens, r from 0 to 1): stitched rows bit-exact, selection invariants, and
+    logits / recomputed rows vs the bf16-emulating oracle (injection mode)."""
+    from paper_2601_12904_b200 import fusion as F
+    from oracle import oracle as O
+    eng = F.Engine("tiny", seed=99)
+    c = eng.cfg
+    store = F.ChunkKVStore(c)
+    rng = np.random.default_rng(sum(lens) + S)
+    system = rng.integers(0, c.vocab, S).tolist()
+    chunks = [rng.integers(0, c.vocab, n).tolist() for n in lens]
+    ids = [eng.preprocess_isolated(store, ch, system=system) for ch in chunks]
+    question = rng.integers(0, c.vocab, nq).tolist()
+    N = sum(lens)
+    T = S + N + nq
+    res = F.Result(eng, T)
+    eng.reprocess(store, question, ids, ratio, res, system=system)
+    k, v = res.fused_kv()
+    crit = res.crit()
+    assert len(crit) == int(np.floor(ratio * N + 0.5))
+    assert np.all(np.diff(crit) > 0) and (len(crit) == 0 or (crit.min() > S and crit.max() <= S + N))
+    om = O.Model(c).load_from_engine(eng)
+    recs = []
+    for i, ch in zip(ids, chunks):
+        rk, rv = store.read_kv(i)
+        recs.append({"k": O.bf16_bits_to_f32(rk), "v": O.bf16_bits_to_f32(rv), "tokens": ch, "native_start": S + 1})
+    sys_kv = (O.bf16_bits_to_f32(k[:, :S]), O.bf16_bits_to_f32(v[:, :S])) if S else None
+    out = om.reprocess(sys_kv, recs, question, ratio, inject=crit, emulate_bf16=True)
+    fresh = np.zeros(T, bool)
+    fresh[crit - 1] = True
+    fresh[T - nq:] = True
+    ok = O.f32_to_bf16_bits(out["k"])
+    assert np.array_equal(k[:, ~fresh], ok[:, ~fresh])  # stitched rows (K1) bit-exact
+    assert _rel_l2(res.logits()[0], out["logits"]) <= 2e-2 and _cos(res.logits()[0], out["logits"]) >= 0.999
+    gk, rk = O.bf16_bits_to_f32(k[:, fresh]), O.bf16_bits_to_f32(ok[:, fresh])
+    assert _rel_l2(gk, rk) <= 2e-2
+
+
+def test_no_chunks_is_question_prefill(cuda):
+    """A request with no retrieved chunks is the plain prefill of cat(S, Q)."""
+    from paper_2601_12904_b200 import fusion as F
+    eng = F.Engine("tiny", seed=99)
+    store = F.ChunkKVStore(eng.cfg)
+    rng = np.random.default_rng(3)
+    system = rng.integers(0, eng.cfg.vocab, 4).tolist()
+    question = rng.integers(0, eng.cfg.vocab, 12).tolist()
+    res = F.Result(eng, 16)
+    eng.reprocess(store, question, [], 0.15, res, system=system)
+    assert len(res.crit()) == 0
+    fa = F.Result(eng, 16)
+    eng.full_prefill(question, fa, system=system)
+    assert _rel_l2(res.logits()[0], fa.logits()[0]) <= 1e-2
+    assert np.argmax(res.logits()[0]) == np.argmax(fa.logits()[0]) or \
+        np.sort(fa.logits()[0])[-1] - np.sort(fa.logits()[0])[-2] < 1e-2
