@@ -64,11 +64,15 @@ struct AttCfg {
 // (slot t takes keys t*64 .. t*64+63), so both softmax warp groups and the
 // MMA ping-pong stay busy; the two partial softmaxes (m, l, O) are merged in
 // the epilogue.
-template <int DH, int POLY, bool DUAL = false>
-__global__ void __launch_bounds__(AT_THREADS, 1)
+// SPLIT (default for dh=128): two softmax threads per query
+// row (16 softmax warps: warps w and w+4 of a tile share TMEM lanes and take
+// 64 of the 128 keys each, the row max exchanged through shared memory).
+template <int DH, int POLY, bool DUAL = false, bool SPLIT = false>
+__global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int G, int n_qblocks) {
   using C = AttCfg<DH>;
+  static_assert(!(DUAL && SPLIT), "DUAL and SPLIT are separate variants");
   constexpr int KT = DUAL ? AT_KEYS / 2 : AT_KEYS;  // keys per tile slot per K/V tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   // warps 0-3 softmax A, 4-7 softmax B, 8 TMA, 9 MMA (the highest warp id wins
   // issue arbitration on its sub-partition, which keeps MMA issue off the
   // softmax critical path)
-  constexpr int W_TMA = 8, W_MMA = 9;
+  constexpr int W_TMA = SPLIT ? 16 : 8, W_MMA = W_TMA + 1;
   if (warp == W_TMA && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     }
     for (int t = 0; t < AT_QT; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 4);
+      mbar_init(&p_full[t], SPLIT ? 8 : 4);
       mbar_init(&pv_done[t], 1);
     }
     fence_mbar_init();
@@ -215,6 +219,135 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           if (j + 1 < n_tiles) issue_s(t, j + 1);
         }
       }
+    }
+  } else if constexpr (SPLIT) {
+    // ------------------------------------------------------------ split-row softmax / epilogue
+    __shared__ float xm[AT_QT][2][2][AT_ROWS];  // [tile][iteration parity][half][row] partial max
+    __shared__ float xl[AT_QT][2][AT_ROWS];     // [tile][half][row] partial row sum
+    const int t = warp >> 3, half = (warp >> 2) & 1, q4 = warp & 3;
+    if (t < n_qt) {
+      const int r = q4 * 32 + lane;
+      const int tl = (t * AT_ROWS + r) / G;
+      const int tok = t0 + tl;
+      const int head = hk * G + r % G;
+      const bool live = tok < a.M;
+      const int prow = live ? a.rows[tok] - a.row_base : -1;
+      const int p_min = a.rows[t0 + t * tok_per_tile] - a.row_base;
+      const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16) + t * C::T_TILE;
+      const float c = a.scale * 1.4426950408889634f;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int key0 = k_lo + j * AT_KEYS + half * 64;
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+        uint32_t sa[32], sb[32];
+        tmem_ld32(lane_base + C::T_S + half * 64, sa);
+        tmem_ld32(lane_base + C::T_S + half * 64 + 32, sb);
+        tmem_ld_wait();
+#define SV(k) (*((k) < 32 ? &sa[(k) & 31] : &sb[(k) & 31]))
+        const int lim = min(prow, k_hi - 1) - key0;
+        if ((key0 + 63 > p_min) || (key0 + 64 > k_hi)) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k)
+            if (k > lim) SV(k) = 0xff800000u;
+        }
+        float mx4[4] = {__uint_as_float(sa[0]), __uint_as_float(sa[1]), __uint_as_float(sa[2]), __uint_as_float(sa[3])};
+#pragma unroll
+        for (int k = 4; k < 60; k += 8)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) mx4[e] = fmax3(mx4[e], __uint_as_float(SV(k + e)), __uint_as_float(SV(k + 4 + e)));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mx4[e] = fmaxf(mx4[e], __uint_as_float(sb[28 + e]));
+        xm[t][j & 1][half][r] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
+        const float mt = fmaxf(xm[t][j & 1][0][r], xm[t][j & 1][1][r]) * c;
+        const bool grow = mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt != -INFINITY);
+        const float m_new = grow ? fmaxf(mt, m_used) : m_used;
+        const float alpha = (grow && m_used != -INFINITY) ? ex2_approx(m_used - m_new) : 1.f;
+        const bool resc = grow && m_used != -INFINITY;
+        l *= alpha;
+        m_used = m_new;
+        const float mneg = m_used == -INFINITY ? 0.f : -m_used;
+        float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {  // packed in place: sa[e] <- P(keys 2e, 2e+1)
+          const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(SV(2 * e)), c, mneg));
+          const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(SV(2 * e + 1)), c, mneg));
+          rs8[(2 * e) & 7] += p0;
+          rs8[(2 * e + 1) & 7] += p1;
+          sa[e] = pack_bf16(p0, p1);
+        }
+#undef SV
+        tmem_st32(lane_base + C::T_S + half * 32, sa);  // P of keys half*64.. = packed columns half*32..
+        l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        tmem_st_wait();
+        // O rescale after P is out (fewer live registers); PV(j) waits on p_full anyway
+        if (__any_sync(0xffffffffu, resc) && j > 0) {
+          mbar_wait(&pv_done[t], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int cc = 0; cc < DH / 64; ++cc) {  // this half's 64 of the DH O columns
+            uint32_t o[32];
+            const uint32_t ocol = C::T_O + half * (DH / 2) + cc * 32;
+            tmem_ld32(lane_base + ocol, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(lane_base + ocol, o);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        if (a.trace && blockIdx.x == 0 && lane == 0 && q4 == 0 && half == 0 && j < 256) {
+          a.trace[(t * 256 + j) * 4 + 0] = 0;  // (S-ready stamp not taken in this variant)
+          a.trace[(t * 256 + j) * 4 + 1] = clock64();
+        }
+      }
+      // ---- epilogue: row sum = both halves' partial sums (same reference max)
+      if (n_tiles > 0) {
+        mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
+        tc_fence_after();
+      }
+      xl[t][half][r] = l;
+      asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
+      const float lt = xl[t][0][r] + xl[t][1][r];
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      const size_t qi = (size_t)tok * a.Hq + head;
+#pragma unroll 1
+      for (int cc = 0; cc < DH / 64; ++cc) {
+        uint32_t o[32];
+        const int dcol = half * (DH / 2) + cc * 32;
+        if (n_tiles > 0) {
+          tmem_ld32(lane_base + C::T_O + dcol, o);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = 0u;
+        }
+        if (!live) continue;
+        if (a.n_splits > 1) {
+          float4* po = reinterpret_cast<float4*>(a.part_o + ((size_t)split * a.M * a.Hq + qi) * DH + dcol);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            po[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+        } else {
+          uint4* po = reinterpret_cast<uint4*>(a.out + qi * DH + dcol);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[8 * e + 0]) * inv, __uint_as_float(o[8 * e + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv);
+            po[e] = v;
+          }
+        }
+      }
+      if (live && half == 0 && a.n_splits > 1)
+        a.part_lse[(size_t)split * a.M * a.Hq + qi] =
+            lt > 0.f ? m_used * 0.6931471805599453f + __logf(lt) : -INFINITY;
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
@@ -425,9 +558,16 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
     cudaMemsetAsync(trace_dev, 0, 2 * 256 * 4 * sizeof(unsigned long long), stream);
     at.trace = trace_dev;
   }
+  // two softmax threads per row (default for dh=128; FRAG_ATTN_SPLIT=0 selects
+  // the one-thread-per-row kernel): 2-3% faster alone, see DESIGN.md §5
+  static const bool split_rows = [] {
+    const char* v = std::getenv("FRAG_ATTN_SPLIT");
+    return !(v && v[0] == '0');
+  }();
+  int threads = AT_THREADS;
   auto go = [&](auto kern, int smem) {
     smem_attr_once(kern, smem);
-    launch_pdl(kern, grid, dim3(AT_THREADS), smem, stream, tq, tk, tv, at, G, n_qblocks);
+    launch_pdl(kern, grid, dim3(threads), smem, stream, tq, tk, tv, at, G, n_qblocks);
     if (trace_path) {
       unsigned long long h[2 * 256 * 4];
       cudaMemcpyAsync(h, trace_dev, sizeof(h), cudaMemcpyDeviceToHost, stream);
@@ -448,6 +588,11 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
       go(attn_tc_kernel<64, 0, true>, (int)AttCfg<64>::SMEM);
     else
       return -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+  }
+  if (split_rows && a.dh == 128 && poly == 0) {
+    threads = 576;
+    go(attn_tc_kernel<128, 0, false, true>, (int)AttCfg<128>::SMEM);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
   }
   if (a.dh == 128) {

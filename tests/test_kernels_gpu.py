@@ -101,6 +101,22 @@ def test_sparse_q_attention_vs_torch(cuda, Hq, Hkv, dh, T, M, split):
     assert err < 2e-2, err
 
 
+def test_attention_one_thread_per_row_variant(cuda):
+    """The dh=128 kernel defaults to two softmax threads per query row; the
+    one-thread-per-row kernel (FRAG_ATTN_SPLIT=0, read once per process) must
+    stay correct too."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FRAG_ATTN_SPLIT="0")
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_kernels_gpu.py", "-k", "sparse_q_attention_vs_torch"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    assert "4 passed" in p.stdout, p.stdout[-500:]
+
+
 def _rope_shift_ref(kbits, delta, base):
     dh = kbits.shape[-1]
     k = (kbits.astype(np.uint32) << 16).view(np.float32)
