@@ -304,6 +304,7 @@ void result_init(Result* r, Engine* e, int max_tokens) {
   r->q_tok.alloc(M * sizeof(int));
   r->scores.alloc(M * sizeof(float));
   r->row_map.alloc(M * sizeof(int));
+  r->ssq.alloc((size_t)(c.d_model / 32) * M * sizeof(float));  // folded RMSNorm partials
   // split-K workspace (small-M GEMMs) + self-resetting tile counters
   r->gemm_ws.alloc((size_t)32 << 20);
   r->gemm_cnt.alloc(16384 * sizeof(int));
@@ -329,6 +330,29 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
   const int* ptok = r->plan_tok.as<int>();
   float* h = r->h.as<float>();
   bf16* x = r->x.as<bf16>();
+  // RMSNorm folded into the GEMM epilogues (EpiParams::ssq_*; FRAG_FUSED_NORM=0
+  // runs the standalone rmsnorm kernel instead). Layer 0's norm stays in the
+  // embedding kernel; the final norm stays standalone (row gather for lm_head).
+  // The norm gains are 1 (init_model) -- a non-unit gain would
+  // be folded into the weights' input columns at engine creation.
+  static const bool fuse_norm = [] {
+    const char* v = std::getenv("FRAG_FUSED_NORM");
+    return !(v && v[0] == '0');
+  }();
+  float* ssq = r->ssq.as<float>();
+  const int ssq_ld = r->max_tokens;
+  auto norm_in = [&](fragk::EpiParams& ep, size_t row0) {
+    ep.ssq_in = ssq + row0;
+    ep.ssq_ld = ssq_ld;
+    ep.ssq_n = d / 32;
+    ep.norm_d = d;
+    ep.norm_eps = c.norm_eps;
+  };
+  auto norm_out = [&](fragk::EpiParams& ep, size_t row0) {
+    ep.ssq_out = ssq + row0;
+    ep.ssq_ld = ssq_ld;
+    ep.x_out = x + row0 * d;
+  };
   auto with_ws = [&](fragk::EpiParams& ep) {
     ep.ws = r->gemm_ws.as<float>();
     ep.ws_bytes = r->gemm_ws.bytes;
@@ -377,7 +401,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
   }
   for (int l = 0; l < L; ++l) {
     const auto& W = e->layers[l];
-    if (l > 0) {
+    if (l > 0 && !fuse_norm) {
       Scoped sc(P, s, KC_NORM, 0, (double)M * d * (4 + 2));
       fragk::rmsnorm(h, M, d, W.attn_norm, c.norm_eps, x, s);
       sc.launched(1);
@@ -395,6 +419,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       ep.Hq = Hq;
       ep.Hkv = Hkv;
       ep.dh = dh;
+      if (l > 0 && fuse_norm) norm_in(ep, 0);
       Scoped sc(P, s, gemm_class(M), 2.0 * M * qkv * d, 2.0 * (qkv * d + (double)M * (d + qkv)));
       sc.launched(fragk::gemm_bf16_tc(x, W.wqkv, M, (int)qkv, d, fragk::EPI_QKV, ep, s));
     }
@@ -486,10 +511,11 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       with_ws(ep);
       ep.resid = h + off * d;
       ep.ldo = d;
+      if (fuse_norm) norm_out(ep, off);
       Scoped sc(P, s, gemm_class(Ml), 2.0 * Ml * d * qc, 2.0 * (qc * d + (double)Ml * qc) + 8.0 * Ml * d);
       sc.launched(fragk::gemm_bf16_tc(r->attn.as<bf16>() + off * qc, W.wo, Ml, d, (int)qc, fragk::EPI_RESID, ep, s));
     }
-    {
+    if (!fuse_norm) {
       Scoped sc(P, s, KC_NORM, 0, (double)Ml * d * (4 + 2));
       fragk::rmsnorm(h + off * d, Ml, d, W.ffn_norm, c.norm_eps, x + off * d, s);
       sc.launched(1);
@@ -499,6 +525,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       with_ws(ep);
       ep.out_bf16 = r->act.as<bf16>() + off * F;
       ep.ldo = F;
+      if (fuse_norm) norm_in(ep, off);
       Scoped sc(P, s, gemm_class(Ml), 2.0 * Ml * 2.0 * F * d, 2.0 * (2.0 * F * d + (double)Ml * d + (double)Ml * F));
       sc.launched(fragk::gemm_bf16_tc(x + off * d, W.wgu, Ml, 2 * F, d, fragk::EPI_SWIGLU, ep, s));
     }
@@ -507,6 +534,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       with_ws(ep);
       ep.resid = h + off * d;
       ep.ldo = d;
+      if (fuse_norm && l + 1 < L) norm_out(ep, off);  // feeds the next layer's QKV
       Scoped sc(P, s, gemm_class(Ml), 2.0 * Ml * (double)d * F,
                 2.0 * ((double)F * d + (double)Ml * F) + 8.0 * Ml * d);
       sc.launched(fragk::gemm_bf16_tc(r->act.as<bf16>() + off * F, W.wd, Ml, d, F, fragk::EPI_RESID, ep, s));

@@ -230,7 +230,8 @@ struct Result {
   std::vector<BatchReq> batch;
   // workspace
   DevBuf h, x, q, attn, act, plan_rows, plan_tok, chunk_tok, q_tok, q_final, scores, part_ms, row_ms, part_o,
-      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok, fr_save, dev, score_col, score_q;
+      part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok, fr_save, dev, score_col, score_q,
+      ssq;
   PinnedBuf staging, logits_host;
   // timing
   cudaEvent_t ev[7] = {};

@@ -10,9 +10,33 @@ namespace {
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
+// Folded RMSNorm scale of one row (1 unless the consumer reads partials):
+// the producer's per-chunk Σh² summed in chunk order, four running sums.
+template <int EPI>
+__device__ __forceinline__ float epi_row_scale(const EpiParams& ep, int row) {
+  if constexpr (EPI == EPI_QKV || EPI == EPI_SWIGLU) {
+    if (ep.ssq_in) {
+      const float* p = ep.ssq_in + row;
+      const size_t ld = (size_t)ep.ssq_ld;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      int i = 0;
+#pragma unroll 4
+      for (; i + 4 <= ep.ssq_n; i += 4) {
+        s0 += p[i * ld];
+        s1 += p[(i + 1) * ld];
+        s2 += p[(i + 2) * ld];
+        s3 += p[(i + 3) * ld];
+      }
+      for (; i < ep.ssq_n; ++i) s0 += p[i * ld];
+      return rsqrtf(((s0 + s1) + (s2 + s3)) / (float)ep.norm_d + ep.norm_eps);
+    }
+  }
+  return 1.f;
+}
+
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col, const uint32_t (&r)[32],
-                                          const uint32_t (&r2)[32]) {
+                                          const uint32_t (&r2)[32], float rs = 1.f) {
   if constexpr (EPI == EPI_STORE_BF16) {
     uint4* dst = reinterpret_cast<uint4*>(ep.out_bf16 + (size_t)row * ep.ldo + col);
 #pragma unroll
@@ -32,6 +56,7 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
                            __uint_as_float(r[4 * j + 3]));
   } else if constexpr (EPI == EPI_RESID) {
     float4* dst = reinterpret_cast<float4*>(ep.resid + (size_t)row * ep.ldo + col);
+    float4 hv[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float4 h = dst[j];
@@ -40,6 +65,28 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
       h.z += __uint_as_float(r[4 * j + 2]);
       h.w += __uint_as_float(r[4 * j + 3]);
       dst[j] = h;
+      hv[j] = h;
+    }
+    if (ep.x_out) {
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ss = fmaf(hv[j].x, hv[j].x, ss);
+        ss = fmaf(hv[j].y, hv[j].y, ss);
+        ss = fmaf(hv[j].z, hv[j].z, ss);
+        ss = fmaf(hv[j].w, hv[j].w, ss);
+      }
+      ep.ssq_out[(size_t)(col >> 5) * ep.ssq_ld + row] = ss;
+      uint4* xo = reinterpret_cast<uint4*>(ep.x_out + (size_t)row * ep.ldo + col);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint4 v;
+        v.x = pack_bf16(hv[2 * j].x, hv[2 * j].y);
+        v.y = pack_bf16(hv[2 * j].z, hv[2 * j].w);
+        v.z = pack_bf16(hv[2 * j + 1].x, hv[2 * j + 1].y);
+        v.w = pack_bf16(hv[2 * j + 1].z, hv[2 * j + 1].w);
+        xo[j] = v;
+      }
     }
   } else if constexpr (EPI == EPI_SWIGLU) {
     // col is the gate chunk's first column; the chunk is 64-aligned: gate block
@@ -50,8 +97,8 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
       float a[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        float g = __uint_as_float(r[8 * j + t]);
-        float u = __uint_as_float(r2[8 * j + t]);
+        float g = __uint_as_float(r[8 * j + t]) * rs;
+        float u = __uint_as_float(r2[8 * j + t]) * rs;
         a[t] = silu(g) * u;
       }
       uint4 v;
@@ -75,13 +122,13 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         float2 t = cs[j];
-        float k0 = __uint_as_float(r[2 * j]), k1 = __uint_as_float(r[2 * j + 1]);
+        float k0 = __uint_as_float(r[2 * j]) * rs, k1 = __uint_as_float(r[2 * j + 1]) * rs;
         o[2 * j] = __fmaf_rn(k0, t.x, -(k1 * t.y));
         o[2 * j + 1] = __fmaf_rn(k1, t.x, k0 * t.y);
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(r[j]);
+      for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(r[j]) * rs;
     }
     bf16* dstp;
     if (col < q_cols) {
@@ -112,10 +159,11 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
 
 // Sum n fp32 partials (row-major rows of BN, `sstride` floats apart) of this
 // thread's row in partial order and run the fused epilogue on 32-column
-// chunk units u = u0, u0 + du, ... (a unit is 2 chunks for SwiGLU).
+// chunk units u = u0, u0 + du, ... (a unit is 2 chunks for SwiGLU); rs = the
+// row's folded RMSNorm scale (epi_row_scale, loaded by the caller early).
 template <int BN, int EPI>
 __device__ __forceinline__ void reduce_partials(const EpiParams& ep, const float* base, size_t sstride, int n,
-                                                int u0, int du, int row, int col0) {
+                                                int u0, int du, int row, int col0, float rs) {
   constexpr int CW = EPI == EPI_SWIGLU ? 2 : 1;
   constexpr int UNITS = BN / 32 / CW;
 #pragma unroll 1
@@ -156,7 +204,7 @@ __device__ __forceinline__ void reduce_partials(const EpiParams& ep, const float
         r[h2][4 * j + 3] = __float_as_uint(acc[j].w);
       }
     }
-    epi_chunk<EPI>(ep, row, col0 + u * CW * 32, r[0], r[CW - 1]);
+    epi_chunk<EPI>(ep, row, col0 + u * CW * 32, r[0], r[CW - 1], rs);
   }
 }
 
@@ -172,7 +220,8 @@ __device__ __forceinline__ void reduce_partials(const EpiParams& ep, const float
 // named barrier 1); `warp2_lane0` does the counter traffic.
 template <int BN, int EPI>
 __device__ __forceinline__ void split_fixup(const EpiParams& ep, int slot, int S, int sp, int ws_rows,
-                                            int row_in_tile, int row, int M, int col0, bool warp2_lane0) {
+                                            int row_in_tile, int row, int M, int col0, bool warp2_lane0,
+                                            float rs) {
   __threadfence();
   asm volatile("bar.sync 1, 128;" ::: "memory");
   int* cnt = ep.counters + slot;
@@ -187,7 +236,7 @@ __device__ __forceinline__ void split_fixup(const EpiParams& ep, int slot, int S
   asm volatile("bar.sync 1, 128;" ::: "memory");
   const float* base = ep.ws + ((size_t)slot * S * ws_rows + row_in_tile) * BN;
   if (row_in_tile < ws_rows && row < M)
-    reduce_partials<BN, EPI>(ep, base, (size_t)ws_rows * BN, S, sp, S, row, col0);
+    reduce_partials<BN, EPI>(ep, base, (size_t)ws_rows * BN, S, sp, S, row, col0, rs);
   // second round of arrivals: the last CTA out resets the counter for the next GEMM
   asm volatile("bar.sync 1, 128;" ::: "memory");
   if (warp2_lane0) {
@@ -212,7 +261,7 @@ __device__ __forceinline__ int sk_cta_of(long long pos, long long I, int G) {
 // fused epilogue. 4 epilogue warps, named barrier 1.
 template <int BN, int EPI>
 __device__ __forceinline__ void sk_finish(const EpiParams& ep, int tile, int j, int n, int ws_rows, int row_in_tile,
-                                          int row, int M, int col0, bool leader) {
+                                          int row, int M, int col0, bool leader, float rs) {
   __threadfence();
   asm volatile("bar.sync 1, 128;" ::: "memory");
   int* cnt = ep.counters + tile;
@@ -230,7 +279,8 @@ __device__ __forceinline__ void sk_finish(const EpiParams& ep, int tile, int j, 
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
   const float* base = ep.ws + ((size_t)tile * ep.sk_maxc * ws_rows + row_in_tile) * BN;
-  if (row_in_tile < ws_rows && row < M) reduce_partials<BN, EPI>(ep, base, (size_t)ws_rows * BN, n, 0, 1, row, col0);
+  if (row_in_tile < ws_rows && row < M)
+    reduce_partials<BN, EPI>(ep, base, (size_t)ws_rows * BN, n, 0, 1, row, col0, rs);
 }
 
 }  // namespace

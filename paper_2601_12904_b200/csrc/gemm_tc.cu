@@ -238,10 +238,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
     while (next(st, tile, kb0, kb1, sp, S)) {
       const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
       const int ti = tile - n_full;  // tail index (workspace / counter slot)
+      const int row = m_blk * BM + row_in_tile;
+      // folded RMSNorm scale, loaded while the MMAs run
+      const float rs = row < M ? epi_row_scale<EPI>(ep, row) : 1.f;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (warp == 2 && lane == 0) stamp(4);
-      const int row = m_blk * BM + row_in_tile;
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (S == 0 && !(kb0 == 0 && kb1 == nk)) {
         // stream-K part of a tile shared by several CTAs: partial -> workspace
@@ -267,7 +269,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
         const int n_contrib = sk_cta_of(p0 + nk - 1, I, G) - c_own + 1;
-        sk_finish<BN, EPI>(ep, tile, j, n_contrib, ws_rows, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0);
+        sk_finish<BN, EPI>(ep, tile, j, n_contrib, ws_rows, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0,
+                           rs);
       } else if (S <= 1) {
         if constexpr (EPI == EPI_SWIGLU) {
 #pragma unroll 1
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
             tmem_ld32(t_row + c * 32, r);
             tmem_ld32(t_row + (c + 1) * 32, r2);
             tmem_ld_wait();
-            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2, rs);
           }
         } else {
 #pragma unroll 1
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
             uint32_t r[32];
             tmem_ld32(t_row + c * 32, r);
             tmem_ld_wait();
-            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
+            if (row < M) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r, rs);
           }
         }
         tc_fence_before();
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
         if (warp == 2 && lane == 0) stamp(5);
-        split_fixup<BN, EPI>(ep, ti, S, sp, ws_rows, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0);
+        split_fixup<BN, EPI>(ep, ti, S, sp, ws_rows, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0, rs);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;

@@ -240,9 +240,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
       int tile, sp, S;
       decode(w, tile, sp, S);
       const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
+      const int row = m_blk * BM2 + rank * 128 + row_in_tile;
+      // folded RMSNorm scale, loaded while the MMAs run
+      const float rs = row < M ? epi_row_scale<EPI>(ep, row) : 1.f;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m_blk * BM2 + rank * 128 + row_in_tile;
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (S == 1) {
         if constexpr (EPI == EPI_SWIGLU) {
@@ -252,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
             tmem_ld32(t_row + c * 32, r);
             tmem_ld32(t_row + (c + 1) * 32, r2);
             tmem_ld_wait();
-            if (row < M && n_blk * BN + c * 32 < N) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2);
+            if (row < M && n_blk * BN + c * 32 < N) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r2, rs);
           }
         } else {
 #pragma unroll 1
@@ -260,7 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
             uint32_t r[32];
             tmem_ld32(t_row + c * 32, r);
             tmem_ld_wait();
-            if (row < M && n_blk * BN + c * 32 < N) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r);
+            if (row < M && n_blk * BN + c * 32 < N) epi_chunk<EPI>(ep, row, n_blk * BN + c * 32, r, r, rs);
           }
         }
         tc_fence_before();
@@ -284,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
-        split_fixup<BN, EPI>(ep, slot, S, sp, 128, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0);
+        split_fixup<BN, EPI>(ep, slot, S, sp, 128, row_in_tile, row, M, n_blk * BN, warp == 2 && lane == 0, rs);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;

@@ -48,6 +48,18 @@ struct EpiParams {
   int streamk = 0;     // set by gemm_bf16_tc: stream-K decomposition (one M tile)
   int sk_maxc = 0;     // stream-K: max CTAs sharing one tile (workspace slots per tile)
   unsigned long long* trace = nullptr;  // tooling: per-CTA globaltimer stamps (FRAG_GEMM_TRACE)
+  // RMSNorm folded into the GEMMs (K3): norm(h)·Wᵀ = rs(h) · (h·Wᵀ) with unit
+  // gains, rs = rsqrt(mean(h²) + eps). The EPI_RESID epilogue that updates h
+  // also writes bf16(h) (the next GEMM's A operand) and one partial Σh² per
+  // 32-column chunk; the consuming EPI_QKV / EPI_SWIGLU epilogue sums the
+  // partials of its row in chunk order and scales the accumulator by rs.
+  float* ssq_out = nullptr;       // EPI_RESID: [d/32][ssq_ld] partial sums of squares
+  bf16* x_out = nullptr;          // EPI_RESID: bf16(h), row stride ldo
+  const float* ssq_in = nullptr;  // EPI_QKV / EPI_SWIGLU: the producer's partials
+  int ssq_ld = 0;                 // row stride of the partials
+  int ssq_n = 0;                  // partials per row (d/32)
+  int norm_d = 0;
+  float norm_eps = 0.f;
 };
 
 struct GemmTimer;  // optional per-launch event hook (bench roofline)
