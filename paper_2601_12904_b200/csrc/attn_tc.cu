@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
         for (int at = 0; at < C::ATOMS; ++at)
           tma_load_2d(sV + st * C::KV_BYTES + at * C::KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64, key0);
       }
+      // consume the last two kv_empty phases (no phase completes unobserved)
+      for (int j = n_tiles > 2 ? n_tiles - 2 : 0; j < n_tiles; ++j) mbar_wait(&kv_empty[j & 1], (j >> 1) & 1);
     }
   } else if (warp == W_MMA) {
     // ------------------------------------------------------------ MMA issuer
@@ -239,6 +241,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
       for (int j = 0; j < n_tiles; ++j) {
         const int key0 = k_lo + j * AT_KEYS + half * 64;
         mbar_wait(&s_full[t], j & 1);
+        // S(j) was committed after PV(j-1): consume every pv_done phase (free)
+        if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
         tc_fence_after();
         uint32_t sa[32], sb[32];
         tmem_ld32(lane_base + C::T_S + half * 64, sa);
@@ -283,8 +287,6 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
         tmem_st_wait();
         // O rescale after P is out (fewer live registers); PV(j) waits on p_full anyway
         if (__any_sync(0xffffffffu, resc) && j > 0) {
-          mbar_wait(&pv_done[t], (j - 1) & 1);
-          tc_fence_after();
 #pragma unroll 1
           for (int cc = 0; cc < DH / 64; ++cc) {  // this half's 64 of the DH O columns
             uint32_t o[32];
@@ -368,6 +370,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
       for (int j = 0; j < n_tiles; ++j) {
         const int key0 = k_lo + j * AT_KEYS + (DUAL ? t * KT : 0);
         mbar_wait(&s_full[t], j & 1);
+        // S(j) was committed after PV(j-1): consume every pv_done phase (free)
+        if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && (warp & 3) == 0 && j < 256)
           a.trace[(t * 256 + j) * 4 + 0] = clock64();
@@ -398,9 +402,7 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
         const float m_new = grow ? fmaxf(mt, m_used) : m_used;
         const float alpha = (grow && m_used != -INFINITY) ? ex2_approx(m_used - m_new) : 1.f;
         if (__any_sync(0xffffffffu, grow && m_used != -INFINITY) && j > 0) {
-          // rescale this lane quarter's O rows in TMEM; PV_t(j-1) must have landed
-          mbar_wait(&pv_done[t], (j - 1) & 1);
-          tc_fence_after();
+          // rescale this lane quarter's O rows in TMEM; PV_t(j-1) has landed (waited above)
 #pragma unroll 1
           for (int cc = 0; cc < DH / 32; ++cc) {
             uint32_t o[32];

@@ -261,3 +261,45 @@ def test_stitch_overlap_is_bit_identical(cuda):
         assert p.returncode == 0, p.stderr[-2000:]
         out[ov] = p.stdout.strip().splitlines()[-1]
     assert out["0"] == out["1"]
+
+
+_NORM_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+from paper_2601_12904_b200 import fusion as F
+eng = F.Engine("tiny", seed=1234)
+store = F.ChunkKVStore(eng.cfg)
+rng = np.random.default_rng(6)
+chunks = [rng.integers(0, eng.cfg.vocab, 256).tolist() for _ in range(8)]
+ids = [eng.preprocess_isolated(store, c) for c in chunks]
+question = rng.integers(0, eng.cfg.vocab, 32).tolist()
+res = F.Result(eng, 8 * 256 + 32)
+eng.reprocess(store, question, ids, 0.15, res)
+k, v = res.fused_kv()
+np.savez(sys.argv[1], logits=res.logits(), k=k.astype(np.float32), crit=res.crit())
+"""
+
+
+def test_folded_norm_matches_standalone_rmsnorm(cuda, tmp_path):
+    """The RMSNorm folded into the GEMM epilogues (default) against the
+    standalone rmsnorm kernel (FRAG_FUSED_NORM=0): same math, different bf16
+    rounding point (bf16(h)·W·rs vs bf16(h·rs)·W), so close, not bit-equal."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    out = {}
+    for fn in ("1", "0"):
+        path = tmp_path / f"n{fn}.npz"
+        env = dict(os.environ, FRAG_FUSED_NORM=fn)
+        p = subprocess.run([sys.executable, "-c", _NORM_SNIPPET, str(path)], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[fn] = np.load(path)
+    a, b = out["1"], out["0"]
+    rel = np.linalg.norm(a["logits"] - b["logits"]) / np.linalg.norm(b["logits"])
+    assert rel < 1e-2, rel
+    relk = np.linalg.norm(a["k"] - b["k"]) / np.linalg.norm(b["k"])
+    assert relk < 1e-2, relk
+    assert len(set(a["crit"].tolist()) ^ set(b["crit"].tolist())) <= len(b["crit"]) // 10
