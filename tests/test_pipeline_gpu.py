@@ -276,7 +276,8 @@ question = rng.integers(0, eng.cfg.vocab, 32).tolist()
 res = F.Result(eng, 8 * 256 + 32)
 eng.reprocess(store, question, ids, 0.15, res)
 k, v = res.fused_kv()
-np.savez(sys.argv[1], logits=res.logits(), k=k.astype(np.float32), crit=res.crit())
+kf = (np.asarray(k).astype(np.uint32) << 16).view(np.float32)  # bf16 bits -> values
+np.savez(sys.argv[1], logits=res.logits(), k=kf, crit=res.crit())
 """
 
 
@@ -300,6 +301,12 @@ def test_folded_norm_matches_standalone_rmsnorm(cuda, tmp_path):
     a, b = out["1"], out["0"]
     rel = np.linalg.norm(a["logits"] - b["logits"]) / np.linalg.norm(b["logits"])
     assert rel < 1e-2, rel
-    relk = np.linalg.norm(a["k"] - b["k"]) / np.linalg.norm(b["k"])
+    diff = set(a["crit"].tolist()) ^ set(b["crit"].tolist())
+    assert len(diff) <= len(b["crit"]) // 10
+    # fused K away from the rows only one side recomputed (row = position - 1)
+    keep = np.ones(a["k"].shape[1], bool)
+    for c in diff:
+        keep[max(c - 1, 0):c + 1] = False
+    ka, kb = a["k"][:, keep], b["k"][:, keep]
+    relk = np.linalg.norm(ka - kb) / np.linalg.norm(kb)
     assert relk < 1e-2, relk
-    assert len(set(a["crit"].tolist()) ^ set(b["crit"].tolist())) <= len(b["crit"]) // 10
