@@ -1,7 +1,7 @@
 # compute-sanitizer sweep (memcheck / racecheck / synccheck / initcheck) over
-# the tiny end-to-end reprocess (eager: FRAG_NO_GRAPH=1) and the dh=128
-# attention kernel in both softmax variants. Output: gpurun_out/sanitizer.log
-export FRAG_NO_GRAPH=1
+# the tiny end-to-end reprocess (one call: the first request of a shape runs
+# eagerly, before any graph capture) and the dh=128 attention kernel in both
+# softmax variants. Output: gpurun_out/sanitizer.log
 out=gpurun_out/sanitizer.log
 : > $out
 for tool in memcheck racecheck synccheck initcheck; do
