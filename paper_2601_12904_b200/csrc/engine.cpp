@@ -399,6 +399,34 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     fragk::embed_rmsnorm(e->emb, ptok, M, d, e->layers[0].attn_norm, c.norm_eps, h, x, s);
     sc.launched(1);
   }
+  auto qkv_ep = [&](int l) {
+    fragk::EpiParams ep;
+    with_ws(ep);
+    ep.rows = prow;
+    ep.rope = e->rope.as<float2>();
+    ep.q_out = r->q.as<bf16>();
+    ep.q_out_f32 = (mode == PASS_QUESTION && l == L - 1) ? r->q_final.as<float>() : nullptr;
+    ep.k_cache = kf + l * lstride;
+    ep.v_cache = vf + l * lstride;
+    ep.rows_per_seq = r->rows_per_seq;
+    ep.Hq = Hq;
+    ep.Hkv = Hkv;
+    ep.dh = dh;
+    if (l > 0 && fuse_norm) norm_in(ep, 0);
+    return ep;
+  };
+  // <= 32 rows (question pass, decode, r = 0): the O -> gate/up -> down ->
+  // next-QKV projections of a layer run as one persistent GEMM chain
+  // (gemm_chain.cu; FRAG_GEMM_CHAIN=0 launches them one by one)
+  static const bool chain_env = [] {
+    const char* v = std::getenv("FRAG_GEMM_CHAIN");
+    return !(v && v[0] == '0');
+  }();
+  const bool use_chain = chain_env && fuse_norm && fragk::gemm_chain_supported(M, (int)qkv, d) &&
+                         fragk::gemm_chain_supported(M, d, (int)qc) && fragk::gemm_chain_supported(M, 2 * F, d) &&
+                         fragk::gemm_chain_supported(M, d, F);
+  int* chain_done = r->gemm_cnt.as<int>() + (r->gemm_cnt.bytes / sizeof(int) - 2 * fragk::CHAIN_MAX_OPS);
+  bool qkv_done = false;  // this layer's QKV already ran inside the previous layer's chain
   for (int l = 0; l < L; ++l) {
     const auto& W = e->layers[l];
     if (l > 0 && !fuse_norm) {
@@ -406,23 +434,12 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       fragk::rmsnorm(h, M, d, W.attn_norm, c.norm_eps, x, s);
       sc.launched(1);
     }
-    {
-      fragk::EpiParams ep;
-      with_ws(ep);
-      ep.rows = prow;
-      ep.rope = e->rope.as<float2>();
-      ep.q_out = r->q.as<bf16>();
-      ep.q_out_f32 = (mode == PASS_QUESTION && l == L - 1) ? r->q_final.as<float>() : nullptr;
-      ep.k_cache = kf + l * lstride;
-      ep.v_cache = vf + l * lstride;
-      ep.rows_per_seq = r->rows_per_seq;
-      ep.Hq = Hq;
-      ep.Hkv = Hkv;
-      ep.dh = dh;
-      if (l > 0 && fuse_norm) norm_in(ep, 0);
+    if (!qkv_done) {
+      fragk::EpiParams ep = qkv_ep(l);
       Scoped sc(P, s, gemm_class(M), 2.0 * M * qkv * d, 2.0 * (qkv * d + (double)M * (d + qkv)));
       sc.launched(fragk::gemm_bf16_tc(x, W.wqkv, M, (int)qkv, d, fragk::EPI_QKV, ep, s));
     }
+    qkv_done = false;
     if (mode != PASS_FULL && l == L - 1) break;
     if (layer_ready) check_cuda(cudaStreamWaitEvent(s, layer_ready[l], 0), "wait stitched layer");
     // Last layer: every row's K/V are in the cache now (the QKV epilogue), and
@@ -505,6 +522,40 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       a.scale = 1.0f / std::sqrt((float)dh);
       Scoped sc(P, s, KC_ATTN, 0, 0);
       sc.launched(fragk::sparse_q_attention(a, s));
+    }
+    if (use_chain && Ml == M && off == 0) {
+      fragk::ChainStep st[fragk::CHAIN_MAX_OPS];
+      int n = 0;
+      st[n].A = r->attn.as<bf16>(), st[n].B = W.wo, st[n].N = d, st[n].K = (int)qc, st[n].epi = fragk::EPI_RESID;
+      with_ws(st[n].ep);
+      st[n].ep.resid = h, st[n].ep.ldo = d;
+      norm_out(st[n].ep, 0);
+      ++n;
+      st[n].A = x, st[n].B = W.wgu, st[n].N = 2 * F, st[n].K = d, st[n].epi = fragk::EPI_SWIGLU;
+      with_ws(st[n].ep);
+      st[n].ep.out_bf16 = r->act.as<bf16>(), st[n].ep.ldo = F;
+      norm_in(st[n].ep, 0);
+      ++n;
+      st[n].A = r->act.as<bf16>(), st[n].B = W.wd, st[n].N = d, st[n].K = F, st[n].epi = fragk::EPI_RESID;
+      with_ws(st[n].ep);
+      st[n].ep.resid = h, st[n].ep.ldo = d;
+      if (l + 1 < L) norm_out(st[n].ep, 0);
+      ++n;
+      double flop = 2.0 * M * d * qc + 2.0 * M * 2.0 * F * d + 2.0 * M * (double)d * F;
+      double bytes = 2.0 * (qc * d + 2.0 * F * d + (double)F * d);
+      if (l + 1 < L) {
+        st[n].A = x, st[n].B = e->layers[l + 1].wqkv, st[n].N = (int)qkv, st[n].K = d;
+        st[n].epi = fragk::EPI_QKV;
+        st[n].ep = qkv_ep(l + 1);
+        ++n;
+        flop += 2.0 * M * qkv * d;
+        bytes += 2.0 * qkv * d;
+        qkv_done = true;
+      }
+      Scoped sc(P, s, gemm_class(M), flop, bytes);
+      sc.launched(fragk::gemm_chain_tc(st, n, M, chain_done, s));
+      peek("layer");
+      continue;
     }
     {
       fragk::EpiParams ep;

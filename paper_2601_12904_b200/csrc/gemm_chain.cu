@@ -1,0 +1,403 @@
+// Weight-streaming GEMM chain for M <= 32 rows (question pass, decode): the
+// per-layer projection sequence  O -> gate/up -> down -> next layer's QKV
+// (K7, K8, K8, K4+K5 of SPEC.md:435-444 at |Q| rows) in ONE persistent launch.
+//
+// Each op is the same computation as gemm_tc_kernel<128, EPI, 32> (A = the
+// live 32 activation rows, B = the weights, BN = 128, deterministic split-K
+// with the cooperative fixup of gemm_epi.cuh) -- the chain only removes the
+// kernel boundaries: the TMA ring, the TMEM accumulators and the CTAs stay
+// alive from one op to the next, so op i+1's weights stream into the ring
+// while op i's last MMAs, split-K fixups and epilogues finish. Op i+1's A
+// operand is op i's output: its TMA loads wait on op i's completion counter
+// (release/acquire + async-proxy fence), everything else (weights, TMEM,
+// barriers) runs ahead.
+//
+// All CTAs are co-resident (one per SM, grid = #SMs), so spinning on another
+// CTA's progress cannot deadlock; the counters are zero at launch and the last
+// CTA out resets them.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "gemm_epi.cuh"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace fragk {
+
+namespace {
+
+constexpr int CBM = 128;  // UMMA M (accumulator rows; rows >= M are never stored)
+constexpr int CBN = 128;
+constexpr int CBK = 64;
+constexpr int CAR = 32;  // live A rows loaded per stage
+constexpr int CSTAGES = 10;
+constexpr int CHAIN_THREADS = 192;
+constexpr uint32_t CA_BYTES = CAR * CBK * 2;
+constexpr uint32_t CB_BYTES = CBN * CBK * 2;
+constexpr uint32_t CSTAGE_BYTES = CA_BYTES + CB_BYTES;  // 20 KB; UMMA rows 32..127 alias B bytes
+constexpr int CTMEM_COLS = 256;                          // 2 x BN accumulators
+constexpr size_t CSMEM = 1024 + (size_t)CSTAGES * CSTAGE_BYTES + 256;
+static_assert(CSTAGE_BYTES >= CBM * CBK * 2, "aliased A rows must stay inside the stage");
+
+struct ChainArgs {
+  CUtensorMap tmA[CHAIN_MAX_OPS];
+  CUtensorMap tmB[CHAIN_MAX_OPS];
+  ChainOp op[CHAIN_MAX_OPS];
+  int n_ops;
+  int M;
+  int* done;  // [CHAIN_MAX_OPS] op completion counters, [CHAIN_MAX_OPS] CTA exit counter
+  unsigned long long* trace;  // tooling (FRAG_CHAIN_TRACE): [cta][op][4] globaltimer stamps
+};
+
+__device__ __forceinline__ void chain_stamp(const ChainArgs& a, int o, int k) {
+  if (a.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[((size_t)blockIdx.x * CHAIN_MAX_OPS + o) * 4 + k] = t;
+  }
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_count(const int* p, int target) {
+  while (ld_acquire(p) < target) __nanosleep(32);
+}
+
+// unit u of an op: N tile and K range (split sp of S)
+__device__ __forceinline__ void chain_unit(const ChainOp& op, int u, int& tile, int& kb0, int& kb1, int& sp,
+                                           int& S) {
+  S = op.splits > 1 ? op.splits : 1;
+  tile = u / S, sp = u % S;
+  const int nk = op.K / CBK;
+  kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
+}
+__device__ __forceinline__ int chain_units(const ChainOp& op) {
+  return (op.N / CBN) * (op.splits > 1 ? op.splits : 1);
+}
+
+// Epilogue of one unit (4 warps, named barrier 1): direct fused epilogue, or
+// the split partial + the cooperative deterministic fixup.
+template <int EPI>
+__device__ __forceinline__ void chain_epilogue(const EpiParams& ep, int M, int tile, int sp, int S, int row_in_tile,
+                                               int q, int lane, int warp, uint32_t t_row, uint64_t* tempty_acc,
+                                               float rs) {
+  const int row = row_in_tile;  // one M tile
+  const int col0 = tile * CBN;
+  if (S <= 1) {
+    if constexpr (EPI == EPI_SWIGLU) {
+#pragma unroll 1
+      for (int c = 0; c < CBN / 32; c += 2) {
+        uint32_t r[32], r2[32];
+        tmem_ld32(t_row + c * 32, r);
+        tmem_ld32(t_row + (c + 1) * 32, r2);
+        tmem_ld_wait();
+        if (row < M) epi_chunk<EPI>(ep, row, col0 + c * 32, r, r2, rs);
+      }
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < CBN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(t_row + c * 32, r);
+        tmem_ld_wait();
+        if (row < M) epi_chunk<EPI>(ep, row, col0 + c * 32, r, r, rs);
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty_acc);
+  } else {
+    float* wsp = ep.ws + ((size_t)(tile * S + sp) * M + row_in_tile) * CBN;
+#pragma unroll 1
+    for (int c = 0; c < CBN / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(t_row + c * 32, r);
+      tmem_ld_wait();
+      if (row_in_tile < M) {
+        float4* dst = reinterpret_cast<float4*>(wsp + c * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty_acc);
+    split_fixup<CBN, EPI>(ep, tile, S, sp, M, row_in_tile, row, M, col0, warp == 2 && lane == 0, rs);
+  }
+}
+
+__global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __grid_constant__ ChainArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + CA_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CSTAGES * CSTAGE_BYTES);
+  uint64_t* empty = full + CSTAGES;
+  uint64_t* tfull = empty + CSTAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int G = gridDim.x;
+  const int n_ops = args.n_ops;
+  const int M = args.M;
+
+  if (warp == 0 && lane == 0) {
+    for (int o = 0; o < n_ops; ++o) {
+      tma_prefetch_desc(&args.tmA[o]);
+      tma_prefetch_desc(&args.tmB[o]);
+    }
+    for (int s = 0; s < CSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<CTMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      pdl_launch_dependents();
+      int stage = 0;
+      uint32_t phase = 0;
+      auto advance = [&]() {
+        if (++stage == CSTAGES) stage = 0, phase ^= 1;
+      };
+      for (int o = 0; o < n_ops; ++o) {
+        const ChainOp& op = args.op[o];
+        const CUtensorMap* tA = &args.tmA[o];
+        const CUtensorMap* tB = &args.tmB[o];
+        const int units = chain_units(op);
+        // weights first: the first unit's leading stages, before waiting on
+        // the op that produces this op's A rows
+        int npre = 0, st_pre = stage;
+        int tile, kb0, kb1, sp, S;
+        if ((int)blockIdx.x < units) {
+          chain_unit(op, blockIdx.x, tile, kb0, kb1, sp, S);
+          npre = kb1 - kb0 < CSTAGES ? kb1 - kb0 : CSTAGES;
+          for (int i = 0; i < npre; ++i) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], CSTAGE_BYTES);
+            tma_load_2d(sB + stage * CSTAGE_BYTES, tB, &full[stage], (kb0 + i) * CBK, tile * CBN);
+            advance();
+          }
+        }
+        if ((int)blockIdx.x >= units) continue;
+        if (o == 0) {
+          pdl_wait();
+        } else {
+          wait_count(&args.done[o - 1], chain_units(args.op[o - 1]));
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+        }
+        chain_stamp(args, o, 0);
+        for (int i = 0, s2 = st_pre; i < npre; ++i, s2 = s2 + 1 == CSTAGES ? 0 : s2 + 1)
+          tma_load_2d(sA + s2 * CSTAGE_BYTES, tA, &full[s2], (kb0 + i) * CBK, 0);
+        for (int kb = kb0 + npre; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], CSTAGE_BYTES);
+          tma_load_2d(sB + stage * CSTAGE_BYTES, tB, &full[stage], kb * CBK, tile * CBN);
+          tma_load_2d(sA + stage * CSTAGE_BYTES, tA, &full[stage], kb * CBK, 0);
+          advance();
+        }
+        for (int u = blockIdx.x + G; u < units; u += G) {
+          chain_unit(op, u, tile, kb0, kb1, sp, S);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], CSTAGE_BYTES);
+            tma_load_2d(sB + stage * CSTAGE_BYTES, tB, &full[stage], kb * CBK, tile * CBN);
+            tma_load_2d(sA + stage * CSTAGE_BYTES, tA, &full[stage], kb * CBK, 0);
+            advance();
+          }
+        }
+        chain_stamp(args, o, 1);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(CBM, CBN, 0, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int o = 0; o < n_ops; ++o) {
+      const ChainOp& op = args.op[o];
+      const int units = chain_units(op);
+      for (int u = blockIdx.x; u < units; u += G) {
+        int tile, kb0, kb1, sp, S;
+        chain_unit(op, u, tile, kb0, kb1, sp, S);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * CBN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_base = smem_u32(sA + stage * CSTAGE_BYTES);
+            const uint32_t b_base = smem_u32(sB + stage * CSTAGE_BYTES);
+#pragma unroll
+            for (int k = 0; k < CBK / 16; ++k) {
+              const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
+              const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
+              umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            }
+            umma_commit(&empty[stage]);
+            if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == CSTAGES) stage = 0, phase ^= 1;
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    pdl_wait();
+    const int q = warp & 3;
+    const int row_in_tile = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int o = 0; o < n_ops; ++o) {
+      const ChainOp& op = args.op[o];
+      const int units = chain_units(op);
+      if ((int)blockIdx.x >= units) continue;
+      // this op's epilogue reads / writes what the earlier ops of the chain wrote
+      if (o > 0) wait_count(&args.done[o - 1], chain_units(args.op[o - 1]));
+      if (o > 1) wait_count(&args.done[o - 2], chain_units(args.op[o - 2]));
+      const EpiParams& ep = op.ep;
+      float rs = 1.f;
+      if (row_in_tile < M) {
+        switch (op.epi) {
+          case EPI_QKV: rs = epi_row_scale<EPI_QKV>(ep, row_in_tile); break;
+          case EPI_SWIGLU: rs = epi_row_scale<EPI_SWIGLU>(ep, row_in_tile); break;
+          default: break;
+        }
+      }
+      for (int u = blockIdx.x; u < units; u += G) {
+        int tile, kb0, kb1, sp, S;
+        chain_unit(op, u, tile, kb0, kb1, sp, S);
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        if (u == (int)blockIdx.x && warp == 2 && lane == 0) chain_stamp(args, o, 2);
+        const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * CBN;
+        switch (op.epi) {
+          case EPI_RESID:
+            chain_epilogue<EPI_RESID>(ep, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs);
+            break;
+          case EPI_SWIGLU:
+            chain_epilogue<EPI_SWIGLU>(ep, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs);
+            break;
+          case EPI_QKV:
+            chain_epilogue<EPI_QKV>(ep, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs);
+            break;
+          default:
+            chain_epilogue<EPI_STORE_BF16>(ep, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc],
+                                           rs);
+            break;
+        }
+        // unit complete (its outputs written): publish
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) atomicAdd(&args.done[o], 1);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+      if (warp == 2 && lane == 0) chain_stamp(args, o, 3);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<CTMEM_COLS>(tmem_base);
+  }
+  if (threadIdx.x == 0) {
+    // the last CTA out re-arms the counters for the next launch (graph replay)
+    int* exit_cnt = args.done + CHAIN_MAX_OPS;
+    __threadfence();
+    if (atomicAdd(exit_cnt, 1) == G - 1) {
+      for (int o = 0; o < n_ops; ++o) args.done[o] = 0;
+      *exit_cnt = 0;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace
+
+bool gemm_chain_supported(int M, int N, int K) { return M >= 1 && M <= CAR && N % CBN == 0 && K % CBK == 0; }
+
+int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStream_t stream) {
+  if (n_ops < 1 || n_ops > CHAIN_MAX_OPS || !done) return -1;
+  ChainArgs args{};
+  args.n_ops = n_ops;
+  args.M = M;
+  args.done = done;
+  const long sms = num_sms();
+  for (int o = 0; o < n_ops; ++o) {
+    const ChainStep& st = steps[o];
+    if (!gemm_chain_supported(M, st.N, st.K) || !st.ep.ws || !st.ep.counters) return -1;
+    if (!make_tmap_2d(&args.tmA[o], st.A, M, st.K, st.K, CAR)) return -1;
+    if (!make_tmap_2d(&args.tmB[o], st.B, st.N, st.K, st.K, CBN)) return -1;
+    // the one-M-tile policy of gemm_bf16_tc: split-K up to one full wave (a
+    // cost model that balanced the 224-tile gate/up with 5 splits and the
+    // down projection with 9 -- several fixup rounds per op -- measured 47 %
+    // slower: fixup waits that straddle rounds serialise)
+    const long tiles = st.N / CBN, nk = st.K / CBK;
+    long s = 1;
+    while (s < 8 && tiles * (s + 1) <= sms && nk / (s + 1) >= 4) ++s;
+    if (s > nk) s = nk;
+    if (tiles > st.ep.counters_cap || (size_t)(tiles * s * M * CBN) * sizeof(float) > st.ep.ws_bytes) s = 1;
+    ChainOp& op = args.op[o];
+    op.N = st.N;
+    op.K = st.K;
+    op.epi = st.epi;
+    op.splits = (int)s;
+    op.ep = st.ep;
+    op.ep.splits = (int)s;
+    op.ep.full_tiles = 0;
+    op.ep.streamk = 0;
+  }
+  // FRAG_CHAIN_TRACE=<file>: tooling only -- per-CTA, per-op globaltimer
+  // stamps [A ready, loads issued, first accumulator, all units published]
+  static const char* trace_path = std::getenv("FRAG_CHAIN_TRACE");
+  static unsigned long long* trace_dev = nullptr;
+  const size_t tn = (size_t)sms * CHAIN_MAX_OPS * 4;
+  if (trace_path) {
+    if (!trace_dev) cudaMalloc(&trace_dev, tn * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_dev, 0, tn * sizeof(unsigned long long), stream);
+    args.trace = trace_dev;
+  }
+  smem_attr_once(gemm_chain_kernel, (int)CSMEM);
+  launch_pdl(gemm_chain_kernel, dim3((unsigned)sms), dim3(CHAIN_THREADS), CSMEM, stream, args);
+  if (trace_path) {
+    std::vector<unsigned long long> h(tn);
+    cudaMemcpyAsync(h.data(), trace_dev, tn * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    if (FILE* f = std::fopen(trace_path, "ab")) {
+      std::fwrite(h.data(), tn * sizeof(unsigned long long), 1, f);
+      std::fclose(f);
+    }
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace fragk

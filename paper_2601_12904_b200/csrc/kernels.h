@@ -74,6 +74,24 @@ int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind
                       cudaStream_t stream, int bn, bool tail_split = true);
 int num_sms();
 
+// Weight-streaming GEMM chain (gemm_chain.cu): up to CHAIN_MAX_OPS one-M-tile
+// GEMMs (M <= 32 rows, BN = 128) in one persistent launch, op i+1's A = op i's
+// output. `done` = 2*CHAIN_MAX_OPS ints, zero before the first launch (left zero).
+constexpr int CHAIN_MAX_OPS = 4;
+struct ChainStep {
+  const bf16* A = nullptr;
+  const bf16* B = nullptr;
+  int N = 0, K = 0;
+  EpiKind epi = EPI_STORE_BF16;
+  EpiParams ep;
+};
+struct ChainOp {
+  int N, K, epi, splits;
+  EpiParams ep;
+};
+bool gemm_chain_supported(int M, int N, int K);
+int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStream_t stream);
+
 // TMA descriptors (bf16, SWIZZLE_128B, 64-element inner box), encoded through the
 // driver entry point so the library needs no link-time libcuda.
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,

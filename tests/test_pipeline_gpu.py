@@ -310,3 +310,48 @@ def test_folded_norm_matches_standalone_rmsnorm(cuda, tmp_path):
     ka, kb = a["k"][:, keep], b["k"][:, keep]
     relk = np.linalg.norm(ka - kb) / np.linalg.norm(kb)
     assert relk < 1e-2, relk
+
+
+_CHAIN_SNIPPET = r"""
+import hashlib, sys, numpy as np
+sys.path.insert(0, '.')
+from paper_2601_12904_b200 import fusion as F
+h = hashlib.sha256()
+big = F.preset("llama3-8b")
+big.layers = 2
+for preset in ("tiny", big):
+    eng = F.Engine(preset, seed=1234)
+    store = F.ChunkKVStore(eng.cfg)
+    rng = np.random.default_rng(8)
+    n = 256 if preset == "tiny" else 512
+    ids = [eng.preprocess_isolated(store, rng.integers(0, eng.cfg.vocab, n).tolist()) for _ in range(4)]
+    question = rng.integers(0, eng.cfg.vocab, 32).tolist()
+    res = F.Result(eng, 4 * n + 32 + 8)
+    for ratio in (0.0, 0.15):
+        for i in range(2):  # eager, then captured graph
+            eng.reprocess(store, question, ids, ratio, res)
+            k, v = res.fused_kv()
+            h.update(k.tobytes()); h.update(v.tobytes()); h.update(res.logits().tobytes())
+    h.update(eng.decode(res, 4).tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_gemm_chain_is_bit_identical(cuda):
+    """The <= 32-row projection chain (gemm_chain.cu: O -> gate/up -> down ->
+    next QKV in one persistent launch) computes exactly what the four separate
+    weight-streaming GEMMs compute (same tiles, splits and fixup order):
+    question pass, r = 0 sparse pass and decode, tiny and 8B width."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    out = {}
+    for ch in ("0", "1"):
+        env = dict(os.environ, FRAG_GEMM_CHAIN=ch)
+        p = subprocess.run([sys.executable, "-c", _CHAIN_SNIPPET], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[ch] = p.stdout.strip().splitlines()[-1]
+    assert out["0"] == out["1"]
