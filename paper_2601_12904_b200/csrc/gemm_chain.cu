@@ -39,7 +39,8 @@ constexpr int CHAIN_THREADS = 192;
 constexpr uint32_t CA_BYTES = CAR * CBK * 2;
 constexpr uint32_t CB_BYTES = CBN * CBK * 2;
 constexpr uint32_t CSTAGE_BYTES = CA_BYTES + CB_BYTES;  // 20 KB; UMMA rows 32..127 alias B bytes
-constexpr int CTMEM_COLS = 256;                          // 2 x BN accumulators
+constexpr int CTMEM_COLS = 256;
+constexpr int CHAIN_CNT_STRIDE = 512;  // fixup counter slots per op (tiles <= 512)                          // 2 x BN accumulators
 constexpr size_t CSMEM = 1024 + (size_t)CSTAGES * CSTAGE_BYTES + 256;
 static_assert(CSTAGE_BYTES >= CBM * CBK * 2, "aliased A rows must stay inside the stage");
 
@@ -57,7 +58,7 @@ __device__ __forceinline__ void chain_stamp(const ChainArgs& a, int o, int k) {
   if (a.trace) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[((size_t)blockIdx.x * CHAIN_MAX_OPS + o) * 4 + k] = t;
+    a.trace[((size_t)blockIdx.x * CHAIN_MAX_OPS + o) * 8 + k] = t;
   }
 }
 
@@ -68,6 +69,41 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 __device__ __forceinline__ void wait_count(const int* p, int target) {
   while (ld_acquire(p) < target) __nanosleep(32);
+}
+// release-increment without waiting for the result (the writer does not stall
+// on the atomic's round trip); cumulative over the CTA's writes ordered before
+// it by bar.sync
+__device__ __forceinline__ void red_release(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Split-K fixup of one chain op (cf. split_fixup in gemm_epi.cuh): every
+// split CTA of the tile waits for all S partials and reduces its share of the
+// 32-column chunks in split order (bit-identical to split_fixup). Each op has
+// its own counter slots (reset by the chain's last CTA), so there is no second
+// round of arrivals, and the arrival is a release-reduction: two fewer
+// dependent L2 round trips per op than the standalone kernel's fixup.
+__device__ __forceinline__ void tstamp(unsigned long long* p) {
+  if (p) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *p = t;
+  }
+}
+template <int EPI>
+__device__ __forceinline__ void chain_fixup(const EpiParams& ep, int* cnt, int slot, int S, int sp, int M,
+                                            int row_in_tile, int col0, bool leader, float rs,
+                                            unsigned long long* ts) {
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (leader) {
+    tstamp(ts ? ts + 4 : nullptr);
+    red_release(cnt, 1);
+    wait_count(cnt, S);
+    tstamp(ts ? ts + 5 : nullptr);
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const float* base = ep.ws + ((size_t)slot * S * M + row_in_tile) * CBN;
+  if (row_in_tile < M) reduce_partials<CBN, EPI>(ep, base, (size_t)M * CBN, S, sp, S, row_in_tile, col0, rs);
 }
 
 // unit u of an op: N tile and K range (split sp of S)
@@ -85,9 +121,9 @@ __device__ __forceinline__ int chain_units(const ChainOp& op) {
 // Epilogue of one unit (4 warps, named barrier 1): direct fused epilogue, or
 // the split partial + the cooperative deterministic fixup.
 template <int EPI>
-__device__ __forceinline__ void chain_epilogue(const EpiParams& ep, int M, int tile, int sp, int S, int row_in_tile,
-                                               int q, int lane, int warp, uint32_t t_row, uint64_t* tempty_acc,
-                                               float rs) {
+__device__ __forceinline__ void chain_epilogue(const EpiParams& ep, int* cnt, int M, int tile, int sp, int S,
+                                               int row_in_tile, int q, int lane, int warp, uint32_t t_row,
+                                               uint64_t* tempty_acc, float rs, unsigned long long* ts) {
   const int row = row_in_tile;  // one M tile
   const int col0 = tile * CBN;
   if (S <= 1) {
@@ -130,7 +166,7 @@ __device__ __forceinline__ void chain_epilogue(const EpiParams& ep, int M, int t
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(tempty_acc);
-    split_fixup<CBN, EPI>(ep, tile, S, sp, M, row_in_tile, row, M, col0, warp == 2 && lane == 0, rs);
+    chain_fixup<EPI>(ep, cnt + tile, tile, S, sp, M, row_in_tile, col0, warp == 2 && lane == 0, rs, ts);
   }
 }
 
@@ -283,6 +319,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
       if (o > 0) wait_count(&args.done[o - 1], chain_units(args.op[o - 1]));
       if (o > 1) wait_count(&args.done[o - 2], chain_units(args.op[o - 2]));
       const EpiParams& ep = op.ep;
+      int* cnt = ep.counters + o * CHAIN_CNT_STRIDE;  // this op's fixup counters
+      unsigned long long* ts = args.trace ? args.trace + ((size_t)blockIdx.x * CHAIN_MAX_OPS + o) * 8 : nullptr;
       float rs = 1.f;
       if (row_in_tile < M) {
         switch (op.epi) {
@@ -300,23 +338,22 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * CBN;
         switch (op.epi) {
           case EPI_RESID:
-            chain_epilogue<EPI_RESID>(ep, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs);
+            chain_epilogue<EPI_RESID>(ep, cnt, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs, ts);
             break;
           case EPI_SWIGLU:
-            chain_epilogue<EPI_SWIGLU>(ep, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs);
+            chain_epilogue<EPI_SWIGLU>(ep, cnt, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs, ts);
             break;
           case EPI_QKV:
-            chain_epilogue<EPI_QKV>(ep, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs);
+            chain_epilogue<EPI_QKV>(ep, cnt, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc], rs, ts);
             break;
           default:
-            chain_epilogue<EPI_STORE_BF16>(ep, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc],
-                                           rs);
+            chain_epilogue<EPI_STORE_BF16>(ep, cnt, M, tile, sp, S, row_in_tile, q, lane, warp, t_row, &tempty[acc],
+                                           rs, ts);
             break;
         }
         // unit complete (its outputs written): publish
-        __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && lane == 0) atomicAdd(&args.done[o], 1);
+        if (warp == 2 && lane == 0) red_release(&args.done[o], 1);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -334,7 +371,12 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
     int* exit_cnt = args.done + CHAIN_MAX_OPS;
     __threadfence();
     if (atomicAdd(exit_cnt, 1) == G - 1) {
-      for (int o = 0; o < n_ops; ++o) args.done[o] = 0;
+      for (int o = 0; o < n_ops; ++o) {
+        args.done[o] = 0;
+        const int tiles = args.op[o].N / CBN;
+        int* cnt = args.op[o].ep.counters + o * CHAIN_CNT_STRIDE;
+        for (int t = 0; t < tiles; ++t) cnt[t] = 0;
+      }
       *exit_cnt = 0;
       __threadfence();
     }
@@ -365,7 +407,8 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
     long s = 1;
     while (s < 8 && tiles * (s + 1) <= sms && nk / (s + 1) >= 4) ++s;
     if (s > nk) s = nk;
-    if (tiles > st.ep.counters_cap || (size_t)(tiles * s * M * CBN) * sizeof(float) > st.ep.ws_bytes) s = 1;
+    if ((size_t)(tiles * s * M * CBN) * sizeof(float) > st.ep.ws_bytes) s = 1;
+    if (tiles > CHAIN_CNT_STRIDE || (o + 1) * CHAIN_CNT_STRIDE > st.ep.counters_cap) return -1;
     ChainOp& op = args.op[o];
     op.N = st.N;
     op.K = st.K;
@@ -380,7 +423,7 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
   // stamps [A ready, loads issued, first accumulator, all units published]
   static const char* trace_path = std::getenv("FRAG_CHAIN_TRACE");
   static unsigned long long* trace_dev = nullptr;
-  const size_t tn = (size_t)sms * CHAIN_MAX_OPS * 4;
+  const size_t tn = (size_t)sms * CHAIN_MAX_OPS * 8;
   if (trace_path) {
     if (!trace_dev) cudaMalloc(&trace_dev, tn * sizeof(unsigned long long));
     cudaMemsetAsync(trace_dev, 0, tn * sizeof(unsigned long long), stream);

@@ -1,7 +1,7 @@
 """Per-op timeline of the weight-streaming GEMM chain (gemm_chain.cu) inside
 one 8B question pass, from its FRAG_CHAIN_TRACE globaltimer stamps (ns):
 per op and CTA [A operand ready, all loads issued, first accumulator ready,
-all units published]; prints min / median / max over CTAs relative to the
+all units published, (split ops) partial written, all siblings arrived]; prints min / median / max over CTAs relative to the
 chain's first stamp, for one mid-depth layer."""
 import os
 import sys
@@ -25,12 +25,12 @@ if os.path.exists(path):
     os.remove(path)
 eng.reprocess(store, question, ids, 0.15, res)  # first request of the shape: eager
 sms = 148
-rec = np.fromfile(path, dtype=np.uint64).reshape(-1, sms, 4, 4).astype(np.int64)
+rec = np.fromfile(path, dtype=np.uint64).reshape(-1, sms, 4, 8).astype(np.int64)
 print(f"{len(rec)} chain launches recorded")
 names = ["O", "gate/up", "down", "QKV(next)"]
 for li in (1, len(rec) // 2):
     r = rec[li]
-    t0 = r[r > 0].min()
+    t0 = r[:, :, :4][r[:, :, :4] > 0].min()
     print(f"-- chain {li}: span {(r.max() - t0) / 1e3:.1f} us")
     for o in range(4):
         x = r[:, o, :]
@@ -38,8 +38,10 @@ for li in (1, len(rec) // 2):
         if len(x) == 0:
             continue
         cols = []
-        for k in range(4):
+        for k in range(6):
             v = (x[:, k] - t0) / 1e3
             cols.append(f"{v.min():6.1f}/{np.median(v):6.1f}/{v.max():6.1f}")
         print(f"{names[o]:>10} ({len(x):3d} CTAs)  A-ready {cols[0]}  issued {cols[1]}  first-acc {cols[2]}  "
               f"published {cols[3]}")
+        if (x[:, 4] > 0).all():
+            print(f"{'':>10}  split-K fixup: partial written {cols[4]}  all siblings arrived {cols[5]}")
