@@ -333,6 +333,8 @@ for preset in ("tiny", big):
             k, v = res.fused_kv()
             h.update(k.tobytes()); h.update(v.tobytes()); h.update(res.logits().tobytes())
     h.update(eng.decode(res, 4).tobytes())
+    eng.reprocess(store, question[:7], ids, 0.15, res)  # 7-row question pass
+    h.update(res.logits().tobytes())
 print(h.hexdigest())
 """
 
