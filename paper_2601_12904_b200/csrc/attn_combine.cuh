@@ -1,0 +1,72 @@
+// Split-KV combine of the sparse-Q attention (K6c), shared by the standalone
+// combine kernel (attn.cu) and the GEMM chain's pre-op (gemm_chain.cu).
+#pragma once
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace fragk {
+
+// Merge split partials: out = sum_s w_s O_s / sum_s w_s, w_s = exp(lse_s - max).
+// One warp per (token, head) row qi: the split weights are computed
+// lane-parallel (one split per lane), then every lane accumulates DH/32
+// columns over the splits with coalesced loads, four splits in flight.
+template <int DH>
+__device__ __forceinline__ void attn_combine_row(const AttnArgs& a, size_t qi, int lane) {
+  constexpr int V = DH / 32;  // columns per lane
+  const size_t MH = (size_t)a.M * a.Hq;
+  const int S = a.n_splits;
+  float wl[2] = {0.f, 0.f};  // weights of splits lane and lane + 32 (S <= 64)
+  float mx = -INFINITY;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int sp = lane + 32 * h;
+    wl[h] = sp < S ? a.part_lse[sp * MH + qi] : -INFINITY;
+    mx = fmaxf(mx, wl[h]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float wsum = 0.f;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    wl[h] = (wl[h] == -INFINITY) ? 0.f : __expf(wl[h] - mx);
+    wsum += wl[h];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+  float acc[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) acc[e] = 0.f;
+  const float* base = a.part_o + qi * DH + lane * V;
+  for (int s0 = 0; s0 < S; s0 += 4) {
+    float v[4][V];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int sp = s0 + u;
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[u][e] = 0.f;
+      if (sp < S) {
+        if constexpr (V == 4) {
+          const float4 t = __ldcg(reinterpret_cast<const float4*>(base + sp * MH * DH));
+          v[u][0] = t.x, v[u][1] = t.y, v[u][2] = t.z, v[u][3] = t.w;
+        } else {
+          const float2 t = __ldcg(reinterpret_cast<const float2*>(base + sp * MH * DH));
+          v[u][0] = t.x, v[u][1] = t.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int sp = s0 + u;
+      const float w = __shfl_sync(0xffffffffu, sp < 32 ? wl[0] : wl[1], sp & 31);
+      if (sp < S)
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] += w * v[u][e];
+    }
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  bf16* out = a.out + qi * DH + lane * V;
+#pragma unroll
+  for (int e = 0; e < V; e += 2) *reinterpret_cast<uint32_t*>(out + e) = pack_bf16(acc[e] * inv, acc[e + 1] * inv);
+}
+
+}  // namespace fragk

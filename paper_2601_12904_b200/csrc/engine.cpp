@@ -500,6 +500,12 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     static const std::vector<Seg> no_segs;
     const std::vector<Seg>& asegs = prune ? last_seg : (seg_prune ? no_segs : segs);
     const std::vector<std::pair<int, int>>& asplit = prune ? last_split : seg_split;
+    // the layer's projections run as a GEMM chain: a single sequence's
+    // split-KV combine moves into the chain (pre-op writing op 0's A rows)
+    const bool chain_layer = use_chain && Ml == M && off == 0;
+    const bool defer_ok = chain_layer && asegs.size() == 1;
+    bool deferred = false;
+    fragk::AttnArgs deferred_args{};
     for (size_t si = 0; si < asegs.size(); ++si) {
       const Seg& g = asegs[si];
       if (g.M <= 0) continue;
@@ -521,9 +527,10 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       a.n_splits = asplit[si].first;
       a.scale = 1.0f / std::sqrt((float)dh);
       Scoped sc(P, s, KC_ATTN, 0, 0);
-      sc.launched(fragk::sparse_q_attention(a, s));
+      sc.launched(fragk::sparse_q_attention(a, s, defer_ok ? &deferred : nullptr));
+      if (deferred) deferred_args = a;
     }
-    if (use_chain && Ml == M && off == 0) {
+    if (chain_layer) {
       fragk::ChainStep st[fragk::CHAIN_MAX_OPS];
       int n = 0;
       st[n].A = r->attn.as<bf16>(), st[n].B = W.wo, st[n].N = d, st[n].K = (int)qc, st[n].epi = fragk::EPI_RESID;
@@ -553,7 +560,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
         qkv_done = true;
       }
       Scoped sc(P, s, gemm_class(M), flop, bytes);
-      sc.launched(fragk::gemm_chain_tc(st, n, M, chain_done, s));
+      sc.launched(fragk::gemm_chain_tc(st, n, M, chain_done, s, deferred ? &deferred_args : nullptr));
       peek("layer");
       continue;
     }

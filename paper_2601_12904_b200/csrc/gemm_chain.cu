@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "attn_combine.cuh"
 #include "gemm_epi.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -50,7 +51,10 @@ struct ChainArgs {
   ChainOp op[CHAIN_MAX_OPS];
   int n_ops;
   int M;
-  int* done;  // [CHAIN_MAX_OPS] op completion counters, [CHAIN_MAX_OPS] CTA exit counter
+  int* done;  // [CHAIN_MAX_OPS] op completion counters, [CHAIN_MAX_OPS] CTA exit counter,
+              // [CHAIN_MAX_OPS + 1] pre-op (attention combine) completion
+  AttnArgs pre;  // split-KV attention whose combine writes op 0's A operand
+  int pre_rows;  // (token, head) rows to combine; 0 = no pre-op
   unsigned long long* trace;  // tooling (FRAG_CHAIN_TRACE): [cta][op][4] globaltimer stamps
 };
 
@@ -239,6 +243,10 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         if ((int)blockIdx.x >= units) continue;
         if (o == 0) {
           pdl_wait();
+          if (args.pre_rows > 0) {  // op 0's A rows come from the in-chain combine
+            wait_count(&args.done[CHAIN_MAX_OPS + 1], G);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
         } else {
           wait_count(&args.done[o - 1], chain_units(args.op[o - 1]));
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
@@ -309,6 +317,18 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
     pdl_wait();
     const int q = warp & 3;
     const int row_in_tile = q * 32 + lane;
+    if (args.pre_rows > 0) {
+      // pre-op: merge the attention's split-KV partials into op 0's A rows,
+      // one warp per (token, head) row, then publish (every CTA counts once)
+      for (size_t qi = (size_t)blockIdx.x * 4 + q; qi < (size_t)args.pre_rows; qi += (size_t)G * 4) {
+        if (args.pre.dh == 128)
+          attn_combine_row<128>(args.pre, qi, lane);
+        else
+          attn_combine_row<64>(args.pre, qi, lane);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 2 && lane == 0) red_release(&args.done[CHAIN_MAX_OPS + 1], 1);
+    }
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int o = 0; o < n_ops; ++o) {
@@ -371,6 +391,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
     int* exit_cnt = args.done + CHAIN_MAX_OPS;
     __threadfence();
     if (atomicAdd(exit_cnt, 1) == G - 1) {
+      args.done[CHAIN_MAX_OPS + 1] = 0;
       for (int o = 0; o < n_ops; ++o) {
         args.done[o] = 0;
         const int tiles = args.op[o].N / CBN;
@@ -387,9 +408,15 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
 
 bool gemm_chain_supported(int M, int N, int K) { return M >= 1 && M <= CAR && N % CBN == 0 && K % CBK == 0; }
 
-int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStream_t stream) {
+int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStream_t stream,
+                  const AttnArgs* pre_combine) {
   if (n_ops < 1 || n_ops > CHAIN_MAX_OPS || !done) return -1;
   ChainArgs args{};
+  if (pre_combine) {
+    if (pre_combine->dh != 64 && pre_combine->dh != 128) return -1;
+    args.pre = *pre_combine;
+    args.pre_rows = pre_combine->M * pre_combine->Hq;
+  }
   args.n_ops = n_ops;
   args.M = M;
   args.done = done;

@@ -78,6 +78,7 @@ int num_sms();
 // GEMMs (M <= 32 rows, BN = 128) in one persistent launch, op i+1's A = op i's
 // output. `done` = 2*CHAIN_MAX_OPS ints, zero before the first launch (left zero).
 constexpr int CHAIN_MAX_OPS = 4;
+struct AttnArgs;
 struct ChainStep {
   const bf16* A = nullptr;
   const bf16* B = nullptr;
@@ -90,7 +91,10 @@ struct ChainOp {
   EpiParams ep;
 };
 bool gemm_chain_supported(int M, int N, int K);
-int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStream_t stream);
+// pre_combine: split-KV attention whose combine (-> op 0's A operand) runs
+// inside the chain before op 0 (nullptr: none)
+int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStream_t stream,
+                  const AttnArgs* pre_combine = nullptr);
 
 // TMA descriptors (bf16, SWIZZLE_128B, 64-element inner box), encoded through the
 // driver entry point so the library needs no link-time libcuda.
@@ -135,7 +139,9 @@ struct AttnArgs {
   float scale;           // 1/sqrt(dh)
   unsigned long long* trace = nullptr;  // tooling: clock64 timeline of CTA 0 (FRAG_ATTN_TRACE)
 };
-int sparse_q_attention(const AttnArgs& a, cudaStream_t stream);  // returns launches
+// returns launches; with combine_deferred != nullptr a split-KV launch leaves
+// the combine to the caller (*combine_deferred = true)
+int sparse_q_attention(const AttnArgs& a, cudaStream_t stream, bool* combine_deferred = nullptr);
 int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream);
 int attn_rows_per_cta();
 
