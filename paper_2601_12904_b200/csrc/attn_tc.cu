@@ -53,6 +53,9 @@ struct AttCfg {
   static constexpr uint32_t KV_ATOM = AT_KEYS * 128;       // [128 keys][64 cols] bf16
   static constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;   // K (or V) per stage
   static constexpr size_t SMEM = 1024 + AT_QT * (size_t)Q_TILE + 4 * (size_t)KV_BYTES + 256;
+  // DUAL (one query tile): the second Q slot holds a third K/V stage
+  static constexpr size_t SMEM_DUAL = 1024 + (size_t)Q_TILE + 6 * (size_t)KV_BYTES + 256;
+  static_assert(SMEM_DUAL <= 232448, "3-stage attention tile exceeds the 227 KB shared-memory limit");
   static constexpr uint32_t T_S = 0, T_O = 128, T_TILE = 256;  // TMEM columns per tile
   static_assert(SMEM <= 232448, "attention tile exceeds the 227 KB shared-memory limit");
 };
@@ -76,18 +79,22 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
   constexpr int KT = DUAL ? AT_KEYS / 2 : AT_KEYS;  // keys per tile slot per K/V tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                       // [QT][Q_TILE]
-  uint8_t* sK = sQ + AT_QT * C::Q_TILE;     // [2 stages][KV_BYTES]
-  uint8_t* sV = sK + 2 * C::KV_BYTES;       // [2 stages][KV_BYTES]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * C::KV_BYTES);
+  // K/V ring depth: 2 stages next to two Q tiles; DUAL keeps one Q tile and
+  // spends the other slot on a third stage (the question pass / decode CTAs
+  // stream ~8 K/V tiles each and are latency-bound on the ring)
+  constexpr int NS = DUAL ? 3 : 2;
+  uint8_t* sQ = smem;                                    // [QT or 1][Q_TILE]
+  uint8_t* sK = sQ + (DUAL ? 1 : AT_QT) * C::Q_TILE;     // [NS stages][KV_BYTES]
+  uint8_t* sV = sK + NS * C::KV_BYTES;                   // [NS stages][KV_BYTES]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + NS * C::KV_BYTES);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;    // [2]
-  uint64_t* v_full = bar + 3;    // [2]
-  uint64_t* kv_empty = bar + 5;  // [2]
-  uint64_t* s_full = bar + 7;    // [QT]
-  uint64_t* p_full = bar + 9;    // [QT]
-  uint64_t* pv_done = bar + 11;  // [QT]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint64_t* k_full = bar + 1;              // [NS]
+  uint64_t* v_full = bar + 1 + NS;         // [NS]
+  uint64_t* kv_empty = bar + 1 + 2 * NS;   // [NS]
+  uint64_t* s_full = bar + 1 + 3 * NS;     // [QT]
+  uint64_t* p_full = s_full + AT_QT;       // [QT]
+  uint64_t* pv_done = p_full + AT_QT;      // [QT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + AT_QT);
 
   const int warp = warp_id(), lane = lane_id();
   // global longest-first order: q-block work grows with its row positions, so
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -148,8 +155,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
           tma_load_3d(sQ + t * C::Q_TILE + at * (AT_ROWS * 128), &tmQ, q_full, at * 64, hk * G,
                       t0 + t * tok_per_tile);
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);  // PV(j-2) done with this stage
+        const int st = j % NS;
+        mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);  // PV(j-NS) done with this stage
         const int key0 = k_lo + j * AT_KEYS;
         mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
 #pragma unroll
@@ -160,8 +167,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
         for (int at = 0; at < C::ATOMS; ++at)
           tma_load_2d(sV + st * C::KV_BYTES + at * C::KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64, key0);
       }
-      // consume the last two kv_empty phases (no phase completes unobserved)
-      for (int j = n_tiles > 2 ? n_tiles - 2 : 0; j < n_tiles; ++j) mbar_wait(&kv_empty[j & 1], (j >> 1) & 1);
+      // consume the last NS kv_empty phases (no phase completes unobserved)
+      for (int j = n_tiles > NS ? n_tiles - NS : 0; j < n_tiles; ++j) mbar_wait(&kv_empty[j % NS], (j / NS) & 1);
     }
   } else if (warp == W_MMA) {
     // ------------------------------------------------------------ MMA issuer
@@ -174,8 +181,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
       const uint64_t dk = umma_desc_sw128(smem_u32(sK), 16, 1024);
       const uint64_t dv = umma_desc_sw128(smem_u32(sV), C::KV_ATOM, 1024);
       auto issue_s = [&](int t, int j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
+        const int st = j % NS;
+        mbar_wait(&k_full[st], (j / NS) & 1);
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256) a.trace[(t * 256 + j) * 4 + 2] = clock64();
         if (elect_one()) {
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
         __syncwarp();
       };
       auto issue_pv = [&](int t, int j) {
-        const int st = j & 1;
+        const int st = j % NS;
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256) a.trace[(t * 256 + j) * 4 + 3] = clock64();
@@ -215,7 +222,7 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
       };
       for (int t = 0; t < n_slots; ++t) issue_s(t, 0);
       for (int j = 0; j < n_tiles; ++j) {
-        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&v_full[j % NS], (j / NS) & 1);
         for (int t = 0; t < n_slots; ++t) {
           issue_pv(t, j);
           if (j + 1 < n_tiles) issue_s(t, j + 1);
@@ -585,9 +592,9 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   const bool dual = a.M <= AT_ROWS / G;
   if (dual) {
     if (a.dh == 128)
-      go(attn_tc_kernel<128, 0, true>, (int)AttCfg<128>::SMEM);
+      go(attn_tc_kernel<128, 0, true>, (int)AttCfg<128>::SMEM_DUAL);
     else if (a.dh == 64)
-      go(attn_tc_kernel<64, 0, true>, (int)AttCfg<64>::SMEM);
+      go(attn_tc_kernel<64, 0, true>, (int)AttCfg<64>::SMEM_DUAL);
     else
       return -1;
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
