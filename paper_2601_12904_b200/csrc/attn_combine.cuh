@@ -9,12 +9,36 @@ namespace fragk {
 // Merge split partials: out = sum_s w_s O_s / sum_s w_s, w_s = exp(lse_s - max).
 // One warp per (token, head) row qi: the split weights are computed
 // lane-parallel (one split per lane), then every lane accumulates DH/32
-// columns over the splits with coalesced loads, four splits in flight.
+// columns over the splits with coalesced loads.
+template <int DH>
+__device__ __forceinline__ void attn_combine_ld(const float* p, float (&v)[DH / 32]) {
+  if constexpr (DH / 32 == 4) {
+    const float4 t = __ldcg(reinterpret_cast<const float4*>(p));
+    v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+  } else {
+    const float2 t = __ldcg(reinterpret_cast<const float2*>(p));
+    v[0] = t.x, v[1] = t.y;
+  }
+}
+
+// Latency-bound (a handful of rows per warp, ~17 splits): the first batch of
+// partial O loads is issued together with the split LSE loads, and the next
+// batch is in flight while the current one is accumulated (batches of 8
+// splits, accumulated in split order -> deterministic).
 template <int DH>
 __device__ __forceinline__ void attn_combine_row(const AttnArgs& a, size_t qi, int lane) {
   constexpr int V = DH / 32;  // columns per lane
+  constexpr int B = 8;        // splits per batch
   const size_t MH = (size_t)a.M * a.Hq;
   const int S = a.n_splits;
+  const float* base = a.part_o + qi * DH + lane * V;
+  float cur[B][V], nxt[B][V];
+#pragma unroll
+  for (int u = 0; u < B; ++u) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) cur[u][e] = 0.f;
+    if (u < S) attn_combine_ld<DH>(base + u * MH * DH, cur[u]);
+  }
   float wl[2] = {0.f, 0.f};  // weights of splits lane and lane + 32 (S <= 64)
   float mx = -INFINITY;
 #pragma unroll
@@ -36,32 +60,25 @@ __device__ __forceinline__ void attn_combine_row(const AttnArgs& a, size_t qi, i
   float acc[V];
 #pragma unroll
   for (int e = 0; e < V; ++e) acc[e] = 0.f;
-  const float* base = a.part_o + qi * DH + lane * V;
-  for (int s0 = 0; s0 < S; s0 += 4) {
-    float v[4][V];
+  for (int s0 = 0; s0 < S; s0 += B) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int sp = s0 + u;
+    for (int u = 0; u < B; ++u) {  // next batch in flight
 #pragma unroll
-      for (int e = 0; e < V; ++e) v[u][e] = 0.f;
-      if (sp < S) {
-        if constexpr (V == 4) {
-          const float4 t = __ldcg(reinterpret_cast<const float4*>(base + sp * MH * DH));
-          v[u][0] = t.x, v[u][1] = t.y, v[u][2] = t.z, v[u][3] = t.w;
-        } else {
-          const float2 t = __ldcg(reinterpret_cast<const float2*>(base + sp * MH * DH));
-          v[u][0] = t.x, v[u][1] = t.y;
-        }
-      }
+      for (int e = 0; e < V; ++e) nxt[u][e] = 0.f;
+      if (s0 + B + u < S) attn_combine_ld<DH>(base + (s0 + B + u) * MH * DH, nxt[u]);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < B; ++u) {
       const int sp = s0 + u;
       const float w = __shfl_sync(0xffffffffu, sp < 32 ? wl[0] : wl[1], sp & 31);
       if (sp < S)
 #pragma unroll
-        for (int e = 0; e < V; ++e) acc[e] += w * v[u][e];
+        for (int e = 0; e < V; ++e) acc[e] += w * cur[u][e];
     }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+#pragma unroll
+      for (int e = 0; e < V; ++e) cur[u][e] = nxt[u][e];
   }
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
   bf16* out = a.out + qi * DH + lane * V;

@@ -55,15 +55,30 @@ struct ChainArgs {
               // [CHAIN_MAX_OPS + 1] pre-op (attention combine) completion
   AttnArgs pre;  // split-KV attention whose combine writes op 0's A operand
   int pre_rows;  // (token, head) rows to combine; 0 = no pre-op
-  unsigned long long* trace;  // tooling (FRAG_CHAIN_TRACE): [cta][op][4] globaltimer stamps
+  int timeline;  // tooling (FRAG_CHAIN_TRACE=1): globaltimer stamps into g_chain_tl
 };
 
-__device__ __forceinline__ void chain_stamp(const ChainArgs& a, int o, int k) {
-  if (a.trace) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[((size_t)blockIdx.x * CHAIN_MAX_OPS + o) * 8 + k] = t;
-  }
+// Tooling timeline, graph-replay safe: launch n writes ring slot n % TL_LAUNCHES
+// (n = g_chain_seq, read after griddepcontrol.wait and bumped by the last CTA
+// out); per CTA [0] entry, [1] PDL wait done, [2] exit, [8 + 8 op + k] op
+// stamps k = A ready, loads issued, first accumulator, published, fixup
+// partial written, fixup siblings arrived. Read by frag_debug_chain_timeline.
+constexpr int TL_LAUNCHES = 64, TL_CTAS = 160, TL_SLOTS = 8 + 8 * CHAIN_MAX_OPS;
+__device__ unsigned long long g_chain_tl[TL_LAUNCHES][TL_CTAS][TL_SLOTS];
+__device__ int g_chain_seq;
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long* chain_tl(const ChainArgs& a) {
+  if (!a.timeline || blockIdx.x >= TL_CTAS) return nullptr;
+  const int n = *reinterpret_cast<volatile int*>(&g_chain_seq);
+  return &g_chain_tl[n % TL_LAUNCHES][blockIdx.x][0];
+}
+__device__ __forceinline__ void chain_stamp(unsigned long long* tl, int o, int k) {
+  if (tl) tl[8 + 8 * o + k] = gtime();
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -215,6 +230,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
+      const unsigned long long t_entry = gtime();
+      unsigned long long* tl = nullptr;
       pdl_launch_dependents();
       int stage = 0;
       uint32_t phase = 0;
@@ -240,9 +257,13 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
             advance();
           }
         }
+        if (o == 0) {
+          pdl_wait();  // every CTA, before it reads any counter of this launch
+          tl = chain_tl(args);
+          if (tl) tl[0] = t_entry, tl[1] = gtime();
+        }
         if ((int)blockIdx.x >= units) continue;
         if (o == 0) {
-          pdl_wait();
           if (args.pre_rows > 0) {  // op 0's A rows come from the in-chain combine
             wait_count(&args.done[CHAIN_MAX_OPS + 1], G);
             asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -251,7 +272,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
           wait_count(&args.done[o - 1], chain_units(args.op[o - 1]));
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
         }
-        chain_stamp(args, o, 0);
+        chain_stamp(tl, o, 0);
         for (int i = 0, s2 = st_pre; i < npre; ++i, s2 = s2 + 1 == CSTAGES ? 0 : s2 + 1)
           tma_load_2d(sA + s2 * CSTAGE_BYTES, tA, &full[s2], (kb0 + i) * CBK, 0);
         for (int kb = kb0 + npre; kb < kb1; ++kb) {
@@ -271,7 +292,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
             advance();
           }
         }
-        chain_stamp(args, o, 1);
+        chain_stamp(tl, o, 1);
       }
     }
   } else if (warp == 1) {
@@ -315,6 +336,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     pdl_wait();
+    unsigned long long* tl = (warp == 2 && lane == 0) ? chain_tl(args) : nullptr;
     const int q = warp & 3;
     const int row_in_tile = q * 32 + lane;
     if (args.pre_rows > 0) {
@@ -340,7 +362,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
       if (o > 1) wait_count(&args.done[o - 2], chain_units(args.op[o - 2]));
       const EpiParams& ep = op.ep;
       int* cnt = ep.counters + o * CHAIN_CNT_STRIDE;  // this op's fixup counters
-      unsigned long long* ts = args.trace ? args.trace + ((size_t)blockIdx.x * CHAIN_MAX_OPS + o) * 8 : nullptr;
+      unsigned long long* ts = tl ? tl + 8 + 8 * o : nullptr;
       float rs = 1.f;
       if (row_in_tile < M) {
         switch (op.epi) {
@@ -354,7 +376,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         chain_unit(op, u, tile, kb0, kb1, sp, S);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        if (u == (int)blockIdx.x && warp == 2 && lane == 0) chain_stamp(args, o, 2);
+        if (u == (int)blockIdx.x) chain_stamp(tl, o, 2);
         const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * CBN;
         switch (op.epi) {
           case EPI_RESID:
@@ -377,7 +399,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
-      if (warp == 2 && lane == 0) chain_stamp(args, o, 3);
+      chain_stamp(tl, o, 3);
     }
   }
   tc_fence_before();
@@ -387,6 +409,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
     tmem_dealloc<CTMEM_COLS>(tmem_base);
   }
   if (threadIdx.x == 0) {
+    if (unsigned long long* tl = chain_tl(args)) tl[2] = gtime();
     // the last CTA out re-arms the counters for the next launch (graph replay)
     int* exit_cnt = args.done + CHAIN_MAX_OPS;
     __threadfence();
@@ -399,6 +422,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         for (int t = 0; t < tiles; ++t) cnt[t] = 0;
       }
       *exit_cnt = 0;
+      if (args.timeline) g_chain_seq = g_chain_seq + 1;
       __threadfence();
     }
   }
@@ -446,28 +470,21 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
     op.ep.full_tiles = 0;
     op.ep.streamk = 0;
   }
-  // FRAG_CHAIN_TRACE=<file>: tooling only -- per-CTA, per-op globaltimer
-  // stamps [A ready, loads issued, first accumulator, all units published]
-  static const char* trace_path = std::getenv("FRAG_CHAIN_TRACE");
-  static unsigned long long* trace_dev = nullptr;
-  const size_t tn = (size_t)sms * CHAIN_MAX_OPS * 8;
-  if (trace_path) {
-    if (!trace_dev) cudaMalloc(&trace_dev, tn * sizeof(unsigned long long));
-    cudaMemsetAsync(trace_dev, 0, tn * sizeof(unsigned long long), stream);
-    args.trace = trace_dev;
-  }
+  static const bool timeline = std::getenv("FRAG_CHAIN_TRACE") != nullptr;  // tooling only
+  args.timeline = timeline ? 1 : 0;
   smem_attr_once(gemm_chain_kernel, (int)CSMEM);
   launch_pdl(gemm_chain_kernel, dim3((unsigned)sms), dim3(CHAIN_THREADS), CSMEM, stream, args);
-  if (trace_path) {
-    std::vector<unsigned long long> h(tn);
-    cudaMemcpyAsync(h.data(), trace_dev, tn * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
-    cudaStreamSynchronize(stream);
-    if (FILE* f = std::fopen(trace_path, "ab")) {
-      std::fwrite(h.data(), tn * sizeof(unsigned long long), 1, f);
-      std::fclose(f);
-    }
-  }
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace fragk
+
+// Tooling (tools/chain_trace.py; not part of the frag C API): copy the chain
+// timeline ring. Returns the number of chain launches recorded so far.
+extern "C" __attribute__((visibility("default"))) int frag_debug_chain_timeline(unsigned long long* out, int max_launches) {
+  int seq = 0;
+  cudaMemcpyFromSymbol(&seq, fragk::g_chain_seq, sizeof(int));
+  const int n = max_launches < fragk::TL_LAUNCHES ? max_launches : fragk::TL_LAUNCHES;
+  cudaMemcpyFromSymbol(out, fragk::g_chain_tl, (size_t)n * fragk::TL_CTAS * fragk::TL_SLOTS * 8);
+  return seq;
+}
