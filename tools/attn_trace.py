@@ -1,5 +1,6 @@
 """Timeline of one attention CTA (the first-dispatched, longest q-block) at the
-8B sparse-pass shape, from the kernel's FRAG_ATTN_TRACE clock64 stamps:
+8B sparse-pass shape (argv[1] = "question": the 32-row question pass, split-KV
+DUAL kernel, the CTA of split 0), from the kernel's FRAG_ATTN_TRACE clock64 stamps:
 per key tile j and query tile t: S ready (softmax wakes), P done (softmax
 arrives), S issue and PV issue times in the MMA warp. Prints per-tile
 softmax durations, S waits and the MMA issue gaps (SM cycles)."""
@@ -19,15 +20,21 @@ from paper_2601_12904_b200 import _lib as L  # noqa: E402
 
 dev = torch.device("cuda")
 M, T, Hq, Hkv, dh = 2490, 16416, 32, 8, 128
+question = len(sys.argv) > 1 and sys.argv[1] == "question"  # 32 rows at the end, split-KV (DUAL kernel)
+split = 0
+if question:
+    M, split = 32, 1024
 g = torch.Generator(device="cuda").manual_seed(0)
 q = torch.randn(M, Hq, dh, device=dev, generator=g).to(torch.bfloat16)
 k = torch.randn(T, Hkv, dh, device=dev, generator=g).to(torch.bfloat16)
 v = torch.randn(T, Hkv, dh, device=dev, generator=g).to(torch.bfloat16)
 rows = torch.sort(torch.randperm(T, device=dev, generator=g)[:M]).values.to(torch.int32)
+if question:
+    rows = torch.arange(T - M, T, device=dev, dtype=torch.int32)
 out = torch.empty(M, Hq, dh, device=dev, dtype=torch.bfloat16)
 for _ in range(3):
     L.check(L.lib.frag_kernel_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), rows.data_ptr(), out.data_ptr(),
-                                        M, T, Hq, Hkv, dh, 0, None))
+                                        M, T, Hq, Hkv, dh, split, None))
 torch.cuda.synchronize()
 rec = np.fromfile(path, dtype=np.uint64).reshape(-1, 2, 256, 4)[-1].astype(np.int64)
 base = rec[rec > 0].min()
