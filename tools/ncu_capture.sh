@@ -16,6 +16,9 @@ ncu --profile-from-start off --set full --clock-control none --import-source on 
 # question pass, layer 0: the four weight-streaming GEMMs
 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:gemm_tc_kernel -s 0 -c 4 -o $OUT/gemmq_$TAG python tools/profile_step.py > /dev/null 2>&1
+# question pass, layer 0: the GEMM chain (combine pre-op + O, gate/up, down, next QKV)
+ncu --profile-from-start off --set full --clock-control none --import-source on \
+    -k regex:gemm_chain -s 0 -c 1 -o $OUT/chain_$TAG python tools/profile_step.py > /dev/null 2>&1
 # sparse pass, layer 0 attention (after the 32 question-pass launches) + one question-pass attention
 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:attn_tc -s 32 -c 1 -o $OUT/attn_$TAG python tools/profile_step.py > /dev/null 2>&1

@@ -101,7 +101,7 @@ def main():
            f"Sum of launch times: reprocess {tot1 / 1e3:.2f} ms vs full prefill {tot2 / 1e3:.2f} ms "
            f"({tot2 / tot1:.2f}x).", ""]
     traffic = {}
-    for name in ("gemm", "gemmq", "attn", "attnq", "mem"):
+    for name in ("gemm", "gemmq", "chain", "attn", "attnq", "mem"):
         rep = src / f"{name}_{tag}.ncu-rep"
         if not rep.exists():
             continue
