@@ -415,7 +415,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     if (l > 0 && fuse_norm) norm_in(ep, 0);
     return ep;
   };
-  // <= 32 rows (question pass, decode, r = 0): the O -> gate/up -> down ->
+  // <= 128 rows (question pass, decode, r = 0): the O -> gate/up -> down ->
   // next-QKV projections of a layer run as one persistent GEMM chain
   // (gemm_chain.cu; FRAG_GEMM_CHAIN=0 launches them one by one)
   static const bool chain_env = [] {

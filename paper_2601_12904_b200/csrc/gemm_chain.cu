@@ -1,9 +1,9 @@
-// Weight-streaming GEMM chain for M <= 32 rows (question pass, decode): the
+// Weight-streaming GEMM chain for M <= 128 rows (question pass, decode): the
 // per-layer projection sequence  O -> gate/up -> down -> next layer's QKV
 // (K7, K8, K8, K4+K5 of SPEC.md:435-444 at |Q| rows) in ONE persistent launch.
 //
-// Each op is the same computation as gemm_tc_kernel<128, EPI, 32> (A = the
-// live 32 activation rows, B = the weights, BN = 128, deterministic split-K
+// Each op is the same computation as gemm_tc_kernel<128, EPI, AR> (A = the
+// live AR >= M activation rows, B = the weights, BN = 128, deterministic split-K
 // with the cooperative fixup of gemm_epi.cuh) -- the chain only removes the
 // kernel boundaries: the TMA ring, the TMEM accumulators and the CTAs stay
 // alive from one op to the next, so op i+1's weights stream into the ring
@@ -34,16 +34,21 @@ namespace {
 constexpr int CBM = 128;  // UMMA M (accumulator rows; rows >= M are never stored)
 constexpr int CBN = 128;
 constexpr int CBK = 64;
-constexpr int CAR = 32;  // live A rows loaded per stage
-constexpr int CSTAGES = 10;
+// AR = live A rows loaded per stage (32 / 64 / 128: M <= AR); stage = AR x 64
+// activations + 128 x 64 weights, as many stages as fit in ~200 KB
+template <int AR>
+struct ChainCfg {
+  static constexpr uint32_t A_BYTES = AR * 64 * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + 128 * 64 * 2;
+  static constexpr int STAGES = AR == 32 ? 10 : (AR == 64 ? 8 : 6);
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static_assert(STAGE_BYTES >= 128 * 64 * 2, "aliased A rows must stay inside the stage");
+  static_assert(SMEM <= 232448, "chain ring exceeds the 227 KB shared-memory limit");
+};
 constexpr int CHAIN_THREADS = 192;
-constexpr uint32_t CA_BYTES = CAR * CBK * 2;
 constexpr uint32_t CB_BYTES = CBN * CBK * 2;
-constexpr uint32_t CSTAGE_BYTES = CA_BYTES + CB_BYTES;  // 20 KB; UMMA rows 32..127 alias B bytes
 constexpr int CTMEM_COLS = 256;
 constexpr int CHAIN_CNT_STRIDE = 512;  // fixup counter slots per op (tiles <= 512)                          // 2 x BN accumulators
-constexpr size_t CSMEM = 1024 + (size_t)CSTAGES * CSTAGE_BYTES + 256;
-static_assert(CSTAGE_BYTES >= CBM * CBK * 2, "aliased A rows must stay inside the stage");
 
 struct ChainArgs {
   CUtensorMap tmA[CHAIN_MAX_OPS];
@@ -189,7 +194,11 @@ __device__ __forceinline__ void chain_epilogue(const EpiParams& ep, int* cnt, in
   }
 }
 
+template <int AR>
 __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __grid_constant__ ChainArgs args) {
+  constexpr int CSTAGES = ChainCfg<AR>::STAGES;
+  constexpr uint32_t CA_BYTES = ChainCfg<AR>::A_BYTES;
+  constexpr uint32_t CSTAGE_BYTES = ChainCfg<AR>::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -430,7 +439,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
 
 }  // namespace
 
-bool gemm_chain_supported(int M, int N, int K) { return M >= 1 && M <= CAR && N % CBN == 0 && K % CBK == 0; }
+bool gemm_chain_supported(int M, int N, int K) { return M >= 1 && M <= CBM && N % CBN == 0 && K % CBK == 0; }
 
 int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStream_t stream,
                   const AttnArgs* pre_combine) {
@@ -448,7 +457,7 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
   for (int o = 0; o < n_ops; ++o) {
     const ChainStep& st = steps[o];
     if (!gemm_chain_supported(M, st.N, st.K) || !st.ep.ws || !st.ep.counters) return -1;
-    if (!make_tmap_2d(&args.tmA[o], st.A, M, st.K, st.K, CAR)) return -1;
+    if (!make_tmap_2d(&args.tmA[o], st.A, M, st.K, st.K, M <= 32 ? 32 : (M <= 64 ? 64 : 128))) return -1;
     if (!make_tmap_2d(&args.tmB[o], st.B, st.N, st.K, st.K, CBN)) return -1;
     // the one-M-tile policy of gemm_bf16_tc: split-K up to one full wave (a
     // cost model that balanced the 224-tile gate/up with 5 splits and the
@@ -472,8 +481,16 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
   }
   static const bool timeline = std::getenv("FRAG_CHAIN_TRACE") != nullptr;  // tooling only
   args.timeline = timeline ? 1 : 0;
-  smem_attr_once(gemm_chain_kernel, (int)CSMEM);
-  launch_pdl(gemm_chain_kernel, dim3((unsigned)sms), dim3(CHAIN_THREADS), CSMEM, stream, args);
+  auto go = [&](auto kern, size_t smem) {
+    smem_attr_once(kern, (int)smem);
+    launch_pdl(kern, dim3((unsigned)sms), dim3(CHAIN_THREADS), smem, stream, args);
+  };
+  if (M <= 32)
+    go(gemm_chain_kernel<32>, ChainCfg<32>::SMEM);
+  else if (M <= 64)
+    go(gemm_chain_kernel<64>, ChainCfg<64>::SMEM);
+  else
+    go(gemm_chain_kernel<128>, ChainCfg<128>::SMEM);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

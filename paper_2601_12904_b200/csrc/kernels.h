@@ -75,7 +75,7 @@ int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind
 int num_sms();
 
 // Weight-streaming GEMM chain (gemm_chain.cu): up to CHAIN_MAX_OPS one-M-tile
-// GEMMs (M <= 32 rows, BN = 128) in one persistent launch, op i+1's A = op i's
+// GEMMs (M <= 128 rows, BN = 128) in one persistent launch, op i+1's A = op i's
 // output. `done` = 2*CHAIN_MAX_OPS ints, zero before the first launch (left zero).
 constexpr int CHAIN_MAX_OPS = 4;
 struct AttnArgs;

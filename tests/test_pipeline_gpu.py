@@ -335,12 +335,16 @@ for preset in ("tiny", big):
     h.update(eng.decode(res, 4).tobytes())
     eng.reprocess(store, question[:7], ids, 0.15, res)  # 7-row question pass
     h.update(res.logits().tobytes())
+    long_q = rng.integers(0, eng.cfg.vocab, 100).tolist()  # 100 rows: the 128-row A stages
+    res2 = F.Result(eng, 4 * n + 100 + 8)
+    eng.reprocess(store, long_q, ids, 0.05, res2)
+    h.update(res2.logits().tobytes())
 print(h.hexdigest())
 """
 
 
 def test_gemm_chain_is_bit_identical(cuda):
-    """The <= 32-row projection chain (gemm_chain.cu: O -> gate/up -> down ->
+    """The <= 128-row projection chain (gemm_chain.cu: O -> gate/up -> down ->
     next QKV in one persistent launch) computes exactly what the four separate
     weight-streaming GEMMs compute (same tiles, splits and fixup order):
     question pass, r = 0 sparse pass and decode, tiny and 8B width."""
