@@ -335,10 +335,11 @@ for preset in ("tiny", big):
     h.update(eng.decode(res, 4).tobytes())
     eng.reprocess(store, question[:7], ids, 0.15, res)  # 7-row question pass
     h.update(res.logits().tobytes())
-    long_q = rng.integers(0, eng.cfg.vocab, 100).tolist()  # 100 rows: the 128-row A stages
-    res2 = F.Result(eng, 4 * n + 100 + 8)
-    eng.reprocess(store, long_q, ids, 0.05, res2)
-    h.update(res2.logits().tobytes())
+    for nq in (50, 100):  # the 64- and 128-row A stages
+        long_q = rng.integers(0, eng.cfg.vocab, nq).tolist()
+        res2 = F.Result(eng, 4 * n + nq + 8)
+        eng.reprocess(store, long_q, ids, 0.05, res2)
+        h.update(res2.logits().tobytes())
 print(h.hexdigest())
 """
 
