@@ -46,7 +46,6 @@ struct ChainCfg {
   static_assert(SMEM <= 232448, "chain ring exceeds the 227 KB shared-memory limit");
 };
 constexpr int CHAIN_THREADS = 192;
-constexpr uint32_t CB_BYTES = CBN * CBK * 2;
 constexpr int CTMEM_COLS = 256;
 constexpr int CHAIN_CNT_STRIDE = 512;  // fixup counter slots per op (tiles <= 512)                          // 2 x BN accumulators
 
