@@ -766,7 +766,11 @@ void stitch(Engine* e, Result* r, cudaStream_t s, Stage& stg, const SysKV* sys, 
 // eagerly (first sighting, per-stage timing, or profiling).
 template <class Body>
 void run_graphed(Result* r, cudaStream_t s, bool graphable, const GraphKey& key, Body&& body) {
-  if (!graphable) {
+  static const bool graphs_env = [] {  // FRAG_GRAPHS=0: always launch eagerly
+    const char* v = std::getenv("FRAG_GRAPHS");
+    return !(v && v[0] == '0');
+  }();
+  if (!graphable || !graphs_env) {
     body(s);
     return;
   }
