@@ -955,6 +955,7 @@ void finish(Result* r, bool timing, cudaStream_t s) {
 void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
                bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio,
                const frag_reprocess_opts* o, cudaStream_t s, Result* r) {
+  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
   const auto& c = e->cfg;
   const auto t_entry = std::chrono::steady_clock::now();
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
@@ -1200,6 +1201,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
 // (same kernels, same per-request plans; GEMM rows are independent).
 void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int slot, const frag_reprocess_opts* o,
                      cudaStream_t s, Result* r) {
+  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (!st) fail(FRAG_E_CONTRACT, "store is null");
@@ -1390,6 +1392,7 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
 
 void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                   const frag_reprocess_opts* o, cudaStream_t s, Result* r) {
+  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (n_tok < 1) fail(FRAG_E_CONTRACT, "full prefill needs at least one token");
@@ -1436,6 +1439,7 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
 
 void kv_deviation(Engine* e, Store* st, const int32_t* sys, int n_sys, const frag_chunk_id* ids, int n_chunks,
                   int n_layers, cudaStream_t s, Result* r, float* dev_host) {
+  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (!st) fail(FRAG_E_CONTRACT, "store is null");
@@ -1488,6 +1492,7 @@ void kv_deviation(Engine* e, Store* st, const int32_t* sys, int n_sys, const fra
 }
 
 void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) {
+  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (n_new < 1) fail(FRAG_E_CONTRACT, "max_new_tokens must be >= 1");
@@ -1546,6 +1551,7 @@ void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) 
 
 void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                          bool overwrite, frag_chunk_id* id_out) {
+  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
   const auto& c = e->cfg;
   if (n_tok < 1) fail(FRAG_E_CONTRACT, "chunk must have at least one token (SPEC.md:197)");
   for (int i = 0; i < n_tok; ++i)
@@ -1599,6 +1605,7 @@ void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, co
 // preprocess_isolated's (same launches, bit-identical record data).
 void preprocess_fused(Engine* e, Store* src, Store* dst, const int32_t* sys, int n_sys, const int32_t* tokens,
                       int n_tok, const frag_chunk_id* nb, int n_nb, int budget, bool overwrite, frag_chunk_id* id_out) {
+  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
   const auto& c = e->cfg;
   if (n_tok < 1) fail(FRAG_E_CONTRACT, "chunk must have at least one token (SPEC.md:197)");
   if (n_nb < 0 || (n_nb > 0 && !nb)) fail(FRAG_E_CONTRACT, "bad neighbour list");

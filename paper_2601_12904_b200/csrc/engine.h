@@ -179,6 +179,11 @@ struct Engine {
   std::vector<double> theta;  // theta_i, i = 1..dh/2
   std::mutex rope_mu;         // guards rope-table growth
   std::mutex mu;              // guards the system-prompt cache and the scratch result
+  // serialises the device work of this engine's calls: the persistent GEMMs
+  // (split-K fixups, the GEMM chain) spin on other CTAs of their own grid and
+  // assume it is co-resident, i.e. owns the GPU while it runs (every call
+  // synchronises before it returns, so holding this for the call suffices)
+  std::recursive_mutex gpu_mu;
   std::map<std::vector<int32_t>, std::unique_ptr<SysKV>> sys_cache;
   Profiler prof;
   std::unique_ptr<Result> scratch;  // preprocess / system-prompt prefill workspace

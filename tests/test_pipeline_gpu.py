@@ -52,6 +52,41 @@ def test_reprocess_runs_and_selects(tiny):
     assert t["total_ms"] > 0
 
 
+def test_concurrent_requests_on_one_engine(tiny):
+    """Host threads issuing requests on their own streams and results: the
+    engine serialises their device work (its persistent GEMMs assume they own
+    the GPU), and every request gets the logits of a sequential run."""
+    import threading
+
+    import torch
+    F, eng, store, ids, q = tiny["F"], tiny["eng"], tiny["store"], tiny["ids"], tiny["question"]
+    sys_ = tiny["system"]
+    want = {}
+    for k, r in enumerate((0.05, 0.15, 0.3, 1.0)):
+        eng.reprocess(store, q, ids[k:], r, tiny["res"], system=sys_)
+        want[k] = tiny["res"].logits().copy()
+    got, err = {}, []
+
+    def worker(k, r):
+        try:
+            res = F.Result(eng, 8 + 8 * 256 + 32 + 64)
+            st = torch.cuda.Stream()
+            for _ in range(3):
+                eng.reprocess(store, q, ids[k:], r, res, system=sys_, stream=st.cuda_stream)
+            got[k] = res.logits().copy()
+        except Exception as ex:  # surfaced below
+            err.append(ex)
+
+    ths = [threading.Thread(target=worker, args=(k, r)) for k, r in enumerate((0.05, 0.15, 0.3, 1.0))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=300)
+    assert not err, err
+    for k in want:
+        assert np.array_equal(got[k], want[k]), k
+
+
 def test_store_immutable_during_reprocess(tiny):
     store, ids = tiny["store"], tiny["ids"]
     before = [store.read_kv(i) for i in ids[:2]]
