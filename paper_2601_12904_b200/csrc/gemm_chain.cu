@@ -348,11 +348,13 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
     if (args.pre_rows > 0) {
       // pre-op: merge the attention's split-KV partials into op 0's A rows,
       // one warp per (token, head) row, then publish (every CTA counts once)
-      for (size_t qi = (size_t)blockIdx.x * 4 + q; qi < (size_t)args.pre_rows; qi += (size_t)G * 4) {
+      const size_t step = (size_t)G * 4;
+      for (size_t qi = (size_t)blockIdx.x * 4 + q; qi < (size_t)args.pre_rows; qi += 2 * step) {
+        const bool has_b = qi + step < (size_t)args.pre_rows;
         if (args.pre.dh == 128)
-          attn_combine_row<128>(args.pre, qi, lane);
+          attn_combine_row2<128>(args.pre, qi, qi + step, has_b, lane);
         else
-          attn_combine_row<64>(args.pre, qi, lane);
+          attn_combine_row2<64>(args.pre, qi, qi + step, has_b, lane);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (warp == 2 && lane == 0) red_release(&args.done[CHAIN_MAX_OPS + 1], 1);
