@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     pdl_wait();
+    __shared__ float rs_part[4][32];  // cooperative RMSNorm scale (M <= 32)
     unsigned long long* tl = (warp == 2 && lane == 0) ? chain_tl(args) : nullptr;
     const int q = warp & 3;
     const int row_in_tile = q * 32 + lane;
@@ -372,7 +373,30 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
       int* cnt = ep.counters + o * CHAIN_CNT_STRIDE;  // this op's fixup counters
       unsigned long long* ts = tl ? tl + 8 + 8 * o : nullptr;
       float rs = 1.f;
-      if (row_in_tile < M) {
+      const bool need_rs = (op.epi == EPI_QKV || op.epi == EPI_SWIGLU) && ep.ssq_in;
+      if (need_rs && M <= 32 && (ep.ssq_n & 3) == 0 && ep.ssq_n <= 4 * 32) {
+        // rows live in warp 0 only: the four epilogue warps each take one of
+        // epi_row_scale's four running sums (chunks w, w+4, ... in order, all
+        // loads in flight at once, from L2), combined in its order -> same bits
+        const int row = lane;
+        float sw = 0.f;
+        if (row < M) {
+          const float* p = ep.ssq_in + row;
+          const size_t ld = (size_t)ep.ssq_ld;
+          float v[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] = (q + 4 * k < ep.ssq_n) ? __ldcg(p + (q + 4 * k) * ld) : 0.f;
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (q + 4 * k < ep.ssq_n) sw += v[k];
+        }
+        rs_part[q][lane] = sw;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && row < M)
+          rs = rsqrtf(((rs_part[0][row] + rs_part[1][row]) + (rs_part[2][row] + rs_part[3][row])) /
+                          (float)ep.norm_d + ep.norm_eps);
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // rs_part reusable by the next op
+      } else if (row_in_tile < M) {
         switch (op.epi) {
           case EPI_QKV: rs = epi_row_scale<EPI_QKV>(ep, row_in_tile); break;
           case EPI_SWIGLU: rs = epi_row_scale<EPI_SWIGLU>(ep, row_in_tile); break;
@@ -475,6 +499,7 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
     op.splits = (int)s;
     op.ep = st.ep;
     op.ep.splits = (int)s;
+    op.ep.l2_reads = 1;
     op.ep.full_tiles = 0;
     op.ep.streamk = 0;
   }

@@ -21,13 +21,24 @@ __device__ __forceinline__ float epi_row_scale(const EpiParams& ep, int row) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       int i = 0;
 #pragma unroll 4
-      for (; i + 4 <= ep.ssq_n; i += 4) {
-        s0 += p[i * ld];
-        s1 += p[(i + 1) * ld];
-        s2 += p[(i + 2) * ld];
-        s3 += p[(i + 3) * ld];
+      if (ep.l2_reads) {  // GEMM chain: written by other CTAs of the same launch
+#pragma unroll 4
+        for (; i + 4 <= ep.ssq_n; i += 4) {
+          s0 += __ldcg(p + i * ld);
+          s1 += __ldcg(p + (i + 1) * ld);
+          s2 += __ldcg(p + (i + 2) * ld);
+          s3 += __ldcg(p + (i + 3) * ld);
+        }
+      } else {
+#pragma unroll 4
+        for (; i + 4 <= ep.ssq_n; i += 4) {
+          s0 += p[i * ld];
+          s1 += p[(i + 1) * ld];
+          s2 += p[(i + 2) * ld];
+          s3 += p[(i + 3) * ld];
+        }
       }
-      for (; i < ep.ssq_n; ++i) s0 += p[i * ld];
+      for (; i < ep.ssq_n; ++i) s0 += __ldcg(p + i * ld);
       return rsqrtf(((s0 + s1) + (s2 + s3)) / (float)ep.norm_d + ep.norm_eps);
     }
   }
@@ -59,7 +70,8 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
     float4 hv[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      float4 h = dst[j];
+      // GEMM chain: an earlier op of the same launch may have written it on another SM
+      float4 h = ep.l2_reads ? __ldcg(dst + j) : dst[j];
       h.x += __uint_as_float(r[4 * j]);
       h.y += __uint_as_float(r[4 * j + 1]);
       h.z += __uint_as_float(r[4 * j + 2]);

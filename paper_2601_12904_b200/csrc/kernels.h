@@ -60,6 +60,10 @@ struct EpiParams {
   int ssq_n = 0;                  // partials per row (d/32)
   int norm_d = 0;
   float norm_eps = 0.f;
+  // 1 inside the GEMM chain: ops of one launch read data other CTAs wrote
+  // earlier in it (residual, Σh² partials), which L1 does not keep coherent --
+  // those reads go to L2 (ld.global.cg)
+  int l2_reads = 0;
 };
 
 struct GemmTimer;  // optional per-launch event hook (bench roofline)
