@@ -1,7 +1,7 @@
 # Round evidence run (one gpurun call): GPU tests, smoke, the default bench
 # line, the reference arm, the other configs' bench lines and the ncu captures.
 # Usage: bash tools/_gpu_final.sh <tag>
-TAG=${1:-r01g}
+TAG=${1:-r01h}
 set -x
 timeout 900 python -m pytest tests -q -x -m gpu -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
