@@ -16,7 +16,9 @@ logits). Chunk records are HBM-resident (preprocessed on the GPU at setup).
 `--impl reference` times the reference's CPU path (the C++ oracle restatement;
 the reference ships no implementation) on the host cores.
 
-Launch: python bench.py [--gpus N --steps K --warmup W]; N>1 under torchrun.
+Launch: python bench.py [--gpus N --steps K --warmup W]. N>1: under torchrun
+(one rank per GPU), or without it bench.py spawns the N ranks itself through
+torch.distributed.run on 127.0.0.1.
 """
 from __future__ import annotations
 
@@ -53,18 +55,28 @@ CONFIGS = {
 }
 
 
-def l2_note(w):
-    from paper_2601_12904_b200 import fusion as F
-    c = F.preset(w["preset"])
-    per_layer = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim * c.d_model + c.n_heads * c.head_dim * c.d_model \
-        + 3 * c.d_model * c.ffn_dim
-    wbytes = 2 * (c.layers * per_layer + 2 * c.vocab * c.d_model)
+def l2_note(w, c):
+    """c: model shape as a dict (layers, d_model, n_heads, ...)."""
+    per_layer = (c["n_heads"] + 2 * c["n_kv_heads"]) * c["head_dim"] * c["d_model"] \
+        + c["n_heads"] * c["head_dim"] * c["d_model"] + 3 * c["d_model"] * c["ffn_dim"]
+    wbytes = 2 * (c["layers"] * per_layer + 2 * c["vocab"] * c["d_model"])
     T = w["chunks"] * w["chunk_len"] + w["qlen"]
-    kv = 2 * c.layers * T * c.n_kv_heads * c.head_dim * 2
+    kv = 2 * c["layers"] * T * c["n_kv_heads"] * c["head_dim"] * 2
     if wbytes + kv < 126e6:
         return "fits in L2 (tiny test config, not a headline run)"
     return (f"inputs larger than L2 ({wbytes / 1e9:.1f} GB weights, {kv / 1e9:.1f} GB fused KV per request "
             f"streamed every step)")
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def parse():
@@ -86,6 +98,8 @@ def parse():
                         "the other ranks read it over NVLink inside K1 (SURVEY.md §8(e))")
     p.add_argument("--batch", type=int, default=4,
                    help="also time multi-request batching (frag_reprocess_batch) with this many requests; 0 = skip")
+    p.add_argument("--selftest", action="store_true",
+                   help="CPU/gloo check of the multi-rank launcher (no GPU work)")
     p.add_argument("--with-load", action="store_true",
                    help="also time TTFT including the FKVC record load (DISK -> GPU, SPEC.md:301-308)")
     return p.parse_args()
@@ -168,37 +182,72 @@ def peaks():
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle)
+class CpuBaseline:
+    """The reference's CPU path (the C++/OpenMP oracle restatement, the
+    reference ships no implementation) on this host's cores, on a bounded
+    sample of the workload: the full request at full width and prompt length
+    on `layers` of the model's layers (synthetic random chunk KV). A step is
+    one oracle reprocess of that sample; its per-layer stage times are
+    extrapolated to the model depth (labelled as such). Reads the shapes from
+    oracle/presets.py: nothing here loads the product library."""
+
+    def __init__(self, cfg_name, ratio, layers, seed=1234):
+        from oracle import oracle as O
+        from oracle import presets as OP
+        self.O = O
+        self.w = CONFIGS[cfg_name]
+        self.name, self.ratio = cfg_name, ratio
+        self.full = OP.preset(self.w["preset"])
+        c = dict(self.full)
+        c["layers"] = layers = min(layers, self.full["layers"])
+        self.layers = layers
+        self.om = O.Model(c).init_seed(seed)
+        rng = np.random.default_rng(seed)
+        Hkv, dh = c["n_kv_heads"], c["head_dim"]
+        self.recs = []
+        for _ in range(self.w["chunks"]):
+            n = self.w["chunk_len"]
+            self.recs.append({"k": (rng.standard_normal((layers, n, Hkv, dh), dtype=np.float32) * 0.5),
+                              "v": (rng.standard_normal((layers, n, Hkv, dh), dtype=np.float32) * 0.5),
+                              "tokens": rng.integers(0, c["vocab"], n).astype(np.int32), "native_start": 1})
+        self.qrng = np.random.default_rng(seed + 1)
+        self.cores = O.threads()
+
+    def step(self):
+        """One sample request: returns (wall seconds, extrapolated full-depth TTFT seconds, T)."""
+        q = self.qrng.integers(0, self.full["vocab"], self.w["qlen"])
+        t0 = time.perf_counter()
+        out = self.om.reprocess(None, self.recs, q, self.ratio, emulate_bf16=False)
+        wall = time.perf_counter() - t0
+        st = out["stage_seconds"]  # stitch, question, select, sparse(+lm_head)
+        scale = self.full["layers"] / self.layers
+        return wall, (st[0] + st[1] + st[3]) * scale + st[2], out["T"]
+
+    def sample(self, wall=None):
+        s = (f"oracle reprocess (C++/OpenMP fp32, {self.cores} threads, {cpu_model()}), {self.name} width, "
+             f"{self.layers}/{self.full['layers']} layers, T={self.w['chunks'] * self.w['chunk_len'] + self.w['qlen']}, "
+             f"r={self.ratio}, random chunk KV; value = per-layer stage times x{self.full['layers'] / self.layers:g} "
+             f"(extrapolated to the full depth)")
+        return s + (f"; wall {wall:.1f}s per sample" if wall is not None else "")
+
+
+def tiny_reference(seed=1234):
+    """configs[0] measured in full on the CPU (2 layers, d=256, 8x256 chunks +
+    32 question, r=0.15): no extrapolation."""
+    b = CpuBaseline("tiny", 0.15, 2, seed)
+    b.step()
+    walls = [b.step()[0] for _ in range(3)]
+    T = b.w["chunks"] * b.w["chunk_len"] + b.w["qlen"]
+    ms = statistics.median(walls) * 1e3
+    return {"config": "tiny (BASELINE.json configs[0]), all layers, measured", "ttft_ms": ms,
+            "tok_s": T / (ms / 1e3), "cores": b.cores}
+
+
 def cpu_baseline(cfg_name, ratio, layers, seed=1234):
-    """Oracle reprocess of the same workload at full width and length on `layers`
-    layers (synthetic random chunk KV); per-layer stage times extrapolated to the
-    model depth. Returns (tok/s, ttft_s, cores, sample description)."""
-    from oracle import oracle as O
-    from paper_2601_12904_b200 import fusion as F
-    w = CONFIGS[cfg_name]
-    full = F.preset(w["preset"])
-    c = dict(full.as_dict())
-    c["layers"] = layers
-    om = O.Model(c).init_seed(seed)
-    rng = np.random.default_rng(seed)
-    L, Hkv, dh = layers, c["n_kv_heads"], c["head_dim"]
-    recs = []
-    for i in range(w["chunks"]):
-        n = w["chunk_len"]
-        recs.append({"k": (rng.standard_normal((L, n, Hkv, dh), dtype=np.float32) * 0.5),
-                     "v": (rng.standard_normal((L, n, Hkv, dh), dtype=np.float32) * 0.5),
-                     "tokens": rng.integers(0, c["vocab"], n).astype(np.int32), "native_start": 1})
-    q = rng.integers(0, c["vocab"], w["qlen"])
-    cores = O.threads()
-    t0 = time.perf_counter()
-    out = om.reprocess(None, recs, q, ratio, emulate_bf16=False)
-    wall = time.perf_counter() - t0
-    st = out["stage_seconds"]  # stitch, question, select, sparse(+lm_head)
-    scale = full.layers / layers
-    ttft = (st[0] + st[1] + st[3]) * scale + st[2]
-    T = out["T"]
-    sample = (f"oracle reprocess, {cfg_name} width, {layers}/{full.layers} layers, T={T}, r={ratio}, "
-              f"random chunk KV; per-layer stage times x{scale:g} (extrapolated); wall {wall:.1f}s")
-    return T / ttft, ttft, cores, sample
+    """One bounded sample of the oracle on the host (rank 0, N=1 only)."""
+    b = CpuBaseline(cfg_name, ratio, layers, seed)
+    wall, ttft, T = b.step()
+    return T / ttft, ttft, b.cores, b.sample(wall)
 
 
 # ---------------------------------------------------------------- ours
@@ -441,18 +490,59 @@ def run_ours(args, rank, world, local_rank):
                 cacheblend_ms=cacheblend_ms, cacheblend_stages=cacheblend_stages, batch_leg=batch_leg)
 
 
+def spawn_ranks(n: int, argv: list[str], backend_env: dict | None = None) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one process per
+    GPU) through torch.distributed.run on 127.0.0.1 and return its exit code;
+    rank 0's JSON line goes to this process's stdout."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
+    env = dict(os.environ, **(backend_env or {}))
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or n) // n)))
+    print(f"bench: spawning {n} ranks (torch.distributed.run, master 127.0.0.1:{port})", file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=env).returncode
+
+
+def selftest_ranks(args, rank, world):
+    """CPU check of the launcher plumbing (gloo): every rank reports a
+    rank-dependent 'device time', rank 0 prints the contract line built from
+    the max over ranks. tests/test_bench_multirank.py runs it at world 2."""
+    import torch
+    torch.distributed.init_process_group("gloo")
+    ms = max_over_ranks([100.0 + 10.0 * rank], torch.device("cpu"))[0]
+    T = 16416
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": job_throughput(world, args.steps, T, ms), "unit": "tok/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                          "selftest": True}), flush=True)
+    torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus, sys.argv[1:])
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}", file=sys.stderr)
+    if args.selftest:
+        return selftest_ranks(args, rank, world)
     w = CONFIGS[args.config]
     ratio = w["ratio"] if args.ratio is None else args.ratio
     cfg_json = {"workload": f"{args.config}: {w['chunks']}x{w['chunk_len']}-token chunks + {w['qlen']}-token "
                             f"question, r={ratio}", "model": w["preset"], "chunks": w["chunks"],
                 "chunk_len": w["chunk_len"], "question_len": w["qlen"], "recompute_ratio": ratio,
-                "seq_len": w["chunks"] * w["chunk_len"] + w["qlen"], "parallelism": f"dp{args.gpus} (independent queries)",
-                "l2": l2_note(w)}
+                "seq_len": w["chunks"] * w["chunk_len"] + w["qlen"],
+                "parallelism": f"dp{world} (independent queries)"}
     part = args.partition or w.get("partition", False)
     cfg_json["store"] = ("partitioned: record on rank hash(chunk_id) mod N only, read by the other ranks over "
                          "NVLink inside K1 (CUDA IPC views)") if part else "replicated per rank"
@@ -463,26 +553,44 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        vals, ttfts = [], []
-        cores, sample = None, None
-        for _ in range(args.warmup and 1):
-            pass
+        from oracle import presets as OP
+        cfg_json["l2"] = l2_note(w, OP.preset(w["preset"]))
+        base = CpuBaseline(args.config, ratio, args.cpu_layers, args.seed)
+        for _ in range(args.warmup):
+            base.step()
+        walls, ttfts = [], []
         for _ in range(max(1, args.steps)):
-            v, t, cores, sample = cpu_baseline(args.config, ratio, args.cpu_layers, args.seed)
-            vals.append(v)
-            ttfts.append(t)
-        value = statistics.median(vals)
-        line = {"metric": METRIC, "value": value, "unit": "tok/s", "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(ttfts) * 1e3,
+            wall, ttft, T = base.step()
+            walls.append(wall)
+            ttfts.append(ttft)
+        value = T / statistics.median(ttfts)
+        ms_step = statistics.mean(walls) * 1e3
+        line = {"metric": METRIC, "value": value, "unit": "tok/s", "impl": "reference", "n_gpus": 1,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": cfg_json,
-                "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample},
+                "value_basis": (f"extrapolated: each step measures the full request on {base.layers} of "
+                                f"{base.full['layers']} layers (ms_per_step = that measured wall time); value = "
+                                f"prompt tokens / (per-layer stage times x{base.full['layers'] / base.layers:g})"),
+                "ttft_ms_extrapolated": statistics.median(ttfts) * 1e3,
+                "cpu": {"model": cpu_model(), "threads": base.cores, "host_cpus": os.cpu_count()},
+                "cpu_baseline": {"value": value, "unit": "tok/s", "cores": base.cores, "kind": "port",
+                                 "sample": base.sample(statistics.mean(walls))},
                 "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        try:
+            line["tiny_config"] = tiny_reference(args.seed)
+        except Exception as ex:  # reported, never fatal
+            line["tiny_config"] = {"failed": str(ex)}
         print(json.dumps(line), flush=True)
         return 0
 
+    from paper_2601_12904_b200 import fusion as F
+    cfg_json["l2"] = l2_note(w, F.preset(w["preset"]).as_dict())
     if world > 1:
         import torch
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPUs "
+                             "(one process per GPU)")
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     r = run_ours(args, rank, world, local_rank)
     import torch

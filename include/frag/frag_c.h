@@ -359,6 +359,12 @@ FRAG_API frag_status frag_engine_profile(frag_engine* eng, int32_t enable);
  * device ms, algorithmic FLOPs, algorithmic bytes, launch count. */
 FRAG_API frag_status frag_engine_profile_read(frag_engine* eng, int32_t klass, double* ms, double* flops,
                                               double* bytes, int64_t* launches, int32_t reset);
+/* Limit of the persistent kernels' inter-CTA waits (a grid that is not
+ * co-resident -- another context holding SMs -- abandons the wait after this
+ * long and the call returns FRAG_E_CUDA instead of hanging). Process wide;
+ * default FRAG_SPIN_LIMIT_MS or 2000 ms; ms <= 0 restores the default.
+ * Returns the previous limit in ms. */
+FRAG_API double frag_set_spin_limit_ms(double ms);
 
 /* ------------------------------------------------------------------ kernels
  * Kernel-level entry points over device pointers (parity tests, bench roofline). */

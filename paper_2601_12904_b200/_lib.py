@@ -93,6 +93,7 @@ _SIGS = {
     "frag_model_preset": (C.c_int, [C.c_char_p, C.POINTER(ModelCfg)]),
     "frag_hash_tokens": (None, [_I32P, C.c_int32, C.c_uint64, C.POINTER(ChunkId)]),
     "frag_launch_count": (C.c_uint64, []),
+    "frag_set_spin_limit_ms": (C.c_double, [C.c_double]),
     "frag_memcpy": (C.c_int, [_P, _P, C.c_size_t]),
     "frag_engine_create": (C.c_int, [C.POINTER(ModelCfg), C.c_int, C.c_uint64, C.POINTER(_P)]),
     "frag_engine_destroy": (C.c_int, [_P]),

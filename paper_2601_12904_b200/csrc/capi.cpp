@@ -107,6 +107,16 @@ FRAG_API void frag_hash_tokens(const int32_t* tokens, int32_t n, uint64_t salt, 
 
 FRAG_API uint64_t frag_launch_count(void) { return g_launches.load(); }
 
+FRAG_API double frag_set_spin_limit_ms(double ms) {
+  const double prev = (double)fragk::spin_limit_ns() / 1e6;
+  if (ms <= 0) {
+    const char* e = std::getenv("FRAG_SPIN_LIMIT_MS");
+    ms = e && std::atof(e) > 0 ? std::atof(e) : 2000.0;
+  }
+  fragk::set_spin_limit_ns((unsigned long long)(ms * 1e6));
+  return prev;
+}
+
 FRAG_API frag_status frag_memcpy(void* dst, const void* src, size_t bytes) {
   return guard([&] {
     need(dst && src, "null argument");
@@ -581,6 +591,9 @@ FRAG_API frag_status frag_kernel_gemm(const void* a, const void* b, void* c, int
     // for kernel-level tests and is serialised by the mutex)
     static std::mutex ws_mu;
     static DevBuf ws, cnt;
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::recursive_mutex> gd(fragimpl::device_mutex(dev));  // co-residency (engine.h)
     std::lock_guard<std::mutex> g(ws_mu);
     if (!ws.p) {
       ws.alloc((size_t)32 << 20);
@@ -595,7 +608,14 @@ FRAG_API frag_status frag_kernel_gemm(const void* a, const void* b, void* c, int
                                       static_cast<cudaStream_t>(stream), force_bn);
     // flag 0x80000 (tuning tools): no synchronise, so back-to-back launches can
     // be timed; the caller keeps them on one stream
-    if (!(force_bn & 0x80000)) check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "gemm");
+    if (!(force_bn & 0x80000)) {
+      check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "gemm");
+      if (fragk::fault_take(dev)) {
+        check_cuda(cudaMemset(cnt.p, 0, cnt.bytes), "counter re-arm");
+        check_cuda(cudaDeviceSynchronize(), "counter re-arm");
+        fail(FRAG_E_CUDA, "gemm: the persistent grid was not co-resident (inter-CTA wait limit exceeded)");
+      }
+    }
     if (n < 0) fail(FRAG_E_CONTRACT, "unsupported GEMM shape (K % 64, N % 64 and N % BN required)");
     g_launches += n;
     check_cuda(cudaPeekAtLastError(), "gemm launch");

@@ -14,6 +14,28 @@
 
 namespace fragimpl {
 
+std::recursive_mutex& device_mutex(int device) {
+  static std::recursive_mutex mu[64];
+  return mu[(unsigned)device % 64u];
+}
+
+// Stream synchronisation at the end of a call + the co-residency check of its
+// persistent grids (ptx.cuh spin_until_ge): a grid that abandoned an
+// inter-CTA wait voids the call's results; its counters are re-armed here.
+void sync_checked(Engine* e, Result* r, cudaStream_t s, const char* what) {
+  check_cuda(cudaStreamSynchronize(s), what);
+  if (!fragk::fault_take(e->device)) return;
+  check_cuda(cudaDeviceSynchronize(), "co-residency fault drain");
+  if (r && r->gemm_cnt.p) check_cuda(cudaMemset(r->gemm_cnt.p, 0, r->gemm_cnt.bytes), "counter re-arm");
+  if (e->scratch && e->scratch.get() != r && e->scratch->gemm_cnt.p)
+    check_cuda(cudaMemset(e->scratch->gemm_cnt.p, 0, e->scratch->gemm_cnt.bytes), "counter re-arm");
+  check_cuda(cudaDeviceSynchronize(), "counter re-arm");
+  fail(FRAG_E_CUDA, std::string(what) +
+                        ": a persistent kernel grid was not co-resident (an inter-CTA wait exceeded "
+                        "FRAG_SPIN_LIMIT_MS; another context holds SMs?) -- the call's results are void");
+}
+
+
 std::atomic<uint64_t> g_launches{0};
 std::atomic<uint64_t> g_alloc_epoch{0};
 
@@ -855,7 +877,7 @@ SysKV* get_sys_kv(Engine* e, const int32_t* sys, int n_sys, cudaStream_t s) {
   check_cuda(cudaMemcpy2DAsync(kv->kv.as<char>() + c.layers * w, w, r->v_fused.p, pitch, w, c.layers,
                                cudaMemcpyDeviceToDevice, s),
              "sysV");
-  check_cuda(cudaStreamSynchronize(s), "system prompt prefill");
+  sync_checked(e, r, s, "system prompt prefill");
   SysKV* out = kv.get();
   e->sys_cache.emplace(std::move(key), std::move(kv));
   return out;
@@ -930,7 +952,7 @@ void finish(Result* r, bool timing, cudaStream_t s) {
   Engine* e = r->eng;
   ev_record(r, timing, 6, s);
   r->last_stream = s;
-  check_cuda(cudaStreamSynchronize(s), "reprocess");
+  sync_checked(e, r, s, "reprocess");
   e->prof.collect();
   r->timing_valid = timing;
   if (timing) {
@@ -955,7 +977,7 @@ void finish(Result* r, bool timing, cudaStream_t s) {
 void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* q_tokens, int n_q,
                bool q_on_device, const frag_chunk_id* ids, int n_chunks, float ratio,
                const frag_reprocess_opts* o, cudaStream_t s, Result* r) {
-  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
+  std::lock_guard<std::recursive_mutex> gpu_lock(device_mutex(e->device));
   const auto& c = e->cfg;
   const auto t_entry = std::chrono::steady_clock::now();
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
@@ -1201,7 +1223,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
 // (same kernels, same per-request plans; GEMM rows are independent).
 void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int slot, const frag_reprocess_opts* o,
                      cudaStream_t s, Result* r) {
-  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
+  std::lock_guard<std::recursive_mutex> gpu_lock(device_mutex(e->device));
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (!st) fail(FRAG_E_CONTRACT, "store is null");
@@ -1392,7 +1414,7 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
 
 void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                   const frag_reprocess_opts* o, cudaStream_t s, Result* r) {
-  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
+  std::lock_guard<std::recursive_mutex> gpu_lock(device_mutex(e->device));
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (n_tok < 1) fail(FRAG_E_CONTRACT, "full prefill needs at least one token");
@@ -1439,7 +1461,7 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
 
 void kv_deviation(Engine* e, Store* st, const int32_t* sys, int n_sys, const frag_chunk_id* ids, int n_chunks,
                   int n_layers, cudaStream_t s, Result* r, float* dev_host) {
-  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
+  std::lock_guard<std::recursive_mutex> gpu_lock(device_mutex(e->device));
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (!st) fail(FRAG_E_CONTRACT, "store is null");
@@ -1488,11 +1510,11 @@ void kv_deviation(Engine* e, Store* st, const int32_t* sys, int n_sys, const fra
   deviation_body(e, r, s, S, N, n_layers, r->dev.as<float>(), nullptr, 0);
   check_cuda(cudaMemcpyAsync(dev_host, r->dev.p, (size_t)N * n_layers * 2 * sizeof(float), cudaMemcpyDefault, s),
              "deviation D2H");
-  check_cuda(cudaStreamSynchronize(s), "kv_deviation");
+  sync_checked(e, r, s, "kv_deviation");
 }
 
 void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) {
-  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
+  std::lock_guard<std::recursive_mutex> gpu_lock(device_mutex(e->device));
   const auto& c = e->cfg;
   if (!r || r->eng != e) fail(FRAG_E_CONTRACT, "result does not belong to this engine");
   if (n_new < 1) fail(FRAG_E_CONTRACT, "max_new_tokens must be >= 1");
@@ -1543,7 +1565,7 @@ void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) 
     }
   }
   r->last_stream = s;
-  check_cuda(cudaStreamSynchronize(s), "decode");
+  sync_checked(e, r, s, "decode");
   std::memcpy(out_host, stage, (size_t)n_new * sizeof(int));
   r->T = T0 + n_new - 1;  // the fused cache now also holds the decoded tokens' K/V
   r->timing_valid = false;
@@ -1551,7 +1573,7 @@ void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) 
 
 void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_t* tokens, int n_tok,
                          bool overwrite, frag_chunk_id* id_out) {
-  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
+  std::lock_guard<std::recursive_mutex> gpu_lock(device_mutex(e->device));
   const auto& c = e->cfg;
   if (n_tok < 1) fail(FRAG_E_CONTRACT, "chunk must have at least one token (SPEC.md:197)");
   for (int i = 0; i < n_tok; ++i)
@@ -1585,6 +1607,7 @@ void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, co
   check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "rows");
   check_cuda(cudaMemcpyAsync(r->plan_tok.p, tok_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "tok");
   run_rows(e, r, s, n_tok, T, PASS_KV_ONLY, nullptr, 0);
+  sync_checked(e, r, s, "preprocess");  // never store a record computed by a faulted grid
   const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
   store_put(st, id, tokens, n_tok, S + 1, FRAG_VARIANT_ISOLATED, r->k_fused.as<bf16>() + (size_t)S * kvc,
             r->v_fused.as<bf16>() + (size_t)S * kvc, overwrite, (size_t)r->max_tokens * kvc, s);
@@ -1605,7 +1628,7 @@ void preprocess_isolated(Engine* e, Store* st, const int32_t* sys, int n_sys, co
 // preprocess_isolated's (same launches, bit-identical record data).
 void preprocess_fused(Engine* e, Store* src, Store* dst, const int32_t* sys, int n_sys, const int32_t* tokens,
                       int n_tok, const frag_chunk_id* nb, int n_nb, int budget, bool overwrite, frag_chunk_id* id_out) {
-  std::lock_guard<std::recursive_mutex> gpu_lock(e->gpu_mu);
+  std::lock_guard<std::recursive_mutex> gpu_lock(device_mutex(e->device));
   const auto& c = e->cfg;
   if (n_tok < 1) fail(FRAG_E_CONTRACT, "chunk must have at least one token (SPEC.md:197)");
   if (n_nb < 0 || (n_nb > 0 && !nb)) fail(FRAG_E_CONTRACT, "bad neighbour list");
@@ -1662,6 +1685,7 @@ void preprocess_fused(Engine* e, Store* src, Store* dst, const int32_t* sys, int
   check_cuda(cudaMemcpyAsync(r->plan_rows.p, rows_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "rows");
   check_cuda(cudaMemcpyAsync(r->plan_tok.p, tok_h, n_tok * sizeof(int), cudaMemcpyHostToDevice, s), "tok");
   run_rows(e, r, s, n_tok, T, PASS_KV_ONLY, nullptr, 0);
+  sync_checked(e, r, s, "preprocess_fused");
   const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
   store_put(dst, id, tokens, n_tok, X + 1, FRAG_VARIANT_FUSED,
             r->k_fused.as<bf16>() + (size_t)X * kvc, r->v_fused.as<bf16>() + (size_t)X * kvc, overwrite,

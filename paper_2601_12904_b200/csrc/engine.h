@@ -179,11 +179,6 @@ struct Engine {
   std::vector<double> theta;  // theta_i, i = 1..dh/2
   std::mutex rope_mu;         // guards rope-table growth
   std::mutex mu;              // guards the system-prompt cache and the scratch result
-  // serialises the device work of this engine's calls: the persistent GEMMs
-  // (split-K fixups, the GEMM chain) spin on other CTAs of their own grid and
-  // assume it is co-resident, i.e. owns the GPU while it runs (every call
-  // synchronises before it returns, so holding this for the call suffices)
-  std::recursive_mutex gpu_mu;
   std::map<std::vector<int32_t>, std::unique_ptr<SysKV>> sys_cache;
   Profiler prof;
   std::unique_ptr<Result> scratch;  // preprocess / system-prompt prefill workspace
@@ -191,6 +186,14 @@ struct Engine {
   void ensure_rope(int rows);
   size_t qkv_cols() const { return (size_t)(cfg.n_heads + 2 * cfg.n_kv_heads) * cfg.head_dim; }
 };
+
+// Serialises the device work of every engine's calls on one device, process
+// wide: the persistent GEMMs (split-K fixups, stream-K owners, the GEMM chain)
+// spin on other CTAs of their own grid and assume it is co-resident, i.e. owns
+// the GPU while it runs. Every call synchronises before it returns, so holding
+// this for the call suffices inside one process; across processes the bounded
+// waits (ptx.cuh spin_until_ge) turn a missing co-residency into FRAG_E_CUDA.
+std::recursive_mutex& device_mutex(int device);
 
 // Shape of a request body; a captured CUDA graph is valid for one key.
 struct GraphKey {

@@ -85,13 +85,10 @@ __device__ __forceinline__ void chain_stamp(unsigned long long* tl, int o, int k
   if (tl) tl[8 + 8 * o + k] = gtime();
 }
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void wait_count(const int* p, int target) {
-  while (ld_acquire(p) < target) __nanosleep(32);
+// bounded wait on a counter of this launch (ptx.cuh spin_until_ge); the fault
+// slot and limit travel in every op's EpiParams (op 0's are used)
+__device__ __forceinline__ void wait_count(const int* p, int target, const EpiParams& ep) {
+  spin_until_ge(p, target, ep.fault, ep.spin_ns);
 }
 // release-increment without waiting for the result (the writer does not stall
 // on the atomic's round trip); cumulative over the CTA's writes ordered before
@@ -119,7 +116,7 @@ __device__ __forceinline__ void chain_fixup(const EpiParams& ep, int* cnt, int s
   if (leader) {
     tstamp(ts ? ts + 4 : nullptr);
     red_release(cnt, 1);
-    wait_count(cnt, S);
+    wait_count(cnt, S, ep);
     tstamp(ts ? ts + 5 : nullptr);
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -271,11 +268,11 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         if ((int)blockIdx.x >= units) continue;
         if (o == 0) {
           if (args.pre_rows > 0) {  // op 0's A rows come from the in-chain combine
-            wait_count(&args.done[CHAIN_MAX_OPS + 1], G);
+            wait_count(&args.done[CHAIN_MAX_OPS + 1], G, args.op[0].ep);
             asm volatile("fence.proxy.async.global;" ::: "memory");
           }
         } else {
-          wait_count(&args.done[o - 1], chain_units(args.op[o - 1]));
+          wait_count(&args.done[o - 1], chain_units(args.op[o - 1]), args.op[0].ep);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
         }
         chain_stamp(tl, o, 0);
@@ -367,8 +364,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
       const int units = chain_units(op);
       if ((int)blockIdx.x >= units) continue;
       // this op's epilogue reads / writes what the earlier ops of the chain wrote
-      if (o > 0) wait_count(&args.done[o - 1], chain_units(args.op[o - 1]));
-      if (o > 1) wait_count(&args.done[o - 2], chain_units(args.op[o - 2]));
+      if (o > 0) wait_count(&args.done[o - 1], chain_units(args.op[o - 1]), args.op[0].ep);
+      if (o > 1) wait_count(&args.done[o - 2], chain_units(args.op[o - 2]), args.op[0].ep);
       const EpiParams& ep = op.ep;
       int* cnt = ep.counters + o * CHAIN_CNT_STRIDE;  // this op's fixup counters
       unsigned long long* ts = tl ? tl + 8 + 8 * o : nullptr;
@@ -500,6 +497,8 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
     op.ep = st.ep;
     op.ep.splits = (int)s;
     op.ep.l2_reads = 1;
+    if (!op.ep.fault) op.ep.fault = fault_slot_current();
+    op.ep.spin_ns = spin_limit_ns();
     op.ep.full_tiles = 0;
     op.ep.streamk = 0;
   }

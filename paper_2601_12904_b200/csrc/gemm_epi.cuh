@@ -20,7 +20,6 @@ __device__ __forceinline__ float epi_row_scale(const EpiParams& ep, int row) {
       const size_t ld = (size_t)ep.ssq_ld;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       int i = 0;
-#pragma unroll 4
       if (ep.l2_reads) {  // GEMM chain: written by other CTAs of the same launch
 #pragma unroll 4
         for (; i + 4 <= ep.ssq_n; i += 4) {
@@ -239,11 +238,7 @@ __device__ __forceinline__ void split_fixup(const EpiParams& ep, int slot, int S
   int* cnt = ep.counters + slot;
   if (warp2_lane0) {
     atomicAdd(cnt, 1);
-    int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-      if (v < S) __nanosleep(64);
-    } while (v < S);
+    spin_until_ge(cnt, S, ep.fault, ep.spin_ns, 64);
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
   const float* base = ep.ws + ((size_t)slot * S * ws_rows + row_in_tile) * BN;
@@ -282,11 +277,7 @@ __device__ __forceinline__ void sk_finish(const EpiParams& ep, int tile, int j, 
     return;
   }
   if (leader) {
-    int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-      if (v < n - 1) __nanosleep(32);
-    } while (v < n - 1);
+    spin_until_ge(cnt, n - 1, ep.fault, ep.spin_ns);
     *cnt = 0;  // every contributor has arrived: reset for the next GEMM
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");

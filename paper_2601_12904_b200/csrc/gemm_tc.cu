@@ -18,7 +18,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
 // ----------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
-int g_num_sms = 0;
+constexpr int kMaxDevices = 64;
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   std::call_once(g_encode_once, [] {
@@ -394,6 +396,8 @@ int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& e
   static const char* trace_path = std::getenv("FRAG_GEMM_TRACE");
   static unsigned long long* trace_dev = nullptr;
   EpiParams et = ep;
+  if (!et.fault) et.fault = fault_slot_current();
+  et.spin_ns = spin_limit_ns();
   if (trace_path) {
     if (!trace_dev) cudaMalloc(&trace_dev, 256 * 8 * sizeof(unsigned long long));
     cudaMemsetAsync(trace_dev, 0, 256 * 8 * sizeof(unsigned long long), stream);
@@ -439,13 +443,76 @@ bool smem_attr_needed(const void* fn, int dev) {
 }
 
 int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static std::atomic<int> cache[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
-  return g_num_sms;
+  return n;
+}
+
+namespace {
+std::atomic<unsigned long long> g_spin_ns{0};
+int* g_fault_host = nullptr;  // kMaxDevices ints, mapped + portable pinned memory
+std::mutex g_fault_mu;
+}  // namespace
+
+unsigned long long spin_limit_ns() {
+  unsigned long long v = g_spin_ns.load(std::memory_order_relaxed);
+  if (v == 0) {
+    const char* e = std::getenv("FRAG_SPIN_LIMIT_MS");
+    const double ms = e ? std::atof(e) : 2000.0;
+    v = ms > 0 ? (unsigned long long)(ms * 1e6) : 2000000000ull;
+    g_spin_ns.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+void set_spin_limit_ns(unsigned long long ns) { g_spin_ns.store(ns, std::memory_order_relaxed); }
+
+int* fault_slot(int dev) {
+  if (dev < 0 || dev >= kMaxDevices) return nullptr;
+  std::lock_guard<std::mutex> g(g_fault_mu);
+  if (!g_fault_host) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, kMaxDevices * 32 * sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+      return nullptr;
+    std::memset(p, 0, kMaxDevices * 32 * sizeof(int));
+    g_fault_host = static_cast<int*>(p);
+  }
+  int* h = g_fault_host + dev * 32;  // one 128-byte line per device
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return nullptr;
+  return static_cast<int*>(d);
+}
+
+int* fault_slot_current() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static thread_local int last_dev = -1;
+  static thread_local int* last_slot = nullptr;
+  if (dev != last_dev || !last_slot) {
+    last_slot = fault_slot(dev);
+    last_dev = dev;
+  }
+  return last_slot;
+}
+
+bool fault_take(int dev) {
+  if (dev < 0 || dev >= kMaxDevices) return false;
+  {
+    std::lock_guard<std::mutex> g(g_fault_mu);
+    if (!g_fault_host) return false;
+  }
+  volatile int* h = g_fault_host + dev * 32;
+  if (*h == 0) return false;
+  *h = 0;
+  return true;
 }
 
 // Pick the N tile: maximise useful MMA work per wave while keeping tiles wide

@@ -328,6 +328,8 @@ int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind
   if (K % BK2 != 0 || N % 64 != 0 || (bn != 192 && N % bn != 0)) return -1;
   EpiParams ep2 = ep;
   ep2.splits = 1;
+  if (!ep2.fault) ep2.fault = fault_slot_current();
+  ep2.spin_ns = spin_limit_ns();
   if (tail_split && N % bn == 0 && ep.ws && ep.counters) {
     // split-K only the last partial wave of CTA pairs (deterministic reduction
     // per 128-row half by the last-arriving CTA)

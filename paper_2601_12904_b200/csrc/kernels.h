@@ -64,6 +64,10 @@ struct EpiParams {
   // earlier in it (residual, Σh² partials), which L1 does not keep coherent --
   // those reads go to L2 (ld.global.cg)
   int l2_reads = 0;
+  // bounded inter-CTA waits (ptx.cuh spin_until_ge): the device's mapped host
+  // fault slot and the wait limit; filled in by the launchers
+  int* fault = nullptr;
+  unsigned long long spin_ns = 0;
 };
 
 struct GemmTimer;  // optional per-launch event hook (bench roofline)
@@ -76,7 +80,16 @@ int gemm_pick_bn(int M, int N, int K);
 // partial wave split along K unless tail_split is false.
 int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
                       cudaStream_t stream, int bn, bool tail_split = true);
-int num_sms();
+int num_sms();  // SM count of the current device (cached per device)
+// Co-residency fault slot of `dev` (mapped pinned host memory, device-visible)
+// and the inter-CTA wait limit (FRAG_SPIN_LIMIT_MS, default 2000 ms).
+int* fault_slot(int dev);
+int* fault_slot_current();
+unsigned long long spin_limit_ns();
+void set_spin_limit_ns(unsigned long long ns);  // tests / tooling
+// Reads and clears the slot after the stream has been synchronised: true if a
+// persistent grid abandoned an inter-CTA wait since the last call.
+bool fault_take(int dev);
 
 // Weight-streaming GEMM chain (gemm_chain.cu): up to CHAIN_MAX_OPS one-M-tile
 // GEMMs (M <= 128 rows, BN = 128) in one persistent launch, op i+1's A = op i's

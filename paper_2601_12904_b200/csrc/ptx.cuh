@@ -57,6 +57,53 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- bounded inter-CTA waits
+// The persistent GEMMs (split-K fixups, stream-K owners, the GEMM chain) wait
+// on counters other CTAs of the same grid advance, i.e. they assume the grid
+// is co-resident. The host serialises every engine's device work per device
+// (engine.cpp device_mutex) and sizes grids from the per-device SM count, but
+// another process (MPS, a second context) can still hold SMs. So every such
+// wait is bounded: after `limit_ns` of globaltimer time it records the fault
+// in a mapped host slot (`fault`, one int per device) and gives up, and every
+// other waiter polls that slot (every 256 spins) so the whole grid drains in
+// ~0.1 ms instead of timing out one by one. The host reads the slot after the
+// call's stream synchronisation, resets the counters and returns FRAG_E_CUDA.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Wait until *p >= target. Returns false (and the grid's results are void)
+// when the wait was abandoned.
+static __device__ __noinline__ bool spin_until_ge_slow(const int* p, int target, int* fault, unsigned long long limit_ns,
+                                                int sleep_ns) {
+  const unsigned long long t0 = global_ns();
+  for (unsigned n = 1;; ++n) {
+    __nanosleep(sleep_ns);
+    if (ld_acquire_gpu(p) >= target) return true;
+    if ((n & 255) == 0) {
+      if (fault && *reinterpret_cast<volatile int*>(fault)) return false;
+      if (limit_ns && global_ns() - t0 > limit_ns) {
+        if (fault) {
+          *reinterpret_cast<volatile int*>(fault) = 1;
+          __threadfence_system();
+        }
+        return false;
+      }
+    }
+  }
+}
+__device__ __forceinline__ bool spin_until_ge(const int* p, int target, int* fault, unsigned long long limit_ns,
+                                              int sleep_ns = 32) {
+  if (ld_acquire_gpu(p) >= target) return true;
+  return spin_until_ge_slow(p, target, fault, limit_ns, sleep_ns);
+}
+
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch: wait for the preceding grid's memory, and let
 // the next grid in the stream start its prologue early.

@@ -27,6 +27,15 @@ def test_exports_every_declared_symbol():
     assert set(L._SIGS) == set(declared)  # the ctypes binding covers the whole header
 
 
+def test_oracle_presets_equal_library_presets():
+    """bench.py's oracle legs read the shapes from oracle/presets.py (plain
+    data, so the reference arm never maps libfrag.so); they must equal the
+    library's frag_model_preset table."""
+    from oracle import presets as OP
+    for name, want in OP.PRESETS.items():
+        assert F.preset(name).as_dict() == pytest.approx(want), name
+
+
 def test_presets_match_survey_table():
     c = F.preset("llama3-8b")
     assert (c.layers, c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn_dim, c.vocab) == \

@@ -288,3 +288,76 @@ def test_topk_ties_go_to_lower_index(cuda, N, k):
                                         sel.data_ptr(), None))
     assert torch.all(scores == scores[0])
     assert sel[:k].cpu().tolist() == list(range(k))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("T,M,split", [(16416, 2490, 0), (16416, 32, 1024), (32800, 4947, 0)])
+def test_sparse_q_attention_headline_shapes(cuda, T, M, split):
+    """K6 at the bench's shapes: the sparse pass (2490 rows x 16416 keys, 8B;
+    4947 x 32800, Mistral-7B) with the longest-first two-tile dispatch, and the
+    question pass (32 rows, split-KV 1024 keys = the engine's split policy for
+    16416 keys on 148 SMs) with its LSE combine. The last rows and 64 sampled
+    rows are checked against fp64 (|err| < 2e-2 on unit-normal inputs)."""
+    import torch
+    Hq, Hkv, dh = 32, 8, 128
+    g = torch.Generator(device="cuda").manual_seed(T + M)
+    q = torch.randn(M, Hq, dh, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(T, Hkv, dh, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(T, Hkv, dh, device=cuda, generator=g).to(torch.bfloat16)
+    if M == 32:
+        rows = torch.arange(T - M, T, device=cuda, dtype=torch.int32)
+    else:
+        sel = torch.sort(torch.randperm(T - 32, device=cuda, generator=g)[:M - 32]).values
+        rows = torch.cat([sel, torch.arange(T - 32, T, device=cuda)]).to(torch.int32)
+    out = torch.empty(M, Hq, dh, device=cuda, dtype=torch.bfloat16)
+    L = _lib()
+    L.check(L.lib.frag_kernel_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), rows.data_ptr(), out.data_ptr(),
+                                        M, T, Hq, Hkv, dh, split, None))
+    torch.cuda.synchronize()
+    pick = torch.unique(torch.cat([torch.randperm(M, device=cuda, generator=g)[:64],
+                                   torch.arange(max(0, M - 4), M, device=cuda), torch.zeros(1, device=cuda).long()]))
+    ref = _attn_ref(q[pick], k, v, rows[pick].cpu(), 1.0 / math.sqrt(dh))
+    err = (out[pick].double() - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("N,K,epi", [(4096, 14336, 2), (6144, 4096, 1), (28672, 4096, 3), (4096, 4096, 2)])
+def test_gemm_headline_shapes(cuda, N, K, epi):
+    """The sparse pass's GEMMs at M = 2490 rows (8B, r = 0.15) through the
+    engine's own dispatch policy (CTA-pair tiles, the tail split along K for
+    the down projection K = 14336): QKV (N = 6144), O (4096 x 4096, residual),
+    gate/up (SwiGLU over the 32-row interleave), down (residual)."""
+    import torch
+    M = 2490
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    a = (torch.randn(M, K, device=cuda, generator=g) * 0.5).to(torch.bfloat16)
+    b = (torch.randn(N, K, device=cuda, generator=g) * 0.02).to(torch.bfloat16)
+    ref = a.double() @ b.double().T
+    if epi == 1:
+        c = torch.empty(M, N, device=cuda, dtype=torch.float32)
+        _gemm(a, b, c, 1)
+        torch.cuda.synchronize()
+        err = (c.double() - ref).abs().max().item()
+        assert err <= 2e-5 * math.sqrt(K) * ref.abs().max().item() + 1e-4, err
+    elif epi == 2:
+        r0 = torch.randn(M, N, device=cuda, generator=g)
+        r = r0.clone()
+        _gemm(a, b, r, 2)
+        torch.cuda.synchronize()
+        err = (r.double() - r0.double() - ref).abs().max().item()
+        assert err <= 2e-5 * math.sqrt(K) * ref.abs().max().item() + 1e-4, err
+        r2 = r0.clone()
+        _gemm(a, b, r2, 2)
+        torch.cuda.synchronize()
+        assert torch.equal(r, r2)  # deterministic split-K reduction
+    else:
+        F = N // 2
+        out = torch.empty(M, F, device=cuda, dtype=torch.bfloat16)
+        _gemm(a, b, out, 3)
+        torch.cuda.synchronize()
+        idx = torch.arange(F, device=cuda)
+        gg = ref[:, (idx // 32) * 64 + idx % 32]
+        uu = ref[:, (idx // 32) * 64 + 32 + idx % 32]
+        want = torch.nn.functional.silu(gg) * uu
+        assert (out.double() - want).abs().max().item() <= 1e-2 * want.abs().max().item() + 1e-3

@@ -144,16 +144,29 @@ def test_reprocess_selection_injection_parity(tiny):
             assert np.argmax(g["logits"]) == np.argmax(out["logits"])
 
 
-def test_end_to_end_selection_overlap(tiny):
-    # full pipeline, each side selects on its own: bf16 drift through the layers
-    # may swap near-tied boundary tokens only
+def test_end_to_end_selection_window(tiny):
+    """Full pipeline, each side runs its own question pass and selector. With
+    delta = max_j |score_gpu[j] - score_oracle[j]| (the score perturbation the
+    bf16 drift of q_final induces), every index in the symmetric difference of
+    the two critical sets lies within 2*delta of the oracle's k-th score: the
+    GPU's top-k is exact on its own scores, so a swap needs both scores within
+    delta of the boundary. q_final itself: rel L2 <= 1e-2 vs the oracle's."""
     O, S = tiny["O"], tiny["S"]
     g = _gpu_run(tiny, 0.15)
     sys_kv = (O.bf16_bits_to_f32(g["k"][:, :S]), O.bf16_bits_to_f32(g["v"][:, :S]))
     out = tiny["om"].reprocess(sys_kv, tiny["recs"], tiny["question"], 0.15, emulate_bf16=True)
-    a, b = set(g["crit"].tolist()), set(out["crit"].tolist())
+    assert _rel_l2(g["debug"]["q_final"], out["q_final"]) <= 1e-2
+    a, b = g["crit"] - S - 1, out["crit"] - S - 1
     assert len(a) == len(b)
-    assert len(a & b) / len(a) >= 0.9
+    so = out["scores"]
+    delta = float(np.abs(g["debug"]["scores"].astype(np.float64) - so).max())
+    tau = np.sort(so)[::-1][len(b) - 1]
+    win = 2.0 * delta + 1e-6 * abs(tau)
+    diff = set(a.tolist()) ^ set(b.tolist())
+    print(f"tiny e2e selection: score delta {delta:.3e} (mean {so.mean():.3e}), {len(diff) // 2} swaps "
+          f"of {len(a)}, window {win:.3e}")
+    assert delta <= 5e-2 * so.mean(), (delta, so.mean())
+    assert all(abs(so[j] - tau) <= win for j in diff), [(j, so[j] - tau) for j in diff if abs(so[j] - tau) > win]
 
 
 @pytest.mark.slow
