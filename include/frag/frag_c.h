@@ -95,6 +95,14 @@ typedef struct {
   int32_t selector;            /* FRAG_SELECT_QUERY_GUIDED (default) or FRAG_SELECT_CACHEBLEND */
   int32_t deviation_layer;     /* CacheBlend: 1-based layer of the deviation (0 -> 2: Delta_KV[:, 2], Eq. 8) */
   int32_t deviation_component; /* CacheBlend: FRAG_DEV_K (default, Delta_KV[:, 2, 1]), FRAG_DEV_V, FRAG_DEV_KV */
+  /* Unmatched-chunk fallback (flag-gated): when non-null,
+   * fallback_tokens[i] / fallback_lens[i] are the token ids of chunk i (null /
+   * 0 for none). A chunk whose record the store does not hold is then
+   * prefilled on the fly in isolation (Eq. 5, native_start = n_sys + 1, the
+   * tokens must hash to chunk_ids[i]) and inserted into the store before the
+   * stitch; without it a missing record is FRAG_E_STORE. */
+  const int32_t* const* fallback_tokens;
+  const int32_t* fallback_lens;
 } frag_reprocess_opts;
 /* Critical-token selectors of the reprocessing module: select_query_guided
  * (FusionRAG §3.2) and select_cacheblend (SPEC.md:417-425,

@@ -34,7 +34,19 @@ inline void check(frag_status s) {
   switch (s) {
     case FRAG_E_CONTRACT: throw ContractError(m);
     case FRAG_E_STORE: throw StoreError(m);
-    case FRAG_E_FORMAT: throw FormatError(FormatError::Kind::Malformed, m);
+    case FRAG_E_FORMAT: {
+      // the library's thread-local kind of the last FRAG_E_FORMAT (frag_c.h) ->
+      // the reference's FormatError::Kind (common.hpp:33)
+      FormatError::Kind k = FormatError::Kind::Malformed;
+      switch (frag_last_format_kind()) {
+        case FRAG_FORMAT_BAD_MAGIC: k = FormatError::Kind::BadMagic; break;
+        case FRAG_FORMAT_BAD_VERSION: k = FormatError::Kind::BadVersion; break;
+        case FRAG_FORMAT_TRUNCATED: k = FormatError::Kind::Truncated; break;
+        case FRAG_FORMAT_IO: k = FormatError::Kind::Io; break;
+        default: break;
+      }
+      throw FormatError(k, m);
+    }
     case FRAG_E_OOM: throw std::bad_alloc();
     default: throw CudaError(m);
   }

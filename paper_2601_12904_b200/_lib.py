@@ -73,7 +73,8 @@ class ReprocessOpts(C.Structure):
     _fields_ = [("raw_scores", C.c_int32), ("all_logits", C.c_int32), ("timing", C.c_int32),
                 ("inject_crit", C.POINTER(C.c_int32)), ("n_inject", C.c_int32),
                 ("logits_on_device", C.c_int32), ("selector", C.c_int32), ("deviation_layer", C.c_int32),
-                ("deviation_component", C.c_int32)]
+                ("deviation_component", C.c_int32),
+                ("fallback_tokens", C.POINTER(C.POINTER(C.c_int32))), ("fallback_lens", C.POINTER(C.c_int32))]
 
 
 class Timing(C.Structure):

@@ -114,6 +114,7 @@ FRAG_API double frag_set_spin_limit_ms(double ms) {
     ms = e && std::atof(e) > 0 ? std::atof(e) : 2000.0;
   }
   fragk::set_spin_limit_ns((unsigned long long)(ms * 1e6));
+  fragimpl::g_alloc_epoch++;  // captured request graphs hold the old limit in their kernel parameters
   return prev;
 }
 

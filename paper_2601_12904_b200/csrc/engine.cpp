@@ -414,7 +414,8 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       r->part_lse.ensure((size_t)seg_split[i].first * segs[i].M * Hq * sizeof(float));
     }
   }
-  if (mode == PASS_QUESTION) r->q_final.ensure((size_t)M * qc * sizeof(float));
+  const bool want_qf = mode == PASS_QUESTION || (mode == PASS_FULL && r->q_final_in_full);
+  if (want_qf) r->q_final.ensure((size_t)M * qc * sizeof(float));
 
   {
     Scoped sc(P, s, KC_NORM, 0, (double)M * d * (2 + 4 + 2));
@@ -427,7 +428,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     ep.rows = prow;
     ep.rope = e->rope.as<float2>();
     ep.q_out = r->q.as<bf16>();
-    ep.q_out_f32 = (mode == PASS_QUESTION && l == L - 1) ? r->q_final.as<float>() : nullptr;
+    ep.q_out_f32 = (want_qf && l == L - 1) ? r->q_final.as<float>() : nullptr;
     ep.k_cache = kf + l * lstride;
     ep.v_cache = vf + l * lstride;
     ep.rows_per_seq = r->rows_per_seq;
@@ -761,6 +762,15 @@ bool stitch_overlap_enabled() {
   }();
   return on;
 }
+// r = 0 fast path (one full pass over the question rows instead of question
+// pass + sparse pass); FRAG_R0_FAST=0 restores the two passes (A/B, tests)
+bool r0_fast_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("FRAG_R0_FAST");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
 void stitch_fork(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p) {
   const int L = e->cfg.layers;
   if (!r->side) check_cuda(cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking), "side stream");
@@ -996,7 +1006,23 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   PinGuard pins{st, {}};
   std::vector<Record*> recs;
   for (int i = 0; i < n_chunks; ++i) {
-    recs.push_back(store_fetch(st, ids[i]));  // heat++, pin
+    Record* rec = store_try_fetch(st, ids[i]);  // heat++, pin
+    if (!rec) {
+      const int32_t* ft = (o && o->fallback_tokens) ? o->fallback_tokens[i] : nullptr;
+      const int fl = (o && o->fallback_lens) ? o->fallback_lens[i] : 0;
+      if (!ft || fl < 1)
+        fail(FRAG_E_STORE, "missing chunk record " + std::to_string(i) +
+                               " (SPEC.md:287); stitch_full_reuse needs every chunk matched -- pass its tokens in "
+                               "frag_reprocess_opts.fallback_tokens for an on-the-fly isolated prefill (SPEC.md:403)");
+      // flag-gated fallback: isolated prefill of the chunk (Eq. 5) into the store
+      frag_chunk_id got;
+      hash_tokens(ft, fl, 0, &got);
+      if (std::memcmp(got.bytes, ids[i].bytes, 16) != 0)
+        fail(FRAG_E_CONTRACT, "fallback tokens of chunk " + std::to_string(i) + " do not hash to its chunk id");
+      preprocess_isolated(e, st, sys, n_sys, ft, fl, false, &got);
+      rec = store_fetch(st, ids[i]);
+    }
+    recs.push_back(rec);
     pins.ids.push_back(ids[i]);
   }
   const int S = n_sys;
@@ -1119,6 +1145,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   if (!r->logits_on_device) r->logits_host.ensure((size_t)r->logit_rows * c.vocab * sizeof(float));
 
   // ---- device body
+  const bool full_reuse = k == 0 && !cacheblend && !inject && r0_fast_enabled();
   // K1 overlapped with the question pass (the stitch_ms stage is then ~0 and
   // question_ms covers both); CacheBlend's 2-layer FA pass needs it up front
   const bool overlap = !cacheblend && sp.n_desc > 0 && c.layers > 1 && stitch_overlap_enabled();
@@ -1129,6 +1156,19 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     else
       stitch_launch(e, r, bs, sp);  // K1: stitch_full_reuse
     ev_record(r, timing, 1, bs);
+    if (full_reuse) {
+      // r = 0 (Full Reuse): the plan is exactly the
+      // question rows, so the sparse pass would recompute what the question
+      // pass computes; one full pass over those rows gives the logits (and
+      // q_final from its last QKV) -- bit-identical to question pass + sparse pass
+      r->q_final_in_full = true;
+      run_rows(e, r, bs, n_q, T, PASS_FULL, nullptr, 0, 0, overlap ? r->layer_ev.data() : nullptr, nullptr,
+               r->logit_rows);
+      r->q_final_in_full = false;
+      if (overlap) check_cuda(cudaStreamWaitEvent(bs, r->layer_ev[c.layers - 1], 0), "join stitch");
+      ev_record(r, timing, 2, bs);
+      ev_record(r, timing, 3, bs);
+    } else {
     // question pass: last_layer_query_states against the stitched cache
     if (!cacheblend) run_rows(e, r, bs, n_q, T, PASS_QUESTION, nullptr, 0, 0, overlap ? r->layer_ev.data() : nullptr);
     if (overlap)  // join: every stitched layer (the last one feeds the selection keys)
@@ -1178,6 +1218,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     ev_record(r, timing, 3, bs);
     // sparse_prefill (Eq. 9) to the first-token logits
     run_rows(e, r, bs, M, T, PASS_FULL, nullptr, 0, 0, nullptr, nullptr, r->logit_rows);
+    }
     ev_record(r, timing, 4, bs);
     {
       // final norm + lm_head on the logit rows (K3 + K11)
@@ -1206,7 +1247,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
 
   const bool graphable = !timing && !e->prof.on;
   GraphKey key{T, S, N, n_q, k, (int)inject, (int)all_logits, (int)raw, (int)r->logits_on_device, sp.n_desc,
-               sp.max_rows, (cacheblend ? 1 + dev_layer * 4 + dev_comp : 0) + (overlap ? 1000 : 0),
+               sp.max_rows, (cacheblend ? 1 + dev_layer * 4 + dev_comp : 0) + (overlap ? 1000 : 0) + (full_reuse ? 2000 : 0),
                (uint64_t)(uintptr_t)e->rope.p};
   r->timing.host_prep_ms =
       std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_entry).count();

@@ -241,6 +241,7 @@ struct Result {
       part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok, fr_save, dev, score_col, score_q,
       ssq;
   PinnedBuf staging, logits_host;
+  bool q_final_in_full = false;  // PASS_FULL also keeps the last layer's fp32 queries (r = 0 fast path)
   // timing
   cudaEvent_t ev[7] = {};
   bool timing_valid = false;
@@ -304,7 +305,8 @@ Store* store_create(const frag_model_cfg& cfg, int device, size_t cap);
 void store_put(Store* st, const frag_chunk_id& id, const int32_t* tokens, int n_tok, int native_start, int variant,
                const void* k, const void* v, bool overwrite, size_t src_layer_pitch_elems = 0,
                cudaStream_t s = nullptr);
-Record* store_fetch(Store* st, const frag_chunk_id& id);  // heat++, pin
+Record* store_fetch(Store* st, const frag_chunk_id& id);      // heat++, pin; StoreError when missing
+Record* store_try_fetch(Store* st, const frag_chunk_id& id);  // same, nullptr when missing
 // FKVC record files (serialize_record / deserialize_record): fp32
 // K then V per layer; tokens are supplied by the caller (the format omits them).
 void store_save(Store* st, const frag_chunk_id& id, const char* path);

@@ -149,7 +149,7 @@ bool release_local(Store* st, const ChunkKey& key) {
 // A miss in this store falls through to the attached same-process peers (the
 // owning store keeps heat and pins); cross-process records were imported into
 // the local index as FRAG_TIER_PEER views and hit locally.
-Record* store_fetch(Store* st, const frag_chunk_id& id) {
+Record* store_try_fetch(Store* st, const frag_chunk_id& id) {
   const ChunkKey key = key_of(id);
   if (Record* r = fetch_local(st, key)) return r;
   std::vector<Store*> peers;
@@ -159,6 +159,11 @@ Record* store_fetch(Store* st, const frag_chunk_id& id) {
   }
   for (Store* p : peers)
     if (Record* r = fetch_local(p, key)) return r;
+  return nullptr;
+}
+
+Record* store_fetch(Store* st, const frag_chunk_id& id) {
+  if (Record* r = store_try_fetch(st, id)) return r;
   fail(FRAG_E_STORE, "missing chunk record (SPEC.md:287)");
 }
 

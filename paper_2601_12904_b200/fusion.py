@@ -145,11 +145,14 @@ class Engine:
                   all_logits: bool = False, timing: bool = False, inject_crit: Sequence[int] | None = None,
                   logits_on_device: bool = False, stream=None, question_dev_ptr: int | None = None,
                   n_question: int | None = None, selector: str = "query_guided", deviation_layer: int = 2,
-                  deviation_component: str = "k") -> "Result":
+                  deviation_component: str = "k", fallback: Sequence[Sequence[int] | None] | None = None
+                  ) -> "Result":
         """One request of the online reprocessing stage.
         selector: "query_guided" (FusionRAG, SPEC.md:426) or "cacheblend"
         (layer-`deviation_layer` KV deviation; component "k", "v"
-        or "kv")."""
+        or "kv"). fallback: per chunk its token ids (or None) -- a chunk the
+        store does not hold is then prefilled in isolation on the fly and
+        inserted (flag-gated); without it a miss is StoreError."""
         s = _i32(system)
         ids = (ChunkId * max(len(chunk_ids), 1))(*chunk_ids)
         opts = ReprocessOpts()
@@ -160,6 +163,18 @@ class Engine:
         opts.selector = SELECTORS[selector]
         opts.deviation_layer = int(deviation_layer)
         opts.deviation_component = DEV_COMPONENTS[deviation_component]
+        keep = []
+        if fallback is not None:
+            if len(fallback) != len(chunk_ids):
+                raise ContractError("fallback needs one entry per chunk id")
+            arrs = [None if f is None else _i32(f) for f in fallback]
+            keep.append(arrs)
+            ptrs = (C.POINTER(C.c_int32) * max(len(arrs), 1))(
+                *[C.POINTER(C.c_int32)() if a is None else _i32p(a) for a in arrs])
+            lens = _i32([0 if a is None else len(a) for a in arrs])
+            keep += [ptrs, lens]
+            opts.fallback_tokens = C.cast(ptrs, C.POINTER(C.POINTER(C.c_int32)))
+            opts.fallback_lens = _i32p(lens)
         inj = None
         if inject_crit is not None:
             inj = _i32(inject_crit)

@@ -397,3 +397,35 @@ def test_gemm_chain_is_bit_identical(cuda):
         assert p.returncode == 0, p.stderr[-2000:]
         out[ch] = p.stdout.strip().splitlines()[-1]
     assert out["0"] == out["1"]
+
+
+@pytest.mark.parametrize("preset,layers", [("tiny", 0), ("llama3-8b", 2)])
+def test_r0_full_reuse_fast_path_bit_identical(cuda, preset, layers):
+    """r = 0 (Full Reuse): one full pass over the question rows
+    replaces the question pass + the sparse pass over the same rows. Its
+    logits, fused K/V and q_final equal the two-pass path (forced here by an
+    empty injected critical set) bit for bit, eager and graph-replayed."""
+    from paper_2601_12904_b200 import fusion as F
+    cfg = F.preset(preset)
+    if layers:
+        cfg.layers = layers
+    eng = F.Engine(cfg, seed=21)
+    store = F.ChunkKVStore(cfg)
+    rng = np.random.default_rng(5)
+    ids = [eng.preprocess_isolated(store, rng.integers(0, cfg.vocab, 200).tolist()) for _ in range(3)]
+    T = 600 + 32
+    a, b = F.Result(eng, T), F.Result(eng, T)
+    for _ in range(3):  # eager, capture, replay
+        q = rng.integers(0, cfg.vocab, 32).tolist()
+        eng.reprocess(store, q, ids, 0.0, a)
+        eng.reprocess(store, q, ids, 0.0, b, inject_crit=[])
+        assert len(a.crit()) == 0 and len(b.crit()) == 0
+        assert np.array_equal(a.logits(), b.logits())
+        ka, va = a.fused_kv()
+        kb, vb = b.fused_kv()
+        assert np.array_equal(ka, kb) and np.array_equal(va, vb)
+        assert np.array_equal(a.debug()["q_final"], b.debug()["q_final"])
+    a.close()
+    b.close()
+    store.close()
+    eng.close()
