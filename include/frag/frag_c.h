@@ -188,6 +188,18 @@ FRAG_API frag_status frag_store_save(frag_store* st, const frag_chunk_id* id, co
  * threads run frag_reprocess on other streams. */
 FRAG_API frag_status frag_store_load(frag_store* st, const char* path, const int32_t* tokens, int32_t n_tok,
                                      int32_t overwrite, void* stream, frag_chunk_id* id_out);
+/* Manifest ("JSON file mapping chunk_id -> relative path + variant
+ * + native_start"; each entry also lists the chunk's token ids, which FKVC
+ * omits): save every record this store owns as <dir>/<chunk id hex>.fkvc plus
+ * <dir>/<name> (default "manifest.json"); load every entry of a manifest
+ * through frag_store_load (all entries are validated against their files'
+ * headers first: FRAG_E_FORMAT Io / Malformed / FKVC kinds, nothing inserted). */
+FRAG_API frag_status frag_store_save_manifest(frag_store* st, const char* dir, const char* name, int32_t* n_saved);
+FRAG_API frag_status frag_store_load_manifest(frag_store* st, const char* manifest_path, int32_t overwrite,
+                                              void* stream, int32_t* n_loaded);
+/* Host-only manifest check (no device): parses the manifest and every file
+ * header it references; *n_records = number of entries. */
+FRAG_API frag_status frag_manifest_validate(const char* manifest_path, int32_t* n_records);
 /* Chunk-partitioned store across the GPUs of one box (the
  * spec's single-copy invariant, held across GPUs): each chunk's
  * record lives in exactly one GPU's store (owner = frag_chunk_owner) and the

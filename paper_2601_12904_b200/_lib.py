@@ -125,6 +125,9 @@ _SIGS = {
     "frag_fkvc_read": (C.c_int, [C.c_char_p, C.POINTER(FkvcHeader), _P, _P, C.c_size_t]),
     "frag_store_save": (C.c_int, [_P, C.POINTER(ChunkId), C.c_char_p]),
     "frag_store_load": (C.c_int, [_P, C.c_char_p, _I32P, C.c_int32, C.c_int32, _P, C.POINTER(ChunkId)]),
+    "frag_store_save_manifest": (C.c_int, [_P, C.c_char_p, C.c_char_p, _I32P]),
+    "frag_store_load_manifest": (C.c_int, [_P, C.c_char_p, C.c_int32, _P, _I32P]),
+    "frag_manifest_validate": (C.c_int, [C.c_char_p, _I32P]),
     "frag_store_bytes_used": (C.c_uint64, [_P]),
     "frag_preprocess_isolated": (C.c_int, [_P, _P, _I32P, C.c_int32, _I32P, C.c_int32, C.c_int32,
                                            C.POINTER(ChunkId)]),

@@ -317,6 +317,31 @@ FRAG_API frag_status frag_store_load(frag_store* st, const char* path, const int
   });
 }
 
+FRAG_API frag_status frag_store_save_manifest(frag_store* st, const char* dir, const char* name, int32_t* n_saved) {
+  return guard([&] {
+    need(st && dir, "null argument");
+    const int n = manifest_save(st->s, dir, name);
+    if (n_saved) *n_saved = n;
+  });
+}
+
+FRAG_API frag_status frag_store_load_manifest(frag_store* st, const char* manifest_path, int32_t overwrite,
+                                              void* stream, int32_t* n_loaded) {
+  return guard([&] {
+    need(st && manifest_path, "null argument");
+    const int n = manifest_load(st->s, manifest_path, overwrite != 0, static_cast<cudaStream_t>(stream));
+    if (n_loaded) *n_loaded = n;
+  });
+}
+
+FRAG_API frag_status frag_manifest_validate(const char* manifest_path, int32_t* n_records) {
+  return guard([&] {
+    need(manifest_path, "null argument");
+    const auto es = manifest_read(manifest_path);
+    if (n_records) *n_records = (int32_t)es.size();
+  });
+}
+
 FRAG_API int32_t frag_chunk_owner(const frag_chunk_id* id, int32_t n_owners) {
   if (!id || n_owners < 1) return -1;
   return chunk_owner(*id, n_owners);

@@ -315,6 +315,18 @@ void store_load(Store* st, const char* path, const int32_t* tokens, int n_tok, b
 void fkvc_write(const char* path, const frag_fkvc_header& h, const float* k, const float* v);
 void fkvc_read(const char* path, frag_fkvc_header* h, float* k, float* v, size_t cap_floats);
 void store_release(Store* st, const frag_chunk_id& id);
+// FKVC manifest (manifest.cpp): chunk_id -> relative path +
+// variant + native_start (+ the chunk's token ids)
+struct ManifestEntry {
+  frag_chunk_id id{};
+  std::string path;  // resolved against the manifest's directory
+  int variant = FRAG_VARIANT_ISOLATED;
+  int32_t native_start = 1;
+  std::vector<int32_t> tokens;
+};
+std::vector<ManifestEntry> manifest_read(const char* path);  // host only; checks every file header
+int manifest_save(Store* st, const char* dir, const char* name);
+int manifest_load(Store* st, const char* path, bool overwrite, cudaStream_t s);
 // chunk-partitioned store across GPUs: same-process peers and
 // cross-process CUDA-IPC export/import of record pages
 int32_t chunk_owner(const frag_chunk_id& id, int32_t n);

@@ -22,7 +22,7 @@ from ._lib import (ChunkId, FkvcHeader, ContractError, CudaError, FormatError, F
 __all__ = ["ModelCfg", "ChunkId", "Engine", "ChunkKVStore", "Result", "preset", "hash_tokens",
            "ContractError", "StoreError", "FormatError", "CudaError", "OutOfMemory", "FragError",
            "ISOLATED", "FUSED", "launch_count", "memcpy", "fkvc_write", "fkvc_read", "chunk_owner",
-           "PeerRecord", "TIER_GPU", "TIER_PEER"]
+           "PeerRecord", "TIER_GPU", "TIER_PEER", "manifest_validate"]
 
 ISOLATED, FUSED = 0, 1
 TIER_GPU, TIER_CPU, TIER_DISK, TIER_PEER = 0, 1, 2, 3
@@ -337,6 +337,20 @@ class ChunkKVStore:
                                   _stream_ptr(stream), C.byref(cid)))
         return cid
 
+    def save_manifest(self, directory: str, name: str = "manifest.json") -> int:
+        """Every record this store owns as <directory>/<id hex>.fkvc plus the
+        JSON manifest; returns the number of records."""
+        n = C.c_int32()
+        check(lib.frag_store_save_manifest(self._h, str(directory).encode(), name.encode(), C.byref(n)))
+        return n.value
+
+    def load_manifest(self, path: str, *, overwrite: bool = False, stream=None) -> int:
+        """Load every record a manifest lists (DISK -> GPU)."""
+        n = C.c_int32()
+        check(lib.frag_store_load_manifest(self._h, str(path).encode(), int(overwrite), _stream_ptr(stream),
+                                           C.byref(n)))
+        return n.value
+
     # ------------------------------------------------ alternative_path_match (SPEC.md:274-282)
     def register_prefix(self, path: Sequence[ChunkId], system: Sequence[int] | None = None):
         """Record that path[-1]'s record was computed under (system, path[:-1])."""
@@ -482,6 +496,14 @@ class Result:
         if n.value:
             memcpy(s.ctypes.data, sc.value, n.value * 4)
         return {"q_final": q, "scores": s[:n.value]}
+
+
+def manifest_validate(path: str) -> int:
+    """Host-only check of an FKVC manifest and the headers of the files it
+    lists (no device); returns the number of records."""
+    n = C.c_int32()
+    check(lib.frag_manifest_validate(str(path).encode(), C.byref(n)))
+    return n.value
 
 
 def fkvc_write(path: str, chunk_id: ChunkId, k: np.ndarray, v: np.ndarray, native_start: int,

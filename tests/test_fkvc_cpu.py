@@ -69,3 +69,78 @@ def test_fkvc_missing_file_is_io_error(tmp_path):
     with pytest.raises(F.FormatError) as ei:
         F.fkvc_read(tmp_path / "nope.fkvc")
     assert ei.value.kind == "Io"
+
+
+def _manifest(tmp_path, n=3, mutate=None):
+    import json
+    recs = []
+    for i in range(n):
+        k, v = _rec(10 + i, (2, 4 + i, 2, 8))
+        toks = list(range(i, i + 4 + i))
+        cid = F.hash_tokens(toks)
+        name = f"{cid.hex()}.fkvc"
+        F.fkvc_write(tmp_path / name, cid, k, v, native_start=3 + i, variant=i % 2)
+        recs.append({"chunk_id": cid.hex(), "path": name, "variant": ["ISOLATED", "FUSED"][i % 2],
+                     "native_start": 3 + i, "tokens": toks})
+    doc = {"format": "FKVC-manifest", "version": 1, "records": recs}
+    if mutate:
+        doc = mutate(doc)
+    p = tmp_path / "manifest.json"
+    p.write_text(doc if isinstance(doc, str) else json.dumps(doc))
+    return p
+
+
+def test_manifest_written_independently_validates(tmp_path):
+    """SPEC.md:322 manifest (chunk_id -> relative path + variant +
+    native_start, plus the token ids FKVC omits), written here by Python's
+    json module, is read by the library's parser and checked against every
+    file header."""
+    assert F.manifest_validate(_manifest(tmp_path)) == 3
+
+
+@pytest.mark.parametrize("mutate,kind", [
+    (lambda d: "{\"format\": \"FKVC-manifest\", \"version\": 1, \"records\": [", "Malformed"),
+    (lambda d: {**d, "version": 2}, "BadVersion"),
+    (lambda d: {**d, "format": "other"}, "Malformed"),
+    (lambda d: {**d, "records": [{**d["records"][0], "chunk_id": d["records"][1]["chunk_id"]}]}, "Malformed"),
+    (lambda d: {**d, "records": [{**d["records"][0], "native_start": 99}]}, "Malformed"),
+    (lambda d: {**d, "records": [{**d["records"][0], "tokens": [1]}]}, "Malformed"),
+    (lambda d: {**d, "records": [{**d["records"][0], "path": "missing.fkvc"}]}, "Io"),
+])
+def test_manifest_errors(tmp_path, mutate, kind):
+    p = _manifest(tmp_path, mutate=mutate)
+    with pytest.raises(F.FormatError) as ei:
+        F.manifest_validate(p)
+    assert ei.value.kind == kind
+
+
+def test_cpp_wrapper_maps_format_error_kinds(tmp_path):
+    """frag::check re-throws FRAG_E_FORMAT as FormatError with the library's
+    kind (common.hpp:33), not a blanket Malformed."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+    from paper_2601_12904_b200 import _lib as L
+    gxx = shutil.which("g++")
+    if not gxx:
+        pytest.skip("no g++")
+    root = Path(__file__).resolve().parent.parent
+    src = tmp_path / "kinds.cpp"
+    src.write_text('#include "frag/fusion.hpp"\n#include <cstdio>\n'
+                   'int main(int argc, char** argv){ frag_fkvc_header h{};\n'
+                   '  try { frag::check(frag_fkvc_read(argv[1], &h, nullptr, nullptr, 0)); return 9; }\n'
+                   '  catch (const frag::FormatError& e) { std::printf("%d\\n", (int)e.kind()); return 0; } }\n')
+    exe = tmp_path / "kinds"
+    subprocess.run([gxx, "-std=c++20", f"-I{root / 'include'}", str(src), f"-L{L.LIB_PATH.parent}", "-lfrag",
+                    f"-Wl,-rpath,{L.LIB_PATH.parent}", "-o", str(exe)], check=True, capture_output=True)
+    k, v = _rec(3)
+    good = _spec_bytes(F.hash_tokens([1]), 0, 1, k, v)
+    cases = {"bad_magic": (b"XXXX" + good[4:], 0), "bad_version": (good[:4] + struct.pack("<I", 9) + good[8:], 1),
+             "truncated": (good[:30], 2), "malformed": (good[:24] + bytes([5]) + good[25:], 3)}
+    for name, (blob, want) in cases.items():
+        p = tmp_path / f"{name}.fkvc"
+        p.write_bytes(blob)
+        r = subprocess.run([str(exe), str(p)], capture_output=True, text=True)
+        assert r.returncode == 0 and int(r.stdout) == want, (name, r.stdout, r.stderr)
+    r = subprocess.run([str(exe), str(tmp_path / "none.fkvc")], capture_output=True, text=True)
+    assert int(r.stdout) == 4  # Io

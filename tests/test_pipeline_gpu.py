@@ -429,3 +429,25 @@ def test_r0_full_reuse_fast_path_bit_identical(cuda, preset, layers):
     b.close()
     store.close()
     eng.close()
+
+
+def test_manifest_round_trip(tiny, tmp_path):
+    """save_manifest -> load_manifest into a fresh store: the
+    same records (bytes, variant, native_start, tokens) and the same request."""
+    F, eng = tiny["F"], tiny["eng"]
+    store, ids = tiny["store"], tiny["ids"]
+    n = store.save_manifest(tmp_path)
+    assert n == len(store) and (tmp_path / "manifest.json").exists()
+    assert F.manifest_validate(tmp_path / "manifest.json") == n
+    fresh = F.ChunkKVStore(eng.cfg)
+    assert fresh.load_manifest(tmp_path / "manifest.json") == n
+    for cid in ids:
+        a, b = store.peek(cid), fresh.peek(cid)
+        assert (a.n_tok, a.native_start, a.variant) == (b.n_tok, b.native_start, b.variant)
+        ka, va = store.read_kv(cid)
+        kb, vb = fresh.read_kv(cid)
+        assert np.array_equal(ka, kb) and np.array_equal(va, vb)
+    with pytest.raises(F.StoreError):
+        fresh.load_manifest(tmp_path / "manifest.json")  # duplicates without overwrite
+    assert fresh.load_manifest(tmp_path / "manifest.json", overwrite=True) == n
+    fresh.close()
