@@ -44,7 +44,8 @@ constexpr int AT_QT = 2;      // query tiles per CTA
 constexpr int AT_KEYS = 128;  // keys per K/V tile
 constexpr int AT_THREADS = 320;
 constexpr float RESCALE_THRESH = 8.0f;  // log2 units
-constexpr int kDefaultPoly = 0;  // measured: MUFU-only is fastest at dh=128 (tools/attn_bench.py)
+constexpr int kDefaultPoly = 0;
+constexpr int kQtmPoly = 4;  // Q-in-TMEM kernel: every 4th exp pair on the FMA pipe  // measured: MUFU-only is fastest at dh=128 (tools/attn_bench.py)
 
 template <int DH>
 struct AttCfg {
@@ -539,6 +540,366 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- Q in TMEM
+// One 128-row query tile per CTA (128/G tokens x G heads of one GQA group)
+// with Q resident in TMEM as the A operand of S = Q K^T (tcgen05.mma with A
+// from TMEM): the S MMA reads only K from shared memory. The r01 kernels
+// read Q and K from shared memory (8 KB per K=16 step = the whole 128 B/clk
+// port), which bound them at ~1370 cycles per tile pair against 1024 ideal,
+// and their per-tile chain softmax -> PV -> next S serialised each tile.
+// TMEM (448 of 512 cols): S/P double buffer 2 x 128 (P aliased into the
+// first 64 cols of its S buffer) + O (DH) + Q (DH/2 packed bf16). With two S
+// buffers the tensor pipe computes S(u+1) -- and PV(u-1) -- while the
+// softmax works on S(u):
+//   S(0) S(1) | PV(0) S(2) | PV(1) S(3) | ...
+// 16 softmax warps: warp w owns TMEM lane quarter w%4 (its SMSP) and key
+// columns 32*(w/4).. of each 128-key slice; the row max is exchanged through
+// shared memory behind one named barrier per lane quarter and slice (the same
+// barrier orders every warp's S load before any P store over those columns).
+// An O rescale (lazy, > 2^8) waits for PV(u-1); otherwise the softmax of
+// slice u never waits on the tensor pipe.
+template <int DH, int PE>
+__global__ void __launch_bounds__(576, 1)
+    attn_qtm_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                    const AttnArgs a, int G, int n_qblocks) {
+  constexpr int ATOMS = DH / 64;
+  constexpr uint32_t KV_ATOM = AT_KEYS * 128;
+  constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;
+  constexpr int NS = DH == 128 ? 3 : 6;
+  // S buffer b at b*128; O; the row sums L (16 cols, every one = sum_k P); Q
+  constexpr uint32_t T_S0 = 0, T_O = 256, T_L = T_O + DH, T_Q = 448;
+  constexpr int QC = DH / 8;                           // packed Q columns per column-group warp
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;                   // [NS][KV_BYTES]
+  uint8_t* sV = sK + NS * KV_BYTES;     // [NS][KV_BYTES]
+  uint8_t* sOnes = sV + NS * KV_BYTES;  // 16 KB of bf16 1.0: B operand of the row-sum MMA
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + 16384);
+  uint64_t* k_full = bar;               // [NS]
+  uint64_t* v_full = bar + NS;          // [NS]
+  uint64_t* kv_empty = bar + 2 * NS;    // [NS]
+  uint64_t* q_full = bar + 3 * NS;
+  uint64_t* s_full = q_full + 1;        // [2] per S buffer
+  uint64_t* p_full = s_full + 2;        // [2]
+  uint64_t* pv_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  __shared__ float xm[2][4][AT_ROWS];   // [slice parity][column group][row] partial max
+
+  const int warp = warp_id(), lane = lane_id();
+  const int qb = n_qblocks - 1 - (int)blockIdx.x / a.Hkv;  // longest-first (see attn_tc_kernel)
+  const int hk = (int)blockIdx.x % a.Hkv;
+  const int split = blockIdx.z;
+  const int tok_per_tile = AT_ROWS / G;
+  const int t0 = qb * tok_per_tile;
+  const int t_end = min(t0 + tok_per_tile, a.M);
+  const int k_lo = a.n_splits > 1 ? split * a.split_keys : 0;
+  constexpr int W_TMA = 16, W_MMA = 17;
+  if (warp == W_TMA && lane == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(q_full, 16);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 16);
+    }
+    mbar_init(pv_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+  const int p_max = a.rows[t_end - 1] - a.row_base;
+  int k_hi = p_max + 1;
+  if (a.n_splits > 1) k_hi = min(k_hi, (split + 1) * a.split_keys);
+  const int n_tiles = k_hi > k_lo ? (k_hi - k_lo + AT_KEYS - 1) / AT_KEYS : 0;
+
+  if (warp == W_TMA) {
+    if (n_tiles > 0 && elect_one()) {
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j % NS;
+        mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
+        const int key0 = k_lo + j * AT_KEYS;
+        mbar_arrive_expect_tx(&k_full[st], KV_BYTES);
+#pragma unroll
+        for (int at = 0; at < ATOMS; ++at)
+          tma_load_2d(sK + st * KV_BYTES + at * KV_ATOM, &tmK, &k_full[st], hk * DH + at * 64, key0);
+        mbar_arrive_expect_tx(&v_full[st], KV_BYTES);
+#pragma unroll
+        for (int at = 0; at < ATOMS; ++at)
+          tma_load_2d(sV + st * KV_BYTES + at * KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64, key0);
+      }
+      for (int j = n_tiles > NS ? n_tiles - NS : 0; j < n_tiles; ++j) mbar_wait(&kv_empty[j % NS], (j / NS) & 1);
+    }
+  } else if (warp == W_MMA) {
+    if (n_tiles > 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(AT_ROWS, AT_KEYS, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(AT_ROWS, DH, 0, 1);
+      constexpr uint32_t idesc_l = umma_idesc_bf16(AT_ROWS, 16, 0, 0);
+      const uint64_t d_ones = umma_desc_sw128(smem_u32(sOnes), 16, 1024);
+      const uint64_t dk = umma_desc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dv = umma_desc_sw128(smem_u32(sV), KV_ATOM, 1024);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto issue_s = [&](int u) {
+        const int st = u % NS;
+        mbar_wait(&k_full[st], (u / NS) & 1);
+        tc_fence_after();
+        if (a.trace && blockIdx.x == 0 && lane == 0 && u < 256) a.trace[u * 4 + 2] = clock64();
+        if (elect_one()) {
+          const uint64_t k0 = dk + ((st * KV_BYTES) >> 4);
+          const uint32_t d_tmem = tmem + T_S0 + (u & 1) * 128;
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * KV_ATOM + (kk & 3) * 32) >> 4;
+            umma_bf16_ts(d_tmem, tmem + T_Q + kk * 8, k0 + off, idesc_s, kk != 0);
+          }
+          umma_commit(&s_full[u & 1]);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int u) {
+        const int st = u % NS;
+        mbar_wait(&p_full[u & 1], (u >> 1) & 1);
+        mbar_wait(&v_full[st], (u / NS) & 1);
+        tc_fence_after();
+        if (a.trace && blockIdx.x == 0 && lane == 0 && u < 256) a.trace[u * 4 + 3] = clock64();
+        if (elect_one()) {
+          const uint64_t v0 = dv + ((st * KV_BYTES) >> 4);
+          const uint32_t p_tmem = tmem + T_S0 + (u & 1) * 128;
+#pragma unroll
+          for (int kk = 0; kk < AT_KEYS / 16; ++kk)
+            umma_bf16_ts(tmem + T_O, p_tmem + kk * 8, v0 + ((kk * 16 * 128) >> 4), idesc_o, (u | kk) != 0);
+          // row sums on the tensor pipe: L += P . 1 (the bf16 P that also multiplies V)
+#pragma unroll
+          for (int kk = 0; kk < AT_KEYS / 16; ++kk)
+            umma_bf16_ts(tmem + T_L, p_tmem + kk * 8, d_ones, idesc_l, (u | kk) != 0);
+          umma_commit(pv_done);
+          umma_commit(&kv_empty[st]);
+        }
+        __syncwarp();
+      };
+      issue_s(0);
+      if (n_tiles > 1) issue_s(1);
+      for (int u = 0; u < n_tiles; ++u) {
+        issue_pv(u);
+        if (u + 2 < n_tiles) issue_s(u + 2);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue (16 warps)
+    const int q4 = warp & 3, cg = warp >> 2;
+    const int r = q4 * 32 + lane;
+    const int tok = t0 + r / G;
+    const int head = hk * G + r % G;
+    const bool live = tok < a.M;
+    const int prow = live ? a.rows[tok] - a.row_base : -1;
+    const int p_min = a.rows[t0] - a.row_base;
+    const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
+    const size_t qi = (size_t)tok * a.Hq + head;
+    const int nbar = 1 + q4;  // named barrier of this lane quarter (its 4 column-group warps)
+    {  // Q row, this warp's DH/4 columns -> TMEM (A operand of S)
+      uint32_t qr[QC];
+      if (live) {
+        const uint4* src = reinterpret_cast<const uint4*>(a.q + qi * DH + cg * (DH / 4));
+#pragma unroll
+        for (int e = 0; e < QC / 4; ++e) {
+          const uint4 v = __ldg(src + e);
+          qr[4 * e] = v.x, qr[4 * e + 1] = v.y, qr[4 * e + 2] = v.z, qr[4 * e + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < QC; ++e) qr[e] = 0u;
+      }
+      if constexpr (QC == 16)
+        tmem_st16(lane_base + T_Q + cg * QC, qr);
+      else
+        tmem_st8(lane_base + T_Q + cg * QC, qr);
+      {  // this thread's 32 bytes of the 16 KB ones tile
+        uint4* o1 = reinterpret_cast<uint4*>(sOnes) + 2 * (cg * 128 + r);
+        const uint4 one = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+        o1[0] = one;
+        o1[1] = one;
+        fence_async_smem();  // generic writes -> visible to the tensor pipe's reads
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
+    }
+    const float c = a.scale * 1.4426950408889634f;
+    float m_used = -INFINITY;
+    for (int u = 0; u < n_tiles; ++u) {
+      const int b = u & 1;
+      const int key0 = k_lo + u * AT_KEYS + cg * 32;
+      mbar_wait(&s_full[b], (u >> 1) & 1);
+      tc_fence_after();
+      if (a.trace && blockIdx.x == 0 && lane == 0 && warp == 0 && u < 256) a.trace[u * 4 + 0] = clock64();
+      uint32_t s[32];
+      tmem_ld32(lane_base + T_S0 + b * 128 + cg * 32, s);
+      tmem_ld_wait();
+      if (a.trace && blockIdx.x == 0 && lane == 0 && warp == 0 && u < 256) a.trace[1024 + u * 4 + 0] = clock64();
+      const int lim = min(prow, k_hi - 1) - key0;
+      if ((key0 + 31 > p_min) || (key0 + 32 > k_hi)) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k > lim) s[k] = 0xff800000u;
+      }
+      float mx4[4] = {__uint_as_float(s[0]), __uint_as_float(s[1]), __uint_as_float(s[2]), __uint_as_float(s[3])};
+#pragma unroll
+      for (int k = 4; k < 28; k += 8)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mx4[e] = fmax3(mx4[e], __uint_as_float(s[k + e]), __uint_as_float(s[k + 4 + e]));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mx4[e] = fmaxf(mx4[e], __uint_as_float(s[28 + e]));
+      const float lmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c;
+      // lazy rescale: the row max matters only if some column group's max
+      // exceeds m_used + 2^8; one OR-barrier decides for the lane quarter (it
+      // also orders every warp's S load before any P store over those columns)
+      const bool need = lmax > m_used + RESCALE_THRESH || (m_used == -INFINITY && lmax != -INFINITY);
+      float mt = -INFINITY;
+      if (bar_red_or(nbar, 128, need)) {
+        xm[b][cg][r] = lmax;
+        asm volatile("bar.sync %0, 128;" ::"r"(nbar) : "memory");
+        mt = fmaxf(fmaxf(xm[b][0][r], xm[b][1][r]), fmaxf(xm[b][2][r], xm[b][3][r]));
+      }
+      if (a.trace && blockIdx.x == 0 && lane == 0 && warp == 0 && u < 256) a.trace[1024 + u * 4 + 1] = clock64();
+      const bool grow = mt > m_used + RESCALE_THRESH || (m_used == -INFINITY && mt != -INFINITY);
+      const float m_new = grow ? fmaxf(mt, m_used) : m_used;
+      const float alpha = (grow && m_used != -INFINITY) ? ex2_approx(m_used - m_new) : 1.f;
+      const bool resc = grow && m_used != -INFINITY;
+      m_used = m_new;
+      const float mneg = m_used == -INFINITY ? 0.f : -m_used;
+      // packed fp32x2 arithmetic (FFMA2 / FADD2: one FMA-pipe issue per two
+      // elements); every PE-th pair takes the FMA-pipe polynomial instead of
+      // MUFU.EX2: the four softmax warps of an SMSP share its MUFU (4/clk)
+      const unsigned long long c2 = f2_pack(c, c), m2 = f2_pack(mneg, mneg);
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const unsigned long long x = f2_fma(f2_pack(__uint_as_float(s[2 * e]), __uint_as_float(s[2 * e + 1])), c2, m2);
+        float x0, x1, p0, p1;
+        f2_unpack(x, x0, x1);
+        if (PE > 0 && (e % (PE > 0 ? PE : 1)) == PE - 1) {
+          ex2_poly2(x0, x1, p0, p1);
+        } else {
+          p0 = ex2_approx(x0);
+          p1 = ex2_approx(x1);
+        }
+        pk[e] = pack_bf16(p0, p1);
+      }
+      if (a.trace && blockIdx.x == 0 && lane == 0 && warp == 0 && u < 256) a.trace[1024 + u * 4 + 2] = clock64();
+      tmem_st16(lane_base + T_S0 + b * 128 + cg * 16, pk);  // P keys cg*32.. = packed cols cg*16..
+      if (__any_sync(0xffffffffu, resc) && u > 0) {
+        // O holds PV(0..u-1) at the old scale: rescale this warp's DH/4 columns
+        // once PV(u-1) has landed; PV(u) waits for p_full below
+        mbar_wait(pv_done, (u - 1) & 1);
+        tc_fence_after();
+        uint32_t o[DH / 4];
+        if constexpr (DH / 4 == 32) {
+          tmem_ld32(lane_base + T_O + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(o));
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(lane_base + T_O + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(o));
+        } else {
+          uint32_t o32[32];
+          tmem_ld32(lane_base + T_O + (cg & 1) * 32, o32);  // DH=64: warps cg<2 own 32 cols each
+          tmem_ld_wait();
+          if (cg < 2) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o32[e] = __float_as_uint(__uint_as_float(o32[e]) * alpha);
+            tmem_st32(lane_base + T_O + cg * 32, o32);
+          }
+        }
+        if (cg == 3) {  // and the row-sum columns
+          uint32_t o16[16];
+          tmem_ld16(lane_base + T_L, o16);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) o16[e] = __float_as_uint(__uint_as_float(o16[e]) * alpha);
+          tmem_st16(lane_base + T_L, o16);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      if (a.trace && blockIdx.x == 0 && lane == 0 && warp == 0 && u < 256) a.trace[u * 4 + 1] = clock64();
+    }
+    // ---- epilogue: the row sum accumulated by the tensor pipe (T_L)
+    float lt = 0.f;
+    if (n_tiles > 0) {
+      mbar_wait(pv_done, (n_tiles - 1) & 1);
+      tc_fence_after();
+      uint32_t l16[16];
+      tmem_ld16(lane_base + T_L, l16);
+      tmem_ld_wait();
+      lt = __uint_as_float(l16[0]);
+    }
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    constexpr int OC = DH / 4;  // output columns of this warp
+    if (OC == 32 || cg < 2) {
+      const int dcol = (OC == 32 ? cg : cg) * 32;
+      uint32_t o[32];
+      if (n_tiles > 0) {
+        tmem_ld32(lane_base + T_O + dcol, o);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = 0u;
+      }
+      if (live) {
+        if (a.n_splits > 1) {
+          float4* po = reinterpret_cast<float4*>(a.part_o + ((size_t)split * a.M * a.Hq + qi) * DH + dcol);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            po[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+        } else {
+          uint4* po = reinterpret_cast<uint4*>(a.out + qi * DH + dcol);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[8 * e + 0]) * inv, __uint_as_float(o[8 * e + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv);
+            po[e] = v;
+          }
+        }
+      }
+    } else if (n_tiles > 0) {
+      uint32_t o[32];  // DH=64, cg >= 2: keep the warp's tcgen05.ld count uniform (no columns to write)
+      tmem_ld32(lane_base + T_O, o);
+      tmem_ld_wait();
+    }
+    if (live && cg == 0 && a.n_splits > 1)
+      a.part_lse[(size_t)split * a.M * a.Hq + qi] = lt > 0.f ? m_used * 0.6931471805599453f + __logf(lt) : -INFINITY;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int DH>
+constexpr size_t qtm_smem() {
+  return 1024 + (size_t)(DH == 128 ? 3 : 6) * 2 * AT_KEYS * DH * 2 + 16384 + 256;
+}
+static_assert(qtm_smem<128>() <= 232448 - 4 * 1024 && qtm_smem<64>() <= 232448 - 4 * 1024,
+              "Q-in-TMEM attention exceeds 227 KB");
+
 }  // namespace
 
 int attn_rows_per_cta() { return AT_ROWS * AT_QT; }
@@ -597,6 +958,45 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
       go(attn_tc_kernel<64, 0, true>, (int)AttCfg<64>::SMEM_DUAL);
     else
       return -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+  }
+  // Q-in-TMEM kernel (default; FRAG_ATTN_QTM=0 selects the r01 SS kernels)
+  static const bool qtm = [] {
+    const char* v = std::getenv("FRAG_ATTN_QTM");
+    return !(v && v[0] == '0');
+  }();
+  if (qtm && poly == 0 && (a.dh == 128 || a.dh == 64)) {
+    const int nqb1 = (a.M + AT_ROWS / G - 1) / (AT_ROWS / G);  // one 128-row tile per CTA
+    const dim3 grid1(nqb1 * a.Hkv, 1, a.n_splits);
+    auto go2 = [&](auto kern, int smem) {
+      smem_attr_once(kern, smem);
+      launch_pdl(kern, grid1, dim3(576), smem, stream, tk, tv, at, G, nqb1);
+      if (trace_path) {
+        unsigned long long h[2 * 256 * 4];
+        cudaMemcpyAsync(h, trace_dev, sizeof(h), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        if (FILE* f = std::fopen(trace_path, "ab")) {
+          std::fwrite(h, sizeof(h), 1, f);
+          std::fclose(f);
+        }
+      }
+    };
+    // FRAG_ATTN_QTM_POLY: every n-th exp pair on the FMA pipe (0 = MUFU only)
+    static const int qpoly = [] {
+      const char* v = std::getenv("FRAG_ATTN_QTM_POLY");
+      return v ? std::atoi(v) : kQtmPoly;
+    }();
+    if (a.dh == 128) {
+      switch (qpoly) {
+        case 0: go2(attn_qtm_kernel<128, 0>, (int)qtm_smem<128>()); break;
+        case 2: go2(attn_qtm_kernel<128, 2>, (int)qtm_smem<128>()); break;
+        case 3: go2(attn_qtm_kernel<128, 3>, (int)qtm_smem<128>()); break;
+        case 8: go2(attn_qtm_kernel<128, 8>, (int)qtm_smem<128>()); break;
+        default: go2(attn_qtm_kernel<128, 4>, (int)qtm_smem<128>()); break;
+      }
+    } else {
+      go2(attn_qtm_kernel<64, kQtmPoly>, (int)qtm_smem<64>());
+    }
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
   }
   if (split_rows && a.dh == 128 && poly == 0) {
