@@ -38,8 +38,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-N_CLASSES = 6  # frag_engine_profile_read classes (frag_c.h)
-CLASS_NAMES = ["gemm", "attention", "stitch", "norm", "select", "gemm_stream"]
+N_CLASSES = 7  # frag_engine_profile_read classes (frag_c.h)
+CLASS_NAMES = ["gemm", "attention", "stitch", "norm", "select", "gemm_stream", "gemm_gateup"]
 METRIC = "TTFT ms at 16k-token RAG prompt, 15% recompute vs full prefill; prefill tok/s"
 CONFIGS = {
     "llama3-8b": dict(preset="llama3-8b", chunks=8, chunk_len=2048, qlen=32, ratio=0.15),
@@ -604,12 +604,20 @@ def main():
     sus, burst, hbm, src = peaks()
     g = r["prof"][0]
     gemm_tflops = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
-    traffic = None
+    # roofline kernel: the gate/up projection GEMM of the sparse pass
+    # (gemm_tc2_kernel<256, EPI_SWIGLU>, the single largest launch: its own
+    # profile class, events around each of its launches); traffic = its DRAM
+    # bytes per launch from the committed ncu --set full capture of the same
+    # kernel (profiles/ncu_traffic.json, cold-cache, one launch)
+    gu = r["prof"][6]
+    gu_tflops = gu["flops"] / (gu["ms"] / 1e3) / 1e12 if gu["ms"] > 0 else None
+    traffic, traffic_src = None, None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
             js = json.loads(tf.read_text())
-            traffic = js.get("gemm_tc2_kernel_bytes_per_launch", js.get("gemm_tc_kernel_bytes_per_launch"))
+            traffic = js.get("gemm_tc2_gateup_bytes_per_launch")
+            traffic_src = js.get("source")
         except Exception:
             traffic = None
     c = r["cfg"]
@@ -640,11 +648,18 @@ def main():
         "e2e": {"value": e2e_value, "unit": "tok/s", "ttft_ms": e2e_ms / args.steps,
                 "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"],
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc2_kernel / gemm_tc_kernel (tcgen05, K4/K7/K8 at M>128)",
-                     "achieved": gemm_tflops, "peak": sus, "unit": "TFLOP/s",
-                     "frac": (gemm_tflops / sus) if gemm_tflops else None, "traffic": traffic,
+        "roofline": {"bound": "tensor",
+                     "kernel": "gemm_tc2_kernel<256, SWIGLU> (K8 gate/up projection of the sparse pass, tcgen05 "
+                               "cta_group::2)",
+                     "achieved": gu_tflops, "peak": sus, "unit": "TFLOP/s",
+                     "frac": (gu_tflops / sus) if gu_tflops else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "algorithmic_flop_per_launch": (gu["flops"] / gu["launches"]) if gu["launches"] else None,
+                     "launch_ms": (gu["ms"] / gu["launches"]) if gu["launches"] else None,
                      "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside the long step)",
-                     "gemm_share_of_step": g["ms"] / ms if ms else None},
+                     "kernel_share_of_step": gu["ms"] / args.steps / ttft if ttft else None,
+                     "all_tensor_gemms": {"achieved": gemm_tflops, "frac": (gemm_tflops / sus) if gemm_tflops else None,
+                                          "share_of_step": g["ms"] / ms if ms else None}},
         "kernels": {name: {"ms_per_step": r["prof"][k]["ms"] / args.steps,
                            "launches_per_step": r["prof"][k]["launches"] / args.steps}
                     for k, name in enumerate(CLASS_NAMES)},

@@ -373,7 +373,9 @@ FRAG_API frag_status frag_result_debug(const frag_result* res, const float** q_f
  * launching stream) for the bench roofline. class: 0 tensor-bound GEMM
  * (K4/K7/K8/K11 at > 128 rows), 1 attention (K6), 2 stitch (K1), 3 norms/gather
  * (K2/K3), 4 select (K9/K10), 5 weight-streaming GEMM (<= 128 rows: the
- * question pass and lm_head rows; algorithmic bytes = weight bytes). */
+ * question pass and lm_head rows; algorithmic bytes = weight bytes), 6 the
+ * gate/up projection GEMM alone at > 128 rows (a subset of class 0: the
+ * single largest kernel, the bench's roofline kernel). */
 FRAG_API frag_status frag_engine_profile(frag_engine* eng, int32_t enable);
 /* Sums over launches since the last reset (call after frag_result_sync):
  * device ms, algorithmic FLOPs, algorithmic bytes, launch count. */

@@ -77,7 +77,9 @@ struct DeviceGuard {
 // ---------------------------------------------------------------- profiling
 // KC_GEMM: tensor-bound GEMMs (M > 128 rows); KC_GEMM_STREAM: one-M-tile
 // GEMMs (question pass, lm_head rows), bound by the weight stream from HBM.
-enum KClass { KC_GEMM = 0, KC_ATTN = 1, KC_STITCH = 2, KC_NORM = 3, KC_SELECT = 4, KC_GEMM_STREAM = 5, KC_N = 6 };
+// KC_GEMM_GU: the gate/up projection at M > 128 alone (also counted in KC_GEMM)
+enum KClass { KC_GEMM = 0, KC_ATTN = 1, KC_STITCH = 2, KC_NORM = 3, KC_SELECT = 4, KC_GEMM_STREAM = 5, KC_GEMM_GU = 6,
+              KC_N = 7 };
 inline int gemm_class(int M) { return M <= 128 ? KC_GEMM_STREAM : KC_GEMM; }
 struct Profiler {
   bool on = false;

@@ -21,7 +21,7 @@ ncu --profile-from-start off --set full --clock-control none --import-source on 
     -k regex:gemm_chain -s 0 -c 1 -o $OUT/chain_$TAG python tools/profile_step.py > /dev/null 2>&1
 # sparse pass, layer 0 attention (after the 32 question-pass launches) + one question-pass attention
 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:attn_tc -s 32 -c 1 -o $OUT/attn_$TAG python tools/profile_step.py > /dev/null 2>&1
+    -k regex:"attn_qtm|attn_tc" -s 32 -c 1 -o $OUT/attn_$TAG python tools/profile_step.py > /dev/null 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:"attn_tc|attn_combine" -s 0 -c 2 -o $OUT/attnq_$TAG python tools/profile_step.py > /dev/null 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on \

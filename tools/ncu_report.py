@@ -116,6 +116,9 @@ def main():
                       f"{d.get('sm_pct', '')} | {d.get('regs', '')} |")
             key = d["kernel"].split("<")[0] + "_bytes_per_launch"
             traffic.setdefault(key, []).append(d.get("dram_read", 0) + d.get("dram_write", 0))
+            if d["kernel"].startswith("gemm_tc2_kernel<256, 3>"):  # the gate/up GEMM (bench roofline kernel)
+                traffic.setdefault("gemm_tc2_gateup_bytes_per_launch", []).append(
+                    d.get("dram_read", 0) + d.get("dram_write", 0))
         md.append("")
     js = {k: sum(v) / len(v) for k, v in traffic.items()}
     js["source"] = f"profiles/ncu_{tag}.md (dram__bytes_read.sum + dram__bytes_write.sum per launch, --set full)"
