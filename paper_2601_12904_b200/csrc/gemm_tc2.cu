@@ -45,22 +45,6 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, ui
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar), "r"(x), "r"(y)
       : "memory");
 }
-// weight (B) tiles: each is read by one pair once per M-tile wave and then not
-// again soon -- evict-first, so the activation rows (A, re-read by every N
-// tile) stay in L2 instead of being pushed out by the weight stream
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const void* tmap, uint32_t leader_bar, int x, int y,
-                                                      uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar), "r"(x), "r"(y), "l"(pol)
-      : "memory");
-}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -164,7 +148,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
   if (warp == 0) {
     if (elect_one()) {
       pdl_launch_dependents();
-      const uint64_t pol_b = l2_evict_first_policy();
       // weight (B) loads of the first stages go out before the dependency wait
       int npre = 0;
       if (pair < num_work) {
@@ -179,7 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
             mbar_arrive_expect_tx(&full[i], 2 * C::STAGE_BYTES);
           else
             mbar_arrive_cluster(fb);
-          tma_load_2d_pair_hint(sB + i * C::B_BYTES, &tmB, fb, (kb0 + i) * BK2, n_blk * BN + rank * (BN / 2), pol_b);
+          tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, fb, (kb0 + i) * BK2, n_blk * BN + rank * (BN / 2));
         }
       }
       pdl_wait();
@@ -198,7 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
               mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             else
               mbar_arrive_cluster(fb);
-            tma_load_2d_pair_hint(sB + stage * C::B_BYTES, &tmB, fb, kb * BK2, n_blk * BN + rank * (BN / 2), pol_b);
+            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK2, n_blk * BN + rank * (BN / 2));
           }
           tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK2, m_blk * BM2 + rank * 128);
           if (++stage == STAGES) {
