@@ -96,8 +96,9 @@ def parse():
     p.add_argument("--partition", action="store_true",
                    help="chunk-partitioned store: each chunk's record lives on rank hash(id) mod N only and "
                         "the other ranks read it over NVLink inside K1 (SURVEY.md §8(e))")
-    p.add_argument("--batch", type=int, default=4,
-                   help="also time multi-request batching (frag_reprocess_batch) with this many requests; 0 = skip")
+    p.add_argument("--batch", type=int, default=None,
+                   help="also time multi-request batching (frag_reprocess_batch) with this many requests; 0 = skip "
+                        "(default 8 for the batched corpus config, else 4)")
     p.add_argument("--selftest", action="store_true",
                    help="CPU/gloo check of the multi-rank launcher (no GPU work)")
     p.add_argument("--with-load", action="store_true",
@@ -257,6 +258,8 @@ def run_ours(args, rank, world, local_rank):
 
     w = CONFIGS[args.config]
     ratio = w["ratio"] if args.ratio is None else args.ratio
+    if args.batch is None:
+        args.batch = 8 if w.get("corpus") else 4
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     eng = F.Engine(w["preset"], device=local_rank, seed=args.seed)

@@ -223,7 +223,8 @@ FRAG_API frag_status frag_manifest_validate(const char* manifest_path, int32_t* 
 typedef struct {
   frag_chunk_id id;
   int32_t n_tok, native_start, variant, owner_device;
-  int32_t layers, n_kv_heads, head_dim, reserved;
+  int32_t layers, n_kv_heads, head_dim;
+  int32_t owner_pci;         /* owner GPU: PCI domain << 16 | bus << 8 | device (process-independent) */
   uint64_t kv_bytes;         /* K|V allocation size, 2*L*n_tok*Hkv*dh*2 */
   uint64_t owner_pid;        /* exporting process */
   uint8_t ipc_handle[64];    /* cudaIpcMemHandle_t of the K|V allocation */

@@ -52,7 +52,7 @@ class PeerRecord(C.Structure):
     """frag_peer_record: one exported record (CUDA IPC handle + metadata), 128 bytes."""
     _fields_ = [("id", ChunkId), ("n_tok", C.c_int32), ("native_start", C.c_int32), ("variant", C.c_int32),
                 ("owner_device", C.c_int32), ("layers", C.c_int32), ("n_kv_heads", C.c_int32),
-                ("head_dim", C.c_int32), ("reserved", C.c_int32), ("kv_bytes", C.c_uint64),
+                ("head_dim", C.c_int32), ("owner_pci", C.c_int32), ("kv_bytes", C.c_uint64),
                 ("owner_pid", C.c_uint64), ("ipc_handle", C.c_uint8 * 64)]
 
 

@@ -950,7 +950,12 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   };
   // one query tile per CTA (question pass, decode): split each key tile
   // between the two slots instead of leaving one idle
-  const bool dual = a.M <= AT_ROWS / G;
+  // FRAG_ATTN_QTM_Q=1: the one-tile (question pass / decode) case on the Q-in-TMEM kernel too
+  static const bool qtm_q = [] {
+    const char* v = std::getenv("FRAG_ATTN_QTM_Q");
+    return v && v[0] == '1';
+  }();
+  const bool dual = a.M <= AT_ROWS / G && !qtm_q;
   if (dual) {
     if (a.dh == 128)
       go(attn_tc_kernel<128, 0, true>, (int)AttCfg<128>::SMEM_DUAL);

@@ -285,6 +285,18 @@ void store_attach_peer(Store* local, Store* remote) {
   local->peers.push_back(remote);
 }
 
+namespace {
+// physical identity of a device (PCI domain / bus / device), independent of
+// each process's device numbering (CUDA_VISIBLE_DEVICES may differ per rank)
+int32_t pci_key(int dev) {
+  int dom = 0, bus = 0, slot = 0;
+  check_cuda(cudaDeviceGetAttribute(&dom, cudaDevAttrPciDomainId, dev), "pci domain");
+  check_cuda(cudaDeviceGetAttribute(&bus, cudaDevAttrPciBusId, dev), "pci bus");
+  check_cuda(cudaDeviceGetAttribute(&slot, cudaDevAttrPciDeviceId, dev), "pci device");
+  return (int32_t)(((uint32_t)(dom & 0xFFFF) << 16) | ((uint32_t)(bus & 0xFF) << 8) | (uint32_t)(slot & 0xFF));
+}
+}  // namespace
+
 void store_export(Store* st, const frag_chunk_id& id, frag_peer_record* out) {
   if (!out) fail(FRAG_E_CONTRACT, "null output");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
@@ -307,6 +319,7 @@ void store_export(Store* st, const frag_chunk_id& id, frag_peer_record* out) {
   out->head_dim = st->cfg.head_dim;
   out->kv_bytes = r->kv.bytes;
   out->owner_pid = (uint64_t)getpid();
+  out->owner_pci = pci_key(st->device);  // owner GPU's PCI id (distinct-device imports)
   std::memcpy(out->ipc_handle, &h, sizeof(h));
   r->exported = true;
 }
@@ -330,6 +343,20 @@ void store_import(Store* st, const frag_peer_record& pr, const int32_t* tokens, 
       fail(FRAG_E_STORE, "duplicate chunk record without overwrite (SPEC.md:269)");
   }
   DeviceGuard dg(st->device);
+  if (pr.owner_pci != 0 && pr.owner_pci != pci_key(st->device)) {
+    // the owner is another GPU: K1 reads its pages over NVLink -- it must be
+    // visible to this process and peer-accessible from this store's device
+    int n_dev = 0, owner = -1;
+    check_cuda(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
+    for (int d = 0; d < n_dev && owner < 0; ++d)
+      if (pci_key(d) == pr.owner_pci) owner = d;
+    if (owner < 0) fail(FRAG_E_CUDA, "peer record's GPU is not visible to this process (CUDA_VISIBLE_DEVICES)");
+    int ok = 0;
+    check_cuda(cudaDeviceCanAccessPeer(&ok, st->device, owner), "cudaDeviceCanAccessPeer");
+    if (!ok)
+      fail(FRAG_E_CUDA, "no peer access from device " + std::to_string(st->device) + " to the owner (device " +
+                            std::to_string(owner) + ")");
+  }
   auto rec = std::make_unique<Record>();
   rec->id = pr.id;
   rec->n_tok = n_tok;
