@@ -61,6 +61,79 @@ struct AttCfg {
   static_assert(SMEM <= 232448, "attention tile exceeds the 227 KB shared-memory limit");
 };
 
+// ---------------------------------------------------------------- shared V pages
+// VSH kernels read V in place from the store's records (AttnArgs::vsegs): the
+// TMA warp loads each 128-key V tile from its primary segment's tensor map
+// (rows outside that record arrive as zeros: OOB fill), and one more warp, the
+// patch warp, writes the rows the box cannot supply -- rows of other segments
+// and this request's fresh rows (critical rows from the per-request plan,
+// question / decoded rows by rule) from the exclusive region -- into the
+// swizzled tile, then releases it to the MMA warp (v_ready). The tile the MMA
+// consumes is byte-identical to the private fused-cache tile.
+template <int DH, int NS>
+__device__ __forceinline__ void vpatch_loop(const AttnArgs& a, int hk, int k_lo, int k_hi, int n_tiles, uint8_t* sV,
+                                            uint64_t* v_full, uint64_t* v_ready, int lane) {
+  constexpr int CPR = DH / 8;      // 16-byte chunks per row
+  constexpr int RPI = 32 / CPR;    // rows per warp-wide pass
+  constexpr int RB = 32;           // rows per register batch
+  constexpr int NI = RB / RPI;     // 16-byte loads per lane per batch
+  constexpr uint32_t KV_ATOM = AT_KEYS * 128;
+  constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;
+  const size_t kvc = (size_t)a.Hkv * DH;
+  const int tile0 = k_lo / AT_KEYS;
+  const int sub = lane / CPR, ch = lane % CPR;
+  const int* starts = a.vtile;
+  int e_next = n_tiles > 0 ? __ldg(starts + tile0) : 0;
+  for (int j = 0; j < n_tiles; ++j) {
+    const int st = j % NS;
+    const int e0 = e_next;
+    const int e1 = __ldg(starts + tile0 + j + 1);
+    e_next = e1;
+    const int key0 = k_lo + j * AT_KEYS;
+    const int tr0 = max(key0, a.tail_row0), tr1 = min(key0 + AT_KEYS, k_hi);
+    const int n_ent = e1 - e0;
+    const int n = n_ent + max(0, tr1 - tr0);
+    uint8_t* sv = sV + st * KV_BYTES;
+    for (int b0 = 0; b0 == 0 || b0 < n; b0 += RB) {
+      uint4 d[NI];
+      int rr[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int p = b0 + i * RPI + sub;
+        rr[i] = -1;
+        if (p < n) {
+          const bf16* src;
+          int r;
+          if (p < n_ent) {
+            const unsigned long long ent = __ldg(a.vent + e0 + p);
+            r = (int)(ent & 127);
+            const int seg = (int)((ent >> 8) & 0xffffff);
+            const size_t srow = (size_t)(ent >> 32);
+            src = seg == 0 ? a.vx + srow * kvc
+                           : a.vsegs[seg - 1].v + ((size_t)a.layer * a.vsegs[seg - 1].n + srow) * kvc;
+          } else {
+            const int row = tr0 + (p - n_ent);
+            r = row - key0;
+            src = a.vx + (size_t)(a.tail_slot0 + row - a.tail_row0) * kvc;
+          }
+          d[i] = __ldg(reinterpret_cast<const uint4*>(src + (size_t)hk * DH) + ch);
+          rr[i] = r;
+        }
+      }
+      if (b0 == 0) mbar_wait(&v_full[st], (j / NS) & 1);  // the TMA box has landed: patch over it
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (rr[i] >= 0) {
+          const int r = rr[i];
+          *reinterpret_cast<uint4*>(sv + (ch >> 3) * KV_ATOM + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) = d[i];
+        }
+    }
+    fence_async_smem();  // generic-proxy stores -> visible to the tensor pipe
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&v_ready[st]);
+  }
+}
+
 // POLY: every POLY-th pair of P elements takes the FMA-pipe 2^x (ex2_poly)
 // instead of MUFU.EX2, balancing the two pipes (0 = all MUFU).
 // DUAL (one query tile per CTA: the question pass and decode): the two tile
@@ -71,12 +144,13 @@ struct AttCfg {
 // SPLIT (default for dh=128): two softmax threads per query
 // row (16 softmax warps: warps w and w+4 of a tile share TMEM lanes and take
 // 64 of the 128 keys each, the row max exchanged through shared memory).
-template <int DH, int POLY, bool DUAL = false, bool SPLIT = false>
-__global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
+template <int DH, int POLY, bool DUAL = false, bool SPLIT = false, bool VSH = false>
+__global__ void __launch_bounds__(SPLIT ? 576 : (VSH ? AT_THREADS + 32 : AT_THREADS), 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int G, int n_qblocks) {
   using C = AttCfg<DH>;
   static_assert(!(DUAL && SPLIT), "DUAL and SPLIT are separate variants");
+  static_assert(!VSH || DUAL, "shared V pages: the DUAL (one query tile) variant");
   constexpr int KT = DUAL ? AT_KEYS / 2 : AT_KEYS;  // keys per tile slot per K/V tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -95,7 +169,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
   uint64_t* s_full = bar + 1 + 3 * NS;     // [QT]
   uint64_t* p_full = s_full + AT_QT;       // [QT]
   uint64_t* pv_done = p_full + AT_QT;      // [QT]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + AT_QT);
+  uint64_t* v_ready = pv_done + AT_QT;     // [NS] VSH: V tile patched
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_ready + NS);
 
   const int warp = warp_id(), lane = lane_id();
   // global longest-first order: q-block work grows with its row positions, so
@@ -113,16 +188,20 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
   // warps 0-3 softmax A, 4-7 softmax B, 8 TMA, 9 MMA (the highest warp id wins
   // issue arbitration on its sub-partition, which keeps MMA issue off the
   // softmax critical path)
-  constexpr int W_TMA = SPLIT ? 16 : 8, W_MMA = W_TMA + 1;
+  constexpr int W_TMA = SPLIT ? 16 : 8, W_MMA = W_TMA + 1, W_PATCH = W_TMA + 2;
+  if constexpr (VSH)
+    if (warp == W_TMA)
+      for (int i = lane; i < a.n_vseg; i += 32) tma_prefetch_desc(&a.vsegs[i].tmap);
   if (warp == W_TMA && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
+    if constexpr (!VSH) tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&kv_empty[s], 1);
+      mbar_init(&v_ready[s], 1);
     }
     for (int t = 0; t < AT_QT; ++t) {
       mbar_init(&s_full[t], 1);
@@ -155,8 +234,14 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
         for (int at = 0; at < C::ATOMS; ++at)
           tma_load_3d(sQ + t * C::Q_TILE + at * (AT_ROWS * 128), &tmQ, q_full, at * 64, hk * G,
                       t0 + t * tok_per_tile);
+      const int tile0 = k_lo / AT_KEYS;
+      int2 pr = make_int2(0, 0);  // VSH: this tile's primary V segment + row coordinate
+      if constexpr (VSH) pr = __ldg(a.vprim + tile0);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % NS;
+        int2 pr_next = pr;
+        if constexpr (VSH)
+          if (j + 1 < n_tiles) pr_next = __ldg(a.vprim + tile0 + j + 1);  // in flight across the wait
         mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);  // PV(j-NS) done with this stage
         const int key0 = k_lo + j * AT_KEYS;
         mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
@@ -164,9 +249,17 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
         for (int at = 0; at < C::ATOMS; ++at)
           tma_load_2d(sK + st * C::KV_BYTES + at * C::KV_ATOM, &tmK, &k_full[st], hk * DH + at * 64, key0);
         mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
+        if constexpr (VSH) {
+          const CUtensorMap* tm = &a.vsegs[pr.x].tmap;
 #pragma unroll
-        for (int at = 0; at < C::ATOMS; ++at)
-          tma_load_2d(sV + st * C::KV_BYTES + at * C::KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64, key0);
+          for (int at = 0; at < C::ATOMS; ++at)
+            tma_load_3d(sV + st * C::KV_BYTES + at * C::KV_ATOM, tm, &v_full[st], hk * DH + at * 64, pr.y, a.layer);
+        } else {
+#pragma unroll
+          for (int at = 0; at < C::ATOMS; ++at)
+            tma_load_2d(sV + st * C::KV_BYTES + at * C::KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64, key0);
+        }
+        pr = pr_next;
       }
       // consume the last NS kv_empty phases (no phase completes unobserved)
       for (int j = n_tiles > NS ? n_tiles - NS : 0; j < n_tiles; ++j) mbar_wait(&kv_empty[j % NS], (j / NS) & 1);
@@ -224,12 +317,16 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
       for (int t = 0; t < n_slots; ++t) issue_s(t, 0);
       for (int j = 0; j < n_tiles; ++j) {
         mbar_wait(&v_full[j % NS], (j / NS) & 1);
+        if constexpr (VSH) mbar_wait(&v_ready[j % NS], (j / NS) & 1);
         for (int t = 0; t < n_slots; ++t) {
           issue_pv(t, j);
           if (j + 1 < n_tiles) issue_s(t, j + 1);
         }
       }
     }
+  } else if (VSH && warp == W_PATCH) {
+    // ------------------------------------------------------------ V patch warp (shared V pages)
+    if (n_tiles > 0) vpatch_loop<DH, NS>(a, hk, k_lo, k_hi, n_tiles, sV, v_full, v_ready, lane);
   } else if constexpr (SPLIT) {
     // ------------------------------------------------------------ split-row softmax / epilogue
     __shared__ float xm[AT_QT][2][2][AT_ROWS];  // [tile][iteration parity][half][row] partial max
@@ -558,8 +655,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : AT_THREADS, 1)
 // barrier orders every warp's S load before any P store over those columns).
 // An O rescale (lazy, > 2^8) waits for PV(u-1); otherwise the softmax of
 // slice u never waits on the tensor pipe.
-template <int DH, int PE>
-__global__ void __launch_bounds__(576, 1)
+template <int DH, int PE, bool VSH = false>
+__global__ void __launch_bounds__(VSH ? 608 : 576, 1)
     attn_qtm_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const AttnArgs a, int G, int n_qblocks) {
   constexpr int ATOMS = DH / 64;
@@ -582,7 +679,8 @@ __global__ void __launch_bounds__(576, 1)
   uint64_t* s_full = q_full + 1;        // [2] per S buffer
   uint64_t* p_full = s_full + 2;        // [2]
   uint64_t* pv_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  uint64_t* v_ready = pv_done + 1;      // [NS] VSH: V tile patched
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_ready + NS);
   __shared__ float xm[2][4][AT_ROWS];   // [slice parity][column group][row] partial max
 
   const int warp = warp_id(), lane = lane_id();
@@ -593,14 +691,18 @@ __global__ void __launch_bounds__(576, 1)
   const int t0 = qb * tok_per_tile;
   const int t_end = min(t0 + tok_per_tile, a.M);
   const int k_lo = a.n_splits > 1 ? split * a.split_keys : 0;
-  constexpr int W_TMA = 16, W_MMA = 17;
+  constexpr int W_TMA = 16, W_MMA = 17, W_PATCH = 18;
+  if constexpr (VSH)
+    if (warp == W_TMA)
+      for (int i = lane; i < a.n_vseg; i += 32) tma_prefetch_desc(&a.vsegs[i].tmap);
   if (warp == W_TMA && lane == 0) {
     tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
+    if constexpr (!VSH) tma_prefetch_desc(&tmV);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&kv_empty[s], 1);
+      mbar_init(&v_ready[s], 1);
     }
     mbar_init(q_full, 16);
     for (int b = 0; b < 2; ++b) {
@@ -624,8 +726,14 @@ __global__ void __launch_bounds__(576, 1)
 
   if (warp == W_TMA) {
     if (n_tiles > 0 && elect_one()) {
+      const int tile0 = k_lo / AT_KEYS;
+      int2 pr = make_int2(0, 0);  // VSH: this tile's primary V segment + row coordinate
+      if constexpr (VSH) pr = __ldg(a.vprim + tile0);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % NS;
+        int2 pr_next = pr;
+        if constexpr (VSH)
+          if (j + 1 < n_tiles) pr_next = __ldg(a.vprim + tile0 + j + 1);  // in flight across the wait
         mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
         const int key0 = k_lo + j * AT_KEYS;
         mbar_arrive_expect_tx(&k_full[st], KV_BYTES);
@@ -633,9 +741,17 @@ __global__ void __launch_bounds__(576, 1)
         for (int at = 0; at < ATOMS; ++at)
           tma_load_2d(sK + st * KV_BYTES + at * KV_ATOM, &tmK, &k_full[st], hk * DH + at * 64, key0);
         mbar_arrive_expect_tx(&v_full[st], KV_BYTES);
+        if constexpr (VSH) {
+          const CUtensorMap* tm = &a.vsegs[pr.x].tmap;
 #pragma unroll
-        for (int at = 0; at < ATOMS; ++at)
-          tma_load_2d(sV + st * KV_BYTES + at * KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64, key0);
+          for (int at = 0; at < ATOMS; ++at)
+            tma_load_3d(sV + st * KV_BYTES + at * KV_ATOM, tm, &v_full[st], hk * DH + at * 64, pr.y, a.layer);
+        } else {
+#pragma unroll
+          for (int at = 0; at < ATOMS; ++at)
+            tma_load_2d(sV + st * KV_BYTES + at * KV_ATOM, &tmV, &v_full[st], hk * DH + at * 64, key0);
+        }
+        pr = pr_next;
       }
       for (int j = n_tiles > NS ? n_tiles - NS : 0; j < n_tiles; ++j) mbar_wait(&kv_empty[j % NS], (j / NS) & 1);
     }
@@ -670,6 +786,7 @@ __global__ void __launch_bounds__(576, 1)
         const int st = u % NS;
         mbar_wait(&p_full[u & 1], (u >> 1) & 1);
         mbar_wait(&v_full[st], (u / NS) & 1);
+        if constexpr (VSH) mbar_wait(&v_ready[st], (u / NS) & 1);
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && u < 256) a.trace[u * 4 + 3] = clock64();
         if (elect_one()) {
@@ -694,6 +811,9 @@ __global__ void __launch_bounds__(576, 1)
         if (u + 2 < n_tiles) issue_s(u + 2);
       }
     }
+  } else if (VSH && warp == W_PATCH) {
+    // ------------------------------------------------------------ V patch warp (shared V pages)
+    if (n_tiles > 0) vpatch_loop<DH, NS>(a, hk, k_lo, k_hi, n_tiles, sV, v_full, v_ready, lane);
   } else {
     // ------------------------------------------------------------ softmax / epilogue (16 warps)
     const int q4 = warp & 3, cg = warp >> 2;
@@ -904,13 +1024,32 @@ static_assert(qtm_smem<128>() <= 232448 - 4 * 1024 && qtm_smem<64>() <= 232448 -
 
 int attn_rows_per_cta() { return AT_ROWS * AT_QT; }
 
+// The shared-V kernels are the default ones (Q-in-TMEM sparse pass, DUAL
+// question pass / decode) with MUFU-only or the default FMA split; the r01
+// tuning switches keep the private fused V.
+bool attn_shared_v_supported(int dh) {
+  if (dh != 64 && dh != 128) return false;
+  const char* q = std::getenv("FRAG_ATTN_QTM");
+  const char* qq = std::getenv("FRAG_ATTN_QTM_Q");
+  const char* p = std::getenv("FRAG_ATTN_POLY");
+  const char* qp = std::getenv("FRAG_ATTN_QTM_POLY");
+  return !(q && q[0] == '0') && !(qq && qq[0] == '1') && !(p && std::atoi(p) != 0) &&
+         !(qp && std::atoi(qp) != kQtmPoly);
+}
+
 int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream) {
   CUtensorMap tq, tk, tv;
   // Q [M][Hq][dh] viewed as (dh, Hq, M); box (64, G, 128/G)
   if (!make_tmap_3d(&tq, a.q, a.dh, a.Hq, a.M, a.dh, (uint64_t)a.Hq * a.dh, 64, G, AT_ROWS / G)) return -1;
   // K/V layer [T][Hkv*dh]; box (64, 128 keys)
   if (!make_tmap_2d(&tk, a.k, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
-  if (!make_tmap_2d(&tv, a.v, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
+  const bool vsh = a.vsegs != nullptr;  // shared V pages: V comes from the segments' maps
+  if (vsh && (!attn_shared_v_supported(a.dh) || a.n_vseg < 1 || (a.n_splits > 1 && a.split_keys % AT_KEYS)))
+    return -1;
+  if (vsh)
+    tv = tk;  // unused by the VSH kernels
+  else if (!make_tmap_2d(&tv, a.v, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS))
+    return -1;
   dim3 grid(n_qblocks * a.Hkv, 1, a.n_splits);
   // FRAG_ATTN_POLY: tuning knob for the MUFU/FMA exp split (default below)
   static const int poly = [] {
@@ -956,6 +1095,14 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
     return v && v[0] == '1';
   }();
   const bool dual = a.M <= AT_ROWS / G && !qtm_q;
+  if (dual && vsh) {
+    threads = AT_THREADS + 32;  // + the V patch warp
+    if (a.dh == 128)
+      go(attn_tc_kernel<128, 0, true, false, true>, (int)AttCfg<128>::SMEM_DUAL);
+    else
+      go(attn_tc_kernel<64, 0, true, false, true>, (int)AttCfg<64>::SMEM_DUAL);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+  }
   if (dual) {
     if (a.dh == 128)
       go(attn_tc_kernel<128, 0, true>, (int)AttCfg<128>::SMEM_DUAL);
@@ -975,7 +1122,7 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
     const dim3 grid1(nqb1 * a.Hkv, 1, a.n_splits);
     auto go2 = [&](auto kern, int smem) {
       smem_attr_once(kern, smem);
-      launch_pdl(kern, grid1, dim3(576), smem, stream, tk, tv, at, G, nqb1);
+      launch_pdl(kern, grid1, dim3(vsh ? 608 : 576), smem, stream, tk, tv, at, G, nqb1);
       if (trace_path) {
         unsigned long long h[2 * 256 * 4];
         cudaMemcpyAsync(h, trace_dev, sizeof(h), cudaMemcpyDeviceToHost, stream);
@@ -991,6 +1138,13 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
       const char* v = std::getenv("FRAG_ATTN_QTM_POLY");
       return v ? std::atoi(v) : kQtmPoly;
     }();
+    if (vsh) {
+      if (a.dh == 128)
+        go2(attn_qtm_kernel<128, kQtmPoly, true>, (int)qtm_smem<128>());
+      else
+        go2(attn_qtm_kernel<64, kQtmPoly, true>, (int)qtm_smem<64>());
+      return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    }
     if (a.dh == 128) {
       switch (qpoly) {
         case 0: go2(attn_qtm_kernel<128, 0>, (int)qtm_smem<128>()); break;

@@ -154,6 +154,12 @@ struct Scoped {
   }
 };
 
+// split-K / stream-K tile counters: the last 2 * CHAIN_MAX_OPS ints of
+// gemm_cnt are the GEMM chain's done / exit counters and never handed out
+inline int gemm_counter_cap(const Result* r) {
+  return (int)(r->gemm_cnt.bytes / sizeof(int)) - 2 * fragk::CHAIN_MAX_OPS;
+}
+
 inline void peek(const char* what) {
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
@@ -380,7 +386,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     ep.ws = r->gemm_ws.as<float>();
     ep.ws_bytes = r->gemm_ws.bytes;
     ep.counters = r->gemm_cnt.as<int>();
-    ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
+    ep.counters_cap = gemm_counter_cap(r);
   };
 
   // one sequence unless batched (segments of plan rows, each over its own
@@ -1241,7 +1247,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
       ep.ws = r->gemm_ws.as<float>();
       ep.ws_bytes = r->gemm_ws.bytes;
       ep.counters = r->gemm_cnt.as<int>();
-      ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
+      ep.counters_cap = gemm_counter_cap(r);
       ep.out_f32 = r->logits.as<float>();
       ep.ldo = c.vocab;
       Scoped sc(e->prof, bs, gemm_class(r->logit_rows), 2.0 * r->logit_rows * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
@@ -1435,7 +1441,7 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
       ep.ws = r->gemm_ws.as<float>();
       ep.ws_bytes = r->gemm_ws.bytes;
       ep.counters = r->gemm_cnt.as<int>();
-      ep.counters_cap = (int)(r->gemm_cnt.bytes / sizeof(int));
+      ep.counters_cap = gemm_counter_cap(r);
       ep.out_f32 = r->logits.as<float>();
       ep.ldo = c.vocab;
       Scoped sc(e->prof, s, gemm_class(B), 2.0 * B * (double)c.vocab * d, 2.0 * c.vocab * (double)d);
@@ -1445,11 +1451,10 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
     ev_record(r, timing, 5, s);
     logits_d2h(r, s);
   };
-  uint64_t sig = 0xcbf29ce484222325ULL;  // batch shape: every request's (T, S, N, |Q|, k)
-  for (const auto& q : br)
-    for (int v : {q.T, q.S, q.N, q.nq, q.k}) sig = (sig ^ (uint64_t)(uint32_t)v) * 0x100000001b3ULL;
   GraphKey key{B * slot, -2 - B, Ntot, Qtot, Mtot - Qtot, 0, 0, (int)raw, (int)r->logits_on_device, sp.n_desc,
-               sp.max_rows, (int)(sig & 0x7fffffff), (uint64_t)(uintptr_t)e->rope.p ^ (sig << 1)};
+               sp.max_rows, 0, (uint64_t)(uintptr_t)e->rope.p};
+  for (const auto& q : br)  // batch shape: every request's exact (T, S, N, |Q|, k)
+    key.shapes.insert(key.shapes.end(), {q.T, q.S, q.N, q.nq, q.k});
   run_graphed(r, s, !timing && !e->prof.on, key, body);
   // per-request critical positions (host copies for frag_result_batch_crit)
   std::vector<int32_t> plan_h((size_t)Mtot);

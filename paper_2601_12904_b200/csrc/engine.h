@@ -201,10 +201,12 @@ std::recursive_mutex& device_mutex(int device);
 struct GraphKey {
   int T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows, selector;
   uint64_t rope;
+  std::vector<int> shapes = {};  // batched reprocess: per-request (T, S, N, |Q|, k), exact
   bool operator<(const GraphKey& o) const {
-    return std::tie(T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows, selector, rope) <
+    return std::tie(T, S, N, nq, k, inject, all_logits, raw, logits_on_device, n_desc, max_rows, selector, rope,
+                    shapes) <
            std::tie(o.T, o.S, o.N, o.nq, o.k, o.inject, o.all_logits, o.raw, o.logits_on_device, o.n_desc,
-                    o.max_rows, o.selector, o.rope);
+                    o.max_rows, o.selector, o.rope, o.shapes);
   }
 };
 struct GraphEntry {

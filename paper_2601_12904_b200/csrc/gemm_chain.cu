@@ -506,15 +506,18 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
   args.timeline = timeline ? 1 : 0;
   auto go = [&](auto kern, size_t smem) {
     smem_attr_once(kern, (int)smem);
+    if (resident_blocks(kern, CHAIN_THREADS, (int)smem) < 1) return false;  // one CTA per SM must fit
     launch_pdl(kern, dim3((unsigned)sms), dim3(CHAIN_THREADS), smem, stream, args);
+    return true;
   };
+  bool ok;
   if (M <= 32)
-    go(gemm_chain_kernel<32>, ChainCfg<32>::SMEM);
+    ok = go(gemm_chain_kernel<32>, ChainCfg<32>::SMEM);
   else if (M <= 64)
-    go(gemm_chain_kernel<64>, ChainCfg<64>::SMEM);
+    ok = go(gemm_chain_kernel<64>, ChainCfg<64>::SMEM);
   else
-    go(gemm_chain_kernel<128>, ChainCfg<128>::SMEM);
-  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    ok = go(gemm_chain_kernel<128>, ChainCfg<128>::SMEM);
+  return ok && cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace fragk

@@ -152,7 +152,8 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
     } else if (col < q_cols + k_cols) {
       dstp = ep.k_cache + (size_t)prow * k_cols + (col - q_cols);
     } else {
-      dstp = ep.v_cache + (size_t)prow * k_cols + (col - q_cols - k_cols);
+      const int vrow = !ep.v_slots ? prow : (prow >= ep.v_tail_row0 ? ep.v_tail_slot0 + (prow - ep.v_tail_row0) : row);
+      dstp = ep.v_cache + (size_t)vrow * k_cols + (col - q_cols - k_cols);
     }
     uint4* dst = reinterpret_cast<uint4*>(dstp);
 #pragma unroll

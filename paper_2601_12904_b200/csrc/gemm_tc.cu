@@ -22,7 +22,9 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <unordered_map>
 
 #include "gemm_epi.cuh"
@@ -390,6 +392,10 @@ int launch(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& e
   const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int slots = num_sms() * C::MIN_BLOCKS;
   const int grid = ep.streamk ? ep.streamk : (work < slots ? work : slots);
+  // split-K fixups / stream-K partial hand-offs wait on other CTAs of the grid
+  if ((ep.splits > 1 || ep.streamk) &&
+      grid > num_sms() * resident_blocks(gemm_tc_kernel<BN, EPI, AR>, GEMM_THREADS, (int)C::SMEM))
+    return -1;
   // FRAG_GEMM_TRACE=<file>: tooling only (tools/gemm_trace.py) -- per-CTA
   // globaltimer stamps [start, after PDL wait, first stage, last MMA,
   // accumulator ready, partial written, end] appended after the launch
@@ -440,6 +446,18 @@ bool smem_attr_needed(const void* fn, int dev) {
   if (m & bit) return false;
   m |= bit;
   return true;
+}
+
+int resident_blocks_cached(const void* fn, int dev, int threads, int smem, int (*calc)(const void*, int, int)) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int>, int> done;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_tuple(fn, dev, threads, smem);
+  auto it = done.find(key);
+  if (it != done.end()) return it->second;
+  const int n = calc(fn, threads, smem);
+  done[key] = n;
+  return n;
 }
 
 int num_sms() {

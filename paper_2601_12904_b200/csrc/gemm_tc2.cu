@@ -311,6 +311,8 @@ int launch2(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& 
   const int work = ep.splits > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.splits : tiles;
   const int pairs = num_sms() / 2;
   const int grid = 2 * (work < pairs ? work : pairs);
+  if (ep.splits > 1 && grid > num_sms() * resident_blocks(gemm_tc2_kernel<BN, EPI>, GEMM2_THREADS, (int)C::SMEM))
+    return -1;  // the tail split's fixup waits on other CTAs of the grid
   launch_pdl(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(GEMM2_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }

@@ -35,7 +35,11 @@ struct EpiParams {
   bf16* q_out = nullptr;           // [M][Hq][dh]
   float* q_out_f32 = nullptr;      // optional fp32 copy (question pass, final layer)
   bf16* k_cache = nullptr;         // layer base, [T][Hkv][dh]
-  bf16* v_cache = nullptr;
+  bf16* v_cache = nullptr;         // layer base: [T] rows, or the exclusive slots (v_slots)
+  // shared V pages: fresh V goes to exclusive slot = row (GEMM row), or for a
+  // position row >= v_tail_row0: v_tail_slot0 + prow - v_tail_row0
+  int v_slots = 0;
+  int v_tail_row0 = 0x7fffffff, v_tail_slot0 = 0;
   int Hq = 0, Hkv = 0, dh = 0;
   // split-K workspace for small-M GEMMs (owned by the caller's result; the
   // counters must start at zero and are left at zero by the kernel)
@@ -140,6 +144,48 @@ void embed_rmsnorm(const bf16* E, const int* tok, int M, int d, const bf16* gain
 void rmsnorm(const float* h, int M, int d, const bf16* gain, float eps, bf16* x, cudaStream_t stream,
              const int* row_map = nullptr);
 
+// ------------------------------------------------------------------ shared V pages
+// A request's V rows are read in place from the store's records (shared
+// pages, never copied: SPEC.md:148-150); only the rows
+// computed for this request (critical + question + decoded tokens) live in its
+// exclusive V region, slot-indexed. One VSeg per statically placed source
+// (KV_S, each chunk record), sorted by first cache row (sequence-local).
+struct alignas(64) VSeg {
+  CUtensorMap tmap;  // V [L][n][Hkv*dh] as (Hkv*dh, n, L), box (64, 128, 1), SW128
+  const bf16* v;     // V base (layer 0, row 0)
+  int row0;          // first sequence-local cache row
+  int n;             // rows
+  int pad[12];
+};
+static_assert(sizeof(VSeg) == 192, "VSeg layout");
+// Per-sequence patch plan over 128-row key tiles (sequence-local rows): tile
+// j's TMA box comes from its primary segment vprim[j] = (segment, row
+// coordinate) -- the segment holding row 128j; none: segment 0 at a row past
+// its end, i.e. an all-zero box -- and its entries vent[vtile[j] ..
+// vtile[j+1]) are the rows that box does not supply: rows of other segments
+// and fresh critical rows, in row order. Rows >= tail_row0 (question rows,
+// decoded tokens) are fresh by rule (slot = tail_slot0 + row - tail_row0) and
+// never planned. entry = row_in_tile | (seg + 1) << 8 (0: exclusive slot) | src_row << 32
+struct VPlanArgs {
+  const VSeg* segs;
+  int n_seg;
+  const int* crit;     // ascending critical rows (n_crit), cache rows = local + row_base
+  int n_crit;
+  int row_base;
+  int crit_slot0;      // exclusive slot of crit[0]
+  int tail_row0;       // sequence-local; rows >= tail_row0 are fresh by rule
+  int n_rows;          // rows covered (tiles = ceil(n_rows / 128))
+  int* vtile;          // [tiles + 1]
+  int2* vprim;         // [tiles]
+  unsigned long long* vent;  // [n_rows]
+};
+int vpatch_plan(const VPlanArgs* seqs_dev, int n_seq, int max_rows, int max_segs, cudaStream_t stream);
+// Materialise V rows [0, n_rows) of every layer into dst [L][ld][Hkv*dh] from
+// the segments + exclusive region (result read-back: frag_result_fused_kv)
+int vpage_gather(const VSeg* segs, const int* vtile, const int2* vprim, const unsigned long long* vent,
+                 const bf16* vx, size_t vx_layer_stride, int tail_row0, int tail_slot0, int n_rows, int L, int kvc,
+                 bf16* dst, size_t dst_layer_stride, cudaStream_t stream);
+
 // ------------------------------------------------------------------ K6
 struct AttnArgs {
   const bf16* q;         // [M][Hq][dh]
@@ -155,12 +201,23 @@ struct AttnArgs {
   int n_splits;
   float scale;           // 1/sqrt(dh)
   unsigned long long* trace = nullptr;  // tooling: clock64 timeline of CTA 0 (FRAG_ATTN_TRACE)
+  // shared V pages (vsegs != nullptr; `v` unused): V tiles come from the
+  // segments' tensor maps, patched from the plan and the exclusive region
+  const VSeg* vsegs = nullptr;
+  int n_vseg = 0;
+  const int* vtile = nullptr;  // this sequence's plan: entry starts [tiles + 1] (tile 0 = sequence row 0)
+  const int2* vprim = nullptr; // [tiles] (primary segment, TMA row coordinate)
+  const unsigned long long* vent = nullptr;
+  const bf16* vx = nullptr;    // exclusive V of this layer: [slot][Hkv][dh]
+  int layer = 0;
+  int tail_row0 = 0x7fffffff, tail_slot0 = 0;
 };
 // returns launches; with combine_deferred != nullptr a split-KV launch leaves
 // the combine to the caller (*combine_deferred = true)
 int sparse_q_attention(const AttnArgs& a, cudaStream_t stream, bool* combine_deferred = nullptr);
 int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream);
 int attn_rows_per_cta();
+bool attn_shared_v_supported(int dh);  // the attention kernels in use read shared V pages
 
 // ------------------------------------------------------------------ K9/K10
 struct ScoreArgs {
@@ -251,5 +308,28 @@ inline void smem_attr_once(Kernel* fn, int bytes) {
   cudaGetDevice(&dev);
   if (!smem_attr_needed(reinterpret_cast<const void*>(fn), dev)) return;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// Co-residency check for the persistent kernels whose CTAs wait on each other
+// (split-K fixups, the GEMM chain): CTAs of `fn` that fit on one SM with this
+// block size and shared memory, from the occupancy calculator, cached per
+// (kernel, device). A grid larger than blocks x SMs could never be resident
+// at once, so the launcher refuses it (FRAG_E_CUDA) instead of launching a
+// grid whose waits could only end at the spin limit.
+int resident_blocks_cached(const void* fn, int dev, int threads, int smem, int (*calc)(const void*, int, int));
+template <class Kernel>
+inline int resident_blocks(Kernel* fn, int threads, int smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return resident_blocks_cached(reinterpret_cast<const void*>(fn), dev, threads, smem,
+                                [](const void* f, int t, int b) {
+                                  int n = 0;
+                                  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, (Kernel*)f, t, (size_t)b) !=
+                                      cudaSuccess) {
+                                    cudaGetLastError();
+                                    return 0;
+                                  }
+                                  return n;
+                                });
 }
 }  // namespace fragk

@@ -38,10 +38,14 @@ __device__ __forceinline__ uint32_t rot_pair(uint32_t kv, float2 cs) {
 // Per layer the record block [n][Hkv][dh] and its fused destination
 // [dst_row : dst_row+n][Hkv][dh] are both contiguous, so all accesses are
 // fully coalesced 128-bit streams.
+// KV = false (shared V pages): only K is rotated into the fused cache, V stays
+// in the records; 4 independent 16-byte loads per thread either way.
+template <bool KV>
 __global__ void __launch_bounds__(256) rope_shift_kernel(const StitchChunk* __restrict__ chunks,
                                                          const float2* __restrict__ tables, bf16* __restrict__ kf,
                                                          bf16* __restrict__ vf, int L, int T, int Hkv, int dh,
                                                          int layer0) {
+  constexpr int U = KV ? 2 : 4;  // rows of K (and V) per unrolled step
   const StitchChunk c = chunks[blockIdx.y];
   const int vec_per_row = (Hkv * dh) >> 3;  // 16-byte vectors per token row
   const long per_layer = (long)c.n_tok * vec_per_row;
@@ -55,44 +59,40 @@ __global__ void __launch_bounds__(256) rope_shift_kernel(const StitchChunk* __re
   uint4* kd = reinterpret_cast<uint4*>(kf);
   uint4* vd = reinterpret_cast<uint4*>(vf);
   const long stride = (long)gridDim.x * blockDim.x;
-  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  // 2-way unrolled so each thread keeps 4 independent 16-byte loads in flight.
-  for (; i + stride < total; i += 2 * stride) {
-    const long i1 = i + stride;
-    uint4 k0 = ld_stream(ks + i), v0 = ld_stream(vs + i);
-    uint4 k1 = ld_stream(ks + i1), v1 = ld_stream(vs + i1);
-    const long l0 = i / per_layer, r0 = i - l0 * per_layer;
-    const long l1 = i1 / per_layer, r1 = i1 - l1 * per_layer;
+  auto rot = [&](uint4& k, long r) {
     if (tab) {
-      const int p0 = (int)(r0 % dvec) * 4, p1 = (int)(r1 % dvec) * 4;
-      k0.x = rot_pair(k0.x, tab[p0]);
-      k0.y = rot_pair(k0.y, tab[p0 + 1]);
-      k0.z = rot_pair(k0.z, tab[p0 + 2]);
-      k0.w = rot_pair(k0.w, tab[p0 + 3]);
-      k1.x = rot_pair(k1.x, tab[p1]);
-      k1.y = rot_pair(k1.y, tab[p1 + 1]);
-      k1.z = rot_pair(k1.z, tab[p1 + 2]);
-      k1.w = rot_pair(k1.w, tab[p1 + 3]);
+      const int p = (int)(r % dvec) * 4;
+      k.x = rot_pair(k.x, tab[p]);
+      k.y = rot_pair(k.y, tab[p + 1]);
+      k.z = rot_pair(k.z, tab[p + 2]);
+      k.w = rot_pair(k.w, tab[p + 3]);
     }
-    const long o0 = l0 * layer_stride_dst + dst0 + r0, o1 = l1 * layer_stride_dst + dst0 + r1;
-    st_stream(kd + o0, k0);
-    st_stream(vd + o0, v0);
-    st_stream(kd + o1, k1);
-    st_stream(vd + o1, v1);
+  };
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < total; i += U * stride) {
+    uint4 k[U], v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      k[u] = ld_stream(ks + i + u * stride);
+      if constexpr (KV) v[u] = ld_stream(vs + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long iu = i + u * stride;
+      const long l = iu / per_layer, r = iu - l * per_layer;
+      rot(k[u], r);
+      const long o = l * layer_stride_dst + dst0 + r;
+      st_stream(kd + o, k[u]);
+      if constexpr (KV) st_stream(vd + o, v[u]);
+    }
   }
   for (; i < total; i += stride) {
-    uint4 k0 = ld_stream(ks + i), v0 = ld_stream(vs + i);
+    uint4 k0 = ld_stream(ks + i);
     const long l0 = i / per_layer, r0 = i - l0 * per_layer;
-    if (tab) {
-      const int p0 = (int)(r0 % dvec) * 4;
-      k0.x = rot_pair(k0.x, tab[p0]);
-      k0.y = rot_pair(k0.y, tab[p0 + 1]);
-      k0.z = rot_pair(k0.z, tab[p0 + 2]);
-      k0.w = rot_pair(k0.w, tab[p0 + 3]);
-    }
+    rot(k0, r0);
     const long o0 = l0 * layer_stride_dst + dst0 + r0;
     st_stream(kd + o0, k0);
-    st_stream(vd + o0, v0);
+    if constexpr (KV) st_stream(vd + o0, ld_stream(vs + i));
   }
 }
 
@@ -229,7 +229,10 @@ void rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_ro
   if (bx > cap) bx = cap;
   if (bx < 1) bx = 1;
   dim3 grid((unsigned)bx, (unsigned)n_chunks);
-  rope_shift_kernel<<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, L, T, Hkv, dh, layer0);
+  if (v_fused)
+    rope_shift_kernel<true><<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, L, T, Hkv, dh, layer0);
+  else  // shared V pages: K only
+    rope_shift_kernel<false><<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, L, T, Hkv, dh, layer0);
 }
 
 void embed_rmsnorm(const bf16* E, const int* tok, int M, int d, const bf16* gain, float eps, float* h, bf16* x,
