@@ -353,7 +353,11 @@ FRAG_API frag_status frag_kv_deviation(frag_engine* eng, frag_store* st, const i
 FRAG_API frag_status frag_decode(frag_engine* eng, frag_result* res, int32_t max_new_tokens, void* stream,
                                  int32_t* tokens_out);
 FRAG_API frag_status frag_result_sync(frag_result* res);
-/* Fused cache: device pointers [L][T][Hkv][dh] bf16, T = tokens in the prompt. */
+/* Fused cache: device pointers [L][max_tokens][Hkv][dh] bf16 (rows [0, T) valid,
+ * T = tokens in the prompt, plus decoded tokens). With shared V pages (the
+ * default for query-guided requests) V is read in place from the records and
+ * the request's exclusive slots; asking for v_dev assembles that view into the
+ * result's V buffer (synchronous, after the request's stream work). */
 FRAG_API frag_status frag_result_fused_kv(const frag_result* res, const void** k_dev, const void** v_dev,
                                           int32_t* n_tokens);
 /* Logits fp32 [rows][V]; host pointer (or device pointer with logits_on_device). */
@@ -388,6 +392,15 @@ FRAG_API frag_status frag_engine_profile_read(frag_engine* eng, int32_t klass, d
  * default FRAG_SPIN_LIMIT_MS or 2000 ms; ms <= 0 restores the default.
  * Returns the previous limit in ms. */
 FRAG_API double frag_set_spin_limit_ms(double ms);
+/* Shared V pages: on (default, FRAG_SHARED_V=0 turns it
+ * off) query-guided requests read their chunks' V rows in place from the
+ * records and keep only their fresh rows in exclusive slots; off: every request
+ * copies V into a private fused cache (the layout of frag_full_prefill).
+ * on = 1 / 0 sets, -1 only queries; returns the previous setting. Process wide. */
+FRAG_API int32_t frag_set_shared_v(int32_t on);
+/* Device memory held by a result (fused K, V view or exclusive V slots, plans
+ * and workspaces) and whether its last request used shared V pages. */
+FRAG_API frag_status frag_result_memory(const frag_result* res, uint64_t* device_bytes, int32_t* shared_v);
 
 /* ------------------------------------------------------------------ kernels
  * Kernel-level entry points over device pointers (parity tests, bench roofline). */

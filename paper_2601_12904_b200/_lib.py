@@ -95,6 +95,8 @@ _SIGS = {
     "frag_hash_tokens": (None, [_I32P, C.c_int32, C.c_uint64, C.POINTER(ChunkId)]),
     "frag_launch_count": (C.c_uint64, []),
     "frag_set_spin_limit_ms": (C.c_double, [C.c_double]),
+    "frag_set_shared_v": (C.c_int32, [C.c_int32]),
+    "frag_result_memory": (C.c_int, [_P, C.POINTER(C.c_uint64), _I32P]),
     "frag_memcpy": (C.c_int, [_P, _P, C.c_size_t]),
     "frag_engine_create": (C.c_int, [C.POINTER(ModelCfg), C.c_int, C.c_uint64, C.POINTER(_P)]),
     "frag_engine_destroy": (C.c_int, [_P]),

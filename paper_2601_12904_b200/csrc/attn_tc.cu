@@ -75,7 +75,7 @@ __device__ __forceinline__ void vpatch_loop(const AttnArgs& a, int hk, int k_lo,
                                             uint64_t* v_full, uint64_t* v_ready, int lane) {
   constexpr int CPR = DH / 8;      // 16-byte chunks per row
   constexpr int RPI = 32 / CPR;    // rows per warp-wide pass
-  constexpr int RB = 32;           // rows per register batch
+  constexpr int RB = DH == 128 ? 24 : 32;  // rows per register batch (608-thread kernel: <= 96 regs)
   constexpr int NI = RB / RPI;     // 16-byte loads per lane per batch
   constexpr uint32_t KV_ATOM = AT_KEYS * 128;
   constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;

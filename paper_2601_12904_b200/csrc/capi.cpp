@@ -118,6 +118,21 @@ FRAG_API double frag_set_spin_limit_ms(double ms) {
   return prev;
 }
 
+FRAG_API int32_t frag_set_shared_v(int32_t on) {
+  const int32_t prev = fragimpl::set_shared_v(on);
+  if (on >= 0 && on != prev) fragimpl::g_alloc_epoch++;  // request graphs captured the other layout
+  return prev;
+}
+
+FRAG_API frag_status frag_result_memory(const frag_result* res, uint64_t* device_bytes, int32_t* shared_v) {
+  return guard([&] {
+    need(res, "null result");
+    const Result* r = res->r;
+    if (device_bytes) *device_bytes = result_device_bytes(r);
+    if (shared_v) *shared_v = r->vshared ? 1 : 0;
+  });
+}
+
 FRAG_API frag_status frag_memcpy(void* dst, const void* src, size_t bytes) {
   return guard([&] {
     need(dst && src, "null argument");
@@ -529,7 +544,15 @@ FRAG_API frag_status frag_result_fused_kv(const frag_result* res, const void** k
   return guard([&] {
     need(res, "null result");
     if (k_dev) *k_dev = res->r->k_fused.p;
-    if (v_dev) *v_dev = res->r->v_fused.p;
+    if (v_dev) {
+      // shared V pages: the request's V view is assembled from its records and
+      // exclusive slots on demand (stream-ordered after the request, synchronous)
+      Result* r = res->r;
+      DeviceGuard dg(r->eng->device);
+      std::lock_guard<std::recursive_mutex> gpu_lock(device_mutex(r->eng->device));
+      materialize_v(r, r->last_stream);
+      *v_dev = r->v_fused.p;
+    }
     if (n_tokens) *n_tokens = res->r->T;
   });
 }

@@ -320,8 +320,7 @@ void result_init(Result* r, Engine* e, int max_tokens) {
   r->max_tokens = max_tokens;
   const size_t kvc = (size_t)c.n_kv_heads * c.head_dim, qc = (size_t)c.n_heads * c.head_dim;
   const size_t M = max_tokens;
-  r->k_fused.alloc((size_t)c.layers * M * kvc * sizeof(bf16));
-  r->v_fused.alloc((size_t)c.layers * M * kvc * sizeof(bf16));
+  r->k_fused.alloc((size_t)c.layers * M * kvc * sizeof(bf16));  // V: use_private_v / shared pages
   r->h.alloc(M * c.d_model * sizeof(float));
   r->x.alloc(M * std::max<size_t>(c.d_model, qc) * sizeof(bf16));
   r->q.alloc(M * qc * sizeof(bf16));
@@ -342,6 +341,66 @@ void result_init(Result* r, Engine* e, int max_tokens) {
   e->ensure_rope(max_tokens);
 }
 
+// FRAG_SHARED_V=0 keeps every request's V private (the r01 layout).
+std::atomic<int> g_shared_v{-1};  // -1: not read from the environment yet
+bool shared_v_enabled() {
+  int v = g_shared_v.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* ev = std::getenv("FRAG_SHARED_V");
+    int want = (ev && ev[0] == '0') ? 0 : 1;
+    g_shared_v.compare_exchange_strong(v, want);
+    v = g_shared_v.load(std::memory_order_relaxed);
+  }
+  return v != 0;
+}
+
+int set_shared_v(int on) {
+  const int prev = shared_v_enabled() ? 1 : 0;
+  if (on >= 0) g_shared_v.store(on ? 1 : 0);
+  return prev;
+}
+
+uint64_t result_device_bytes(const Result* r) {
+  uint64_t b = 0;
+  for (const DevBuf* d : {&r->k_fused, &r->v_fused, &r->h, &r->x, &r->q, &r->attn, &r->act, &r->plan_rows,
+                          &r->plan_tok, &r->chunk_tok, &r->q_tok, &r->q_final, &r->scores, &r->part_ms, &r->row_ms,
+                          &r->part_o, &r->part_lse, &r->logits, &r->row_map, &r->stitch_desc, &r->stitch_tab,
+                          &r->lm_x, &r->gemm_ws, &r->gemm_cnt, &r->dec_tok, &r->fr_save, &r->dev, &r->score_col,
+                          &r->score_q, &r->ssq, &r->vx, &r->vseg, &r->vplan_args, &r->vplan_tile, &r->vplan_prim,
+                          &r->vplan_ent})
+    b += d->bytes;
+  return b;
+}
+
+void use_private_v(Result* r) {
+  const auto& c = r->eng->cfg;
+  r->vshared = false;
+  r->v_materialized = false;
+  r->vrefs.clear();
+  r->vseq.clear();
+  r->v_tail_row0 = 0x7fffffff;
+  r->v_tail_slot0 = 0;
+  r->v_fused.ensure((size_t)c.layers * r->max_tokens * c.n_kv_heads * c.head_dim * sizeof(bf16));
+}
+
+void materialize_v(Result* r, cudaStream_t s) {
+  if (!r->vshared || r->v_materialized) return;
+  const auto& c = r->eng->cfg;
+  const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  r->v_fused.ensure((size_t)c.layers * r->max_tokens * kvc * sizeof(bf16));
+  for (const auto& q : r->vseq) {
+    const int rows = q.T;  // cache rows of the sequence (incl. decoded tokens)
+    const int rc = fragk::vpage_gather(r->vseg.as<fragk::VSeg>() + q.seg0, r->vplan_tile.as<int>() + q.vt_off,
+                                       r->vplan_prim.as<int2>() + q.vp_off,
+                                       r->vplan_ent.as<unsigned long long>() + q.ve_off, r->vx.as<bf16>(),
+                                       (size_t)r->vx_rows * kvc, q.tail_row0, q.tail_slot_s, rows, c.layers, (int)kvc,
+                                       r->v_fused.as<bf16>() + (size_t)q.base * kvc, (size_t)r->max_tokens * kvc, s);
+    if (rc < 0) fail(FRAG_E_CUDA, "shared V read-back launch failed");
+  }
+  check_cuda(cudaStreamSynchronize(s), "shared V read-back");
+  r->v_materialized = true;
+}
+
 // ---------------------------------------------------------------- run_rows
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
               int n_logit_rows, int n_layers, const cudaEvent_t* layer_ready, const std::vector<Seg>* segs_in,
@@ -354,7 +413,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
   const size_t lstride = (size_t)r->max_tokens * kvc;
   Profiler& P = e->prof;
   bf16* kf = r->k_fused.as<bf16>();
-  bf16* vf = r->v_fused.as<bf16>();
+  bf16* vf = r->vshared ? nullptr : r->v_fused.as<bf16>();
   const int* prow = r->plan_rows.as<int>();
   const int* ptok = r->plan_tok.as<int>();
   float* h = r->h.as<float>();
@@ -437,7 +496,14 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     ep.q_out = r->q.as<bf16>();
     ep.q_out_f32 = (want_qf && l == L - 1) ? r->q_final.as<float>() : nullptr;
     ep.k_cache = kf + l * lstride;
-    ep.v_cache = vf + l * lstride;
+    if (r->vshared) {  // fresh V -> exclusive slots
+      ep.v_cache = r->vx.as<bf16>() + (size_t)l * r->vx_rows * kvc;
+      ep.v_slots = 1;
+      ep.v_tail_row0 = r->v_tail_row0;
+      ep.v_tail_slot0 = r->v_tail_slot0;
+    } else {
+      ep.v_cache = vf + l * lstride;
+    }
     ep.rows_per_seq = r->rows_per_seq;
     ep.Hq = Hq;
     ep.Hkv = Hkv;
@@ -456,6 +522,21 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
                          fragk::gemm_chain_supported(M, d, (int)qc) && fragk::gemm_chain_supported(M, 2 * F, d) &&
                          fragk::gemm_chain_supported(M, d, F);
   int* chain_done = r->gemm_cnt.as<int>() + (r->gemm_cnt.bytes / sizeof(int) - 2 * fragk::CHAIN_MAX_OPS);
+  // shared V pages: the attention of sequence g.seq reads V through its plan
+  auto vattn = [&](fragk::AttnArgs& a, const Seg& g, int l) {
+    if (!r->vshared) return;
+    const Result::VSeq& q = r->vseq[g.seq];
+    a.v = nullptr;
+    a.vsegs = r->vseg.as<fragk::VSeg>() + q.seg0;
+    a.n_vseg = q.n_seg;
+    a.vtile = r->vplan_tile.as<int>() + q.vt_off;
+    a.vprim = r->vplan_prim.as<int2>() + q.vp_off;
+    a.vent = r->vplan_ent.as<unsigned long long>() + q.ve_off;
+    a.vx = r->vx.as<bf16>() + (size_t)l * r->vx_rows * kvc;
+    a.layer = l;
+    a.tail_row0 = q.tail_row0;
+    a.tail_slot0 = mode == PASS_QUESTION ? q.tail_slot_q : q.tail_slot_s;
+  };
   bool qkv_done = false;  // this layer's QKV already ran inside the previous layer's chain
   for (int l = 0; l < L; ++l) {
     const auto& W = e->layers[l];
@@ -512,6 +593,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
         a.split_keys = sk;
         a.n_splits = ns;
         a.scale = 1.0f / std::sqrt((float)dh);
+        vattn(a, g, l);
         Scoped sc(P, s, KC_ATTN, 0, 0);
         sc.launched(fragk::sparse_q_attention(a, s));
       }
@@ -519,7 +601,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     std::vector<Seg> last_seg;
     std::vector<std::pair<int, int>> last_split;
     if (prune) {
-      last_seg.push_back(Seg{(int)off, Ml, 0, T});
+      last_seg.push_back(Seg{(int)off, Ml, 0, T, 0});
       last_split.resize(1);
       split_policy(Ml, T, last_split[0].first, last_split[0].second);
       if (last_split[0].first > 1) {
@@ -556,6 +638,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       a.split_keys = asplit[si].second;
       a.n_splits = asplit[si].first;
       a.scale = 1.0f / std::sqrt((float)dh);
+      vattn(a, g, l);
       Scoped sc(P, s, KC_ATTN, 0, 0);
       sc.launched(fragk::sparse_q_attention(a, s, defer_ok ? &deferred : nullptr));
       if (deferred) deferred_args = a;
@@ -739,7 +822,7 @@ StitchPlan stitch_prepare_parts(Engine* e, Result* r, cudaStream_t s, Stage& stg
   if (!tabs.empty())
     check_cuda(cudaMemcpyAsync(r->stitch_tab.p, tab_h, tabs.size() * sizeof(float2), cudaMemcpyHostToDevice, s),
                "stitch tab");
-  for (int i = 0; i < p.n_desc; ++i) p.bytes += 4.0 * c.layers * desc[i].n_tok * kvc * sizeof(bf16);
+  for (int i = 0; i < p.n_desc; ++i) p.bytes += (r->vshared ? 2.0 : 4.0) * c.layers * desc[i].n_tok * kvc * sizeof(bf16);
   return p;
 }
 
@@ -748,14 +831,137 @@ StitchPlan stitch_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, cons
   return stitch_prepare_parts(e, r, s, stg, {StitchPart{sys, &recs, S, 0}});
 }
 
+// ---- shared V pages
+// A request reads V in place only from records in this device's memory (an
+// attached peer's or IPC-imported pages would be re-read over NVLink by every
+// layer's attention: those requests keep the one-pass copy of K1).
+bool records_local(const Engine* e, const std::vector<Record*>& recs) {
+  for (const Record* rec : recs) {
+    if (rec->tier == FRAG_TIER_PEER || rec->ipc_mapped) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, rec->kv.p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.device != e->device) return false;
+  }
+  return true;
+}
+
+// One sequence of a shared-V request: its V segments (KV_S, then the records
+// in prompt order), cache rows and the exclusive slots of its fresh rows.
+struct VPart {
+  const SysKV* sys;
+  const std::vector<Record*>* recs;
+  int S, base, T, nq, k;
+  int plan_off;      // GEMM row of its first critical row (= its exclusive slot)
+  int tail_slot_q;   // exclusive slot of its first question row in the question pass
+  int tail_slot_s;   // ... in the sparse pass (and decode)
+};
+
+// Host prep: segment table with each segment's TMA map, per-sequence plan
+// slices and the two plan-build argument sets ([0, B): question pass, no
+// critical rows; [B, 2B): sparse pass, the selected rows in plan_rows), the
+// exclusive region (vx_rows slots per layer) and references that keep the
+// records' pages alive for as long as this result reads them.
+void vshared_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std::vector<VPart>& parts, int n_rows,
+                     int vx_rows) {
+  const auto& c = e->cfg;
+  const uint64_t kvc = (uint64_t)c.n_kv_heads * c.head_dim;
+  const int B = (int)parts.size();
+  int n_seg = 0;
+  for (const auto& pt : parts) n_seg += (pt.sys && pt.sys->n > 0 ? 1 : 0) + (int)pt.recs->size();
+  const int tiles = (n_rows + 127) / 128;
+  r->vseg.ensure((size_t)std::max(n_seg, 1) * sizeof(fragk::VSeg));
+  r->vplan_tile.ensure((size_t)B * (tiles + 1) * sizeof(int));
+  r->vplan_prim.ensure((size_t)B * tiles * sizeof(int2));
+  r->vplan_ent.ensure((size_t)B * n_rows * sizeof(unsigned long long));
+  r->vplan_args.ensure((size_t)2 * B * sizeof(fragk::VPlanArgs));
+  r->vx_rows = vx_rows;
+  r->vx.ensure((size_t)c.layers * vx_rows * kvc * sizeof(bf16));
+  auto* segs = stg.take<fragk::VSeg>(std::max(n_seg, 1));
+  auto* args = stg.take<fragk::VPlanArgs>(2 * B);
+  r->vseq.clear();
+  r->vrefs.clear();
+  int si = 0;
+  auto add = [&](const bf16* v, int n, int row0) {
+    fragk::VSeg& g = segs[si++];
+    std::memset(&g, 0, sizeof(g));
+    // V [L][n][Hkv*dh] as (Hkv*dh, n, L); box (64 cols, 128 rows, 1 layer)
+    if (!fragk::make_tmap_3d(&g.tmap, v, kvc, (uint64_t)n, (uint64_t)c.layers, kvc, (uint64_t)n * kvc, 64, 128, 1))
+      fail(FRAG_E_CUDA, "shared V: tensor map encoding failed");
+    g.v = v;
+    g.row0 = row0;
+    g.n = n;
+  };
+  fragk::VSeg* seg_dev = r->vseg.as<fragk::VSeg>();
+  for (int b = 0; b < B; ++b) {
+    const VPart& pt = parts[b];
+    Result::VSeq q{};
+    q.seg0 = si;
+    if (pt.sys && pt.sys->n > 0) add(pt.sys->kv.as<bf16>() + (size_t)c.layers * pt.sys->n * kvc, pt.sys->n, 0);
+    int row = pt.S;
+    for (Record* rec : *pt.recs) {
+      add(rec->v(), rec->n_tok, row);
+      row += rec->n_tok;
+      r->vrefs.push_back(rec->shared_from_this());
+    }
+    q.n_seg = si - q.seg0;
+    q.n_rows = n_rows;
+    q.vt_off = b * (tiles + 1);
+    q.vp_off = b * tiles;
+    q.ve_off = b * n_rows;
+    q.base = pt.base;
+    q.T = pt.T;
+    q.tail_row0 = pt.T - pt.nq;
+    q.tail_slot_q = pt.tail_slot_q;
+    q.tail_slot_s = pt.tail_slot_s;
+    r->vseq.push_back(q);
+    for (int w = 0; w < 2; ++w) {
+      fragk::VPlanArgs& a = args[w * B + b];
+      a.segs = seg_dev + q.seg0;
+      a.n_seg = q.n_seg;
+      a.crit = w ? r->plan_rows.as<int>() + pt.plan_off : nullptr;
+      a.n_crit = w ? pt.k : 0;
+      a.row_base = pt.base;
+      a.crit_slot0 = pt.plan_off;
+      a.tail_row0 = q.tail_row0;
+      a.n_rows = n_rows;
+      a.vtile = r->vplan_tile.as<int>() + q.vt_off;
+      a.vprim = r->vplan_prim.as<int2>() + q.vp_off;
+      a.vent = r->vplan_ent.as<unsigned long long>() + q.ve_off;
+    }
+  }
+  check_cuda(cudaMemcpyAsync(r->vseg.p, segs, (size_t)n_seg * sizeof(fragk::VSeg), cudaMemcpyHostToDevice, s),
+             "V segments");
+  check_cuda(cudaMemcpyAsync(r->vplan_args.p, args, (size_t)2 * B * sizeof(fragk::VPlanArgs), cudaMemcpyHostToDevice,
+                             s),
+             "V plan args");
+}
+
+// Build the patch plans (which = 0: question pass, 1: sparse pass) on the
+// request stream (part of the captured body).
+void vplan_launch(Engine* e, Result* r, cudaStream_t s, int which) {
+  if (!r->vshared || r->vseq.empty()) return;
+  const int B = (int)r->vseq.size();
+  int max_segs = 0;
+  for (const auto& q : r->vseq) max_segs = std::max(max_segs, q.n_seg);
+  Scoped sc(e->prof, s, KC_SELECT, 0, 0);
+  const int rc = fragk::vpatch_plan(r->vplan_args.as<fragk::VPlanArgs>() + which * B, B, r->vseq[0].n_rows, max_segs, s);
+  if (rc < 0) fail(FRAG_E_CUDA, "shared V plan launch failed");
+  sc.launched(rc);
+}
+
 void stitch_launch(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p, int l0 = 0, int l1 = -1) {
   if (p.n_desc == 0) return;
   const auto& c = e->cfg;
   if (l1 < 0) l1 = c.layers;
   Scoped sc(e->prof, s, KC_STITCH, 0, p.bytes * (l1 - l0) / c.layers);
+  // shared V pages: K only (V stays in the records)
   fragk::rope_shift_assemble(r->stitch_desc.as<fragk::StitchChunk>(), p.n_desc, p.max_rows,
-                             r->stitch_tab.as<float2>(), r->k_fused.as<bf16>(), r->v_fused.as<bf16>(), l1 - l0,
-                             r->max_tokens, c.n_kv_heads, c.head_dim, s, l0);
+                             r->stitch_tab.as<float2>(), r->k_fused.as<bf16>(),
+                             r->vshared ? nullptr : r->v_fused.as<bf16>(), l1 - l0, r->max_tokens, c.n_kv_heads,
+                             c.head_dim, s, l0);
   sc.launched(1);
   peek("stitch");
 }
@@ -873,6 +1079,7 @@ Result* scratch_for(Engine* e, int tokens) {
     e->scratch = std::make_unique<Result>();
     result_init(e->scratch.get(), e, std::max(tokens, 256));
   }
+  use_private_v(e->scratch.get());
   return e->scratch.get();
 }
 
@@ -1070,6 +1277,19 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   }
   // select_cacheblend replaces the question pass + K9
   const bool cacheblend = selector == FRAG_SELECT_CACHEBLEND && !inject && N > 0;
+  // shared V pages: the default for query-guided / injected requests over this
+  // device's records with at most half of the chunk rows recomputed (the
+  // attention patches every fresh row into its V tiles)
+  const bool vsh = !cacheblend && N > 0 && 2L * k <= N && shared_v_enabled() &&
+                   fragk::attn_shared_v_supported(c.head_dim) && records_local(e, recs);
+  if (vsh) {
+    r->vshared = true;
+    r->v_materialized = false;
+    r->v_tail_row0 = T - n_q;  // question rows (and decoded tokens) -> slots k, k+1, ...
+    r->v_tail_slot0 = k;
+  } else {
+    use_private_v(r);
+  }
   e->ensure_rope(T);
   SysKV* skv = get_sys_kv(e, sys, n_sys, s);
   if (cacheblend)
@@ -1089,7 +1309,8 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   r->logits_on_device = o && o->logits_on_device;
 
   // ---- host prep: everything that depends on this request's chunks / tokens
-  r->staging.ensure(64 * 1024 + (size_t)(n_chunks + 2) * (64 + c.head_dim * 4) + (size_t)(4 * T + 4 * M + 4 * n_q) * 4);
+  r->staging.ensure(64 * 1024 + (size_t)(n_chunks + 2) * (64 + c.head_dim * 4 + sizeof(fragk::VSeg)) +
+                    (size_t)(4 * T + 4 * M + 4 * n_q) * 4);
   Stage stg(r->staging);
   // injected plan first: the captured body copies from these staging slots,
   // so their offsets must depend only on the graph key
@@ -1099,6 +1320,8 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   if (cacheblend)
     for (int i = 0; i < N; ++i) cb_rows[i] = S + i;
   StitchPlan sp = stitch_prepare(e, r, s, stg, skv, recs, S);
+  if (vsh) vshared_prepare(e, r, s, stg, {VPart{skv, &recs, S, 0, T, n_q, k, 0, k, k}}, r->max_tokens,
+                           k + r->max_tokens - (T - n_q));
   {
     int off = 0;  // chunk token ids in prompt order (the recompute gather, K2)
     for (Record* rec : recs) {
@@ -1170,6 +1393,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
     else
       stitch_launch(e, r, bs, sp);  // K1: stitch_full_reuse
     ev_record(r, timing, 1, bs);
+    vplan_launch(e, r, bs, 0);  // shared V: patch plan without critical rows (question pass)
     if (full_reuse) {
       // r = 0 (Full Reuse): the plan is exactly the
       // question rows, so the sparse pass would recompute what the question
@@ -1229,6 +1453,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
                                    T - n_q, r->plan_rows.as<int>(), r->plan_tok.as<int>(), bs));
     }
     peek("select");
+    vplan_launch(e, r, bs, 1);  // shared V: + the critical rows' exclusive slots
     ev_record(r, timing, 3, bs);
     // sparse_prefill (Eq. 9) to the first-token logits
     run_rows(e, r, bs, M, T, PASS_FULL, nullptr, 0, 0, nullptr, nullptr, r->logit_rows);
@@ -1261,7 +1486,9 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
 
   const bool graphable = !timing && !e->prof.on;
   GraphKey key{T, S, N, n_q, k, (int)inject, (int)all_logits, (int)raw, (int)r->logits_on_device, sp.n_desc,
-               sp.max_rows, (cacheblend ? 1 + dev_layer * 4 + dev_comp : 0) + (overlap ? 1000 : 0) + (full_reuse ? 2000 : 0),
+               sp.max_rows,
+               (cacheblend ? 1 + dev_layer * 4 + dev_comp : 0) + (overlap ? 1000 : 0) + (full_reuse ? 2000 : 0) +
+                   (vsh ? 4000 : 0),
                (uint64_t)(uintptr_t)e->rope.p};
   r->timing.host_prep_ms =
       std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
@@ -1336,10 +1563,23 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
   r->logits_on_device = o && o->logits_on_device;
   r->batch = br;
   const size_t kvc = (size_t)c.n_kv_heads * c.head_dim;
+  // shared V pages: every request reads its chunks' V in place (a record
+  // reused by several requests of the batch is one set of pages)
+  bool vsh = shared_v_enabled() && fragk::attn_shared_v_supported(c.head_dim);
+  for (int b = 0; b < B && vsh; ++b)
+    vsh = br[b].N > 0 && 2L * br[b].k <= br[b].N && records_local(e, recs[b]);
+  if (vsh) {
+    r->vshared = true;
+    r->v_materialized = false;
+    r->v_tail_row0 = 0x7fffffff;  // every fresh row at its GEMM row's slot
+    r->v_tail_slot0 = 0;
+  } else {
+    use_private_v(r);
+  }
 
   // ---- host prep
-  r->staging.ensure(64 * 1024 + (size_t)(pins.ids.size() + 2 * B) * (64 + c.head_dim * 4) +
-                    (size_t)(4 * Qtot + 4 * B) * 4);
+  r->staging.ensure(64 * 1024 + (size_t)(pins.ids.size() + 2 * B) * (64 + c.head_dim * 4 + sizeof(fragk::VSeg)) +
+                    (size_t)B * 2 * sizeof(fragk::VPlanArgs) + (size_t)(4 * Qtot + 4 * B) * 4);
   Stage stg(r->staging);
   std::vector<StitchPart> parts;
   for (int b = 0; b < B; ++b) parts.push_back(StitchPart{skv[b], &recs[b], br[b].S, b * slot});
@@ -1374,6 +1614,13 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
     for (int b = 0; b < B; ++b) map_h[b] = compact ? Mtot + b : br[b].plan_off + br[b].k + br[b].nq - 1;
     check_cuda(cudaMemcpyAsync(r->row_map.p, map_h, B * sizeof(int), cudaMemcpyHostToDevice, s), "map");
   }
+  if (vsh) {
+    std::vector<VPart> vp;
+    for (int b = 0; b < B; ++b)
+      vp.push_back(VPart{skv[b], &recs[b], br[b].S, b * slot, br[b].T, br[b].nq, br[b].k, br[b].plan_off, qofs[b],
+                         br[b].plan_off + br[b].k});
+    vshared_prepare(e, r, s, stg, vp, slot, Mtot);
+  }
   if (maxN > 0) {
     r->part_ms.ensure((size_t)((maxN + 31) / 32) * maxQ * c.n_heads * sizeof(float2));
     r->row_ms.ensure((size_t)maxQ * c.n_heads * sizeof(float2));
@@ -1385,8 +1632,8 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
   if (!r->logits_on_device) r->logits_host.ensure((size_t)B * c.vocab * sizeof(float));
   std::vector<Seg> qsegs, psegs;
   for (int b = 0; b < B; ++b) {
-    qsegs.push_back(Seg{qofs[b], br[b].nq, b * slot, br[b].T});
-    psegs.push_back(Seg{br[b].plan_off, br[b].k + br[b].nq, b * slot, br[b].T});
+    qsegs.push_back(Seg{qofs[b], br[b].nq, b * slot, br[b].T, b});
+    psegs.push_back(Seg{br[b].plan_off, br[b].k + br[b].nq, b * slot, br[b].T, b});
   }
 
   // ---- device body: captured into a CUDA graph per batch shape (like a
@@ -1395,6 +1642,7 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
     ev_record(r, timing, 0, s);
     stitch_launch(e, r, s, sp);
     ev_record(r, timing, 1, s);
+    vplan_launch(e, r, s, 0);
     run_rows(e, r, s, Qtot, slot, PASS_QUESTION, nullptr, 0, 0, nullptr, &qsegs);
     ev_record(r, timing, 2, s);
     for (int b = 0; b < B; ++b) {
@@ -1427,6 +1675,7 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
                                    r->plan_tok.as<int>() + q.plan_off, s));
     }
     peek("batch select");
+    vplan_launch(e, r, s, 1);
     ev_record(r, timing, 3, s);
     run_rows(e, r, s, Mtot, slot, PASS_FULL, nullptr, 0, 0, nullptr, &psegs, -1);
     ev_record(r, timing, 4, s);
@@ -1452,7 +1701,7 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
     logits_d2h(r, s);
   };
   GraphKey key{B * slot, -2 - B, Ntot, Qtot, Mtot - Qtot, 0, 0, (int)raw, (int)r->logits_on_device, sp.n_desc,
-               sp.max_rows, 0, (uint64_t)(uintptr_t)e->rope.p};
+               sp.max_rows, vsh ? 4000 : 0, (uint64_t)(uintptr_t)e->rope.p};
   for (const auto& q : br)  // batch shape: every request's exact (T, S, N, |Q|, k)
     key.shapes.insert(key.shapes.end(), {q.T, q.S, q.N, q.nq, q.k});
   run_graphed(r, s, !timing && !e->prof.on, key, body);
@@ -1478,6 +1727,7 @@ void full_prefill(Engine* e, const int32_t* sys, int n_sys, const int32_t* token
   const bool timing = o && o->timing;
   const int S = n_sys, T = S + n_tok;
   if (T > r->max_tokens) fail(FRAG_E_CONTRACT, "prompt exceeds the result capacity");
+  use_private_v(r);  // every row is fresh
   e->ensure_rope(T);
   SysKV* skv = get_sys_kv(e, sys, n_sys, s);
   r->T = T;
@@ -1534,6 +1784,7 @@ void kv_deviation(Engine* e, Store* st, const int32_t* sys, int n_sys, const fra
   for (Record* rec : recs) N += rec->n_tok;
   const int T = S + N;
   if (T > r->max_tokens) fail(FRAG_E_CONTRACT, "context exceeds the result capacity");
+  use_private_v(r);  // the Full-Attention pass rewrites every chunk row
   e->ensure_rope(T);
   SysKV* skv = get_sys_kv(e, sys, n_sys, s);
   r->T = T;
@@ -1622,6 +1873,8 @@ void decode(Engine* e, Result* r, int n_new, cudaStream_t s, int32_t* out_host) 
   sync_checked(e, r, s, "decode");
   std::memcpy(out_host, stage, (size_t)n_new * sizeof(int));
   r->T = T0 + n_new - 1;  // the fused cache now also holds the decoded tokens' K/V
+  if (r->vshared && !r->vseq.empty()) r->vseq[0].T = r->T;
+  r->v_materialized = false;
   r->timing_valid = false;
 }
 

@@ -112,7 +112,9 @@ struct ChunkKeyHash {
 };
 ChunkKey key_of(const frag_chunk_id& id);
 
-struct Record {
+// Shared ownership: a result whose V rows are read in place from a record
+// (shared V pages) keeps the record's pages alive until its next request.
+struct Record : std::enable_shared_from_this<Record> {
   frag_chunk_id id{};
   int n_tok = 0;
   int native_start = 1;
@@ -144,7 +146,7 @@ struct Store {
   size_t capacity = 0, used = 0;
   uint64_t tick = 0;
   mutable std::shared_mutex mu;
-  std::unordered_map<ChunkKey, std::unique_ptr<Record>, ChunkKeyHash> recs;
+  std::unordered_map<ChunkKey, std::shared_ptr<Record>, ChunkKeyHash> recs;
   // same-process stores on other GPUs whose records this store serves on a
   // local miss (frag_store_attach_peer); their pages are read over NVLink
   std::vector<Store*> peers;
@@ -245,6 +247,25 @@ struct Result {
       part_lse, logits, row_map, stitch_desc, stitch_tab, lm_x, gemm_ws, gemm_cnt, dec_tok, fr_save, dev, score_col, score_q,
       ssq;
   PinnedBuf staging, logits_host;
+  // shared V pages: with vshared the V
+  // rows of the chunks (and KV_S) are read in place from their records through
+  // the per-sequence patch plans; only this request's fresh rows live in vx
+  // (exclusive slots: critical rows at their GEMM row, question / decoded rows
+  // by rule). v_fused then exists only as the read-back view.
+  bool vshared = false;
+  bool v_materialized = false;  // v_fused holds the view of the current request
+  int vx_rows = 0;              // exclusive slots per layer
+  int v_tail_row0 = 0x7fffffff, v_tail_slot0 = 0;  // QKV epilogue slot rule (one sequence)
+  struct VSeq {
+    int seg0, n_seg;         // segments in vseg
+    int vt_off, vp_off, ve_off, n_rows;  // plan slices (vplan_tile / vplan_prim / vplan_ent)
+    int base, T;             // cache rows of the sequence
+    int tail_row0;           // sequence-local first question row
+    int tail_slot_q, tail_slot_s;  // exclusive slot of that row in the question / sparse pass
+  };
+  std::vector<VSeq> vseq;
+  DevBuf vx, vseg, vplan_args, vplan_tile, vplan_prim, vplan_ent;
+  std::vector<std::shared_ptr<Record>> vrefs;  // records whose pages the shared V view reads
   bool q_final_in_full = false;  // PASS_FULL also keeps the last layer's fp32 queries (r = 0 fast path)
   // timing
   cudaEvent_t ev[7] = {};
@@ -257,6 +278,14 @@ struct Result {
 
 Engine* engine_create(const frag_model_cfg& cfg, int device, uint64_t seed);
 void result_init(Result* r, Engine* e, int max_tokens);
+// The request about to run keeps a private fused V [L][max_tokens] (full
+// prefill, CacheBlend, peer records, scratch passes) instead of shared pages.
+void use_private_v(Result* r);
+// Shared V pages: write the fused V view of the current request into v_fused
+// (frag_result_fused_kv read-back); a no-op for a private V.
+void materialize_v(Result* r, cudaStream_t s);
+int set_shared_v(int on);  // 1 / 0 sets, -1 queries; returns the previous setting
+uint64_t result_device_bytes(const Result* r);
 
 // Pipeline stages (engine.cpp)
 enum PassMode { PASS_FULL = 0, PASS_QUESTION = 1, PASS_KV_ONLY = 2 };
@@ -270,10 +299,11 @@ enum PassMode { PASS_FULL = 0, PASS_QUESTION = 1, PASS_KV_ONLY = 2 };
 // attention (the stitch of that layer running on another stream).
 // segs: optional batched sequences (plan-row ranges over their own cache slices)
 struct Seg {
-  int off;   // first plan row of the sequence
-  int M;     // plan rows of the sequence
-  int base;  // first fused-cache row of the sequence
-  int T;     // cache rows visible to the sequence
+  int off;      // first plan row of the sequence
+  int M;        // plan rows of the sequence
+  int base;     // first fused-cache row of the sequence
+  int T;        // cache rows visible to the sequence
+  int seq = 0;  // sequence index (shared V pages: Result::vseq)
 };
 void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode, const int* row_map_dev,
               int n_logit_rows, int n_layers = 0, const cudaEvent_t* layer_ready = nullptr,

@@ -80,9 +80,9 @@ void store_insert(Store* st, std::unique_ptr<Record> rec, bool overwrite) {
     fail(FRAG_E_STORE, "GPU tier capacity exhausted (tiering/eviction out of scope in this build)");
   if (it != st->recs.end()) {
     st->used -= freed;
-    it->second = std::move(rec);
+    it->second = std::shared_ptr<Record>(std::move(rec));
   } else {
-    st->recs.emplace(key, std::move(rec));
+    st->recs.emplace(key, std::shared_ptr<Record>(std::move(rec)));
   }
   st->used += bytes;
 }

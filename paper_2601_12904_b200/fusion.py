@@ -65,6 +65,12 @@ def launch_count() -> int:
     return int(lib.frag_launch_count())
 
 
+def set_shared_v(on: bool | None = None) -> bool:
+    """Shared V pages on/off (process wide; None only queries). Returns the
+    previous setting (frag_set_shared_v)."""
+    return bool(lib.frag_set_shared_v(-1 if on is None else int(bool(on))))
+
+
 def memcpy(dst_ptr: int, src_ptr: int, nbytes: int) -> None:
     check(lib.frag_memcpy(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), nbytes))
 
@@ -434,6 +440,12 @@ class Result:
         n = C.c_int32()
         check(lib.frag_result_fused_kv(self._h, None, None, C.byref(n)))
         return n.value
+
+    def memory(self) -> tuple[int, bool]:
+        """(device bytes held by the result, whether its last request used shared V pages)."""
+        b, sv = C.c_uint64(), C.c_int32()
+        check(lib.frag_result_memory(self._h, C.byref(b), C.byref(sv)))
+        return int(b.value), bool(sv.value)
 
     def fused_ptrs(self) -> tuple[int, int]:
         k, v = C.c_void_p(), C.c_void_p()
