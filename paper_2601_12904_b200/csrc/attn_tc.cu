@@ -31,6 +31,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -130,6 +131,11 @@ __device__ __forceinline__ void vpatch_loop(const AttnArgs& a, int hk, int k_lo,
     }
     fence_async_smem();  // generic-proxy stores -> visible to the tensor pipe
     __syncwarp();
+    if (a.vdump && j < 8) {  // tooling: the tile the MMA will consume
+      uint4* dst = reinterpret_cast<uint4*>(a.vdump + (((size_t)blockIdx.z * gridDim.x + blockIdx.x) * 8 + j) * KV_BYTES);
+      for (int i = lane; i < (int)(KV_BYTES / 16); i += 32) dst[i] = reinterpret_cast<const uint4*>(sv)[i];
+      __syncwarp();
+    }
     if (lane == 0) mbar_arrive(&v_ready[st]);
   }
 }
@@ -680,7 +686,11 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
   uint64_t* p_full = s_full + 2;        // [2]
   uint64_t* pv_done = p_full + 2;
   uint64_t* v_ready = pv_done + 1;      // [NS] VSH: V tile patched
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_ready + NS);
+  // every PV (and row-sum) MMA complete: the epilogue cannot use pv_done, whose
+  // last two phases may both be outstanding when the softmax finishes its last
+  // tile (a parity wait cannot tell phase n-1 from n-3)
+  uint64_t* o_done = v_ready + NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
   __shared__ float xm[2][4][AT_ROWS];   // [slice parity][column group][row] partial max
 
   const int warp = warp_id(), lane = lane_id();
@@ -710,6 +720,7 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
       mbar_init(&p_full[b], 16);
     }
     mbar_init(pv_done, 1);
+    mbar_init(o_done, 1);
     fence_mbar_init();
   }
   if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
@@ -810,6 +821,8 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
         issue_pv(u);
         if (u + 2 < n_tiles) issue_s(u + 2);
       }
+      if (elect_one()) umma_commit(o_done);
+      __syncwarp();
     }
   } else if (VSH && warp == W_PATCH) {
     // ------------------------------------------------------------ V patch warp (shared V pages)
@@ -958,7 +971,7 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
     // ---- epilogue: the row sum accumulated by the tensor pipe (T_L)
     float lt = 0.f;
     if (n_tiles > 0) {
-      mbar_wait(pv_done, (n_tiles - 1) & 1);
+      mbar_wait(o_done, 0);
       tc_fence_after();
       uint32_t l16[16];
       tmem_ld16(lane_base + T_L, l16);
@@ -1015,7 +1028,7 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
 
 template <int DH>
 constexpr size_t qtm_smem() {
-  return 1024 + (size_t)(DH == 128 ? 3 : 6) * 2 * AT_KEYS * DH * 2 + 16384 + 256;
+  return 1024 + (size_t)(DH == 128 ? 3 : 6) * 2 * AT_KEYS * DH * 2 + 16384 + 512;  // barriers + TMEM slot
 }
 static_assert(qtm_smem<128>() <= 232448 - 4 * 1024 && qtm_smem<64>() <= 232448 - 4 * 1024,
               "Q-in-TMEM attention exceeds 227 KB");
@@ -1033,8 +1046,8 @@ bool attn_shared_v_supported(int dh) {
   const char* qq = std::getenv("FRAG_ATTN_QTM_Q");
   const char* p = std::getenv("FRAG_ATTN_POLY");
   const char* qp = std::getenv("FRAG_ATTN_QTM_POLY");
-  return !(q && q[0] == '0') && !(qq && qq[0] == '1') && !(p && std::atoi(p) != 0) &&
-         !(qp && std::atoi(qp) != kQtmPoly);
+  (void)qq;
+  return !(q && q[0] == '0') && !(p && std::atoi(p) != 0) && !(qp && std::atoi(qp) != kQtmPoly);
 }
 
 int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream) {
@@ -1062,6 +1075,34 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   static const char* trace_path = std::getenv("FRAG_ATTN_TRACE");
   static unsigned long long* trace_dev = nullptr;
   AttnArgs at = a;
+  // FRAG_VPATCH_DUMP=<file>: tooling only (tools/debug_sharedv.py) -- the
+  // patched V tiles of every CTA (first 8 tiles) appended after each VSH launch
+  static const char* vdump_path = std::getenv("FRAG_VPATCH_DUMP");
+  static uint8_t* vdump_dev = nullptr;
+  static size_t vdump_cap = 0;
+  size_t vdump_bytes = 0;
+  if (vdump_path && a.vsegs) {
+    vdump_bytes = (size_t)a.n_splits * (size_t)((a.M + AT_ROWS / G - 1) / (AT_ROWS / G)) * a.Hkv * 8 * AT_KEYS * a.dh * 2;
+    if (vdump_bytes > vdump_cap) {
+      if (vdump_dev) cudaFree(vdump_dev);
+      cudaMalloc(&vdump_dev, vdump_bytes);
+      vdump_cap = vdump_bytes;
+    }
+    cudaMemsetAsync(vdump_dev, 0, vdump_bytes, stream);
+    at.vdump = vdump_dev;
+  }
+  auto vdump_flush = [&] {
+    if (!vdump_bytes) return;
+    std::vector<uint8_t> h(vdump_bytes);
+    cudaMemcpyAsync(h.data(), vdump_dev, vdump_bytes, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    if (FILE* f = std::fopen(vdump_path, "ab")) {
+      const int hdr[8] = {a.M, a.n_splits, a.Hkv, a.dh, G, a.layer, a.split_keys, (a.M <= AT_ROWS / G) ? 1 : 0};
+      std::fwrite(hdr, sizeof(hdr), 1, f);
+      std::fwrite(h.data(), h.size(), 1, f);
+      std::fclose(f);
+    }
+  };
   if (trace_path) {
     if (!trace_dev) cudaMalloc(&trace_dev, 2 * 256 * 4 * sizeof(unsigned long long));
     cudaMemsetAsync(trace_dev, 0, 2 * 256 * 4 * sizeof(unsigned long long), stream);
@@ -1101,6 +1142,7 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
       go(attn_tc_kernel<128, 0, true, false, true>, (int)AttCfg<128>::SMEM_DUAL);
     else
       go(attn_tc_kernel<64, 0, true, false, true>, (int)AttCfg<64>::SMEM_DUAL);
+    vdump_flush();
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
   }
   if (dual) {
@@ -1143,6 +1185,7 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
         go2(attn_qtm_kernel<128, kQtmPoly, true>, (int)qtm_smem<128>());
       else
         go2(attn_qtm_kernel<64, kQtmPoly, true>, (int)qtm_smem<64>());
+      vdump_flush();
       return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
     }
     if (a.dh == 128) {

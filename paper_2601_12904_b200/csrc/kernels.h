@@ -211,6 +211,7 @@ struct AttnArgs {
   const bf16* vx = nullptr;    // exclusive V of this layer: [slot][Hkv][dh]
   int layer = 0;
   int tail_row0 = 0x7fffffff, tail_slot0 = 0;
+  uint8_t* vdump = nullptr;  // tooling (FRAG_VPATCH_DUMP): patched V tiles [z][x][tile < 8][bytes]
 };
 // returns launches; with combine_deferred != nullptr a split-KV launch leaves
 // the combine to the caller (*combine_deferred = true)
