@@ -366,7 +366,7 @@ uint64_t result_device_bytes(const Result* r) {
                           &r->plan_tok, &r->chunk_tok, &r->q_tok, &r->q_final, &r->scores, &r->part_ms, &r->row_ms,
                           &r->part_o, &r->part_lse, &r->logits, &r->row_map, &r->stitch_desc, &r->stitch_tab,
                           &r->lm_x, &r->gemm_ws, &r->gemm_cnt, &r->dec_tok, &r->fr_save, &r->dev, &r->score_col,
-                          &r->score_q, &r->ssq, &r->vx, &r->vseg, &r->vplan_args, &r->vplan_tile, &r->vplan_prim,
+                          &r->score_q, &r->ssq, &r->vx, &r->vx_map, &r->vseg, &r->vplan_args, &r->vplan_tile, &r->vplan_prim,
                           &r->vplan_ent})
     b += d->bytes;
   return b;
@@ -533,6 +533,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     a.vprim = r->vplan_prim.as<int2>() + q.vp_off;
     a.vent = r->vplan_ent.as<unsigned long long>() + q.ve_off;
     a.vx = r->vx.as<bf16>() + (size_t)l * r->vx_rows * kvc;
+    a.vx_map = r->vx_map.as<CUtensorMap>();
     a.layer = l;
     a.tail_row0 = q.tail_row0;
     a.tail_slot0 = mode == PASS_QUESTION ? q.tail_slot_q : q.tail_slot_s;
@@ -881,6 +882,15 @@ void vshared_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std
   r->vx.ensure((size_t)c.layers * vx_rows * kvc * sizeof(bf16));
   auto* segs = stg.take<fragk::VSeg>(std::max(n_seg, 1));
   auto* args = stg.take<fragk::VPlanArgs>(2 * B);
+  // exclusive slots as one tensor (rows = slots), box (64, 1, 1): patched rows
+  // [0]: box rows 1 (one patched row), [1]: box rows 32 (a staged run of fresh rows)
+  auto* xmap = stg.take<CUtensorMap>(2);
+  r->vx_map.ensure(2 * sizeof(CUtensorMap));
+  for (int i = 0; i < 2; ++i)
+    if (!fragk::make_tmap_3d(&xmap[i], r->vx.p, kvc, (uint64_t)vx_rows, (uint64_t)c.layers, kvc,
+                             (uint64_t)vx_rows * kvc, 64, i ? 32 : 1, 1))
+      fail(FRAG_E_CUDA, "shared V: tensor map encoding failed");
+  check_cuda(cudaMemcpyAsync(r->vx_map.p, xmap, 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s), "V slot maps");
   r->vseq.clear();
   r->vrefs.clear();
   int si = 0;
@@ -888,7 +898,8 @@ void vshared_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std
     fragk::VSeg& g = segs[si++];
     std::memset(&g, 0, sizeof(g));
     // V [L][n][Hkv*dh] as (Hkv*dh, n, L); box (64 cols, 128 rows, 1 layer)
-    if (!fragk::make_tmap_3d(&g.tmap, v, kvc, (uint64_t)n, (uint64_t)c.layers, kvc, (uint64_t)n * kvc, 64, 128, 1))
+    if (!fragk::make_tmap_3d(&g.tmap, v, kvc, (uint64_t)n, (uint64_t)c.layers, kvc, (uint64_t)n * kvc, 64, 128, 1) ||
+        !fragk::make_tmap_3d(&g.tmap1, v, kvc, (uint64_t)n, (uint64_t)c.layers, kvc, (uint64_t)n * kvc, 64, 1, 1))
       fail(FRAG_E_CUDA, "shared V: tensor map encoding failed");
     g.v = v;
     g.row0 = row0;

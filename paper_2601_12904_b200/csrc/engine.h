@@ -264,7 +264,7 @@ struct Result {
     int tail_slot_q, tail_slot_s;  // exclusive slot of that row in the question / sparse pass
   };
   std::vector<VSeq> vseq;
-  DevBuf vx, vseg, vplan_args, vplan_tile, vplan_prim, vplan_ent;
+  DevBuf vx, vx_map, vseg, vplan_args, vplan_tile, vplan_prim, vplan_ent;
   std::vector<std::shared_ptr<Record>> vrefs;  // records whose pages the shared V view reads
   bool q_final_in_full = false;  // PASS_FULL also keeps the last layer's fp32 queries (r = 0 fast path)
   // timing

@@ -151,13 +151,14 @@ void rmsnorm(const float* h, int M, int d, const bf16* gain, float eps, bf16* x,
 // exclusive V region, slot-indexed. One VSeg per statically placed source
 // (KV_S, each chunk record), sorted by first cache row (sequence-local).
 struct alignas(64) VSeg {
-  CUtensorMap tmap;  // V [L][n][Hkv*dh] as (Hkv*dh, n, L), box (64, 128, 1), SW128
-  const bf16* v;     // V base (layer 0, row 0)
-  int row0;          // first sequence-local cache row
-  int n;             // rows
+  CUtensorMap tmap;   // V [L][n][Hkv*dh] as (Hkv*dh, n, L), box (64, 128, 1), SW128: a tile's primary box
+  CUtensorMap tmap1;  // the same tensor, box (64, 1, 1): one patched row
+  const bf16* v;      // V base (layer 0, row 0)
+  int row0;           // first sequence-local cache row
+  int n;              // rows
   int pad[12];
 };
-static_assert(sizeof(VSeg) == 192, "VSeg layout");
+static_assert(sizeof(VSeg) == 320, "VSeg layout");
 // Per-sequence patch plan over 128-row key tiles (sequence-local rows): tile
 // j's TMA box comes from its primary segment vprim[j] = (segment, row
 // coordinate) -- the segment holding row 128j; none: segment 0 at a row past
@@ -209,9 +210,9 @@ struct AttnArgs {
   const int2* vprim = nullptr; // [tiles] (primary segment, TMA row coordinate)
   const unsigned long long* vent = nullptr;
   const bf16* vx = nullptr;    // exclusive V of this layer: [slot][Hkv][dh]
+  const CUtensorMap* vx_map = nullptr;  // exclusive V [L][slots][Hkv*dh] as (Hkv*dh, slots, L): [0] box (64, 1, 1), [1] box (64, 32, 1)
   int layer = 0;
   int tail_row0 = 0x7fffffff, tail_slot0 = 0;
-  uint8_t* vdump = nullptr;  // tooling (FRAG_VPATCH_DUMP): patched V tiles [z][x][tile < 8][bytes]
 };
 // returns launches; with combine_deferred != nullptr a split-KV launch leaves
 // the combine to the caller (*combine_deferred = true)
