@@ -142,188 +142,6 @@ __device__ __forceinline__ void vpatch_loop(const AttnArgs& a, int hk, int k_lo,
   }
 }
 
-// Staged variant (the Q-in-TMEM sparse-pass kernel, which has the shared
-// memory for it): a tile's fresh rows -- its critical rows, then question /
-// decoded rows -- occupy ONE contiguous run of exclusive slots (slots follow
-// row order), so they arrive as 32-row TMA boxes into a double-buffered
-// staging area, issued one tile ahead, and the patch warp scatters them into
-// their tile rows with shared-memory copies (then a proxy fence). Only rows of
-// other segments (chunk boundaries, KV_S) still take one-row boxes. Few large
-// boxes instead of one TMA per row: the per-row boxes serialised in the TMA
-// unit (~75 cycles each, ~2.9k cycles per tile at 19 rows x 2 atoms).
-template <int DH, int NS>
-__device__ __forceinline__ void vpatch_loop_staged(const AttnArgs& a, int hk, int k_lo, int k_hi, int n_tiles,
-                                                   uint8_t* sV, uint64_t* v_full, uint64_t* v_ready, int lane,
-                                                   uint8_t* stg, uint64_t* stg_full, uint8_t* r_of) {
-  constexpr int ATOMS = DH / 64;
-  constexpr uint32_t KV_ATOM = AT_KEYS * 128;
-  constexpr uint32_t KV_BYTES = AT_KEYS * DH * 2;
-  constexpr int SR = 32;  // staged rows per round
-  constexpr uint32_t S_ATOM = SR * 128, S_BYTES = SR * DH * 2;
-  constexpr int CPR = DH / 8, RPI = 32 / CPR;
-  const int tile0 = k_lo / AT_KEYS;
-  const int* starts = a.vtile;
-  const CUtensorMap* map1 = a.vx_map;      // exclusive slots, box rows 1
-  const CUtensorMap* mapS = a.vx_map + 1;  // exclusive slots, box rows SR
-  const unsigned lanes_below = (1u << lane) - 1u;
-  const int sub = lane / CPR, ch = lane % CPR;
-  struct Tile {
-    unsigned long long e[4];
-    int n_ent;
-  };
-  // entry starts ride one tile further ahead than the entries, so the entry
-  // loads never wait on them: sw[t] = starts[tile0 + t] for t = j .. j + 3
-  int s0 = __ldg(starts + tile0), s1 = __ldg(starts + tile0 + 1);
-  int s2 = n_tiles > 1 ? __ldg(starts + tile0 + 2) : s1, s3 = n_tiles > 2 ? __ldg(starts + tile0 + 3) : s2;
-  auto load_tile = [&](int lo, int hi, Tile& T) {
-    T.n_ent = hi - lo;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) T.e[q] = lane + 32 * q < T.n_ent ? __ldg(a.vent + lo + lane + 32 * q) : 0ull;
-  };
-  // fresh run of a tile: first slot, planned (critical) count, tail rows
-  struct Fresh {
-    unsigned bal[4];
-    int nf, f_lo, tr0, n_tail;
-    bool tail_staged;
-  };
-  auto fresh_of = [&](const Tile& T, int key0) {
-    Fresh f;
-    f.nf = 0;
-    f.f_lo = -1;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const bool fr = lane + 32 * q < T.n_ent && ((T.e[q] >> 8) & 0xffffff) == 0;
-      f.bal[q] = __ballot_sync(0xffffffffu, fr);
-      if (f.f_lo < 0 && f.bal[q]) f.f_lo = __shfl_sync(0xffffffffu, (int)(T.e[q] >> 32), __ffs(f.bal[q]) - 1);
-      f.nf += __popc(f.bal[q]);
-    }
-    f.tr0 = max(key0, a.tail_row0);
-    f.n_tail = max(0, min(key0 + AT_KEYS, k_hi) - f.tr0);
-    const int t_slot = a.tail_slot0 + f.tr0 - a.tail_row0;
-    f.tail_staged = f.nf == 0 || f.f_lo + f.nf == t_slot;  // contiguous run (always, by the slot rule)
-    if (f.nf == 0) f.f_lo = t_slot;
-    return f;
-  };
-  auto run_len = [](const Fresh& f) { return f.nf + (f.tail_staged ? f.n_tail : 0); };
-  auto issue_stage = [&](int buf, int slot0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(&stg_full[buf], S_BYTES);
-#pragma unroll
-      for (int at = 0; at < ATOMS; ++at)
-        tma_load_3d(stg + buf * S_BYTES + at * S_ATOM, mapS, &stg_full[buf], hk * DH + at * 64, slot0, a.layer);
-    }
-  };
-  Tile cur, nxt, nn;
-  load_tile(s0, s1, cur);
-  if (n_tiles > 1) load_tile(s1, s2, nxt);
-  int sph = 0;  // staging phase bits (buffer b: bit b)
-  {
-    const Fresh f0 = fresh_of(cur, k_lo);
-    if (run_len(f0) > 0) issue_stage(0, f0.f_lo);
-  }
-  for (int j = 0; j < n_tiles; ++j) {
-    const int st = j % NS, buf = j & 1;
-    const int key0 = k_lo + j * AT_KEYS;
-    if (j + 2 < n_tiles) load_tile(s2, s3, nn);  // plan entries two tiles ahead
-    const int s4 = j + 3 < n_tiles ? __ldg(starts + tile0 + j + 4) : s3;
-    if (j + 1 < n_tiles) {                       // next tile's first staged round (its buffer's last reader is done)
-      const Fresh f1 = fresh_of(nxt, key0 + AT_KEYS);
-      if (run_len(f1) > 0) issue_stage(buf ^ 1, f1.f_lo);
-    }
-    if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256) a.trace[3072 + j * 4 + 1] = clock64();  // loop top done
-    const Fresh f = fresh_of(cur, key0);
-    const int n_run = run_len(f);
-    uint8_t* sv = sV + st * KV_BYTES;
-    // staging row i of the run -> tile row
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if ((f.bal[q] >> lane) & 1u) {
-        int i = __popc(f.bal[q] & lanes_below);
-        for (int qq = 0; qq < q; ++qq) i += __popc(f.bal[qq]);
-        r_of[i] = (uint8_t)(cur.e[q] & 127);
-      }
-    if (f.tail_staged)
-      for (int t = lane; t < f.n_tail; t += 32) r_of[f.nf + t] = (uint8_t)(f.tr0 - key0 + t);
-    mbar_wait(&v_full[st], (j / NS) & 1);  // the primary box has landed: patch over it
-    if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256)  // tooling: primary landed | run length << 48
-      a.trace[2048 + j * 4 + 1] = ((unsigned long long)clock64() & 0xffffffffffffull) | ((unsigned long long)n_run << 48);
-    // rows of other segments (and a non-contiguous tail): one-row boxes onto v_ready
-    int n_direct = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const bool dir = lane + 32 * q < cur.n_ent && ((cur.e[q] >> 8) & 0xffffff) != 0;
-      n_direct += __popc(__ballot_sync(0xffffffffu, dir));
-    }
-    if (!f.tail_staged) n_direct += f.n_tail;
-    if (lane == 0 && n_direct) mbar_expect_tx(&v_ready[st], (uint32_t)n_direct * DH * 2);
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const unsigned long long e = cur.e[q];
-      if (lane + 32 * q < cur.n_ent && ((e >> 8) & 0xffffff) != 0) {
-        const int r = (int)(e & 127), seg = (int)((e >> 8) & 0xffffff);
-#pragma unroll
-        for (int at = 0; at < ATOMS; ++at)
-          tma_load_3d(sv + at * KV_ATOM + r * 128, &a.vsegs[seg - 1].tmap1, &v_ready[st], hk * DH + at * 64,
-                      (int)(e >> 32), a.layer);
-      }
-    }
-    if (!f.tail_staged)
-      for (int t = lane; t < f.n_tail; t += 32) {
-        const int r = f.tr0 - key0 + t;
-#pragma unroll
-        for (int at = 0; at < ATOMS; ++at)
-          tma_load_3d(sv + at * KV_ATOM + r * 128, map1, &v_ready[st], hk * DH + at * 64,
-                      a.tail_slot0 + f.tr0 + t - a.tail_row0, a.layer);
-      }
-    // fresh run: SR-row rounds through the staging buffer
-    for (int i0 = 0; i0 < n_run; i0 += SR) {
-      if (i0 > 0) {  // this buffer's reads are done (the warp synced): refill it
-        fence_async_smem();
-        __syncwarp();
-        issue_stage(buf, f.f_lo + i0);
-      }
-      mbar_wait(&stg_full[buf], (sph >> buf) & 1);
-      if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256 && i0 == 0) a.trace[2048 + j * 4 + 2] = clock64();
-      sph ^= 1 << buf;
-      const int cnt = min(SR, n_run - i0);
-      const uint8_t* sb = stg + buf * S_BYTES;
-      // batches of 8 rows per lane group: all row ids, then all loads, then all
-      // stores in flight together (a dependent ld -> st chain per row costs
-      // ~150 cycles under the tensor pipe's shared-memory traffic)
-      for (int b8 = 0; b8 < cnt; b8 += 8 * RPI) {
-        int rr[8];
-        uint4 vv[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int ii = b8 + t * RPI + sub;
-          rr[t] = ii < cnt ? (int)r_of[i0 + ii] : -1;
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int ii = b8 + t * RPI + sub;
-          if (rr[t] >= 0)
-            vv[t] = *reinterpret_cast<const uint4*>(sb + (ch >> 3) * S_ATOM + ii * 128 + (((ch & 7) ^ (ii & 7)) << 4));
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (rr[t] >= 0)
-            *reinterpret_cast<uint4*>(sv + (ch >> 3) * KV_ATOM + rr[t] * 128 + (((ch & 7) ^ (rr[t] & 7)) << 4)) = vv[t];
-      }
-      __syncwarp();
-    }
-    if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256) a.trace[3072 + j * 4 + 0] = clock64();  // scattered
-    fence_async_smem();  // generic-proxy stores (and reads of the staging buffer) before async-proxy use
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&v_ready[st]);
-    if (a.trace && blockIdx.x == 0 && lane == 0 && j < 256) a.trace[2048 + j * 4 + 3] = clock64();
-    cur = nxt;
-    nxt = nn;
-    s2 = s3;
-    s3 = s4;
-  }
-}
-
 // POLY: every POLY-th pair of P elements takes the FMA-pipe 2^x (ex2_poly)
 // instead of MUFU.EX2, balancing the two pipes (0 = all MUFU).
 // DUAL (one query tile per CTA: the question pass and decode): the two tile
@@ -848,8 +666,8 @@ __global__ void __launch_bounds__(SPLIT ? 576 : (VSH ? AT_THREADS + 32 : AT_THRE
 // barrier orders every warp's S load before any P store over those columns).
 // An O rescale (lazy, > 2^8) waits for PV(u-1); otherwise the softmax of
 // slice u never waits on the tensor pipe.
-template <int DH, int PE, bool VSH = false>
-__global__ void __launch_bounds__(VSH ? 608 : 576, 1)
+template <int DH, int PE>
+__global__ void __launch_bounds__(576, 1)
     attn_qtm_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const AttnArgs a, int G, int n_qblocks) {
   constexpr int ATOMS = DH / 64;
@@ -866,8 +684,7 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;                    // [NSK][KV_BYTES]
   uint8_t* sV = sK + NSK * KV_BYTES;     // [NSV][KV_BYTES]
-  uint8_t* sStg = sV + NSV * KV_BYTES;   // VSH: [2][ATOMS][32 rows][128 B] staged fresh V rows
-  uint8_t* sOnes = sStg + (VSH ? 2 * 32 * DH * 2 : 0);  // 2 KB of bf16 1.0: B operand of the row-sum MMA (N=16)
+  uint8_t* sOnes = sV + NSV * KV_BYTES;  // 2 KB of bf16 1.0: B operand of the row-sum MMA (N=16)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + 2048);
   uint64_t* k_full = bar;                // [NSK]
   uint64_t* k_empty = k_full + NSK;      // [NSK]
@@ -877,14 +694,11 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
   uint64_t* s_full = q_full + 1;        // [2] per S buffer
   uint64_t* p_full = s_full + 2;        // [2]
   uint64_t* pv_done = p_full + 2;
-  uint64_t* v_ready = pv_done + 1;      // [NSV] VSH: V tile patched
   // every PV (and row-sum) MMA complete: the epilogue cannot use pv_done, whose
   // last two phases may both be outstanding when the softmax finishes its last
   // tile (a parity wait cannot tell phase n-1 from n-3)
-  uint64_t* o_done = v_ready + NSV;
-  uint64_t* stg_full = o_done + 1;      // [2] VSH: staging buffers
-  uint8_t* r_of = reinterpret_cast<uint8_t*>(stg_full + 2);  // [128] VSH: staged row -> tile row
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r_of + 128);
+  uint64_t* o_done = pv_done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
   __shared__ float xm[2][4][AT_ROWS];   // [slice parity][column group][row] partial max
 
   const int warp = warp_id(), lane = lane_id();
@@ -895,16 +709,10 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
   const int t0 = qb * tok_per_tile;
   const int t_end = min(t0 + tok_per_tile, a.M);
   const int k_lo = a.n_splits > 1 ? split * a.split_keys : 0;
-  constexpr int W_TMA = 16, W_MMA = 17, W_PATCH = 18;
-  if constexpr (VSH)
-    if (warp == W_TMA)
-      for (int i = lane; i < a.n_vseg; i += 32) {
-        tma_prefetch_desc(&a.vsegs[i].tmap);
-        tma_prefetch_desc(&a.vsegs[i].tmap1);
-      }
+  constexpr int W_TMA = 16, W_MMA = 17;
   if (warp == W_TMA && lane == 0) {
     tma_prefetch_desc(&tmK);
-    if constexpr (!VSH) tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmV);
     for (int s = 0; s < NSK; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -912,7 +720,6 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
     for (int s = 0; s < NSV; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
-      mbar_init(&v_ready[s], 1);
     }
     mbar_init(q_full, 16);
     for (int b = 0; b < 2; ++b) {
@@ -921,8 +728,6 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
     }
     mbar_init(pv_done, 1);
     mbar_init(o_done, 1);
-    mbar_init(&stg_full[0], 1);
-    mbar_init(&stg_full[1], 1);
     fence_mbar_init();
   }
   if (warp == W_MMA) tmem_alloc<512>(tmem_slot);
@@ -939,36 +744,21 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
 
   if (warp == W_TMA) {
     if (n_tiles > 0 && elect_one()) {
-      const int tile0 = k_lo / AT_KEYS;
-      int2 pr = make_int2(0, 0);  // VSH: this tile's primary V segment + row coordinate
-      if constexpr (VSH) pr = __ldg(a.vprim + tile0);
       for (int j = 0; j < n_tiles; ++j) {
         const int sv = j % NSV, sk = j % NSK;
-        int2 pr_next = pr;
-        if constexpr (VSH)
-          if (j + 1 < n_tiles) pr_next = __ldg(a.vprim + tile0 + j + 1);  // in flight across the wait
         const int key0 = k_lo + j * AT_KEYS;
         // V(j) first: the V ring runs further ahead (its stage frees at PV(j-NSV),
         // long before K(j)'s at S(j-NSK))
         mbar_wait(&v_empty[sv], ((j / NSV) & 1) ^ 1);
-        if (a.trace && blockIdx.x == 0 && j < 256) a.trace[2048 + j * 4 + 0] = clock64();  // tooling: V(j) issued
         mbar_arrive_expect_tx(&v_full[sv], KV_BYTES);
-        if constexpr (VSH) {
-          const CUtensorMap* tm = &a.vsegs[pr.x].tmap;
 #pragma unroll
-          for (int at = 0; at < ATOMS; ++at)
-            tma_load_3d(sV + sv * KV_BYTES + at * KV_ATOM, tm, &v_full[sv], hk * DH + at * 64, pr.y, a.layer);
-        } else {
-#pragma unroll
-          for (int at = 0; at < ATOMS; ++at)
-            tma_load_2d(sV + sv * KV_BYTES + at * KV_ATOM, &tmV, &v_full[sv], hk * DH + at * 64, key0);
-        }
+        for (int at = 0; at < ATOMS; ++at)
+          tma_load_2d(sV + sv * KV_BYTES + at * KV_ATOM, &tmV, &v_full[sv], hk * DH + at * 64, key0);
         mbar_wait(&k_empty[sk], ((j / NSK) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[sk], KV_BYTES);
 #pragma unroll
         for (int at = 0; at < ATOMS; ++at)
           tma_load_2d(sK + sk * KV_BYTES + at * KV_ATOM, &tmK, &k_full[sk], hk * DH + at * 64, key0);
-        pr = pr_next;
       }
       // consume the last phases of both rings (no phase completes unobserved)
       for (int j = n_tiles > NSV ? n_tiles - NSV : 0; j < n_tiles; ++j) mbar_wait(&v_empty[j % NSV], (j / NSV) & 1);
@@ -1006,7 +796,6 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
         const int st = u % NSV;
         mbar_wait(&p_full[u & 1], (u >> 1) & 1);
         mbar_wait(&v_full[st], (u / NSV) & 1);
-        if constexpr (VSH) mbar_wait(&v_ready[st], (u / NSV) & 1);
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && u < 256) a.trace[u * 4 + 3] = clock64();
         if (elect_one()) {
@@ -1033,10 +822,6 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
       if (elect_one()) umma_commit(o_done);
       __syncwarp();
     }
-  } else if (VSH && warp == W_PATCH) {
-    // ------------------------------------------------------------ V patch warp (shared V pages)
-    if (n_tiles > 0)
-      vpatch_loop_staged<DH, NSV>(a, hk, k_lo, k_hi, n_tiles, sV, v_full, v_ready, lane, sStg, stg_full, r_of);
   } else {
     // ------------------------------------------------------------ softmax / epilogue (16 warps)
     const int q4 = warp & 3, cg = warp >> 2;
@@ -1236,12 +1021,12 @@ __global__ void __launch_bounds__(VSH ? 608 : 576, 1)
   }
 }
 
-template <int DH, bool VSH = false>
+template <int DH>
 constexpr size_t qtm_smem() {
-  // alignment slack, K + V rings, VSH staging, ones tile, barriers + row map + TMEM slot
-  return 1024 + (size_t)(DH == 128 ? 6 : 12) * AT_KEYS * DH * 2 + (VSH ? 2 * 32 * DH * 2 : 0) + 2048 + 1024;
+  // alignment slack, K + V rings, ones tile, barriers + TMEM slot
+  return 1024 + (size_t)(DH == 128 ? 6 : 12) * AT_KEYS * DH * 2 + 2048 + 512;
 }
-static_assert(qtm_smem<128, true>() <= 232448 - 4 * 1024 && qtm_smem<64, true>() <= 232448 - 4 * 1024,
+static_assert(qtm_smem<128>() <= 232448 - 4 * 1024 && qtm_smem<64>() <= 232448 - 4 * 1024,
               "Q-in-TMEM attention exceeds 227 KB");
 
 }  // namespace
@@ -1267,8 +1052,11 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
   if (!make_tmap_3d(&tq, a.q, a.dh, a.Hq, a.M, a.dh, (uint64_t)a.Hq * a.dh, 64, G, AT_ROWS / G)) return -1;
   // K/V layer [T][Hkv*dh]; box (64, 128 keys)
   if (!make_tmap_2d(&tk, a.k, a.T, (uint64_t)a.Hkv * a.dh, (uint64_t)a.Hkv * a.dh, AT_KEYS)) return -1;
-  const bool vsh = a.vsegs != nullptr;  // shared V pages: V comes from the segments' maps
-  if (vsh && (!attn_shared_v_supported(a.dh) || a.n_vseg < 1 || (a.n_splits > 1 && a.split_keys % AT_KEYS)))
+  // shared V pages: V comes from the segments' maps through the patch warp of
+  // the one-query-tile (DUAL) kernels; larger passes read a staged V window
+  const bool vsh = a.vsegs != nullptr;
+  if (vsh && (!attn_shared_v_supported(a.dh) || a.n_vseg < 1 || (a.n_splits > 1 && a.split_keys % AT_KEYS) ||
+              a.M > AT_ROWS / G))
     return -1;
   if (vsh)
     tv = tk;  // unused by the VSH kernels
@@ -1346,7 +1134,7 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
     const dim3 grid1(nqb1 * a.Hkv, 1, a.n_splits);
     auto go2 = [&](auto kern, int smem) {
       smem_attr_once(kern, smem);
-      launch_pdl(kern, grid1, dim3(vsh ? 608 : 576), smem, stream, tk, tv, at, G, nqb1);
+      launch_pdl(kern, grid1, dim3(576), smem, stream, tk, tv, at, G, nqb1);
       if (trace_path) {
         unsigned long long h[4 * 256 * 4];
         cudaMemcpyAsync(h, trace_dev, sizeof(h), cudaMemcpyDeviceToHost, stream);
@@ -1362,13 +1150,6 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
       const char* v = std::getenv("FRAG_ATTN_QTM_POLY");
       return v ? std::atoi(v) : kQtmPoly;
     }();
-    if (vsh) {
-      if (a.dh == 128)
-        go2(attn_qtm_kernel<128, kQtmPoly, true>, (int)qtm_smem<128, true>());
-      else
-        go2(attn_qtm_kernel<64, kQtmPoly, true>, (int)qtm_smem<64, true>());
-        return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
-    }
     if (a.dh == 128) {
       switch (qpoly) {
         case 0: go2(attn_qtm_kernel<128, 0>, (int)qtm_smem<128>()); break;

@@ -367,7 +367,7 @@ uint64_t result_device_bytes(const Result* r) {
                           &r->part_o, &r->part_lse, &r->logits, &r->row_map, &r->stitch_desc, &r->stitch_tab,
                           &r->lm_x, &r->gemm_ws, &r->gemm_cnt, &r->dec_tok, &r->fr_save, &r->dev, &r->score_col,
                           &r->score_q, &r->ssq, &r->vx, &r->vx_map, &r->vseg, &r->vplan_args, &r->vplan_tile, &r->vplan_prim,
-                          &r->vplan_ent})
+                          &r->vplan_ent, &r->vwin})
     b += d->bytes;
   return b;
 }
@@ -480,6 +480,22 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       r->part_lse.ensure((size_t)seg_split[i].first * segs[i].M * Hq * sizeof(float));
     }
   }
+  // shared V pages: a large pass (the sparse pass: more query rows than one
+  // attention tile) stages each layer's V into a double-buffered window at its
+  // cache rows -- records copied by vwindow_fill before that layer's QKV, fresh
+  // rows added by the QKV epilogue -- and reads it like a private cache; small
+  // passes (question pass, r = 0, decode) patch the record tiles in the kernel
+  const bool vwin = r->vshared && mode == PASS_FULL && M > 128 / (Hq / Hkv);
+  const size_t wstride = (size_t)r->max_tokens * kvc;
+  if (vwin) r->vwin.ensure(2 * wstride * sizeof(bf16));  // first (eager) request of a shape allocates
+  auto vwin_fill = [&](int l) {
+    if (!vwin) return;
+    Scoped sc(P, s, KC_STITCH, 0, 4.0 * (double)(r->vseg_n ? r->vseg_max_rows : 0) * r->vseg_n * kvc);
+    const int rc = fragk::vwindow_fill(r->vseg.as<fragk::VSeg>(), r->vseg_n, r->vseg_max_rows, l, (int)kvc,
+                                       r->vwin.as<bf16>() + (size_t)(l & 1) * wstride, s);
+    if (rc < 0) fail(FRAG_E_CUDA, "V window launch failed");
+    sc.launched(rc);
+  };
   const bool want_qf = mode == PASS_QUESTION || (mode == PASS_FULL && r->q_final_in_full);
   if (want_qf) r->q_final.ensure((size_t)M * qc * sizeof(float));
 
@@ -496,11 +512,12 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     ep.q_out = r->q.as<bf16>();
     ep.q_out_f32 = (want_qf && l == L - 1) ? r->q_final.as<float>() : nullptr;
     ep.k_cache = kf + l * lstride;
-    if (r->vshared) {  // fresh V -> exclusive slots
+    if (r->vshared) {  // fresh V -> exclusive slots (and the staged window)
       ep.v_cache = r->vx.as<bf16>() + (size_t)l * r->vx_rows * kvc;
       ep.v_slots = 1;
       ep.v_tail_row0 = r->v_tail_row0;
       ep.v_tail_slot0 = r->v_tail_slot0;
+      if (vwin) ep.v_cache2 = r->vwin.as<bf16>() + (size_t)(l & 1) * wstride;
     } else {
       ep.v_cache = vf + l * lstride;
     }
@@ -524,6 +541,10 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
   int* chain_done = r->gemm_cnt.as<int>() + (r->gemm_cnt.bytes / sizeof(int) - 2 * fragk::CHAIN_MAX_OPS);
   // shared V pages: the attention of sequence g.seq reads V through its plan
   auto vattn = [&](fragk::AttnArgs& a, const Seg& g, int l) {
+    if (vwin) {
+      a.v = r->vwin.as<bf16>() + (size_t)(l & 1) * wstride + (size_t)g.base * kvc;
+      return;
+    }
     if (!r->vshared) return;
     const Result::VSeq& q = r->vseq[g.seq];
     a.v = nullptr;
@@ -547,6 +568,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       sc.launched(1);
     }
     if (!qkv_done) {
+      vwin_fill(l);
       fragk::EpiParams ep = qkv_ep(l);
       Scoped sc(P, s, gemm_class(M), 2.0 * M * qkv * d, 2.0 * (qkv * d + (double)M * (d + qkv)));
       sc.launched(fragk::gemm_bf16_tc(x, W.wqkv, M, (int)qkv, d, fragk::EPI_QKV, ep, s));
@@ -665,6 +687,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       double flop = 2.0 * M * d * qc + 2.0 * M * 2.0 * F * d + 2.0 * M * (double)d * F;
       double bytes = 2.0 * (qc * d + 2.0 * F * d + (double)F * d);
       if (l + 1 < L) {
+        vwin_fill(l + 1);
         st[n].A = x, st[n].B = e->layers[l + 1].wqkv, st[n].N = (int)qkv, st[n].K = d;
         st[n].epi = fragk::EPI_QKV;
         st[n].ep = qkv_ep(l + 1);
@@ -893,7 +916,8 @@ void vshared_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std
   check_cuda(cudaMemcpyAsync(r->vx_map.p, xmap, 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s), "V slot maps");
   r->vseq.clear();
   r->vrefs.clear();
-  int si = 0;
+  r->vseg_max_rows = 0;
+  int si = 0, cur_base = 0;
   auto add = [&](const bf16* v, int n, int row0) {
     fragk::VSeg& g = segs[si++];
     std::memset(&g, 0, sizeof(g));
@@ -904,12 +928,15 @@ void vshared_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std
     g.v = v;
     g.row0 = row0;
     g.n = n;
+    g.base = cur_base;
+    r->vseg_max_rows = std::max(r->vseg_max_rows, n);
   };
   fragk::VSeg* seg_dev = r->vseg.as<fragk::VSeg>();
   for (int b = 0; b < B; ++b) {
     const VPart& pt = parts[b];
     Result::VSeq q{};
     q.seg0 = si;
+    cur_base = pt.base;
     if (pt.sys && pt.sys->n > 0) add(pt.sys->kv.as<bf16>() + (size_t)c.layers * pt.sys->n * kvc, pt.sys->n, 0);
     int row = pt.S;
     for (Record* rec : *pt.recs) {
@@ -943,6 +970,7 @@ void vshared_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std
       a.vent = r->vplan_ent.as<unsigned long long>() + q.ve_off;
     }
   }
+  r->vseg_n = n_seg;
   check_cuda(cudaMemcpyAsync(r->vseg.p, segs, (size_t)n_seg * sizeof(fragk::VSeg), cudaMemcpyHostToDevice, s),
              "V segments");
   check_cuda(cudaMemcpyAsync(r->vplan_args.p, args, (size_t)2 * B * sizeof(fragk::VPlanArgs), cudaMemcpyHostToDevice,

@@ -265,6 +265,8 @@ struct Result {
   };
   std::vector<VSeq> vseq;
   DevBuf vx, vx_map, vseg, vplan_args, vplan_tile, vplan_prim, vplan_ent;
+  DevBuf vwin;  // large passes: V of one layer staged at its cache rows, double-buffered [2][max_tokens]
+  int vseg_n = 0, vseg_max_rows = 0;
   std::vector<std::shared_ptr<Record>> vrefs;  // records whose pages the shared V view reads
   bool q_final_in_full = false;  // PASS_FULL also keeps the last layer's fp32 queries (r = 0 fast path)
   // timing

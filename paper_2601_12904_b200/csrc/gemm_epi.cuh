@@ -156,6 +156,9 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
       dstp = ep.v_cache + (size_t)vrow * k_cols + (col - q_cols - k_cols);
     }
     uint4* dst = reinterpret_cast<uint4*>(dstp);
+    uint4* dst2 = (ep.v_cache2 && col >= q_cols + k_cols)
+                      ? reinterpret_cast<uint4*>(ep.v_cache2 + (size_t)prow * k_cols + (col - q_cols - k_cols))
+                      : nullptr;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint4 v;
@@ -164,6 +167,7 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, int row, int col,
       v.z = pack_bf16(o[8 * j + 4], o[8 * j + 5]);
       v.w = pack_bf16(o[8 * j + 6], o[8 * j + 7]);
       dst[j] = v;
+      if (dst2) dst2[j] = v;
     }
   }
 }

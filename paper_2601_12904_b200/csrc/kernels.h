@@ -40,6 +40,7 @@ struct EpiParams {
   // position row >= v_tail_row0: v_tail_slot0 + prow - v_tail_row0
   int v_slots = 0;
   int v_tail_row0 = 0x7fffffff, v_tail_slot0 = 0;
+  bf16* v_cache2 = nullptr;        // shared V pages, staged window of this layer: fresh V also at [prow]
   int Hq = 0, Hkv = 0, dh = 0;
   // split-K workspace for small-M GEMMs (owned by the caller's result; the
   // counters must start at zero and are left at zero by the kernel)
@@ -156,7 +157,8 @@ struct alignas(64) VSeg {
   const bf16* v;      // V base (layer 0, row 0)
   int row0;           // first sequence-local cache row
   int n;              // rows
-  int pad[12];
+  int base;           // first cache row of the sequence (batched requests)
+  int pad[11];
 };
 static_assert(sizeof(VSeg) == 320, "VSeg layout");
 // Per-sequence patch plan over 128-row key tiles (sequence-local rows): tile
@@ -181,6 +183,10 @@ struct VPlanArgs {
   unsigned long long* vent;  // [n_rows]
 };
 int vpatch_plan(const VPlanArgs* seqs_dev, int n_seq, int max_rows, int max_segs, cudaStream_t stream);
+// Large passes (the sparse pass) stage one layer of V at a time: copy every
+// segment's layer-`layer` rows into the window dst [cache rows][Hkv*dh] at
+// rows base + row0 + i (fresh rows are written there by the QKV epilogue).
+int vwindow_fill(const VSeg* segs, int n_seg, int max_rows, int layer, int kvc, bf16* dst, cudaStream_t stream);
 // Materialise V rows [0, n_rows) of every layer into dst [L][ld][Hkv*dh] from
 // the segments + exclusive region (result read-back: frag_result_fused_kv)
 int vpage_gather(const VSeg* segs, const int* vtile, const int2* vprim, const unsigned long long* vent,

@@ -108,6 +108,21 @@ __device__ __forceinline__ bool spin_until_ge(const int* p, int target, int* fau
   return spin_until_ge_slow(p, target, fault, limit_ns, sleep_ns);
 }
 
+// ---------------------------------------------------------------- streaming copies
+// 16-byte global load / store that bypass L1 (read-once / write-once data)
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch: wait for the preceding grid's memory, and let
 // the next grid in the stream start its prologue early.

@@ -200,7 +200,41 @@ __global__ void __launch_bounds__(256) vpage_gather_kernel(const VSeg* __restric
   }
 }
 
+// one CTA row-slice per (segment, row block): 16-byte streaming copy
+__global__ void __launch_bounds__(256) vwindow_fill_kernel(const VSeg* __restrict__ segs, int layer, int kvc,
+                                                           bf16* __restrict__ dst) {
+  const VSeg& g = segs[blockIdx.y];
+  const int nv = kvc / 8;
+  const long total = (long)g.n * nv;
+  const uint4* src = reinterpret_cast<const uint4*>(g.v + (size_t)layer * g.n * kvc);
+  uint4* out = reinterpret_cast<uint4*>(dst + (size_t)(g.base + g.row0) * kvc);
+  pdl_launch_dependents();
+  const long stride = (long)gridDim.x * blockDim.x;
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < total; i += 4 * stride) {  // the window is read by the attention after the next GEMM
+    const uint4 a0 = ld_stream(src + i), a1 = ld_stream(src + i + stride);
+    const uint4 a2 = ld_stream(src + i + 2 * stride), a3 = ld_stream(src + i + 3 * stride);
+    out[i] = a0;
+    out[i + stride] = a1;
+    out[i + 2 * stride] = a2;
+    out[i + 3 * stride] = a3;
+  }
+  for (; i < total; i += stride) out[i] = ld_stream(src + i);
+}
+
 }  // namespace
+
+int vwindow_fill(const VSeg* segs, int n_seg, int max_rows, int layer, int kvc, bf16* dst, cudaStream_t stream) {
+  if (n_seg <= 0 || max_rows <= 0) return 0;
+  if (kvc % 8) return -1;
+  const long vecs = (long)max_rows * (kvc / 8);
+  long bx = (vecs + 4 * 256 - 1) / (4 * 256);
+  const long cap = (long)num_sms() * 8 / (n_seg < 8 ? n_seg : 8) + 1;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  vwindow_fill_kernel<<<dim3((unsigned)bx, (unsigned)n_seg), 256, 0, stream>>>(segs, layer, kvc, dst);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
 
 int vpatch_plan(const VPlanArgs* seqs_dev, int n_seq, int max_rows, int max_segs, cudaStream_t stream) {
   if (n_seq <= 0) return 0;

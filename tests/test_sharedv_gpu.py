@@ -81,16 +81,20 @@ def test_shared_v_injected_plan(F, tiny):
     assert np.array_equal(a["v"], b["v"]) and np.array_equal(a["k"], b["k"])
 
 
-def test_records_untouched_and_memory(F, tiny):
+@pytest.mark.parametrize("ratio", [0.0, 0.15])
+def test_records_untouched_and_memory(F, tiny, ratio):
     """The attention reads the records' pages in place; nothing writes them
-    (SPEC.md:173). Without a V read-back the shared request holds no fused V."""
+    (SPEC.md:173). Without a V read-back the shared request holds no fused V:
+    only its exclusive slots and, for a sparse pass, a two-layer staging window
+    (which for this 2-layer model is as large as the whole V -- hence r = 0,
+    whose single pass reads the records directly, for the accounting)."""
     eng, store, system, ids, rng = tiny
     before = [store.read_kv(i) for i in ids]
     q = rng.integers(0, eng.cfg.vocab, 32).tolist()
     T = len(system) + sum(store.peek(i).n_tok for i in ids) + len(q)
     F.set_shared_v(True)
     res = F.Result(eng, T)
-    eng.reprocess(store, q, ids, 0.15, res, system=system)
+    eng.reprocess(store, q, ids, ratio, res, system=system)
     mem_shared, sv = res.memory()
     assert sv
     for i, (k0, v0) in zip(ids, before):
@@ -98,12 +102,13 @@ def test_records_untouched_and_memory(F, tiny):
         assert np.array_equal(k0, k1) and np.array_equal(v0, v1)
     F.set_shared_v(False)
     res2 = F.Result(eng, T)
-    eng.reprocess(store, q, ids, 0.15, res2, system=system)
+    eng.reprocess(store, q, ids, ratio, res2, system=system)
     mem_private, sv2 = res2.memory()
     assert not sv2
     c = eng.cfg
     v_bytes = c.layers * T * c.n_kv_heads * c.head_dim * 2
-    assert mem_private - mem_shared >= v_bytes * 0.7, (mem_private, mem_shared, v_bytes)
+    window = 2 * T * c.n_kv_heads * c.head_dim * 2 if ratio > 0 else 0
+    assert mem_private - mem_shared >= 0.9 * (v_bytes - window) - 65536, (mem_private, mem_shared, v_bytes)
     F.set_shared_v(True)
 
 
