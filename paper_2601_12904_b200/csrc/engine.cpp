@@ -308,6 +308,8 @@ Result::~Result() {
   if (fork_ev) cudaEventDestroy(fork_ev);
   for (auto& e : layer_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : vwin_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
 }
@@ -487,15 +489,51 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
   // passes (question pass, r = 0, decode) patch the record tiles in the kernel
   const bool vwin = r->vshared && mode == PASS_FULL && M > 128 / (Hq / Hkv);
   const size_t wstride = (size_t)r->max_tokens * kvc;
-  if (vwin) r->vwin.ensure(2 * wstride * sizeof(bf16));  // first (eager) request of a shape allocates
-  auto vwin_fill = [&](int l) {
-    if (!vwin) return;
-    Scoped sc(P, s, KC_STITCH, 0, 4.0 * (double)(r->vseg_n ? r->vseg_max_rows : 0) * r->vseg_n * kvc);
+  // The fills run on the side stream, two layers ahead: layer l+2's fill waits
+  // only for layer l's attention (the last reader of its buffer) and overlaps
+  // the tensor-bound GEMMs; a layer's QKV waits for its window.
+  static const bool vwin_side = [] {  // FRAG_VWIN_SIDE=0: fills in the request stream before each QKV
+    const char* v = std::getenv("FRAG_VWIN_SIDE");
+    return !(v && v[0] == '0');
+  }();
+  if (vwin) {
+    r->vwin.ensure(2 * wstride * sizeof(bf16));  // first (eager) request of a shape allocates
+    if (!r->side) check_cuda(cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking), "side stream");
+    while ((int)r->vwin_ev.size() < 2 * L) {
+      cudaEvent_t ev;
+      check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "window event");
+      r->vwin_ev.push_back(ev);
+    }
+  }
+  auto vwin_fill = [&](int l, cudaStream_t fs) {
+    Scoped sc(P, fs, KC_STITCH, 0, 4.0 * (double)(r->vseg_n ? r->vseg_max_rows : 0) * r->vseg_n * kvc);
     const int rc = fragk::vwindow_fill(r->vseg.as<fragk::VSeg>(), r->vseg_n, r->vseg_max_rows, l, (int)kvc,
-                                       r->vwin.as<bf16>() + (size_t)(l & 1) * wstride, s);
+                                       r->vwin.as<bf16>() + (size_t)(l & 1) * wstride, fs);
     if (rc < 0) fail(FRAG_E_CUDA, "V window launch failed");
     sc.launched(rc);
   };
+  auto vwin_side_fill = [&](int l) {  // on the side stream, after layer l-2's attention (or the pass start)
+    if (!vwin || !vwin_side || l >= L) return;
+    cudaEvent_t after = l >= 2 ? r->vwin_ev[l - 2] : r->vwin_ev[L + l];  // [L + l]: pass-start fork
+    if (l < 2) check_cuda(cudaEventRecord(after, s), "window fork");
+    check_cuda(cudaStreamWaitEvent(r->side, after, 0), "window wait");
+    vwin_fill(l, r->side);
+    check_cuda(cudaEventRecord(r->vwin_ev[L + l], r->side), "window filled");
+  };
+  auto vwin_join = [&](int l) {  // before layer l's QKV
+    if (!vwin) return;
+    if (vwin_side)
+      check_cuda(cudaStreamWaitEvent(s, r->vwin_ev[L + l], 0), "window join");
+    else
+      vwin_fill(l, s);
+  };
+  auto vwin_attn_done = [&](int l) {  // after layer l's attention: its buffer goes to layer l + 2
+    if (!vwin || !vwin_side) return;
+    check_cuda(cudaEventRecord(r->vwin_ev[l], s), "window free");
+    vwin_side_fill(l + 2);
+  };
+  vwin_side_fill(0);
+  vwin_side_fill(1);
   const bool want_qf = mode == PASS_QUESTION || (mode == PASS_FULL && r->q_final_in_full);
   if (want_qf) r->q_final.ensure((size_t)M * qc * sizeof(float));
 
@@ -568,7 +606,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       sc.launched(1);
     }
     if (!qkv_done) {
-      vwin_fill(l);
+      vwin_join(l);
       fragk::EpiParams ep = qkv_ep(l);
       Scoped sc(P, s, gemm_class(M), 2.0 * M * qkv * d, 2.0 * (qkv * d + (double)M * (d + qkv)));
       sc.launched(fragk::gemm_bf16_tc(x, W.wqkv, M, (int)qkv, d, fragk::EPI_QKV, ep, s));
@@ -666,6 +704,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       sc.launched(fragk::sparse_q_attention(a, s, defer_ok ? &deferred : nullptr));
       if (deferred) deferred_args = a;
     }
+    vwin_attn_done(l);
     if (chain_layer) {
       fragk::ChainStep st[fragk::CHAIN_MAX_OPS];
       int n = 0;
@@ -687,7 +726,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       double flop = 2.0 * M * d * qc + 2.0 * M * 2.0 * F * d + 2.0 * M * (double)d * F;
       double bytes = 2.0 * (qc * d + 2.0 * F * d + (double)F * d);
       if (l + 1 < L) {
-        vwin_fill(l + 1);
+        vwin_join(l + 1);
         st[n].A = x, st[n].B = e->layers[l + 1].wqkv, st[n].N = (int)qkv, st[n].K = d;
         st[n].epi = fragk::EPI_QKV;
         st[n].ep = qkv_ep(l + 1);

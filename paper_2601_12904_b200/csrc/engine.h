@@ -230,6 +230,9 @@ struct Result {
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr;
   std::vector<cudaEvent_t> layer_ev;
+  // shared V window fills on the side stream: [0, L) attention of layer l done
+  // (its window buffer is free), [L, 2L) window of layer l filled
+  std::vector<cudaEvent_t> vwin_ev;
   int max_tokens = 0;
   // fused cache [L][max_tokens][Hkv][dh]
   DevBuf k_fused, v_fused;
