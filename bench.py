@@ -38,8 +38,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-N_CLASSES = 7  # frag_engine_profile_read classes (frag_c.h)
-CLASS_NAMES = ["gemm", "attention", "stitch", "norm", "select", "gemm_stream", "gemm_gateup"]
+N_CLASSES = 8  # frag_engine_profile_read classes (frag_c.h)
+CLASS_NAMES = ["gemm", "attention", "stitch", "norm", "select", "gemm_stream", "gemm_gateup", "vwindow"]
 METRIC = "TTFT ms at 16k-token RAG prompt, 15% recompute vs full prefill; prefill tok/s"
 CONFIGS = {
     "llama3-8b": dict(preset="llama3-8b", chunks=8, chunk_len=2048, qlen=32, ratio=0.15),
@@ -343,6 +343,7 @@ def run_ours(args, rank, world, local_rank):
     ms = ev0.elapsed_time(ev1)
     launches = F.launch_count() - launches0
     crit = res.crit()
+    mem_shared = res.memory()  # before any V read-back / full prefill allocates a private fused V
 
     # ---- per-kernel-class device time: the same K requests again with CUDA
     # events around every launch on the launching stream (kept out of the
@@ -428,6 +429,7 @@ def run_ours(args, rank, world, local_rank):
     f1.record(stream)
     torch.cuda.synchronize()
     full_ms = f0.elapsed_time(f1) / args.full_steps
+    mem_private = res.memory()  # the full prefill keeps a private fused V [L][max_tokens]
 
     sweep = {}
     for r in [float(x) for x in args.sweep.split(",") if x.strip()]:
@@ -490,7 +492,8 @@ def run_ours(args, rank, world, local_rank):
     return dict(ms=ms, e2e_ms=e2e_ms, full_ms=full_ms, launches=launches, prof=prof, stages=stages, T=T,
                 crit=crit, clocks=clk.summary(), cfg=c, w=w, ratio=ratio, h2d=h2d, d2h=d2h, sweep=sweep,
                 k=len(crit), decode_ms=decode_ms, n_dec=len(answer), load_leg=load_leg,
-                cacheblend_ms=cacheblend_ms, cacheblend_stages=cacheblend_stages, batch_leg=batch_leg)
+                cacheblend_ms=cacheblend_ms, cacheblend_stages=cacheblend_stages, batch_leg=batch_leg,
+                mem_shared=mem_shared, mem_private=mem_private)
 
 
 def spawn_ranks(n: int, argv: list[str], backend_env: dict | None = None) -> int:
@@ -669,7 +672,17 @@ def main():
         "attention": {"achieved_tflops": attn_flops / (a["ms"] / args.steps / 1e3) / 1e12 if a["ms"] else None,
                       "flops_per_step": attn_flops},
         "stitch": {"achieved_gbs": (r["prof"][2]["bytes"] / (r["prof"][2]["ms"] / 1e3) / 1e9)
-                   if r["prof"][2]["ms"] else None, "peak_gbs": hbm},
+                   if r["prof"][2]["ms"] else None, "peak_gbs": hbm,
+                   "bytes_per_step": r["prof"][2]["bytes"] / args.steps},
+        "vwindow": {"achieved_gbs": (r["prof"][7]["bytes"] / (r["prof"][7]["ms"] / 1e3) / 1e9)
+                    if r["prof"][7]["ms"] else None, "peak_gbs": hbm,
+                    "note": "shared V pages: per-layer V window fills of the sparse pass (side stream, overlapped "
+                            "with the GEMMs)"},
+        "hbm_per_request": {"shared_v_bytes": r["mem_shared"][0], "shared_v": r["mem_shared"][1],
+                            "private_v_bytes": r["mem_private"][0],
+                            "note": "device bytes held by the request's result: fused K + exclusive V slots + "
+                                    "staging window + workspaces (shared V pages) vs the same result once it holds "
+                                    "a private fused V (full prefill)"},
         "gemm_stream": {"achieved_gbs": (r["prof"][5]["bytes"] / (r["prof"][5]["ms"] / 1e3) / 1e9)
                         if r["prof"][5]["ms"] else None, "peak_gbs": hbm,
                         "note": "one-M-tile GEMMs (question pass, lm_head): algorithmic bytes = weights + rows"},

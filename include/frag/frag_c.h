@@ -380,7 +380,9 @@ FRAG_API frag_status frag_result_debug(const frag_result* res, const float** q_f
  * (K2/K3), 4 select (K9/K10), 5 weight-streaming GEMM (<= 128 rows: the
  * question pass and lm_head rows; algorithmic bytes = weight bytes), 6 the
  * gate/up projection GEMM alone at > 128 rows (a subset of class 0: the
- * single largest kernel, the bench's roofline kernel). */
+ * single largest kernel, the bench's roofline kernel), 7 the shared-V window
+ * fills of the large passes (records' V of one layer copied into the staging
+ * window; algorithmic bytes = read + write). */
 FRAG_API frag_status frag_engine_profile(frag_engine* eng, int32_t enable);
 /* Sums over launches since the last reset (call after frag_result_sync):
  * device ms, algorithmic FLOPs, algorithmic bytes, launch count. */

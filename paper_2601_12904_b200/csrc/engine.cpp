@@ -482,12 +482,13 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
       r->part_lse.ensure((size_t)seg_split[i].first * segs[i].M * Hq * sizeof(float));
     }
   }
-  // shared V pages: a large pass (the sparse pass: more query rows than one
-  // attention tile) stages each layer's V into a double-buffered window at its
-  // cache rows -- records copied by vwindow_fill before that layer's QKV, fresh
-  // rows added by the QKV epilogue -- and reads it like a private cache; small
-  // passes (question pass, r = 0, decode) patch the record tiles in the kernel
-  const bool vwin = r->vshared && mode == PASS_FULL && M > 128 / (Hq / Hkv);
+  // shared V pages: a large pass (more query rows than one attention tile: the
+  // sparse pass, long or batched questions) stages each layer's V into a
+  // double-buffered window at its cache rows -- records copied by vwindow_fill
+  // before that layer's QKV, fresh rows added by the QKV epilogue -- and reads
+  // it like a private cache; small passes (the question pass of <= 128/G
+  // tokens, r = 0, decode) patch the record tiles inside the attention kernel
+  const bool vwin = r->vshared && M > 128 / (Hq / Hkv);
   const size_t wstride = (size_t)r->max_tokens * kvc;
   // The fills run on the side stream, two layers ahead: layer l+2's fill waits
   // only for layer l's attention (the last reader of its buffer) and overlaps
@@ -506,7 +507,7 @@ void run_rows(Engine* e, Result* r, cudaStream_t s, int M, int T, PassMode mode,
     }
   }
   auto vwin_fill = [&](int l, cudaStream_t fs) {
-    Scoped sc(P, fs, KC_STITCH, 0, 4.0 * (double)(r->vseg_n ? r->vseg_max_rows : 0) * r->vseg_n * kvc);
+    Scoped sc(P, fs, KC_VWIN, 0, 4.0 * (double)r->vseg_rows * kvc);  // read + write, bf16
     const int rc = fragk::vwindow_fill(r->vseg.as<fragk::VSeg>(), r->vseg_n, r->vseg_max_rows, l, (int)kvc,
                                        r->vwin.as<bf16>() + (size_t)(l & 1) * wstride, fs);
     if (rc < 0) fail(FRAG_E_CUDA, "V window launch failed");
@@ -956,6 +957,7 @@ void vshared_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std
   r->vseq.clear();
   r->vrefs.clear();
   r->vseg_max_rows = 0;
+  r->vseg_rows = 0;
   int si = 0, cur_base = 0;
   auto add = [&](const bf16* v, int n, int row0) {
     fragk::VSeg& g = segs[si++];
@@ -969,6 +971,7 @@ void vshared_prepare(Engine* e, Result* r, cudaStream_t s, Stage& stg, const std
     g.n = n;
     g.base = cur_base;
     r->vseg_max_rows = std::max(r->vseg_max_rows, n);
+    r->vseg_rows += n;
   };
   fragk::VSeg* seg_dev = r->vseg.as<fragk::VSeg>();
   for (int b = 0; b < B; ++b) {

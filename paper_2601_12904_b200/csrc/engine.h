@@ -78,8 +78,9 @@ struct DeviceGuard {
 // KC_GEMM: tensor-bound GEMMs (M > 128 rows); KC_GEMM_STREAM: one-M-tile
 // GEMMs (question pass, lm_head rows), bound by the weight stream from HBM.
 // KC_GEMM_GU: the gate/up projection at M > 128 alone (also counted in KC_GEMM)
+// KC_VWIN: shared V pages, the per-layer V window fills of the large passes
 enum KClass { KC_GEMM = 0, KC_ATTN = 1, KC_STITCH = 2, KC_NORM = 3, KC_SELECT = 4, KC_GEMM_STREAM = 5, KC_GEMM_GU = 6,
-              KC_N = 7 };
+              KC_VWIN = 7, KC_N = 8 };
 inline int gemm_class(int M) { return M <= 128 ? KC_GEMM_STREAM : KC_GEMM; }
 struct Profiler {
   bool on = false;
@@ -269,7 +270,7 @@ struct Result {
   std::vector<VSeq> vseq;
   DevBuf vx, vx_map, vseg, vplan_args, vplan_tile, vplan_prim, vplan_ent;
   DevBuf vwin;  // large passes: V of one layer staged at its cache rows, double-buffered [2][max_tokens]
-  int vseg_n = 0, vseg_max_rows = 0;
+  int vseg_n = 0, vseg_max_rows = 0, vseg_rows = 0;
   std::vector<std::shared_ptr<Record>> vrefs;  // records whose pages the shared V view reads
   bool q_final_in_full = false;  // PASS_FULL also keeps the last layer's fp32 queries (r = 0 fast path)
   // timing

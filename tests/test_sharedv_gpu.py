@@ -159,3 +159,27 @@ def test_graph_replay_shared_v(F, tiny):
         assert np.array_equal(cr, ref["crit"]) and np.array_equal(lg, ref["logits"])
         assert np.array_equal(v, ref["v"])
     F.set_shared_v(True)
+
+
+@pytest.mark.parametrize("nq,ratio", [(32, 0.15), (50, 0.05), (32, 0.0)])
+def test_shared_v_8b_width(F, nq, ratio):
+    """Llama-3-8B width (GQA 32/8: one attention tile = 32 tokens), 2 layers,
+    4 x 512 chunks: the sparse pass stages V through the window, the 32-row
+    question pass patches record tiles in the kernel, a 50-row question pass
+    uses the window too; decode patches. Bit-identical to the private layout."""
+    cfg = F.preset("llama3-8b")
+    cfg.layers = 2
+    eng = F.Engine(cfg, seed=77)
+    store = F.ChunkKVStore(eng.cfg)
+    rng = np.random.default_rng(nq)
+    ids = [eng.preprocess_isolated(store, rng.integers(0, eng.cfg.vocab, 512).tolist()) for _ in range(4)]
+    q = rng.integers(0, eng.cfg.vocab, nq).tolist()
+    T = 4 * 512 + nq
+    a = _run(F, eng, store, q, ids, ratio, (), True, T + 8, decode=4)
+    b = _run(F, eng, store, q, ids, ratio, (), False, T + 8, decode=4)
+    assert a["mem"][1] and not b["mem"][1]
+    assert np.array_equal(a["crit"], b["crit"])
+    assert np.array_equal(a["logits"], b["logits"])
+    assert np.array_equal(a["k"], b["k"]) and np.array_equal(a["v"], b["v"])
+    assert np.array_equal(a["tok"], b["tok"]) and np.array_equal(a["logits_dec"], b["logits_dec"])
+    F.set_shared_v(True)
