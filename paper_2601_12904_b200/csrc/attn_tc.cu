@@ -795,6 +795,11 @@ __global__ void __launch_bounds__(576, 1)
       auto issue_pv = [&](int u) {
         const int st = u % NSV;
         mbar_wait(&p_full[u & 1], (u >> 1) & 1);
+        // observe pv_done phase u-1 (no phase completes unwaited; PV(u-2) is
+        // known complete here -- S(u) was, and the pipe is in order -- so the
+        // parity is unambiguous); PV(u-1) has normally finished while the
+        // softmax of slice u ran
+        if (u > 0) mbar_wait(pv_done, (u - 1) & 1);
         mbar_wait(&v_full[st], (u / NSV) & 1);
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && u < 256) a.trace[u * 4 + 3] = clock64();
@@ -821,6 +826,7 @@ __global__ void __launch_bounds__(576, 1)
       }
       if (elect_one()) umma_commit(o_done);
       __syncwarp();
+      mbar_wait(pv_done, (n_tiles - 1) & 1);  // the last phase (PV(n-2) observed above)
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue (16 warps)
