@@ -117,6 +117,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
   const int splits = ep.splits > 1 ? ep.splits : 1;
   const int n_full = splits > 1 ? ep.full_tiles : num_tiles;
   const int num_work = n_full + (num_tiles - n_full) * splits;
+  // tile -> (m_blk, n_blk): groups of GM M-blocks, M fastest inside a group
+  // (GM = m_tiles: plain M-fastest order)
+  const int GM = ep.group_m > 0 && ep.group_m < m_tiles ? ep.group_m : m_tiles;
+  auto tile_mn = [&](int t, int& mb, int& nb) {
+    const int per_group = GM * n_tiles;
+    const int g = t / per_group, idx = t - g * per_group;
+    const int gm = min(GM, m_tiles - g * GM);
+    mb = g * GM + idx % gm;
+    nb = idx / gm;
+  };
   auto decode = [&](int w, int& tile, int& sp, int& S) {
     if (w < n_full) {
       tile = w, sp = 0, S = 1;
@@ -153,7 +163,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
       if (pair < num_work) {
         int tile, sp, S;
         decode(pair, tile, sp, S);
-        const int n_blk = tile / m_tiles;
+        int m_blk, n_blk;
+        tile_mn(tile, m_blk, n_blk);
         const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
         npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
         for (int i = 0; i < npre; ++i) {
@@ -171,7 +182,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
       for (int w = pair; w < num_work; w += n_pairs) {
         int tile, sp, S;
         decode(w, tile, sp, S);
-        const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
+        int m_blk, n_blk;
+        tile_mn(tile, m_blk, n_blk);
         const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
@@ -239,7 +251,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
     for (int w = pair; w < num_work; w += n_pairs) {
       int tile, sp, S;
       decode(w, tile, sp, S);
-      const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
+      int m_blk, n_blk;
+      tile_mn(tile, m_blk, n_blk);
       const int row = m_blk * BM2 + rank * 128 + row_in_tile;
       // folded RMSNorm scale, loaded while the MMAs run
       const float rs = row < M ? epi_row_scale<EPI>(ep, row) : 1.f;
@@ -301,8 +314,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
 }
 
 template <int BN, int EPI>
-int launch2(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& ep, cudaStream_t stream) {
+int launch2(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& ep0, cudaStream_t stream) {
   using C = Gemm2Cfg<BN>;
+  static const int group_env = [] {  // FRAG_GEMM_GROUP_M: tile raster, M blocks per group (tuning)
+    const char* v = std::getenv("FRAG_GEMM_GROUP_M");
+    return v ? std::atoi(v) : 0;
+  }();
+  EpiParams ep = ep0;
+  if (group_env > 0) ep.group_m = group_env;
   smem_attr_once(gemm_tc2_kernel<BN, EPI>, (int)C::SMEM);
   CUtensorMap ta, tb;
   if (!make_tmap_2d(&ta, A, M, K, K, 128)) return -1;

@@ -51,6 +51,7 @@ struct EpiParams {
   int splits = 1;      // set by gemm_bf16_tc: K splits of each tail tile
   int full_tiles = 0;  // tiles before the split tail
   int streamk = 0;     // set by gemm_bf16_tc: stream-K decomposition (one M tile)
+  int group_m = 0;     // CTA-pair GEMM tile raster: M blocks per group (0: all, M fastest)
   int sk_maxc = 0;     // stream-K: max CTAs sharing one tile (workspace slots per tile)
   unsigned long long* trace = nullptr;  // tooling: per-CTA globaltimer stamps (FRAG_GEMM_TRACE)
   // RMSNorm folded into the GEMMs (K3): norm(h)·Wᵀ = rs(h) · (h·Wᵀ) with unit
