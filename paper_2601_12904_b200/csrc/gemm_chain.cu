@@ -60,7 +60,9 @@ struct ChainArgs {
   AttnArgs pre;  // split-KV attention whose combine writes op 0's A operand
   int pre_rows;  // (token, head) rows to combine; 0 = no pre-op
   int timeline;  // tooling (FRAG_CHAIN_TRACE=1): globaltimer stamps into g_chain_tl
+  int flow;      // 1: units continue round-robin across ops and A loads wait per producer tile
 };
+
 
 // Tooling timeline, graph-replay safe: launch n writes ring slot n % TL_LAUNCHES
 // (n = g_chain_seq, read after griddepcontrol.wait and bumped by the last CTA
@@ -134,6 +136,22 @@ __device__ __forceinline__ void chain_unit(const ChainOp& op, int u, int& tile, 
 }
 __device__ __forceinline__ int chain_units(const ChainOp& op) {
   return (op.N / CBN) * (op.splits > 1 ? op.splits : 1);
+}
+
+// Units of op o run on CTAs (unit + base_o) % G, base_o = units of the
+// earlier ops: one round-robin over the whole chain, so op o's first units
+// land on the CTAs op o-1 left idle (its last partial wave). Per-tile
+// completion counters of op o (tdone) let op o+1's A loads wait only for the
+// producer tiles of their k-block: op o+1 streams weights and starts its MMAs
+// while op o's tail, fixups and epilogues finish.
+__device__ __forceinline__ int chain_first_unit(const ChainArgs& a, int o, int G) {
+  if (!a.flow) return blockIdx.x;
+  int base = 0;
+  for (int i = 0; i < o; ++i) base += chain_units(a.op[i]);
+  return ((int)blockIdx.x - base % G + G) % G;
+}
+__device__ __forceinline__ int* chain_tdone(const ChainArgs& a, int o) {
+  return a.op[o].ep.counters + (CHAIN_MAX_OPS + o) * CHAIN_CNT_STRIDE;
 }
 
 // Epilogue of one unit (4 warps, named barrier 1): direct fused epilogue, or
@@ -232,71 +250,114 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
-      const unsigned long long t_entry = gtime();
-      unsigned long long* tl = nullptr;
-      pdl_launch_dependents();
-      int stage = 0;
-      uint32_t phase = 0;
-      auto advance = [&]() {
-        if (++stage == CSTAGES) stage = 0, phase ^= 1;
-      };
-      for (int o = 0; o < n_ops; ++o) {
-        const ChainOp& op = args.op[o];
-        const CUtensorMap* tA = &args.tmA[o];
-        const CUtensorMap* tB = &args.tmB[o];
-        const int units = chain_units(op);
-        // weights first: the first unit's leading stages, before waiting on
-        // the op that produces this op's A rows
-        int npre = 0, st_pre = stage;
-        int tile, kb0, kb1, sp, S;
-        if ((int)blockIdx.x < units) {
-          chain_unit(op, blockIdx.x, tile, kb0, kb1, sp, S);
-          npre = kb1 - kb0 < CSTAGES ? kb1 - kb0 : CSTAGES;
-          for (int i = 0; i < npre; ++i) {
+    // lane 0 issues; with flow the whole warp polls the A producer tiles
+    const unsigned long long t_entry = gtime();
+    unsigned long long* tl = nullptr;
+    if (lane == 0) pdl_launch_dependents();
+    int stage = 0;
+    uint32_t phase = 0;
+    auto advance = [&]() {
+      if (++stage == CSTAGES) stage = 0, phase ^= 1;
+    };
+    for (int o = 0; o < n_ops; ++o) {
+      const ChainOp& op = args.op[o];
+      const CUtensorMap* tA = &args.tmA[o];
+      const CUtensorMap* tB = &args.tmB[o];
+      const int units = chain_units(op);
+      const int u0 = chain_first_unit(args, o, G);
+      // weights first: the first unit's leading stages, before waiting on
+      // the op that produces this op's A rows
+      int npre = 0, st_pre = stage;
+      int tile, kb0, kb1, sp, S;
+      if (u0 < units) {
+        chain_unit(op, u0, tile, kb0, kb1, sp, S);
+        npre = kb1 - kb0 < CSTAGES ? kb1 - kb0 : CSTAGES;
+        for (int i = 0; i < npre; ++i) {
+          if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], CSTAGE_BYTES);
             tma_load_2d(sB + stage * CSTAGE_BYTES, tB, &full[stage], (kb0 + i) * CBK, tile * CBN);
-            advance();
           }
+          advance();
         }
-        if (o == 0) {
-          pdl_wait();  // every CTA, before it reads any counter of this launch
+      }
+      if (o == 0) {
+        pdl_wait();  // every CTA, before it reads any counter of this launch
+        if (lane == 0) {
           tl = chain_tl(args);
           if (tl) tl[0] = t_entry, tl[1] = gtime();
         }
-        if ((int)blockIdx.x >= units) continue;
+      }
+      if (u0 >= units) continue;
+      // A readiness: op 0 -- the in-chain combine (all CTAs); op o > 0 -- with
+      // flow, the producer tile of each k-block (SWIGLU: one tile per 64 act
+      // columns; RESID: one per 128 x columns), polled 32 tiles at a time;
+      // without flow, every unit of op o-1
+      const ChainOp* prev = o > 0 ? &args.op[o - 1] : nullptr;
+      const int* ptd = o > 0 ? chain_tdone(args, o - 1) : nullptr;
+      const int p_tiles = o > 0 ? prev->N / CBN : 0;
+      const int p_need = o > 0 ? (prev->splits > 1 ? prev->splits : 1) : 0;
+      const bool p_swiglu = o > 0 && prev->epi == EPI_SWIGLU;
+      int win_base = -64;
+      unsigned win_mask = 0u;
+      auto a_ready = [&](int kb) {
+        if (o == 0 || !args.flow) return;
+        const int pt = p_swiglu ? kb : (kb >> 1);
+        const int off = pt - win_base;
+        if (off >= 0 && off < 32 && ((win_mask >> off) & 1u)) return;
+        for (;;) {
+          win_base = pt;
+          const int t = pt + lane;
+          const bool ok = t >= p_tiles || ld_acquire_gpu(ptd + t) >= p_need;
+          win_mask = __ballot_sync(0xffffffffu, ok);
+          if (win_mask & 1u) break;
+          if (lane == 0) wait_count(ptd + pt, p_need, args.op[0].ep);
+          __syncwarp();
+        }
+        __syncwarp();  // orders the lanes' acquires before lane 0's loads
+        if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+      };
+      if (lane == 0) {
         if (o == 0) {
           if (args.pre_rows > 0) {  // op 0's A rows come from the in-chain combine
             wait_count(&args.done[CHAIN_MAX_OPS + 1], G, args.op[0].ep);
             asm volatile("fence.proxy.async.global;" ::: "memory");
           }
-        } else {
+        } else if (!args.flow) {
           wait_count(&args.done[o - 1], chain_units(args.op[o - 1]), args.op[0].ep);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
         }
-        chain_stamp(tl, o, 0);
-        for (int i = 0, s2 = st_pre; i < npre; ++i, s2 = s2 + 1 == CSTAGES ? 0 : s2 + 1)
-          tma_load_2d(sA + s2 * CSTAGE_BYTES, tA, &full[s2], (kb0 + i) * CBK, 0);
-        for (int kb = kb0 + npre; kb < kb1; ++kb) {
+      }
+      __syncwarp();
+      if (lane == 0) chain_stamp(tl, o, 0);
+      for (int i = 0, s2 = st_pre; i < npre; ++i, s2 = s2 + 1 == CSTAGES ? 0 : s2 + 1) {
+        a_ready(kb0 + i);
+        if (lane == 0) tma_load_2d(sA + s2 * CSTAGE_BYTES, tA, &full[s2], (kb0 + i) * CBK, 0);
+      }
+      for (int kb = kb0 + npre; kb < kb1; ++kb) {
+        a_ready(kb);
+        if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], CSTAGE_BYTES);
           tma_load_2d(sB + stage * CSTAGE_BYTES, tB, &full[stage], kb * CBK, tile * CBN);
           tma_load_2d(sA + stage * CSTAGE_BYTES, tA, &full[stage], kb * CBK, 0);
-          advance();
         }
-        for (int u = blockIdx.x + G; u < units; u += G) {
-          chain_unit(op, u, tile, kb0, kb1, sp, S);
-          for (int kb = kb0; kb < kb1; ++kb) {
+        advance();
+      }
+      for (int u = u0 + G; u < units; u += G) {
+        chain_unit(op, u, tile, kb0, kb1, sp, S);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          a_ready(kb);
+          if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], CSTAGE_BYTES);
             tma_load_2d(sB + stage * CSTAGE_BYTES, tB, &full[stage], kb * CBK, tile * CBN);
             tma_load_2d(sA + stage * CSTAGE_BYTES, tA, &full[stage], kb * CBK, 0);
-            advance();
           }
+          advance();
         }
-        chain_stamp(tl, o, 1);
       }
+      if (lane == 0) chain_stamp(tl, o, 1);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -308,7 +369,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
     for (int o = 0; o < n_ops; ++o) {
       const ChainOp& op = args.op[o];
       const int units = chain_units(op);
-      for (int u = blockIdx.x; u < units; u += G) {
+      for (int u = chain_first_unit(args, o, G); u < units; u += G) {
         int tile, kb0, kb1, sp, S;
         chain_unit(op, u, tile, kb0, kb1, sp, S);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -362,7 +423,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
     for (int o = 0; o < n_ops; ++o) {
       const ChainOp& op = args.op[o];
       const int units = chain_units(op);
-      if ((int)blockIdx.x >= units) continue;
+      const int u0 = chain_first_unit(args, o, G);
+      if (u0 >= units) continue;
       // this op's epilogue reads / writes what the earlier ops of the chain wrote
       if (o > 0) wait_count(&args.done[o - 1], chain_units(args.op[o - 1]), args.op[0].ep);
       if (o > 1) wait_count(&args.done[o - 2], chain_units(args.op[o - 2]), args.op[0].ep);
@@ -400,12 +462,12 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
           default: break;
         }
       }
-      for (int u = blockIdx.x; u < units; u += G) {
+      for (int u = u0; u < units; u += G) {
         int tile, kb0, kb1, sp, S;
         chain_unit(op, u, tile, kb0, kb1, sp, S);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        if (u == (int)blockIdx.x) chain_stamp(tl, o, 2);
+        if (u == u0) chain_stamp(tl, o, 2);
         const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * CBN;
         switch (op.epi) {
           case EPI_RESID:
@@ -422,9 +484,12 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
                                            rs, ts);
             break;
         }
-        // unit complete (its outputs written): publish
+        // unit complete (its outputs written): publish the unit and its tile share
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && lane == 0) red_release(&args.done[o], 1);
+        if (warp == 2 && lane == 0) {
+          red_release(&args.done[o], 1);
+          if (args.flow) red_release(chain_tdone(args, o) + tile, 1);
+        }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -448,7 +513,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         args.done[o] = 0;
         const int tiles = args.op[o].N / CBN;
         int* cnt = args.op[o].ep.counters + o * CHAIN_CNT_STRIDE;
-        for (int t = 0; t < tiles; ++t) cnt[t] = 0;
+        int* td = chain_tdone(args, o);
+        for (int t = 0; t < tiles; ++t) cnt[t] = 0, td[t] = 0;
       }
       *exit_cnt = 0;
       if (args.timeline) g_chain_seq = g_chain_seq + 1;
@@ -488,7 +554,7 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
     while (s < 8 && tiles * (s + 1) <= sms && nk / (s + 1) >= 4) ++s;
     if (s > nk) s = nk;
     if ((size_t)(tiles * s * M * CBN) * sizeof(float) > st.ep.ws_bytes) s = 1;
-    if (tiles > CHAIN_CNT_STRIDE || (o + 1) * CHAIN_CNT_STRIDE > st.ep.counters_cap) return -1;
+    if (tiles > CHAIN_CNT_STRIDE || (CHAIN_MAX_OPS + o + 1) * CHAIN_CNT_STRIDE > st.ep.counters_cap) return -1;
     ChainOp& op = args.op[o];
     op.N = st.N;
     op.K = st.K;
@@ -504,6 +570,11 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
   }
   static const bool timeline = std::getenv("FRAG_CHAIN_TRACE") != nullptr;  // tooling only
   args.timeline = timeline ? 1 : 0;
+  static const bool flow = [] {  // FRAG_CHAIN_FLOW=0: per-op barriers, every op's units from CTA 0
+    const char* v = std::getenv("FRAG_CHAIN_FLOW");
+    return !(v && v[0] == '0');
+  }();
+  args.flow = flow ? 1 : 0;
   auto go = [&](auto kern, size_t smem) {
     smem_attr_once(kern, (int)smem);
     if (resident_blocks(kern, CHAIN_THREADS, (int)smem) < 1) return false;  // one CTA per SM must fit

@@ -27,7 +27,7 @@ for _ in range(3):
     L.check(L.lib.frag_kernel_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), rows.data_ptr(), out.data_ptr(),
                                         M, T, Hq, Hkv, dh, 0, None))
 torch.cuda.synchronize()
-rec = np.fromfile(path, dtype=np.uint64).reshape(-1, 2, 256, 4)[-1].astype(np.int64)
+rec = np.fromfile(path, dtype=np.uint64).reshape(-1, 4, 256, 4)[-1].astype(np.int64)
 a, b = rec[0], rec[1]
 n = int((a[:, 0] > 0).sum())
 s_ready, p_done, s_iss, pv_iss = (a[:n, i] for i in range(4))
