@@ -694,8 +694,9 @@ FRAG_API frag_status frag_kernel_rope_shift(const void* k_src, void* k_dst, int3
                          delta == 0 ? -1 : 0};
     check_cuda(cudaMemcpy(dtab.p, tab.data(), half * sizeof(float2), cudaMemcpyHostToDevice), "tab");
     check_cuda(cudaMemcpy(ddesc.p, &c, sizeof(c), cudaMemcpyHostToDevice), "desc");
-    fragk::rope_shift_assemble(ddesc.as<fragk::StitchChunk>(), 1, n_tok, dtab.as<float2>(), static_cast<bf16*>(k_dst),
-                               vtmp.as<bf16>(), L, n_tok, Hkv, dh, s);
+    if (fragk::rope_shift_assemble(ddesc.as<fragk::StitchChunk>(), 1, n_tok, dtab.as<float2>(),
+                                   static_cast<bf16*>(k_dst), vtmp.as<bf16>(), L, n_tok, Hkv, dh, s) < 0)
+      fail(FRAG_E_CONTRACT, "kernel launch rejected the shape");
     g_launches += 1;
     check_cuda(cudaStreamSynchronize(s), "rope_shift");
   });

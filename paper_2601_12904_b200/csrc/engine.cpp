@@ -1039,11 +1039,10 @@ void stitch_launch(Engine* e, Result* r, cudaStream_t s, const StitchPlan& p, in
   if (l1 < 0) l1 = c.layers;
   Scoped sc(e->prof, s, KC_STITCH, 0, p.bytes * (l1 - l0) / c.layers);
   // shared V pages: K only (V stays in the records)
-  fragk::rope_shift_assemble(r->stitch_desc.as<fragk::StitchChunk>(), p.n_desc, p.max_rows,
-                             r->stitch_tab.as<float2>(), r->k_fused.as<bf16>(),
-                             r->vshared ? nullptr : r->v_fused.as<bf16>(), l1 - l0, r->max_tokens, c.n_kv_heads,
-                             c.head_dim, s, l0);
-  sc.launched(1);
+  sc.launched(fragk::rope_shift_assemble(r->stitch_desc.as<fragk::StitchChunk>(), p.n_desc, p.max_rows,
+                                         r->stitch_tab.as<float2>(), r->k_fused.as<bf16>(),
+                                         r->vshared ? nullptr : r->v_fused.as<bf16>(), l1 - l0, r->max_tokens,
+                                         c.n_kv_heads, c.head_dim, s, l0));
   peek("stitch");
 }
 

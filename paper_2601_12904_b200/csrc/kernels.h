@@ -135,7 +135,7 @@ struct StitchChunk {
   int table;           // index into the per-chunk cos/sin table; -1 = zero shift (bit copy)
 };
 // fused K/V [L][T][Hkv][dh]; tables: [n_tables][dh/2] float2 for delta*theta_i.
-void rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_rows, const float2* tables,
+int rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_rows, const float2* tables,
                          bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream,
                          int layer0 = 0);
 

@@ -3,6 +3,8 @@
 //                             PAPER.md:1040-1049 Appendix A re-positioning)
 //   K2+K3 embed_rmsnorm, K3 rmsnorm  (SPEC.md:128 pre-norm decoder)
 //   init_normal_bf16          (SPEC.md:94-102 init_model from the common.hpp:45-100 Rng)
+#include <cstdlib>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -26,38 +28,43 @@ __device__ __forceinline__ uint32_t rot_pair(uint32_t kv, float2 cs) {
 // Per layer the record block [n][Hkv][dh] and its fused destination
 // [dst_row : dst_row+n][Hkv][dh] are both contiguous, so all accesses are
 // fully coalesced 128-bit streams.
+// One CTA row-slice per (chunk = blockIdx.y, layer = blockIdx.z): the
+// destination offset of a source vector is then a sum, with no per-vector
+// 64-bit division (those made the K-only copy issue-bound: 4.0 vs 5.0 TB/s).
 // KV = false (shared V pages): only K is rotated into the fused cache, V stays
-// in the records; 4 independent 16-byte loads per thread either way.
-template <bool KV>
+// in the records. U independent 16-byte loads per thread and step.
+template <bool KV, int U>
 __global__ void __launch_bounds__(256) rope_shift_kernel(const StitchChunk* __restrict__ chunks,
                                                          const float2* __restrict__ tables, bf16* __restrict__ kf,
-                                                         bf16* __restrict__ vf, int L, int T, int Hkv, int dh,
-                                                         int layer0) {
-  constexpr int U = KV ? 2 : 4;  // rows of K (and V) per unrolled step
+                                                         bf16* __restrict__ vf, int T, int Hkv, int dh, int layer0) {
   const StitchChunk c = chunks[blockIdx.y];
+  const int l = layer0 + (int)blockIdx.z;
   const int vec_per_row = (Hkv * dh) >> 3;  // 16-byte vectors per token row
-  const long per_layer = (long)c.n_tok * vec_per_row;
-  const long total = per_layer * L;  // layers [layer0, layer0 + L)
-  const int dvec = dh >> 3;
+  const int per_layer = c.n_tok * vec_per_row;
+  const int dmask = (dh >> 3) - 1;  // dh / 8 vectors per head (a power of two: 8 or 16)
   const float2* tab = c.table >= 0 ? tables + (size_t)c.table * (dh >> 1) : nullptr;
-  const uint4* ks = reinterpret_cast<const uint4*>(c.k_src) + layer0 * per_layer;
-  const uint4* vs = reinterpret_cast<const uint4*>(c.v_src) + layer0 * per_layer;
-  const long layer_stride_dst = (long)T * vec_per_row;
-  const long dst0 = (long)c.dst_row * vec_per_row + layer0 * layer_stride_dst;
-  uint4* kd = reinterpret_cast<uint4*>(kf);
-  uint4* vd = reinterpret_cast<uint4*>(vf);
-  const long stride = (long)gridDim.x * blockDim.x;
-  auto rot = [&](uint4& k, long r) {
+  const uint4* ks = reinterpret_cast<const uint4*>(c.k_src) + (size_t)l * per_layer;
+  const uint4* vs = reinterpret_cast<const uint4*>(c.v_src) + (size_t)l * per_layer;
+  const size_t dst0 = ((size_t)l * T + c.dst_row) * vec_per_row;
+  uint4* kd = reinterpret_cast<uint4*>(kf) + dst0;
+  uint4* vd = reinterpret_cast<uint4*>(vf) + dst0;
+  const int stride = gridDim.x * blockDim.x;  // a multiple of dh / 8: a thread's vectors share one head offset
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  float2 cs[4] = {};  // this thread's four cos/sin pairs, loaded once
+  if (tab) {
+    const int p = (i & dmask) * 4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cs[e] = tab[p + e];
+  }
+  auto rot = [&](uint4& k, int) {
     if (tab) {
-      const int p = (int)(r % dvec) * 4;
-      k.x = rot_pair(k.x, tab[p]);
-      k.y = rot_pair(k.y, tab[p + 1]);
-      k.z = rot_pair(k.z, tab[p + 2]);
-      k.w = rot_pair(k.w, tab[p + 3]);
+      k.x = rot_pair(k.x, cs[0]);
+      k.y = rot_pair(k.y, cs[1]);
+      k.z = rot_pair(k.z, cs[2]);
+      k.w = rot_pair(k.w, cs[3]);
     }
   };
-  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + (U - 1) * stride < total; i += U * stride) {
+  for (; i + (U - 1) * stride < per_layer; i += U * stride) {
     uint4 k[U], v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -66,21 +73,16 @@ __global__ void __launch_bounds__(256) rope_shift_kernel(const StitchChunk* __re
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const long iu = i + u * stride;
-      const long l = iu / per_layer, r = iu - l * per_layer;
-      rot(k[u], r);
-      const long o = l * layer_stride_dst + dst0 + r;
-      st_stream(kd + o, k[u]);
-      if constexpr (KV) st_stream(vd + o, v[u]);
+      rot(k[u], i + u * stride);
+      st_stream(kd + i + u * stride, k[u]);
+      if constexpr (KV) st_stream(vd + i + u * stride, v[u]);
     }
   }
-  for (; i < total; i += stride) {
+  for (; i < per_layer; i += stride) {
     uint4 k0 = ld_stream(ks + i);
-    const long l0 = i / per_layer, r0 = i - l0 * per_layer;
-    rot(k0, r0);
-    const long o0 = l0 * layer_stride_dst + dst0 + r0;
-    st_stream(kd + o0, k0);
-    if constexpr (KV) st_stream(vd + o0, ld_stream(vs + i));
+    rot(k0, i);
+    st_stream(kd + i, k0);
+    if constexpr (KV) st_stream(vd + i, ld_stream(vs + i));
   }
 }
 
@@ -207,20 +209,24 @@ __global__ void fill_kernel(bf16* dst, size_t n, float v) {
 
 }  // namespace
 
-void rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_rows, const float2* tables,
-                         bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream,
-                         int layer0) {
-  if (n_chunks <= 0 || max_rows <= 0 || L <= 0) return;
-  const long vecs = (long)max_rows * L * (Hkv * dh / 8);
-  long bx = (vecs + 2 * 256 - 1) / (2 * 256);
-  const long cap = (long)num_sms() * 8 / (n_chunks < 8 ? n_chunks : 8) + 1;
-  if (bx > cap) bx = cap;
+int rope_shift_assemble(const StitchChunk* chunks_dev, int n_chunks, int max_rows, const float2* tables,
+                        bf16* k_fused, bf16* v_fused, int L, int T, int Hkv, int dh, cudaStream_t stream,
+                        int layer0) {
+  if (n_chunks <= 0 || max_rows <= 0 || L <= 0) return 0;
+  if ((long)max_rows * (Hkv * dh / 8) >= (1L << 31) || ((dh / 8) & (dh / 8 - 1)) || L > 65535 || n_chunks > 65535)
+    return -1;
+  // about 8 CTAs per SM over (row slices x chunks x layers)
+  const long slices = (long)n_chunks * L;
+  long bx = ((long)num_sms() * 8 + slices - 1) / slices;
+  const long need = ((long)max_rows * (Hkv * dh / 8) + 255) / 256;  // one vector per thread at most
+  if (bx > need) bx = need;
   if (bx < 1) bx = 1;
-  dim3 grid((unsigned)bx, (unsigned)n_chunks);
+  const dim3 grid((unsigned)bx, (unsigned)n_chunks, (unsigned)L);
   if (v_fused)
-    rope_shift_kernel<true><<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, L, T, Hkv, dh, layer0);
+    rope_shift_kernel<true, 2><<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, T, Hkv, dh, layer0);
   else  // shared V pages: K only
-    rope_shift_kernel<false><<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, L, T, Hkv, dh, layer0);
+    rope_shift_kernel<false, 4><<<grid, 256, 0, stream>>>(chunks_dev, tables, k_fused, v_fused, T, Hkv, dh, layer0);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 void embed_rmsnorm(const bf16* E, const int* tok, int M, int d, const bf16* gain, float eps, float* h, bf16* x,
