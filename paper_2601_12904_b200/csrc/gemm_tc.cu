@@ -616,14 +616,15 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
   // the B200 sweep (profiles/gemm_tune_r01.txt) for the projection shapes.
   if (!force_bn && M >= 256 && N % 256 == 0 && ep.splits == 1) {
     // Wave quantisation on 74 CTA pairs: 192-wide tiles (partial last N tile)
-    // when they cut the wave-weighted tile width by >= 15 % (O and down
-    // projections at M~2.5k: 160 -> 220 tiles, 3 waves of 0.75 the work);
-    // otherwise 256. Tail split-K only pays for long K (the FFN down
+    // when they cut the wave-weighted tile width by >= 5 % (O and down
+    // projections at M~2.5k: 160 -> 220 tiles, 3 waves of 0.75 the work; QKV:
+    // 4 waves x 256 -> 5 x 192, 109.8 -> 103.9 us in the round-2 ncu sweep,
+    // tools/_run9.sh); otherwise 256 (gate/up, every M~16k shape). Tail split-K only pays for long K (the FFN down
     // projection): at K=4096 the partial write + fixup cost what the shorter
     // last wave saves (tools/gemm_tune.py, profiles/gemm_tune_r01.txt).
     const long m_t = (M + 255) / 256, pairs = num_sms() / 2;
     const long w256 = (m_t * (N / 256) + pairs - 1) / pairs, w192 = (m_t * ((N + 191) / 192) + pairs - 1) / pairs;
-    const int bn2 = (w192 * 192 * 100 <= w256 * 256 * 85) ? 192 : 256;
+    const int bn2 = (w192 * 192 * 100 <= w256 * 256 * 95) ? 192 : 256;
     return gemm_bf16_tc_pair(A, B, M, N, K, epi, ep, stream, bn2,
                              (force_bn_flags & 0x20000) == 0 && K >= 8192);
   }
