@@ -1363,6 +1363,7 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   const bool vsh = !cacheblend && N > 0 && 2L * k <= N && shared_v_enabled() &&
                    fragk::attn_shared_v_supported(c.head_dim) && records_local(e, recs);
   if (vsh) {
+    if (!r->vshared) r->v_fused.release();  // an earlier request's private V (a read-back view is kept)
     r->vshared = true;
     r->v_materialized = false;
     r->v_tail_row0 = T - n_q;  // question rows (and decoded tokens) -> slots k, k+1, ...
@@ -1649,6 +1650,7 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
   for (int b = 0; b < B && vsh; ++b)
     vsh = br[b].N > 0 && 2L * br[b].k <= br[b].N && records_local(e, recs[b]);
   if (vsh) {
+    if (!r->vshared) r->v_fused.release();
     r->vshared = true;
     r->v_materialized = false;
     r->v_tail_row0 = 0x7fffffff;  // every fresh row at its GEMM row's slot

@@ -183,3 +183,29 @@ def test_shared_v_8b_width(F, nq, ratio):
     assert np.array_equal(a["k"], b["k"]) and np.array_equal(a["v"], b["v"])
     assert np.array_equal(a["tok"], b["tok"]) and np.array_equal(a["logits_dec"], b["logits_dec"])
     F.set_shared_v(True)
+
+
+def test_result_keeps_shared_pages_alive(F):
+    """A result reading records in place keeps their pages alive: destroying
+    the store (or overwriting its records) after the request leaves the
+    result's V view and its decode intact."""
+    eng = F.Engine("tiny", seed=99)
+    rng = np.random.default_rng(3)
+    chunks = [rng.integers(0, eng.cfg.vocab, 256).tolist() for _ in range(4)]
+    q = rng.integers(0, eng.cfg.vocab, 16).tolist()
+    T = 4 * 256 + 16
+    F.set_shared_v(True)
+    store = F.ChunkKVStore(eng.cfg)
+    ids = [eng.preprocess_isolated(store, ch) for ch in chunks]
+    ref = F.Result(eng, T + 8)
+    eng.reprocess(store, q, ids, 0.15, ref)
+    want_v = ref.fused_kv()[1]
+    want_tok = np.asarray(eng.decode(ref, 6))
+    res = F.Result(eng, T + 8)
+    eng.reprocess(store, q, ids, 0.15, res)
+    assert res.memory()[1]
+    store.close()  # the records' pages are still referenced by res
+    assert np.array_equal(res.fused_kv()[1], want_v)
+    assert np.array_equal(np.asarray(eng.decode(res, 6)), want_tok)
+    res.close()
+    ref.close()
