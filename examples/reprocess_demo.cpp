@@ -54,6 +54,8 @@ int main(int argc, char** argv) {
     std::printf("answer:");
     for (auto tok : answer) std::printf(" %d", tok);
     std::printf("\n");
+    const auto mem = res.memory();  // shared V pages: the chunks' V rows stay in the store's records
+    std::printf("result memory %.1f MB, shared V pages %s\n", mem.first / 1e6, mem.second ? "yes" : "no");
     return 0;
   } catch (const frag::CudaError& e) {
     std::fprintf(stderr, "CudaError: %s\n", e.what());

@@ -17,6 +17,7 @@
 #include <memory>
 #include <span>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "frag/core.hpp"
@@ -141,6 +142,9 @@ class ChunkStore {
 
 class Engine;
 
+// Shared V pages on / off for the process (frag_set_shared_v); returns the previous setting.
+inline bool set_shared_v(bool on) { return frag_set_shared_v(on ? 1 : 0) != 0; }
+
 // Fused KV cache + first-token logits of one request; reusable.
 class Result {
  public:
@@ -183,8 +187,16 @@ class Result {
     check(frag_result_timing(h_, &t));
     return t;
   }
-  // device pointers [L][T][Hkv][dh] bf16
+  // device pointers [L][max_tokens][Hkv][dh] bf16, rows [0, tokens) valid; with
+  // shared V pages the V view is assembled from the records on this call
   void fused_kv(const void** k, const void** v, int32_t* tokens) const { check(frag_result_fused_kv(h_, k, v, tokens)); }
+  // device bytes held by the result and whether its last request read V in place
+  std::pair<uint64_t, bool> memory() const {
+    uint64_t b = 0;
+    int32_t sv = 0;
+    check(frag_result_memory(h_, &b, &sv));
+    return {b, sv != 0};
+  }
   frag_result* handle() const { return h_; }
 
  private:

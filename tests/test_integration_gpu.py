@@ -31,3 +31,4 @@ def test_cpp_demo_runs_on_device(cuda, tmp_path):
     assert ans, r.stdout
     toks = [int(x) for x in ans.group(1).split()]
     assert len(toks) == 16 and toks[0] == int(m.group(3)) and all(0 <= t < 256 for t in toks)
+    assert re.search(r"result memory [\d.]+ MB, shared V pages yes", r.stdout), r.stdout
