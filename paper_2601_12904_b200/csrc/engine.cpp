@@ -1361,7 +1361,8 @@ void reprocess(Engine* e, Store* st, const int32_t* sys, int n_sys, const int32_
   // device's records with at most half of the chunk rows recomputed (the
   // attention patches every fresh row into its V tiles)
   const bool vsh = !cacheblend && N > 0 && 2L * k <= N && shared_v_enabled() &&
-                   fragk::attn_shared_v_supported(c.head_dim) && records_local(e, recs);
+                   fragk::attn_shared_v_supported(c.head_dim) &&
+                   fragk::vpatch_plan_fits(r->max_tokens, n_chunks + 1) && records_local(e, recs);
   if (vsh) {
     if (!r->vshared) r->v_fused.release();  // an earlier request's private V (a read-back view is kept)
     r->vshared = true;
@@ -1648,7 +1649,8 @@ void reprocess_batch(Engine* e, Store* st, const frag_request* reqs, int B, int 
   // reused by several requests of the batch is one set of pages)
   bool vsh = shared_v_enabled() && fragk::attn_shared_v_supported(c.head_dim);
   for (int b = 0; b < B && vsh; ++b)
-    vsh = br[b].N > 0 && 2L * br[b].k <= br[b].N && records_local(e, recs[b]);
+    vsh = br[b].N > 0 && 2L * br[b].k <= br[b].N && fragk::vpatch_plan_fits(slot, (int)recs[b].size() + 1) &&
+          records_local(e, recs[b]);
   if (vsh) {
     if (!r->vshared) r->v_fused.release();
     r->vshared = true;

@@ -184,6 +184,7 @@ struct VPlanArgs {
   unsigned long long* vent;  // [n_rows]
 };
 int vpatch_plan(const VPlanArgs* seqs_dev, int n_seq, int max_rows, int max_segs, cudaStream_t stream);
+bool vpatch_plan_fits(int max_rows, int max_segs);  // the one-CTA plan's shared memory (rows up to ~800k)
 // Large passes (the sparse pass) stage one layer of V at a time: copy every
 // segment's layer-`layer` rows into the window dst [cache rows][Hkv*dh] at
 // rows base + row0 + i (fresh rows are written there by the QKV epilogue).

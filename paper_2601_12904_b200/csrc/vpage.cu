@@ -236,11 +236,17 @@ int vwindow_fill(const VSeg* segs, int n_seg, int max_rows, int layer, int kvc, 
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+static size_t vpatch_plan_smem(int max_rows, int max_segs) {
+  const size_t W = ((size_t)max_rows + 31) / 32, tiles = ((size_t)max_rows + 127) / 128;
+  return (2 * W + tiles + 2 * (size_t)max_segs) * sizeof(int);
+}
+
+bool vpatch_plan_fits(int max_rows, int max_segs) { return vpatch_plan_smem(max_rows, max_segs) <= 227 * 1024 - 256; }
+
 int vpatch_plan(const VPlanArgs* seqs_dev, int n_seq, int max_rows, int max_segs, cudaStream_t stream) {
   if (n_seq <= 0) return 0;
-  const int W = (max_rows + 31) / 32, tiles = (max_rows + 127) / 128;
-  const size_t smem = (size_t)(2 * W + tiles + 2 * max_segs) * sizeof(int);
-  if (smem > 227 * 1024) return -1;
+  const size_t smem = vpatch_plan_smem(max_rows, max_segs);
+  if (!vpatch_plan_fits(max_rows, max_segs)) return -1;
   if (smem > 48 * 1024) smem_attr_once(vpatch_plan_kernel, (int)(227 * 1024));
   launch_pdl(vpatch_plan_kernel, dim3(n_seq), dim3(VP_THREADS), smem, stream, seqs_dev);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
