@@ -209,3 +209,26 @@ def test_result_keeps_shared_pages_alive(F):
     assert np.array_equal(np.asarray(eng.decode(res, 6)), want_tok)
     res.close()
     ref.close()
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13, 14])
+def test_shared_v_random_layouts(F, seed):
+    """Random chunk counts and lengths (boundaries anywhere inside key tiles),
+    random system prompts, question lengths and ratios: shared V pages equal
+    the private layout bit for bit (tiny model)."""
+    rng = np.random.default_rng(seed)
+    eng = F.Engine("tiny", seed=seed)
+    store = F.ChunkKVStore(eng.cfg)
+    n_sys = int(rng.integers(0, 20))
+    system = rng.integers(0, eng.cfg.vocab, n_sys).tolist()
+    lens = rng.integers(1, 400, int(rng.integers(1, 9))).tolist()
+    ids = [eng.preprocess_isolated(store, rng.integers(0, eng.cfg.vocab, n).tolist(), system=system) for n in lens]
+    q = rng.integers(0, eng.cfg.vocab, int(rng.integers(1, 70))).tolist()
+    ratio = float(rng.choice([0.0, 0.02, 0.1, 0.25, 0.5]))
+    T = n_sys + sum(lens) + len(q)
+    a = _run(F, eng, store, q, ids, ratio, system, True, T + 4, decode=4)
+    b = _run(F, eng, store, q, ids, ratio, system, False, T + 4, decode=4)
+    assert np.array_equal(a["crit"], b["crit"]) and np.array_equal(a["logits"], b["logits"])
+    assert np.array_equal(a["k"], b["k"]) and np.array_equal(a["v"], b["v"])
+    assert np.array_equal(a["tok"], b["tok"])
+    F.set_shared_v(True)
