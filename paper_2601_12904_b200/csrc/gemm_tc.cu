@@ -619,7 +619,7 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
     // when they cut the wave-weighted tile width by >= 5 % (O and down
     // projections at M~2.5k: 160 -> 220 tiles, 3 waves of 0.75 the work; QKV:
     // 4 waves x 256 -> 5 x 192, 109.8 -> 103.9 us in the round-2 ncu sweep,
-    // tools/_run9.sh); otherwise 256 (gate/up, every M~16k shape). Tail split-K only pays for long K (the FFN down
+    // tools/gemm_bn_sweep.sh); otherwise 256 (gate/up, every M~16k shape). Tail split-K only pays for long K (the FFN down
     // projection): at K=4096 the partial write + fixup cost what the shorter
     // last wave saves (tools/gemm_tune.py, profiles/gemm_tune_r01.txt).
     const long m_t = (M + 255) / 256, pairs = num_sms() / 2;
