@@ -80,6 +80,17 @@ def test_contract_errors_before_any_device_work():
         F.Engine(cfg)
 
 
+def test_shared_v_switch_is_process_wide_and_queryable():
+    """frag_set_shared_v: -1 queries, 1 / 0 set and return the previous value
+    (no device needed; the request path reads it)."""
+    prev = F.set_shared_v(None)
+    assert prev is True  # default on (FRAG_SHARED_V unset)
+    assert F.set_shared_v(False) is True
+    assert F.set_shared_v(None) is False
+    assert F.set_shared_v(True) is False
+    assert F.set_shared_v(None) is True
+
+
 def _gxx():
     for c in ("/usr/bin/g++", shutil.which("g++")):
         if c and Path(c).exists():
