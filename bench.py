@@ -64,8 +64,8 @@ def l2_note(w, c):
     kv = 2 * c["layers"] * T * c["n_kv_heads"] * c["head_dim"] * 2
     if wbytes + kv < 126e6:
         return "fits in L2 (tiny test config, not a headline run)"
-    return (f"inputs larger than L2 ({wbytes / 1e9:.1f} GB weights, {kv / 1e9:.1f} GB fused KV per request "
-            f"streamed every step)")
+    return (f"inputs larger than L2 ({wbytes / 1e9:.1f} GB weights, {kv / 2e9:.1f} GB fused K + "
+            f"{kv / 2e9:.1f} GB of the records' V pages per request, streamed every step)")
 
 
 def cpu_model() -> str:
