@@ -130,7 +130,12 @@ __device__ __forceinline__ void chain_fixup(const EpiParams& ep, int* cnt, int s
 __device__ __forceinline__ void chain_unit(const ChainOp& op, int u, int& tile, int& kb0, int& kb1, int& sp,
                                            int& S) {
   S = op.splits > 1 ? op.splits : 1;
-  tile = u / S, sp = u % S;
+  if (op.sp_major) {  // the CTAs dealt an op's first units get the lowest k-ranges
+    const int tiles = op.N / CBN;
+    sp = u / tiles, tile = u % tiles;
+  } else {
+    tile = u / S, sp = u % S;
+  }
   const int nk = op.K / CBK;
   kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
 }
@@ -540,6 +545,10 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
   args.M = M;
   args.done = done;
   const long sms = num_sms();
+  static const int sp_major = [] {  // FRAG_CHAIN_SPMAJOR=0: split units tile-major
+    const char* v = std::getenv("FRAG_CHAIN_SPMAJOR");
+    return v ? std::atoi(v) : 1;
+  }();
   for (int o = 0; o < n_ops; ++o) {
     const ChainStep& st = steps[o];
     if (!gemm_chain_supported(M, st.N, st.K) || !st.ep.ws || !st.ep.counters) return -1;
@@ -560,6 +569,7 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
     op.K = st.K;
     op.epi = st.epi;
     op.splits = (int)s;
+    op.sp_major = sp_major;
     op.ep = st.ep;
     op.ep.splits = (int)s;
     op.ep.l2_reads = 1;

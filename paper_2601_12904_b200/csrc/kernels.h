@@ -111,6 +111,7 @@ struct ChainStep {
 };
 struct ChainOp {
   int N, K, epi, splits;
+  int sp_major;  // split units numbered split-major (all tiles' split 0 first)
   EpiParams ep;
 };
 bool gemm_chain_supported(int M, int N, int K);
