@@ -34,13 +34,16 @@ namespace {
 constexpr int CBM = 128;  // UMMA M (accumulator rows; rows >= M are never stored)
 constexpr int CBN = 128;
 constexpr int CBK = 64;
+#ifndef CHAIN_STAGES32
+#define CHAIN_STAGES32 11
+#endif
 // AR = live A rows loaded per stage (32 / 64 / 128: M <= AR); stage = AR x 64
 // activations + 128 x 64 weights, as many stages as fit in ~200 KB
 template <int AR>
 struct ChainCfg {
   static constexpr uint32_t A_BYTES = AR * 64 * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + 128 * 64 * 2;
-  static constexpr int STAGES = AR == 32 ? 10 : (AR == 64 ? 8 : 6);
+  static constexpr int STAGES = AR == 32 ? CHAIN_STAGES32 : (AR == 64 ? 8 : 6);
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
   static_assert(STAGE_BYTES >= 128 * 64 * 2, "aliased A rows must stay inside the stage");
   static_assert(SMEM <= 232448, "chain ring exceeds the 227 KB shared-memory limit");
