@@ -554,6 +554,14 @@ int tail_splits(long tiles, long sms, long nk) {
 // (BN=64, BN=128 for very wide N); at M~2.5k BN=128 wins for the N=4k/6k
 // projections and BN=256 for the wide gate/up; long-K (down projection) wants
 // BN=128 with the tail wave split along K; large M (full prefill) wants BN=256.
+static bool pair224_on() {  // FRAG_GEMM_BN224=0: candidates 256 / 192 only
+  static const bool on = [] {
+    const char* v = std::getenv("FRAG_GEMM_BN224");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int gemm_pick_bn(int M, int N, int K) {
   const int m_tiles = (M + BM - 1) / BM;
   int bn;
@@ -622,9 +630,18 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
     // tools/gemm_bn_sweep.sh); otherwise 256 (gate/up, every M~16k shape). Tail split-K only pays for long K (the FFN down
     // projection): at K=4096 the partial write + fixup cost what the shorter
     // last wave saves (tools/gemm_tune.py, profiles/gemm_tune_r01.txt).
+    // 224-wide tiles (not SWIGLU, whose gate/up pairs are 64-aligned) join
+    // the candidates: QKV at M~2.5k, 4 waves x 224 vs 5 x 192.
     const long m_t = (M + 255) / 256, pairs = num_sms() / 2;
-    const long w256 = (m_t * (N / 256) + pairs - 1) / pairs, w192 = (m_t * ((N + 191) / 192) + pairs - 1) / pairs;
-    const int bn2 = (w192 * 192 * 100 <= w256 * 256 * 95) ? 192 : 256;
+    auto width = [&](long bn) { return (m_t * ((N + bn - 1) / bn) + pairs - 1) / pairs * bn; };
+    const long w256 = width(256);
+    int bn2 = 256;
+    long best = w256;
+    for (int cand : {224, 192}) {
+      if (cand == 224 && (epi == EPI_SWIGLU || !pair224_on())) continue;
+      const long w = width(cand);
+      if (w * 100 <= w256 * 95 && w < best) best = w, bn2 = cand;
+    }
     return gemm_bf16_tc_pair(A, B, M, N, K, epi, ep, stream, bn2,
                              (force_bn_flags & 0x20000) == 0 && K >= 8192);
   }

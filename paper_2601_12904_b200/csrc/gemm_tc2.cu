@@ -108,7 +108,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   const int m_tiles = (M + BM2 - 1) / BM2;
-  const int n_tiles = (N + BN - 1) / BN;  // last N tile may be partial (BN = 192)
+  const int n_tiles = (N + BN - 1) / BN;  // last N tile may be partial (BN = 192, 224)
   const int num_tiles = m_tiles * n_tiles;
   const int nk = K / BK2;
   // work items: the first n_full tiles whole, then each tail tile cut into
@@ -346,7 +346,8 @@ int pair_dispatch(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi
 
 int gemm_bf16_tc_pair(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi, const EpiParams& ep,
                       cudaStream_t s, int bn, bool tail_split) {
-  if (K % BK2 != 0 || N % 64 != 0 || (bn != 192 && N % bn != 0)) return -1;
+  if (K % BK2 != 0 || N % 64 != 0 || (bn != 192 && bn != 224 && N % bn != 0)) return -1;
+  if (bn == 224 && epi == EPI_SWIGLU) return -1;
   EpiParams ep2 = ep;
   ep2.splits = 1;
   if (!ep2.fault) ep2.fault = fault_slot_current();
@@ -385,6 +386,14 @@ int pair_dispatch(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi
       case EPI_RESID: return launch2<192, EPI_RESID>(A, B, M, N, K, ep, s);
       case EPI_SWIGLU: return launch2<192, EPI_SWIGLU>(A, B, M, N, K, ep, s);
       case EPI_QKV: return launch2<192, EPI_QKV>(A, B, M, N, K, ep, s);
+    }
+  } else if (bn == 224) {  // not SWIGLU: its gate/up column pairs are 64-aligned
+    switch (epi) {
+      case EPI_STORE_BF16: return launch2<224, EPI_STORE_BF16>(A, B, M, N, K, ep, s);
+      case EPI_STORE_F32: return launch2<224, EPI_STORE_F32>(A, B, M, N, K, ep, s);
+      case EPI_RESID: return launch2<224, EPI_RESID>(A, B, M, N, K, ep, s);
+      case EPI_QKV: return launch2<224, EPI_QKV>(A, B, M, N, K, ep, s);
+      default: return -1;
     }
   } else if (bn == 128) {
     switch (epi) {

@@ -154,14 +154,14 @@ def test_rope_shift_bit_exact(cuda, delta):
 
 @pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 512, 256), (2490, 1024, 4096), (1000, 768, 512),
                                    (2490, 4096, 4096), (1000, 6144, 512)])
-@pytest.mark.parametrize("bn", [128, 192, 256])
+@pytest.mark.parametrize("bn", [128, 192, 224, 256])
 @pytest.mark.parametrize("tail", [0, 1])
 def test_gemm_cta_pair_vs_torch(cuda, M, N, K, bn, tail):
     """cta_group::2 GEMM (256-row tiles shared by a CTA pair); tail=1 splits the
     last partial wave of pairs along K (deterministic cooperative reduction);
-    BN=192 leaves a partial last N tile when N % 192 != 0."""
+    BN=192 / 224 leave a partial last N tile when N % BN != 0."""
     import torch
-    if bn != 192 and N % bn:
+    if bn not in (192, 224) and N % bn:
         pytest.skip("N not a multiple of BN")
     g = torch.Generator(device="cuda").manual_seed(M + N + K + bn)
     a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
