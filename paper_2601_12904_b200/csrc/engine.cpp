@@ -2094,3 +2094,9 @@ void preprocess_fused(Engine* e, Store* src, Store* dst, const int32_t* sys, int
 }
 
 }  // namespace fragimpl
+
+// Tooling (tools/r0_check.py; not part of the frag C API): the allocation
+// epoch that invalidates captured request graphs.
+extern "C" __attribute__((visibility("default"))) unsigned long long frag_debug_alloc_epoch() {
+  return (unsigned long long)fragimpl::g_alloc_epoch.load();
+}

@@ -16,7 +16,10 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2601_12904_b200 import fusion as F  # noqa: E402
 
-tag = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("FRAG_")) or "defaults"
+ballast = None
+if os.environ.get("QB_BALLAST_GB"):  # extra device memory held during the run (TLB / placement check)
+    ballast = torch.empty(int(float(os.environ["QB_BALLAST_GB"]) * 2**30), dtype=torch.uint8, device="cuda")
+tag = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith(("FRAG_", "QB_"))) or "defaults"
 eng = F.Engine("llama3-8b", seed=1)
 c = eng.cfg
 store = F.ChunkKVStore(c)
