@@ -129,9 +129,10 @@ __device__ __forceinline__ void chain_fixup(const EpiParams& ep, int* cnt, int s
   if (row_in_tile < M) reduce_partials<CBN, EPI>(ep, base, (size_t)M * CBN, S, sp, S, row_in_tile, col0, rs);
 }
 
-// unit u of an op: N tile and K range (split sp of S)
-__device__ __forceinline__ void chain_unit(const ChainOp& op, int u, int& tile, int& kb0, int& kb1, int& sp,
-                                           int& S) {
+// unit u of an op: N tile and k-blocks kb0 + i * ks, i < n_kb (split sp of S:
+// a contiguous range, or with ep.k_strided the blocks sp, sp + S, ...)
+__device__ __forceinline__ void chain_unit(const ChainOp& op, int u, int& tile, int& kb0, int& ks, int& n_kb,
+                                           int& sp, int& S) {
   S = op.splits > 1 ? op.splits : 1;
   if (op.sp_major) {  // the CTAs dealt an op's first units get the lowest k-ranges
     const int tiles = op.N / CBN;
@@ -140,7 +141,11 @@ __device__ __forceinline__ void chain_unit(const ChainOp& op, int u, int& tile, 
     tile = u / S, sp = u % S;
   }
   const int nk = op.K / CBK;
-  kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
+  if (op.ep.k_strided && S > 1) {
+    kb0 = sp, ks = S, n_kb = (nk - sp + S - 1) / S;
+  } else {
+    kb0 = sp * nk / S, ks = 1, n_kb = (sp + 1) * nk / S - kb0;
+  }
 }
 __device__ __forceinline__ int chain_units(const ChainOp& op) {
   return (op.N / CBN) * (op.splits > 1 ? op.splits : 1);
@@ -276,15 +281,15 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
       // weights first: the first unit's leading stages, before waiting on
       // the op that produces this op's A rows
       int npre = 0, st_pre = stage;
-      int tile, kb0, kb1, sp, S;
+      int tile, kb0, ks, n_kb, sp, S;
       if (u0 < units) {
-        chain_unit(op, u0, tile, kb0, kb1, sp, S);
-        npre = kb1 - kb0 < CSTAGES ? kb1 - kb0 : CSTAGES;
+        chain_unit(op, u0, tile, kb0, ks, n_kb, sp, S);
+        npre = n_kb < CSTAGES ? n_kb : CSTAGES;
         for (int i = 0; i < npre; ++i) {
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], CSTAGE_BYTES);
-            tma_load_2d(sB + stage * CSTAGE_BYTES, tB, &full[stage], (kb0 + i) * CBK, tile * CBN);
+            tma_load_2d(sB + stage * CSTAGE_BYTES, tB, &full[stage], (kb0 + i * ks) * CBK, tile * CBN);
           }
           advance();
         }
@@ -339,10 +344,11 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
       __syncwarp();
       if (lane == 0) chain_stamp(tl, o, 0);
       for (int i = 0, s2 = st_pre; i < npre; ++i, s2 = s2 + 1 == CSTAGES ? 0 : s2 + 1) {
-        a_ready(kb0 + i);
-        if (lane == 0) tma_load_2d(sA + s2 * CSTAGE_BYTES, tA, &full[s2], (kb0 + i) * CBK, 0);
+        a_ready(kb0 + i * ks);
+        if (lane == 0) tma_load_2d(sA + s2 * CSTAGE_BYTES, tA, &full[s2], (kb0 + i * ks) * CBK, 0);
       }
-      for (int kb = kb0 + npre; kb < kb1; ++kb) {
+      for (int i = npre; i < n_kb; ++i) {
+        const int kb = kb0 + i * ks;
         a_ready(kb);
         if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -353,8 +359,9 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         advance();
       }
       for (int u = u0 + G; u < units; u += G) {
-        chain_unit(op, u, tile, kb0, kb1, sp, S);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        chain_unit(op, u, tile, kb0, ks, n_kb, sp, S);
+        for (int i = 0; i < n_kb; ++i) {
+          const int kb = kb0 + i * ks;
           a_ready(kb);
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
@@ -378,12 +385,12 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
       const ChainOp& op = args.op[o];
       const int units = chain_units(op);
       for (int u = chain_first_unit(args, o, G); u < units; u += G) {
-        int tile, kb0, kb1, sp, S;
-        chain_unit(op, u, tile, kb0, kb1, sp, S);
+        int tile, kb0, ks, n_kb, sp, S;
+        chain_unit(op, u, tile, kb0, ks, n_kb, sp, S);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * CBN;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int i = 0; i < n_kb; ++i) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
@@ -393,10 +400,10 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
             for (int k = 0; k < CBK / 16; ++k) {
               const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
               const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
-              umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+              umma_bf16_ss(d_tmem, ad, bd, idesc, (i != 0 || k != 0) ? 1u : 0u);
             }
             umma_commit(&empty[stage]);
-            if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+            if (i == n_kb - 1) umma_commit(&tfull[acc]);
           }
           __syncwarp();
           if (++stage == CSTAGES) stage = 0, phase ^= 1;
@@ -471,8 +478,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 1) gemm_chain_kernel(const __gr
         }
       }
       for (int u = u0; u < units; u += G) {
-        int tile, kb0, kb1, sp, S;
-        chain_unit(op, u, tile, kb0, kb1, sp, S);
+        int tile, kb0, ks, n_kb, sp, S;
+        chain_unit(op, u, tile, kb0, ks, n_kb, sp, S);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         if (u == u0) chain_stamp(tl, o, 2);
@@ -575,6 +582,7 @@ int gemm_chain_tc(const ChainStep* steps, int n_ops, int M, int* done, cudaStrea
     op.sp_major = sp_major;
     op.ep = st.ep;
     op.ep.splits = (int)s;
+    op.ep.k_strided = s > 1 && k_strided_for(st.K / CBK) ? 1 : 0;  // same rule as gemm_bf16_tc
     op.ep.l2_reads = 1;
     if (!op.ep.fault) op.ep.fault = fault_slot_current();
     op.ep.spin_ns = spin_limit_ns();

@@ -127,8 +127,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
   const int G = gridDim.x;
   const long long sk_hi = sk ? I * (blockIdx.x + 1) / G : 0;
   auto first = [&]() -> long long { return sk ? I * blockIdx.x / G : (long long)blockIdx.x; };
-  // next part: tile, [kb0, kb1), split sp of S (S = 0 marks a stream-K part)
-  auto next = [&](long long& st, int& tile, int& kb0, int& kb1, int& sp, int& S) -> bool {
+  // next part: tile, split sp of S (S = 0 marks a stream-K part) and its
+  // k-blocks kb0 + i * ks, i < n_kb: the range [kb0, kb1), or with
+  // ep.k_strided the blocks sp, sp + S, ... (every split then holds an equal
+  // share of the late-produced A columns, see the GEMM chain)
+  auto next = [&](long long& st, int& tile, int& kb0, int& kb1, int& sp, int& S, int& ks, int& n_kb) -> bool {
+    ks = 1;
     if (sk) {
       if (st >= sk_hi) return false;
       tile = (int)(st / nk);
@@ -137,6 +141,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
       kb1 = left < nk - kb0 ? kb0 + (int)left : nk;
       sp = 0, S = 0;
       st += kb1 - kb0;
+      n_kb = kb1 - kb0;
       return true;
     }
     if (st >= num_work) return false;
@@ -147,7 +152,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
       const int u = w - n_full;
       tile = n_full + u / splits, sp = u % splits, S = splits;
     }
-    kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
+    if (ep.k_strided && S > 1) {
+      kb0 = sp, kb1 = nk, ks = S, n_kb = (nk - sp + S - 1) / S;
+    } else {
+      kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S, n_kb = kb1 - kb0;
+    }
     st += G;
     return true;
   };
@@ -160,13 +169,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
       int npre = 0;
       {
         long long st = first();
-        int tile, kb0, kb1, sp, S;
-        if (next(st, tile, kb0, kb1, sp, S)) {
+        int tile, kb0, kb1, sp, S, ks, n_kb;
+        if (next(st, tile, kb0, kb1, sp, S, ks, n_kb)) {
           const int n_blk = tile / m_tiles;
-          npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
+          npre = n_kb < STAGES ? n_kb : STAGES;
           for (int i = 0; i < npre; ++i) {
             mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
-            tma_load_2d(sB + i * C::STAGE_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
+            tma_load_2d(sB + i * C::STAGE_BYTES, &tmB, &full[i], (kb0 + i * ks) * BK, n_blk * BN);
           }
         }
       }
@@ -175,10 +184,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
       int stage = 0, it = 0;
       uint32_t phase = 0;
       long long st = first();
-      int tile, kb0, kb1, sp, S;
-      while (next(st, tile, kb0, kb1, sp, S)) {
+      int tile, kb0, kb1, sp, S, ks, n_kb;
+      while (next(st, tile, kb0, kb1, sp, S, ks, n_kb)) {
         const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        for (int i = 0; i < n_kb; ++i, ++it) {
+          const int kb = kb0 + i * ks;
           if (it >= npre) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -199,15 +209,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
     int acc = 0;
     uint32_t acc_phase = 0;
     long long st = first();
-    int tile, kb0, kb1, sp, S;
-    while (next(st, tile, kb0, kb1, sp, S)) {
+    int tile, kb0, kb1, sp, S, ks, n_kb;
+    while (next(st, tile, kb0, kb1, sp, S, ks, n_kb)) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int i = 0; i < n_kb; ++i) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (kb == kb0 && lane == 0) stamp(2);
+        if (i == 0 && lane == 0) stamp(2);
         if (elect_one()) {
           const uint32_t a_base = smem_u32(sA + stage * C::STAGE_BYTES);
           const uint32_t b_base = smem_u32(sB + stage * C::STAGE_BYTES);
@@ -215,13 +225,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
-            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (i != 0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
-          if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+          if (i == n_kb - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (kb == kb1 - 1 && lane == 0) stamp(3);
+        if (i == n_kb - 1 && lane == 0) stamp(3);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -238,8 +248,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, GemmCfg<BN, AR>::MIN_BLOCKS)
     int acc = 0;
     uint32_t acc_phase = 0;
     long long st = first();
-    int tile, kb0, kb1, sp, S;
-    while (next(st, tile, kb0, kb1, sp, S)) {
+    int tile, kb0, kb1, sp, S, ks, n_kb;
+    while (next(st, tile, kb0, kb1, sp, S, ks, n_kb)) {
       const int m_blk = tile % m_tiles, n_blk = tile / m_tiles;
       const int ti = tile - n_full;  // tail index (workspace / counter slot)
       const int row = m_blk * BM + row_in_tile;
@@ -554,6 +564,20 @@ int tail_splits(long tiles, long sms, long nk) {
 // (BN=64, BN=128 for very wide N); at M~2.5k BN=128 wins for the N=4k/6k
 // projections and BN=256 for the wide gate/up; long-K (down projection) wants
 // BN=128 with the tail wave split along K; large M (full prefill) wants BN=256.
+// Long-K split-K (the FFN down projection, K = 14336: 224 k-blocks) takes
+// strided k-blocks: its A operand (the SwiGLU activations) is produced by the
+// gate/up op in two partial waves, and in the GEMM chain a contiguous split
+// whose k-range maps onto the second wave could only start after it; strided,
+// every split holds the same share of late columns and finishes right behind
+// gate/up. Same rule in the chain and here (bit-identical). FRAG_KSTRIDE=0: off.
+bool k_strided_for(long nk) {
+  static const bool on = [] {
+    const char* v = std::getenv("FRAG_KSTRIDE");
+    return !(v && v[0] == '0');
+  }();
+  return on && nk >= 128;
+}
+
 static bool pair224_on() {  // FRAG_GEMM_BN224=0: candidates 256 / 192 only
   static const bool on = [] {
     const char* v = std::getenv("FRAG_GEMM_BN224");
@@ -602,6 +626,7 @@ int gemm_bf16_tc(const bf16* A, const bf16* B, int M, int N, int K, EpiKind epi,
     if (s > nk) s = nk;  // every split needs at least one K block
     if (tiles > ep.counters_cap || (size_t)(tiles * s * M * bn) * sizeof(float) > ep.ws_bytes) s = 1;
     ep.splits = (int)s;
+    ep.k_strided = s > 1 && k_strided_for(nk) ? 1 : 0;
     ep.full_tiles = 0;
   }
   if (N % bn != 0) return -1;

@@ -51,6 +51,7 @@ struct EpiParams {
   int splits = 1;      // set by gemm_bf16_tc: K splits of each tail tile
   int full_tiles = 0;  // tiles before the split tail
   int streamk = 0;     // set by gemm_bf16_tc: stream-K decomposition (one M tile)
+  int k_strided = 0;   // one-M-tile split-K: split sp takes k-blocks sp, sp+S, ... (long K, see gemm_tc.cu)
   int group_m = 0;     // CTA-pair GEMM tile raster: M blocks per group (0: all, M fastest)
   int sk_maxc = 0;     // stream-K: max CTAs sharing one tile (workspace slots per tile)
   unsigned long long* trace = nullptr;  // tooling: per-CTA globaltimer stamps (FRAG_GEMM_TRACE)
@@ -101,6 +102,7 @@ bool fault_take(int dev);
 // GEMMs (M <= 128 rows, BN = 128) in one persistent launch, op i+1's A = op i's
 // output. `done` = 2*CHAIN_MAX_OPS ints, zero before the first launch (left zero).
 constexpr int CHAIN_MAX_OPS = 4;
+bool k_strided_for(long nk);  // one-M-tile split-K over strided k-blocks (gemm_tc.cu)
 struct AttnArgs;
 struct ChainStep {
   const bf16* A = nullptr;

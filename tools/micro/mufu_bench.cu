@@ -27,6 +27,8 @@ __global__ void k(float* out, int iters) {
         asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(a[i]));
       } else if (MODE == 4) {
         asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h[i]) : "f"(a[i]), "f"(__uint_as_float(h[i])));
+      } else if (MODE == 6) {  // truncating pack: the high halves of two fp32 (one PRMT)
+        asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(h[i]) : "r"(__float_as_uint(a[i])), "r"(h[(i + 1) & 7]));
       } else {  // softmax mix: 2 MUFU + 1 pack
         asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
         asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[(i + 1) & 7]));
@@ -48,8 +50,8 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const char* names[6] = {"ex2.f32", "ex2.f16x2", "ex2.bf16x2", "ffma.f32", "f2fp.pack", "2ex2+pack"};
-  for (int m = 0; m < 6; ++m) {
+  const char* names[7] = {"ex2.f32", "ex2.f16x2", "ex2.bf16x2", "ffma.f32", "f2fp.pack", "2ex2+pack", "prmt.pack"};
+  for (int m = 0; m < 7; ++m) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       if (m == 0) k<0><<<blocks, threads>>>(o, iters);
@@ -58,6 +60,7 @@ int main(int argc, char** argv) {
       if (m == 3) k<3><<<blocks, threads>>>(o, iters);
       if (m == 4) k<4><<<blocks, threads>>>(o, iters);
       if (m == 5) k<5><<<blocks, threads>>>(o, iters);
+      if (m == 6) k<6><<<blocks, threads>>>(o, iters);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
