@@ -20,9 +20,11 @@ def _gemm(a, b, c, epi, force_bn=0):
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 256, 64), (37, 512, 256), (128, 768, 256), (300, 1024, 512),
-                                   (2490, 1536, 4096), (129, 64, 192)])
+                                   (2490, 1536, 4096), (129, 64, 192), (32, 4096, 14336), (1, 4096, 14336)])
 @pytest.mark.parametrize("bn", [0, 64, 128, 256])
 def test_gemm_tcgen05_vs_torch(cuda, M, N, K, bn):
+    """1-CTA tcgen05 GEMM; K = 14336 at <= 128 rows is the question pass's down
+    projection: split-K over strided k-blocks (gemm_tc.cu k_strided_for)."""
     import torch
     if bn and N % bn:
         pytest.skip("N not a multiple of BN")
