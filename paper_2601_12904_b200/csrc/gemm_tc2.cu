@@ -17,6 +17,10 @@
 // kernel (gemm_epi.cuh).
 #include <cuda.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "gemm_epi.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -74,6 +78,18 @@ __device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_dst) {
 template <int NCOLS>
 __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+
+// tooling (FRAG_GEMM2_TRACE=<file>, tools/gemm2_trace.py): globaltimer stamps
+// per CTA into ep.trace[cta][32]: 0 entry, 1 prologue done, 2 producer past the
+// PDL wait, 4 + 4t + {0 first MMA, 1 last MMA issued, 2 accumulator seen by the
+// epilogue, 3 epilogue done} for the CTA's t-th tile (t < 6), 30 exit
+__device__ __forceinline__ void g2_stamp(const EpiParams& ep, int slot) {
+  if (ep.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ep.trace[blockIdx.x * 32 + slot] = t;
+  }
 }
 
 template <int BN>
@@ -149,11 +165,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
     }
     fence_mbar_init();
   }
+  if (threadIdx.x == 0) g2_stamp(ep, 0);
   if (warp == 1) tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) g2_stamp(ep, 1);
 
   if (warp == 0) {
     if (elect_one()) {
@@ -177,6 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
         }
       }
       pdl_wait();
+      g2_stamp(ep, 2);
       int stage = 0, it = 0;
       uint32_t phase = 0;
       for (int w = pair; w < num_work; w += n_pairs) {
@@ -212,12 +231,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int w = pair; w < num_work; w += n_pairs) {
+      int tcount = 0;
+      for (int w = pair; w < num_work; w += n_pairs, ++tcount) {
         int tile, sp, S;
         decode(w, tile, sp, S);
         const int kb0 = sp * nk / S, kb1 = (sp + 1) * nk / S;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (tcount < 6 && lane == 0) g2_stamp(ep, 4 + 4 * tcount);
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
@@ -230,6 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
               umma_bf16_pair(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
             umma_commit_pair(&empty[stage]);
             if (kb == kb1 - 1) umma_commit_pair(&tfull[acc]);
+            if (kb == kb1 - 1 && tcount < 6) g2_stamp(ep, 5 + 4 * tcount);
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -248,7 +270,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
     const uint32_t te_leader = smem_u32(tempty) & PEER_MASK;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = pair; w < num_work; w += n_pairs) {
+    int tcount = 0;
+    for (int w = pair; w < num_work; w += n_pairs, ++tcount) {
       int tile, sp, S;
       decode(w, tile, sp, S);
       int m_blk, n_blk;
@@ -258,6 +281,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
       const float rs = row < M ? epi_row_scale<EPI>(ep, row) : 1.f;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (warp == 2 && lane == 0 && tcount < 6) g2_stamp(ep, 6 + 4 * tcount);
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (S == 1) {
         if constexpr (EPI == EPI_SWIGLU) {
@@ -281,6 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+        if (warp == 2 && lane == 0 && tcount < 6) g2_stamp(ep, 7 + 4 * tcount);
       } else {
         // split partial of this CTA's 128 rows -> workspace (fp32); TMEM freed at once
         const int slot = (tile - n_full) * 2 + (int)rank;  // counter / workspace half-tile slot
@@ -307,6 +332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
   }
   tc_fence_before();
   cluster_sync();
+  if (threadIdx.x == 0) g2_stamp(ep, 30);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
@@ -332,7 +358,23 @@ int launch2(const bf16* A, const bf16* B, int M, int N, int K, const EpiParams& 
   const int grid = 2 * (work < pairs ? work : pairs);
   if (ep.splits > 1 && grid > num_sms() * resident_blocks(gemm_tc2_kernel<BN, EPI>, GEMM2_THREADS, (int)C::SMEM))
     return -1;  // the tail split's fixup waits on other CTAs of the grid
+  static const char* trace_path = std::getenv("FRAG_GEMM2_TRACE");  // tooling (tools/gemm2_trace.py)
+  static unsigned long long* trace_dev = nullptr;
+  if (trace_path) {
+    if (!trace_dev) cudaMalloc(&trace_dev, 160 * 32 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_dev, 0, 160 * 32 * sizeof(unsigned long long), stream);
+    ep.trace = trace_dev;
+  }
   launch_pdl(gemm_tc2_kernel<BN, EPI>, dim3(grid), dim3(GEMM2_THREADS), C::SMEM, stream, ta, tb, M, N, K, ep);
+  if (trace_path) {
+    std::vector<unsigned long long> h(160 * 32);
+    cudaMemcpyAsync(h.data(), trace_dev, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    if (FILE* f = std::fopen(trace_path, "ab")) {
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      std::fclose(f);
+    }
+  }
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -1,7 +1,10 @@
 import statistics, sys, torch
 sys.path.insert(0, "/root/repo")
 from paper_2601_12904_b200 import _lib as L
-M, N, K = 16384, 5376, 4096   # 5376 = 21*256 = 28*192 = 24*224
+import sys as _s
+# A (M x K bf16) must stay L2-resident, or the narrower tiles' extra A
+# re-reads from DRAM confound the comparison: M = 2490 (20 MB of A)
+M, N, K = 2490, 26880, 4096   # 26880 = 105*256 = 120*224 = 140*192 = 210*128
 a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
 b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
 c = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
