@@ -1,7 +1,9 @@
 """CTA-pair GEMM at the O-projection tile grid (M = 2490, N = 4096: 220
 192-wide tiles, 3 waves of 74 pairs) for several K: time = fixed + per-k-block
-slope, the fixed part being launch, prologue, pipeline fill and the last
-tile's drain. CUDA events, median of 20, bf16 store."""
+slope. The events bracket each host launch, so the fixed part includes the
+host's launch latency (tensor-map encoding, launch) as well as the kernel's
+prologue, pipeline fill and last-tile drain; tools/gemm2_trace.py separates
+the device part. CUDA events, median of 20, bf16 store."""
 import statistics
 import sys
 from pathlib import Path
