@@ -173,6 +173,38 @@ class ClockSampler:
                 "power_w": statistics.median(pw) if pw else None}
 
 
+class EnergyMeter:
+    """Board energy over a region from NVML's cumulative counter (mJ), plus the
+    enforced power limit: the request runs at the power cap, so its TTFT is
+    set by joules per request (profiles/gemm_tile_width_r02.md)."""
+
+    def __init__(self, gpu: int):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+        except Exception:
+            self.h = None
+
+    def read_mj(self):
+        if self.h is None:
+            return None
+        try:
+            return self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)
+        except Exception:
+            return None
+
+    def limit_w(self):
+        if self.h is None:
+            return None
+        try:
+            return self.nv.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1e3
+        except Exception:
+            return None
+
+
 def peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -332,12 +364,21 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    meter = EnergyMeter(local_rank)
+    e_start, t_start = meter.read_mj(), time.perf_counter()
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for i in range(args.steps):
             step_dev(args.warmup + i)
         ev1.record(stream)
         torch.cuda.synchronize()
+    e_end, t_end = meter.read_mj(), time.perf_counter()
+    energy = None
+    if e_start is not None and e_end is not None and e_end > e_start:
+        energy = {"j_per_request": (e_end - e_start) / 1e3 / args.steps,
+                  "avg_power_w": (e_end - e_start) / 1e3 / (t_end - t_start),
+                  "power_limit_w": meter.limit_w(),
+                  "source": "NVML total energy counter around the timed requests (board, this GPU)"}
     if world > 1:
         torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -502,7 +543,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         torch.distributed.barrier()  # peers may still read this rank's records until every rank is done
     return dict(ms=ms, e2e_ms=e2e_ms, full_ms=full_ms, launches=launches, prof=prof, stages=stages, T=T,
-                crit=crit, clocks=clk.summary(), cfg=c, w=w, ratio=ratio, h2d=h2d, d2h=d2h, sweep=sweep,
+                crit=crit, clocks=clk.summary(), energy=energy, cfg=c, w=w, ratio=ratio, h2d=h2d, d2h=d2h, sweep=sweep,
                 k=len(crit), decode_ms=decode_ms, n_dec=len(answer), load_leg=load_leg,
                 cacheblend_ms=cacheblend_ms, cacheblend_stages=cacheblend_stages, batch_leg=batch_leg,
                 mem_shared=mem_shared, mem_private=mem_private)
@@ -699,6 +740,7 @@ def main():
                         if r["prof"][5]["ms"] else None, "peak_gbs": hbm,
                         "note": "one-M-tile GEMMs (question pass, lm_head): algorithmic bytes = weights + rows"},
         "clocks": r["clocks"],
+        "energy": r.get("energy"),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
