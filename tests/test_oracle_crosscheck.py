@@ -154,3 +154,97 @@ def test_oracle_stitch_equals_independent_shift():
             ref = _rope(torch.from_numpy(k[l]).double(), torch.full((n,), float(delta)), c["rope_base"]).numpy()
             assert np.allclose(ko[l, dst:dst + n], ref, rtol=0, atol=2e-6), (l, dst)
             assert np.array_equal(vo[l, dst:dst + n], v[l])
+
+
+def _layers(m, c, x, pos, cache_k, cache_v, cache_pos, rows=None):
+    """Run hidden states x [n, d] at positions pos through every layer. Each
+    layer writes the new rows' K/V into the cache (at `rows`, or appended when
+    rows is None) and attends over every cache entry whose position is <= the
+    query's. Returns the final hidden states and the last layer's post-RoPE
+    queries."""
+    d, Hq, Hkv, dh, F = c["d_model"], c["n_heads"], c["n_kv_heads"], c["head_dim"], c["ffn_dim"]
+    n = x.shape[0]
+    kv = torch.arange(Hq) // (Hq // Hkv)
+    q_last = None
+    for l in range(c["layers"]):
+        h = _rms(x, _w(m, "attn_norm", l, (d,)), c["norm_eps"])
+        q = _rope((h @ _w(m, "wq", l, (Hq * dh, d)).T).view(n, Hq, dh), pos, c["rope_base"])
+        k = _rope((h @ _w(m, "wk", l, (Hkv * dh, d)).T).view(n, Hkv, dh), pos, c["rope_base"])
+        v = (h @ _w(m, "wv", l, (Hkv * dh, d)).T).view(n, Hkv, dh)
+        if rows is None:
+            K, Vv, P = torch.cat([cache_k[l], k]), torch.cat([cache_v[l], v]), torch.cat([cache_pos, pos])
+        else:
+            cache_k[l][rows], cache_v[l][rows] = k, v  # fresh rows replace the stale ones
+            K, Vv, P = cache_k[l], cache_v[l], cache_pos
+        s = torch.einsum("qhd,khd->hqk", q, K[:, kv]) / dh ** 0.5
+        s = s.masked_fill(~(P[None, :] <= pos[:, None])[None], float("-inf"))
+        o = torch.einsum("hqk,khd->qhd", torch.softmax(s, dim=-1), Vv[:, kv]).reshape(n, Hq * dh)
+        x = x + o @ _w(m, "wo", l, (d, Hq * dh)).T
+        h = _rms(x, _w(m, "ffn_norm", l, (d,)), c["norm_eps"])
+        x = x + (torch.nn.functional.silu(h @ _w(m, "w_gate", l, (F, d)).T) * (h @ _w(m, "w_up", l, (F, d)).T)) \
+            @ _w(m, "w_down", l, (d, F)).T
+        q_last = q
+    return x, q_last
+
+
+@pytest.mark.parametrize("ratio", [0.0, 0.15, 0.4])
+def test_oracle_reprocess_equals_independent_pipeline(ratio):
+    """The whole online reprocessing path restated
+    independently: records = each chunk prefilled alone at positions 1..n;
+    stitch_full_reuse (K re-rotated by target - native, V copied); the
+    question prefilled at T-|Q|+1..T against the stitched cache; query-guided
+    scores over the chunk keys of the last layer, global top-k (k = floor(r N +
+    0.5), lower index on ties); sparse prefill of crit ∪ question through every
+    layer with each layer's fresh K/V replacing the stale rows before that
+    layer's attention; logits of the last row. Oracle: orc_reprocess in fp32
+    (emulate_bf16 off)."""
+    c = CFGS["gqa"]
+    L, Hkv, dh, d = c["layers"], c["n_kv_heads"], c["head_dim"], c["d_model"]
+    m = O.Model(c).init_seed(21)
+    rng = np.random.default_rng(int(ratio * 100) + 1)
+    lens = [13, 9, 17]
+    chunks = [rng.integers(0, c["vocab"], n) for n in lens]
+    question = rng.integers(0, c["vocab"], 6)
+    emb = _w(m, "emb", 0, (c["vocab"], d))
+    records = []
+    for ch in chunks:  # preprocess_isolated: the chunk alone at native positions 1..n
+        n = len(ch)
+        ck = torch.zeros(L, n, Hkv, dh, dtype=torch.float64)
+        cv = torch.zeros_like(ck)
+        _layers(m, c, emb[torch.as_tensor(ch)], torch.arange(1, n + 1), ck, cv, torch.arange(1, n + 1),
+                rows=torch.arange(n))
+        records.append({"k": ck.float().numpy(), "v": cv.float().numpy(), "tokens": ch.tolist(), "native_start": 1})
+    out = m.reprocess(None, records, question.tolist(), ratio, emulate_bf16=False)
+
+    N, nq = sum(lens), len(question)
+    T = N + nq
+    # stitch (records as the oracle got them: fp32)
+    sk = torch.zeros(L, T, Hkv, dh, dtype=torch.float64)
+    sv = torch.zeros_like(sk)
+    off = 0
+    for rec, n in zip(records, lens):
+        k = torch.from_numpy(rec["k"]).double()
+        for l in range(L):
+            sk[l, off:off + n] = _rope(k[l], torch.full((n,), float(off + 1 - rec["native_start"])), c["rope_base"])
+        sv[:, off:off + n] = torch.from_numpy(rec["v"]).double()
+        off += n
+    # question pass against the stitched cache (side-effect free on it)
+    qpos = torch.arange(N + 1, T + 1)
+    _, qf = _layers(m, c, emb[torch.as_tensor(question)], qpos, sk[:, :N].clone(), sv[:, :N].clone(),
+                    torch.arange(1, N + 1))
+    kvh = torch.arange(c["n_heads"]) // (c["n_heads"] // Hkv)
+    sc = torch.softmax(torch.einsum("thd,nhd->thn", qf, sk[L - 1, :N][:, kvh]) / dh ** 0.5, dim=-1).sum(dim=(0, 1))
+    k_sel = int(np.floor(ratio * N + 0.5))
+    crit = sorted(sorted(range(N), key=lambda j: (-float(sc[j]), j))[:k_sel])
+    assert out["crit"].tolist() == [j + 1 for j in crit]  # 1-based positions
+    # sparse prefill of crit ∪ question over the stitched cache
+    rows = torch.tensor(crit + list(range(N, T)), dtype=torch.long)
+    toks = torch.as_tensor(np.concatenate([np.concatenate(chunks), question]))[rows]
+    cache_k, cache_v = sk.clone(), sv.clone()
+    x, _ = _layers(m, c, emb[toks], rows + 1, cache_k, cache_v, torch.arange(1, T + 1), rows=rows)
+    logits = _rms(x[-1:], _w(m, "final_norm", 0, (d,)), c["norm_eps"]) @ _w(m, "lm_head", 0, (c["vocab"], d)).T
+    ref = logits[0].numpy()
+    assert np.linalg.norm(out["logits"] - ref) / np.linalg.norm(ref) <= 1e-5
+    rel_k = np.linalg.norm(out["k"] - cache_k.numpy()) / np.linalg.norm(cache_k.numpy())
+    rel_v = np.linalg.norm(out["v"] - cache_v.numpy()) / np.linalg.norm(cache_v.numpy())
+    assert rel_k <= 1e-5 and rel_v <= 1e-5, (rel_k, rel_v)
