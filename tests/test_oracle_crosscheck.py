@@ -187,8 +187,8 @@ def _layers(m, c, x, pos, cache_k, cache_v, cache_pos, rows=None):
     return x, q_last
 
 
-@pytest.mark.parametrize("ratio", [0.0, 0.15, 0.4])
-def test_oracle_reprocess_equals_independent_pipeline(ratio):
+@pytest.mark.parametrize("ratio,S", [(0.0, 0), (0.15, 0), (0.4, 0), (0.15, 4)])
+def test_oracle_reprocess_equals_independent_pipeline(ratio, S):
     """The whole online reprocessing path restated
     independently: records = each chunk prefilled alone at positions 1..n;
     stitch_full_reuse (K re-rotated by target - native, V copied); the
@@ -206,22 +206,35 @@ def test_oracle_reprocess_equals_independent_pipeline(ratio):
     chunks = [rng.integers(0, c["vocab"], n) for n in lens]
     question = rng.integers(0, c["vocab"], 6)
     emb = _w(m, "emb", 0, (c["vocab"], d))
+    # system prompt (S tokens at positions 1..S), then each chunk prefilled
+    # alone after it at native positions S+1..S+n (preprocess_isolated)
+    sys_tok = rng.integers(0, c["vocab"], S)
+    sys_k = torch.zeros(L, S, Hkv, dh, dtype=torch.float64)
+    sys_v = torch.zeros_like(sys_k)
+    if S:
+        _layers(m, c, emb[torch.as_tensor(sys_tok)], torch.arange(1, S + 1), sys_k, sys_v, torch.arange(1, S + 1),
+                rows=torch.arange(S))
     records = []
-    for ch in chunks:  # preprocess_isolated: the chunk alone at native positions 1..n
+    for ch in chunks:
         n = len(ch)
-        ck = torch.zeros(L, n, Hkv, dh, dtype=torch.float64)
-        cv = torch.zeros_like(ck)
-        _layers(m, c, emb[torch.as_tensor(ch)], torch.arange(1, n + 1), ck, cv, torch.arange(1, n + 1),
-                rows=torch.arange(n))
-        records.append({"k": ck.float().numpy(), "v": cv.float().numpy(), "tokens": ch.tolist(), "native_start": 1})
-    out = m.reprocess(None, records, question.tolist(), ratio, emulate_bf16=False)
+        ck = torch.cat([sys_k, torch.zeros(L, n, Hkv, dh, dtype=torch.float64)], dim=1)
+        cv = torch.cat([sys_v, torch.zeros(L, n, Hkv, dh, dtype=torch.float64)], dim=1)
+        _layers(m, c, emb[torch.as_tensor(ch)], torch.arange(S + 1, S + n + 1), ck, cv, torch.arange(1, S + n + 1),
+                rows=torch.arange(S, S + n))
+        records.append({"k": ck[:, S:].float().numpy(), "v": cv[:, S:].float().numpy(), "tokens": ch.tolist(),
+                        "native_start": S + 1})
+    sys_kv = (sys_k.float().numpy(), sys_v.float().numpy()) if S else None
+    out = m.reprocess(sys_kv, records, question.tolist(), ratio, emulate_bf16=False)
 
     N, nq = sum(lens), len(question)
-    T = N + nq
-    # stitch (records as the oracle got them: fp32)
+    T = S + N + nq
+    # stitch: S rows, then the chunks from row S (records and system KV as the oracle got them: fp32)
     sk = torch.zeros(L, T, Hkv, dh, dtype=torch.float64)
     sv = torch.zeros_like(sk)
-    off = 0
+    if S:
+        sk[:, :S] = torch.from_numpy(sys_kv[0]).double()
+        sv[:, :S] = torch.from_numpy(sys_kv[1]).double()
+    off = S
     for rec, n in zip(records, lens):
         k = torch.from_numpy(rec["k"]).double()
         for l in range(L):
@@ -229,17 +242,18 @@ def test_oracle_reprocess_equals_independent_pipeline(ratio):
         sv[:, off:off + n] = torch.from_numpy(rec["v"]).double()
         off += n
     # question pass against the stitched cache (side-effect free on it)
-    qpos = torch.arange(N + 1, T + 1)
-    _, qf = _layers(m, c, emb[torch.as_tensor(question)], qpos, sk[:, :N].clone(), sv[:, :N].clone(),
-                    torch.arange(1, N + 1))
+    qpos = torch.arange(S + N + 1, T + 1)
+    _, qf = _layers(m, c, emb[torch.as_tensor(question)], qpos, sk[:, :S + N].clone(), sv[:, :S + N].clone(),
+                    torch.arange(1, S + N + 1))
     kvh = torch.arange(c["n_heads"]) // (c["n_heads"] // Hkv)
-    sc = torch.softmax(torch.einsum("thd,nhd->thn", qf, sk[L - 1, :N][:, kvh]) / dh ** 0.5, dim=-1).sum(dim=(0, 1))
+    keys = sk[L - 1, S:S + N][:, kvh]  # chunk keys only: never S or Q
+    sc = torch.softmax(torch.einsum("thd,nhd->thn", qf, keys) / dh ** 0.5, dim=-1).sum(dim=(0, 1))
     k_sel = int(np.floor(ratio * N + 0.5))
     crit = sorted(sorted(range(N), key=lambda j: (-float(sc[j]), j))[:k_sel])
-    assert out["crit"].tolist() == [j + 1 for j in crit]  # 1-based positions
+    assert out["crit"].tolist() == [S + j + 1 for j in crit]  # 1-based positions
     # sparse prefill of crit ∪ question over the stitched cache
-    rows = torch.tensor(crit + list(range(N, T)), dtype=torch.long)
-    toks = torch.as_tensor(np.concatenate([np.concatenate(chunks), question]))[rows]
+    rows = torch.tensor([S + j for j in crit] + list(range(S + N, T)), dtype=torch.long)
+    toks = torch.as_tensor(np.concatenate([sys_tok, np.concatenate(chunks), question]))[rows]
     cache_k, cache_v = sk.clone(), sv.clone()
     x, _ = _layers(m, c, emb[toks], rows + 1, cache_k, cache_v, torch.arange(1, T + 1), rows=rows)
     logits = _rms(x[-1:], _w(m, "final_norm", 0, (d,)), c["norm_eps"]) @ _w(m, "lm_head", 0, (c["vocab"], d)).T
