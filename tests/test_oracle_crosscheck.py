@@ -262,3 +262,45 @@ def test_oracle_reprocess_equals_independent_pipeline(ratio, S):
     rel_k = np.linalg.norm(out["k"] - cache_k.numpy()) / np.linalg.norm(cache_k.numpy())
     rel_v = np.linalg.norm(out["v"] - cache_v.numpy()) / np.linalg.norm(cache_v.numpy())
     assert rel_k <= 1e-5 and rel_v <= 1e-5, (rel_k, rel_v)
+
+
+def test_oracle_kv_deviation_equals_independent_restatement():
+    """kv_deviation (Eq. 7): Full Attention over cat(S,
+    chunks) vs the stitched Full Reuse cache, Δ[t, l, c] = Σ_j (KV_FA −
+    KV_FR)² per chunk token, layer and component (K, V), first layers."""
+    c = CFGS["gqa"]
+    L, Hkv, dh, d = c["layers"], c["n_kv_heads"], c["head_dim"], c["d_model"]
+    m = O.Model(c).init_seed(33)
+    rng = np.random.default_rng(2)
+    lens = [10, 14]
+    chunks = [rng.integers(0, c["vocab"], n) for n in lens]
+    emb = _w(m, "emb", 0, (c["vocab"], d))
+    records = []
+    for ch in chunks:
+        n = len(ch)
+        ck = torch.zeros(L, n, Hkv, dh, dtype=torch.float64)
+        cv = torch.zeros_like(ck)
+        _layers(m, c, emb[torch.as_tensor(ch)], torch.arange(1, n + 1), ck, cv, torch.arange(1, n + 1),
+                rows=torch.arange(n))
+        records.append({"k": ck.float().numpy(), "v": cv.float().numpy(), "tokens": ch.tolist(), "native_start": 1})
+    dev = m.kv_deviation(None, records, n_layers=2, emulate_bf16=False)
+    N = sum(lens)
+    # Full Attention KV of the concatenation
+    fk = torch.zeros(L, N, Hkv, dh, dtype=torch.float64)
+    fv = torch.zeros_like(fk)
+    _layers(m, c, emb[torch.as_tensor(np.concatenate(chunks))], torch.arange(1, N + 1), fk, fv,
+            torch.arange(1, N + 1), rows=torch.arange(N))
+    # Full Reuse (stitched) KV
+    rk = torch.zeros_like(fk)
+    rv = torch.zeros_like(fk)
+    off = 0
+    for rec, n in zip(records, lens):
+        k = torch.from_numpy(rec["k"]).double()
+        for l in range(L):
+            rk[l, off:off + n] = _rope(k[l], torch.full((n,), float(off)), c["rope_base"])
+        rv[:, off:off + n] = torch.from_numpy(rec["v"]).double()
+        off += n
+    ref = np.stack([((fk[:2] - rk[:2]) ** 2).sum(dim=(2, 3)).T.numpy(),
+                    ((fv[:2] - rv[:2]) ** 2).sum(dim=(2, 3)).T.numpy()], axis=-1)  # [N][2 layers][K, V]
+    assert np.allclose(dev, ref, rtol=1e-4, atol=1e-9 * np.abs(ref).max()), np.abs(dev - ref).max()
+    assert np.abs(ref[:, 0]).max() < 1e-9 * max(np.abs(ref).max(), 1.0)  # first layer: FR == FA (SPEC.md:415)
