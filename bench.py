@@ -365,14 +365,14 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     meter = EnergyMeter(local_rank)
-    e_start, t_start = meter.read_mj(), time.perf_counter()
     with ClockSampler(local_rank) as clk:
+        e_start, t_start = meter.read_mj(), time.perf_counter()  # the device is idle here (synchronized)
         ev0.record(stream)
         for i in range(args.steps):
             step_dev(args.warmup + i)
         ev1.record(stream)
         torch.cuda.synchronize()
-    e_end, t_end = meter.read_mj(), time.perf_counter()
+        e_end, t_end = meter.read_mj(), time.perf_counter()  # before the sampler thread is joined
     energy = None
     if e_start is not None and e_end is not None and e_end > e_start:
         energy = {"j_per_request": (e_end - e_start) / 1e3 / args.steps,
