@@ -794,13 +794,16 @@ __global__ void __launch_bounds__(576, 1)
       };
       auto issue_pv = [&](int u) {
         const int st = u % NSV;
-        mbar_wait(&p_full[u & 1], (u >> 1) & 1);
+        // V(u) landed and PV(u-1) done are independent of slice u's softmax:
+        // observe them first, so that P(u) is the only wait between the last
+        // softmax warp's arrival and the PV issue (the tensor pipe idles there)
+        mbar_wait(&v_full[st], (u / NSV) & 1);
         // observe pv_done phase u-1 (no phase completes unwaited; PV(u-2) is
         // known complete here -- S(u) was, and the pipe is in order -- so the
         // parity is unambiguous); PV(u-1) has normally finished while the
         // softmax of slice u ran
         if (u > 0) mbar_wait(pv_done, (u - 1) & 1);
-        mbar_wait(&v_full[st], (u / NSV) & 1);
+        mbar_wait(&p_full[u & 1], (u >> 1) & 1);
         tc_fence_after();
         if (a.trace && blockIdx.x == 0 && lane == 0 && u < 256) a.trace[u * 4 + 3] = clock64();
         if (elect_one()) {
@@ -968,6 +971,8 @@ __global__ void __launch_bounds__(576, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
       if (a.trace && blockIdx.x == 0 && lane == 0 && warp == 0 && u < 256) a.trace[u * 4 + 1] = clock64();
+      if (a.trace && blockIdx.x == 0 && lane == 0 && u < 256)  // the slice's last softmax warp
+        atomicMax(&a.trace[1024 + u * 4 + 3], (unsigned long long)clock64());
     }
     // ---- epilogue: the row sum accumulated by the tensor pipe (T_L)
     float lt = 0.f;
@@ -1135,6 +1140,7 @@ int attn_tc_launch(const AttnArgs& a, int G, int n_qblocks, cudaStream_t stream)
     const char* v = std::getenv("FRAG_ATTN_QTM");
     return !(v && v[0] == '0');
   }();
+
   if (qtm && poly == 0 && (a.dh == 128 || a.dh == 64)) {
     const int nqb1 = (a.M + AT_ROWS / G - 1) / (AT_ROWS / G);  // one 128-row tile per CTA
     const dim3 grid1(nqb1 * a.Hkv, 1, a.n_splits);

@@ -31,11 +31,13 @@ rec = np.fromfile(path, dtype=np.uint64).reshape(-1, 4, 256, 4)[-1].astype(np.in
 a, b = rec[0], rec[1]
 n = int((a[:, 0] > 0).sum())
 s_ready, p_done, s_iss, pv_iss = (a[:n, i] for i in range(4))
-ld, mx, ex = (b[:n, i] for i in range(3))
+ld, mx, ex, p_last = (b[:n, i] for i in range(4))
 med = lambda x: float(np.median(x))  # noqa: E731
 print(f"slices {n}; period {med(np.diff(s_ready)):.0f} cyc per 128 keys")
 print(f"  S ready -> S loaded {med(ld - s_ready):.0f}; -> max exchanged {med(mx - ld):.0f}; "
       f"-> exps done {med(ex - mx):.0f}; -> P done {med(p_done - ex):.0f}; P done -> next S ready "
       f"{med(s_ready[1:] - p_done[:-1]):.0f}")
+print(f"  last of the 16 softmax warps done {med(p_last - p_done):.0f} after warp 0; -> PV issue "
+      f"{med(pv_iss - p_last):.0f}")
 print(f"  P done -> PV issue {med(pv_iss - p_done):.0f}; S(u+2) issue - S(u+2) ready "
       f"{med(s_ready[2:] - s_iss[2:]):.0f}")
