@@ -34,11 +34,14 @@ namespace {
 constexpr int CBM = 128;  // UMMA M (accumulator rows; rows >= M are never stored)
 constexpr int CBN = 128;
 constexpr int CBK = 64;
+// ring depth at <= 32 rows: 11 x 20 KB fills the 227 KB of shared memory with
+// the static epilogue scratch (10 -> 11 measured within noise, kept; a build
+// override for A/Bs)
 #ifndef CHAIN_STAGES32
 #define CHAIN_STAGES32 11
 #endif
 // AR = live A rows loaded per stage (32 / 64 / 128: M <= AR); stage = AR x 64
-// activations + 128 x 64 weights, as many stages as fit in ~200 KB
+// activations + 128 x 64 weights, as many stages as fit in shared memory
 template <int AR>
 struct ChainCfg {
   static constexpr uint32_t A_BYTES = AR * 64 * 2;
